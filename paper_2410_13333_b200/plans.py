@@ -1,0 +1,141 @@
+"""Malleable parallelization plans as plain dicts (host-side input, not the product).
+
+A plan is the paper's four components (§4.1): GPU grouping (stage `ranks`),
+pipeline orchestration (`pipes`, ordered `stages`), layer assignment (`layers` = [begin, end),
+l_ij = end - begin), training-data assignment (`n_micro` = m_i), plus the micro-batch size b and
+global batch B (Table 1) and the removed / standby GPUs.
+North-star extension: per-member split vectors `heads`, `ffn`, `vocab` (uneven TP shards).
+
+The split vectors below are the min-max apportionments of SURVEY §8(d) (reading R7); the tests
+re-derive them with the oracle's split helper.
+"""
+from __future__ import annotations
+
+
+def stage(ranks, heads, ffn, vocab, layers):
+    return {"ranks": list(ranks), "heads": list(heads), "ffn": list(ffn), "vocab": list(vocab),
+            "layers": list(layers)}
+
+
+def even(total: int, k: int, gran: int = 1):
+    """Even split of `total` units of granularity `gran` over k members (remainder to the front)."""
+    units = total // gran
+    base, rem = divmod(units, k)
+    return [(base + (1 if i < rem else 0)) * gran for i in range(k)]
+
+
+def plan(pipes, b, B, standby=(), plan_id=0):
+    return {"plan_id": plan_id, "micro_batch": b, "global_batch": B, "pipes": pipes,
+            "standby": list(standby)}
+
+
+def pipe(stages, n_micro):
+    return {"stages": stages, "n_micro": n_micro}
+
+
+def even_stage(cfg, ranks, layers):
+    k = len(ranks)
+    return stage(ranks, even(cfg.n_heads, k), even(cfg.ffn, k, 16), even(cfg.vocab, k, 16), layers)
+
+
+def single_gpu(cfg, B, b=1, rank=0):
+    return plan([pipe([even_stage(cfg, [rank], [0, cfg.n_layers])], B // b)], b, B)
+
+
+def world_of(p) -> int:
+    ranks = [r for pp in p["pipes"] for st in pp["stages"] for r in st["ranks"]] + p["standby"]
+    return max(ranks) + 1
+
+
+def plan_matrix_c1(cfg, B=8, b=2):
+    """SURVEY §8(d) parity plan matrix P0-P8 on the tiny C1 model (4 heads, F 512, V 256, L 2)."""
+    L = cfg.n_layers
+    m = B // b
+    s31 = lambda ranks, layers: stage(ranks, [3, 1], [384, 128], [192, 64], layers)
+    ev = lambda ranks, layers: even_stage(cfg, ranks, layers)
+    P = {}
+    P["P0"] = plan([pipe([ev([0], [0, L])], m)], b, B)
+    P["P1"] = plan([pipe([ev([0, 1], [0, L])], m)], b, B)
+    P["P2"] = plan([pipe([s31([0, 1], [0, L])], m)], b, B)
+    P["P3"] = plan([pipe([ev([0], [0, L])], 3), pipe([ev([1], [0, L])], 1)], b, B)
+    P["P4"] = plan([pipe([s31([0, 1], [0, L])], 1), pipe([ev([2, 3], [0, L])], 3)], b, B)
+    P["P5"] = plan([pipe([s31([0, 1], [0, L])], 2), pipe([ev([2], [0, L])], 2)], b, B)
+    P["P6"] = plan([pipe([ev([0], [0, 1]), s31([1, 2], [1, L])], m)], b, B)
+    P["P7"] = plan([pipe([ev([0], [0, 1]), s31([1, 2], [1, L])], 1),
+                    pipe([ev([3, 4, 5, 6], [0, L])], 3)], b, B, standby=[7])
+    P["P8"] = plan([pipe([ev([0], [0, L])], 4), pipe([ev([1], [0, L])], 0)], b, B)
+    return P
+
+
+def ladder_plan(cfg, n_gpus: int, B: int, b: int = 1, straggle: bool = True):
+    """1/2/4/8-GPU ladder on the C2 shape (SURVEY §8(d) 'Ladder 1/2/4/8').
+
+    1: TP1.  2: TP2 with a 2x straggler on rank 1 (heads 22/10, min-max).  4: the C2 plan,
+    DP2 x TP2, rank 1 at 1.5x (heads 19/13, FFN tiles 52/34, vocab 148/102 tiles, m = (7, 9)).
+    8: DP2 x TP4, rank 3 at 2x (heads 10/10/10/2 ... min-max), m = (7, 9).
+    straggle=False gives the uniform even plan (T0 / T_u runs)."""
+    L, H, F, V = cfg.n_layers, cfg.n_heads, cfg.ffn, cfg.vocab
+    m = B // b
+    if n_gpus == 1:
+        return plan([pipe([even_stage(cfg, [0], [0, L])], m)], b, B)
+    if not straggle:
+        if n_gpus == 2:
+            return plan([pipe([even_stage(cfg, [0, 1], [0, L])], m)], b, B)
+        if n_gpus == 4:
+            return plan([pipe([even_stage(cfg, [0, 1], [0, L])], m // 2),
+                         pipe([even_stage(cfg, [2, 3], [0, L])], m - m // 2)], b, B)
+        if n_gpus == 8:
+            return plan([pipe([even_stage(cfg, [0, 1, 2, 3], [0, L])], m // 2),
+                         pipe([even_stage(cfg, [4, 5, 6, 7], [0, L])], m - m // 2)], b, B)
+    tiles = lambda v: [t * 128 for t in v]
+    if n_gpus == 2:
+        # x = (1, 2): heads 22/10 (max(22, 20) = 22 vs 21/11 -> 22: both min-max), FFN/vocab by tiles
+        st = stage([0, 1], [22, 10], _ffn_split(F, [1.0, 2.0]), _vocab_split(V, [1.0, 2.0]), [0, L])
+        return plan([pipe([st], m)], b, B)
+    if n_gpus == 4:
+        st0 = stage([0, 1], [19, 13], _ffn_split(F, [1.0, 1.5]), _vocab_split(V, [1.0, 1.5]), [0, L])
+        st1 = even_stage(cfg, [2, 3], [0, L])
+        m0 = (7 * m) // 16
+        return plan([pipe([st0], m0), pipe([st1], m - m0)], b, B)
+    if n_gpus == 8:
+        rates = [1.0, 1.0, 1.0, 2.0]
+        st0 = stage([0, 1, 2, 3], _heads_split(H, rates), _ffn_split(F, rates),
+                    _vocab_split(V, rates), [0, L])
+        st1 = even_stage(cfg, [4, 5, 6, 7], [0, L])
+        m0 = (7 * m) // 16
+        return plan([pipe([st0], m0), pipe([st1], m - m0)], b, B)
+    raise ValueError("ladder is defined for 1, 2, 4, 8 GPUs")
+
+
+def _minmax(n_units, rates):
+    """Min-max integer apportionment (reading R7); duplicated from the host planner side on purpose
+    (the product never imports oracle/).  Fastest members are filled first on ties."""
+    k = len(rates)
+    cands = sorted({round(c * x, 9) for x in rates for c in range(1, n_units + 1)})
+    for C in cands:
+        caps = [int(C / x + 1e-9) for x in rates]
+        if all(c >= 1 for c in caps) and sum(caps) >= n_units:
+            break
+    counts, left = [1] * k, n_units - k
+    for i in sorted(range(k), key=lambda i: (rates[i], i)):
+        add = min(left, caps[i] - counts[i])
+        counts[i] += add
+        left -= add
+    return counts
+
+
+def _heads_split(H, rates):
+    return _minmax(H, rates)
+
+
+def _ffn_split(F, rates, tile=128):
+    """FFN columns in whole 128-column tiles (last member takes the ragged remainder)."""
+    n_t, rem = divmod(F, tile)
+    c = _minmax(n_t, rates)
+    out = [x * tile for x in c]
+    out[-1] += rem
+    return out
+
+
+def _vocab_split(V, rates, tile=128):
+    return _ffn_split(V, rates, tile)

@@ -1,0 +1,43 @@
+"""The BJ invariant on the oracle side: any valid malleable partition yields the same loss,
+gradients and AdamW update as the unpartitioned step (PAPER.md:303 lossless).
+The fp64 partition emulator must match oracle/model.py to <= 1e-12 relative."""
+import numpy as np
+import pytest
+
+from synth.gen import C1_TINY, MICRO, make_weights, make_tokens
+from oracle import model as M
+from oracle.emulator import emulate_step
+from paper_2410_13333_b200 import plans as Pl
+from tests.planutil import random_plan
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def _compare(cfg, plan, B, seed=0, steps=1):
+    P = M.params_f64(make_weights(cfg))
+    tok, tgt = make_tokens(cfg, B)
+    Mo = {k: np.zeros_like(v) for k, v in P.items()}
+    Vo = {k: np.zeros_like(v) for k, v in P.items()}
+    loss, g, nP, nM, nV = M.train_step(cfg, P, Mo, Vo, tok, tgt, 1)
+    eloss, eg, enP, enM, enV, _ = emulate_step(cfg, P, Mo, Vo, plan, tok, tgt, 1)
+    assert abs(eloss - loss) <= 1e-12 * abs(loss)
+    for k in P:
+        assert _rel(eg[k], g[k]) <= 1e-12, (k, _rel(eg[k], g[k]))
+        assert _rel(enP[k], nP[k]) <= 1e-12
+        assert _rel(enM[k], nM[k]) <= 1e-12
+        assert _rel(enV[k], nV[k]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["P0", "P1", "P2", "P3", "P4", "P5", "P6", "P7", "P8"])
+def test_plan_matrix_c1(name):
+    cfg = C1_TINY
+    _compare(cfg, Pl.plan_matrix_c1(cfg)[name], B=8)
+
+
+def test_random_plans_micro():
+    rng = np.random.default_rng(2024)
+    for _ in range(200):
+        p, world = random_plan(rng, MICRO, world_max=8, B=8, b=2)
+        _compare(MICRO, p, B=8)
