@@ -1,0 +1,259 @@
+/* malleus.h — C-ABI of the B200-native Malleus hot path (arXiv 2410.13333).
+ *
+ * The library runs the paper's malleable hybrid-parallel training step on sm_100a:
+ * transformer layers with non-uniform tensor-parallel (TP) shards, non-uniform micro-batch
+ * counts per data-parallel (DP) pipeline, the batch-weighted gradient reduction across
+ * pipelines whose TP layouts differ (ZeRO-1 with varying TP degrees, §5.1),
+ * and model-state migration when the plan changes (§5.1).  The planner is
+ * host-side input (§4.1 defines the plan's four components).
+ *
+ * Conventions (all entry points):
+ *  - Every function returns malleus_status; nothing throws or aborts across the ABI.  On error
+ *    malleus_last_error(ctx) names the violated invariant.  CUDA / NCCL errors are sticky: the
+ *    context must be destroyed.
+ *  - Pointers documented "device" are CUDA device pointers owned by the caller (PyTorch
+ *    allocations); the library borrows them until the next plan_apply / migrate / destroy.
+ *    Pointers documented "host" are read (or written) during the call only; plan and config
+ *    structs are deep-copied.
+ *  - Streams: functions taking a cudaStream_t (passed as void*) only enqueue work on it;
+ *    plan_apply, migrate and probe_speed block.
+ *  - "collective" calls must be made by every rank of the world in the same order (NCCL rule);
+ *    standby ranks take part but do no work.  "local" calls involve one rank only.
+ *  - Activations are bf16 row-major [tokens, hidden], tokens = b * s, replicated across the
+ *    members of a TP group.
+ */
+#ifndef MALLEUS_H
+#define MALLEUS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MALLEUS_OK = 0,
+  MALLEUS_E_ARG = 1,     /* bad argument (null pointer, size, alignment) */
+  MALLEUS_E_PLAN = 2,    /* plan violates an invariant (see malleus_plan) */
+  MALLEUS_E_CUDA = 3,    /* CUDA runtime error (sticky) */
+  MALLEUS_E_NCCL = 4,    /* NCCL error (sticky) */
+  MALLEUS_E_NOMEM = 5,   /* caller-provided arena smaller than malleus_plan_requirements */
+  MALLEUS_E_STATE = 6,   /* call not valid in the current state (e.g. no plan applied) */
+  MALLEUS_E_TIMEOUT = 7
+} malleus_status;
+
+/* ---------------------------------------------------------------- model and plan
+ * Model: LLaMA-2 architecture (§7.1), MHA (n_kv_heads == n_heads, reading R1),
+ * RMSNorm eps, RoPE half-split with theta (readings R2/R3), SwiGLU FFN, untied embedding and
+ * LM head.  Logical tensors are stored split-axis-outermost with hidden innermost (reading R9):
+ * Wq, Wk, Wv, WoT [n*d, h]; Wg, Wu, WdT [ffn, h]; E, Wlm [vocab, h]; norm gains [h]. */
+typedef struct {
+  int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab, seq_len;
+  float rms_eps;    /* 1e-5 */
+  float rope_theta; /* 1e4 */
+} malleus_model_cfg;
+
+/* One pipeline stage = one TP group.  Per-member split vectors are the
+ * north-star extension (uneven TP shards): heads[k], ffn_cols[k], vocab_rows[k] are member k's
+ * share; each sums to n_heads / ffn / vocab.  Whole heads; ffn and vocab multiples of 16; every
+ * member >= 1 head and >= 16 ffn columns / vocab rows.  Layers [layer_begin, layer_end),
+ * l_ij = layer_end - layer_begin >= 1 (zero-layer stages are omitted). */
+typedef struct {
+  int32_t n_members;
+  const int32_t* ranks;      /* host, [n_members] */
+  const int32_t* heads;      /* host, [n_members] */
+  const int32_t* ffn_cols;   /* host, [n_members] */
+  const int32_t* vocab_rows; /* host, [n_members]; used on the last stage (LM head) */
+  int32_t layer_begin, layer_end;
+} malleus_stage;
+
+/* One DP pipeline: ordered stages (embedding on stage 0, final norm + LM head on the last,
+ * PAPER.md:1688) and its micro-batch count m_i >= 0. */
+typedef struct {
+  int32_t n_stages;
+  const malleus_stage* stages; /* host */
+  int32_t n_micro;
+} malleus_pipeline;
+
+/* The plan with b and B (Table 1).  Validation (E_PLAN):
+ * sum_i m_i * b == B (Eq.1); each pipeline's layer ranges partition [0, L) in
+ * stage order; every rank of [0, world) is in exactly one stage or standby. */
+typedef struct {
+  int32_t plan_id;
+  int32_t dp; /* number of pipelines */
+  const malleus_pipeline* pipes; /* host, [dp] */
+  int32_t micro_batch;  /* b */
+  int32_t global_batch; /* B, sequences per step */
+  int32_t n_standby;
+  const int32_t* standby; /* host, [n_standby] */
+} malleus_plan;
+
+/* Device arenas provided by the caller after malleus_plan_requirements.  16-byte aligned.
+ *   state : bf16 params held + fp32 master/m/v of owned pieces (persistent across steps)
+ *   grads : fp32 gradient shards of held tensors (persistent within a step)
+ *   work  : activations, saved tensors, staging (scratch)                                 */
+typedef struct {
+  void* state; size_t state_bytes;
+  void* grads; size_t grads_bytes;
+  void* work;  size_t work_bytes;
+} malleus_arenas;
+
+typedef struct { size_t state, grads, work; } malleus_requirements;
+
+/* AdamW (torch.optim.AdamW semantics, reading R5).  step = global step count t >= 1.
+ * apply_update = 0 -> grad_sync only reduces gradients (no optimizer update; parity mode). */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;
+  int32_t step, apply_update;
+} malleus_adam_cfg;
+
+typedef struct {
+  uint64_t bytes_sent, bytes_recv; /* this rank */
+  double seconds;                  /* wall, this rank, excluding the final barrier */
+  int32_t n_packs;                 /* 4-layer packs */
+} malleus_migrate_stats;
+
+typedef struct malleus_ctx malleus_ctx;
+
+/* Tensor ids: layer*16 + {0 ATTN_NORM g1, 1 WQ, 2 WK, 3 WV, 4 WO(T), 5 MLP_NORM g2, 6 WG, 7 WU,
+ * 8 WD(T)} and the globals below.  Kinds select which copy is read / written. */
+#define MALLEUS_T_EMBED 0x7FFF0000
+#define MALLEUS_T_FINAL_NORM 0x7FFF0001
+#define MALLEUS_T_LM_HEAD 0x7FFF0002
+enum { MALLEUS_KIND_PARAM = 0, MALLEUS_KIND_GRAD = 1, MALLEUS_KIND_MASTER = 2,
+       MALLEUS_KIND_ADAM_M = 3, MALLEUS_KIND_ADAM_V = 4, MALLEUS_KIND_RGRAD = 5 };
+/* PARAM: bf16 held rows; GRAD: fp32 local (pipeline-mean) gradient of held rows;
+ * MASTER/ADAM_M/ADAM_V: fp32 owned pieces; RGRAD: fp32 reduced gradient of owned pieces
+ * (sum_i w_i g_i, written by malleus_grad_sync). */
+
+/* ---------------------------------------------------------------- lifecycle
+ * malleus_nccl_unique_id (local): fills 128 bytes with a fresh ncclUniqueId (rank 0 calls it
+ * and broadcasts the bytes).  malleus_create (collective): binds `device`, creates the world
+ * NCCL communicator.  cfg is deep-copied. */
+malleus_status malleus_nccl_unique_id(uint8_t out[128]);
+malleus_status malleus_create(const malleus_model_cfg* cfg, int32_t rank, int32_t world,
+                              int32_t device, const uint8_t nccl_uid[128], malleus_ctx** out);
+malleus_status malleus_destroy(malleus_ctx* ctx);
+const char* malleus_last_error(const malleus_ctx* ctx); /* never NULL; static if ctx == NULL */
+const char* malleus_version(void);
+
+/* ---------------------------------------------------------------- plans
+ * plan_requirements (local, no GPU work): arena sizes this rank needs for `plan`.
+ * plan_apply (collective, blocking): validate, build layer/stage maps, split vectors, the
+ * common-refinement holder/owner maps (reading R9), TP and stage communicators
+ * (ncclCommSplit), bind arenas; parameters are undefined until written / migrated. */
+malleus_status malleus_plan_requirements(malleus_ctx* ctx, const malleus_plan* plan,
+                                         malleus_requirements* out);
+malleus_status malleus_plan_apply(malleus_ctx* ctx, const malleus_plan* plan,
+                                  const malleus_arenas* arenas);
+
+/* write_tensor (local, blocking): host_full is the whole logical tensor (PARAM: bf16 bits
+ * uint16[numel]; MASTER/ADAM_M/ADAM_V: float[numel]); the rank stores its held rows / owned
+ * pieces.  Writing PARAM also initialises MASTER = param and zeroes m, v of owned pieces.
+ * read_local (local, blocking): copies this rank's elements of (tensor, kind) to host_dst as a
+ * concatenation of flat element ranges [ranges[2i], ranges[2i+1]) of the logical tensor.
+ * Call with host_dst == NULL to get *n_ranges and *n_elems; capacity is *n_ranges on input. */
+malleus_status malleus_write_tensor(malleus_ctx* ctx, int32_t tensor_id, int32_t kind,
+                                    const void* host_full);
+malleus_status malleus_read_local(malleus_ctx* ctx, int32_t tensor_id, int32_t kind,
+                                  void* host_dst, int64_t* ranges, int32_t* n_ranges,
+                                  int64_t* n_elems);
+
+/* layout_query (local, host only, no GPU needed): flat element ranges of (tensor, kind) that
+ * `rank` holds (PARAM/GRAD) or owns (MASTER, ADAM_M, ADAM_V, RGRAD) under `plan` — the range arithmetic
+ * the runtime uses, exposed so it can be checked against the oracle's per-element maps.
+ * ranges capacity in pairs is *n_ranges on input; count on output. */
+malleus_status malleus_layout_query(const malleus_model_cfg* cfg, const malleus_plan* plan,
+                                    int32_t world, int32_t rank, int32_t tensor_id, int32_t kind,
+                                    int64_t* ranges, int32_t* n_ranges);
+
+/* migration_query (local, host only): the transfers of `kind` into (dst_rank) when moving from
+ * plan `from` to plan `to` (readings R10/R11): triples (tensor_id, elem_begin, elem_end) and
+ * the source rank, for every element dst needs and does not have.  Capacity in entries is
+ * *n on input. */
+malleus_status malleus_migration_query(const malleus_model_cfg* cfg, const malleus_plan* from,
+                                       const malleus_plan* to, int32_t world, int32_t dst_rank,
+                                       int32_t kind, int64_t* tensor_begin_end, int32_t* src,
+                                       int32_t* n);
+
+/* ---------------------------------------------------------------- the hot path
+ * layer_fwd / layer_bwd (local to the TP group; collective over it): one transformer layer
+ * held by this rank on one micro-batch `slot` (0 <= slot < b_in_flight).  x_in / x_out / dy /
+ * dx are device bf16 [b*s, h].  Saved activations live in the work arena.
+ * train_step (collective): the whole malleable step of this rank: embedding (first stage),
+ * its layers for all m_i micro-batches in 1F1B order with PP send/recv,
+ * LM head + vocab-parallel CE (last stage), fp32 gradient accumulation over micro-batches,
+ * then malleus_grad_sync.  tokens/targets: device int32 [B, s] (the whole global batch; the
+ * rank reads its pipeline's contiguous slice, reading R14).  loss_dev: device float[1],
+ * receives sum_i w_i * loss_i on every rank.
+ * grad_sync (collective): batch-weighted reduce of every tensor's gradient pieces to their
+ * owners, G = sum_i w_i g_i with w_i = m_i b / B (readings R4, R9),
+ * AdamW on owned pieces (if apply_update), bf16 push of the updated pieces to every holder. */
+malleus_status malleus_layer_fwd(malleus_ctx* ctx, int32_t layer, int32_t slot,
+                                 const void* x_in, void* x_out, void* stream);
+malleus_status malleus_layer_bwd(malleus_ctx* ctx, int32_t layer, int32_t slot,
+                                 const void* dy, void* dx, void* stream);
+malleus_status malleus_train_step(malleus_ctx* ctx, const int32_t* tokens,
+                                  const int32_t* targets, float* loss_dev,
+                                  const malleus_adam_cfg* adam, void* stream);
+malleus_status malleus_grad_sync(malleus_ctx* ctx, const malleus_adam_cfg* adam, void* stream);
+
+/* migrate (collective, blocking): move params (to new holders) and fp32 master/m/v (to new
+ * owners) from the current plan to new_plan, in packs of 4 consecutive layers, each pack one
+ * grouped NCCL send/recv; then new_plan becomes current and new_arenas are
+ * used.  The old arenas may be freed by the caller afterwards.  Bit-exact copies. */
+malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan,
+                               const malleus_arenas* new_arenas, malleus_migrate_stats* stats);
+
+/* probe_speed (collective, blocking): fixed micro-benchmark (bf16 GEMM + HBM copy) timed with
+ * CUDA events (§5.2), all-gathered: ms_per_rank[world] (host).
+ * set_slowdown (local): straggler emulation for tests and benchmarks (PAPER.md:818-825 uses
+ * competing processes).  mode 0 = off, 1 = HOG (persistent kernel occupying a fraction of SMs
+ * on a side stream), 2 = DUTY (spin kernel of (x-1) * t after every compute op on the rank's
+ * stream).  x >= 1. */
+malleus_status malleus_probe_speed(malleus_ctx* ctx, int32_t iters, float* ms_per_rank);
+malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode);
+
+/* compute / comm breakdown of the last train_step on this rank (ms, from CUDA events):
+ * out[0] compute, out[1] tp_comm, out[2] pp_comm, out[3] grad_sync, out[4] total. */
+malleus_status malleus_last_step_timing(malleus_ctx* ctx, float out[5]);
+
+/* ---------------------------------------------------------------- kernel-level entry points
+ * Single-GPU building blocks of the hot path, exposed for parity tests and roofline
+ * measurement.  All pointers are device pointers; all calls enqueue on `stream` and return
+ * immediately.  bf16 = uint16 bit patterns, row-major. */
+
+/* C (op)= A * B.  a_mn = 0: A stored [M][K] (lda >= K); a_mn = 1: A stored [K][M] (lda >= M).
+ * b_mn = 0: B stored [N][K] (ldb >= K, i.e. C = A B^T); b_mn = 1: B stored [K][N] (ldb >= N).
+ * mode 0: C bf16 = AB; 1: C fp32 = AB; 2: C fp32 += AB.  lda, ldb multiples of 8, ldc of 4,
+ * A and B 16-byte aligned.  tcgen05/TMEM/TMA kernel, fp32 accumulation. */
+malleus_status malleus_k_gemm(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda,
+                              int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, void* C,
+                              int64_t ldc, int32_t mode, void* stream);
+
+/* y = x * rsqrt(mean(x^2) + eps) * g; optional fused residual: if partial != NULL then
+ * x_new = bf16(x + partial) is written to x_out and normalised.  x, x_out, y: bf16 [T, h];
+ * partial: fp32 [T, h] or NULL; g: bf16 [h]; rstd: fp32 [T]. */
+malleus_status malleus_k_rmsnorm_fwd(int32_t T, int32_t h, const void* x, const float* partial,
+                                     void* x_out, const void* g, float eps, void* y, float* rstd,
+                                     void* stream);
+/* dx = r*u - x*r^3*mean(x*u) with u = g*dy (dy fp32 [T,h]), plus residual dres (bf16 or NULL):
+ * dx_out bf16 = bf16(dres + dx).  dg_accum fp32 [h] += sum_rows dy*x*r (deterministic). */
+malleus_status malleus_k_rmsnorm_bwd(int32_t T, int32_t h, const void* x, const void* g,
+                                     const float* rstd, const float* dy, const void* dres,
+                                     void* dx_out, float* dg_accum, void* stream);
+/* Causal attention on qkv [T, 3*n*d] (q | k | v column blocks, T = nb * s tokens, sequences of
+ * length s), RoPE applied in place to q and k first (fwd) / to dq, dk last (bwd).
+ * o: bf16 [T, n*d]; lse: fp32 [nb, n, s]. */
+malleus_status malleus_k_attention_fwd(int32_t nb, int32_t s, int32_t n, int32_t d, void* qkv,
+                                       void* o, float* lse, float rope_theta, void* stream);
+malleus_status malleus_k_attention_bwd(int32_t nb, int32_t s, int32_t n, int32_t d,
+                                       const void* qkv, const void* o, const float* lse,
+                                       const void* dout, void* dqkv, float rope_theta,
+                                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MALLEUS_H */

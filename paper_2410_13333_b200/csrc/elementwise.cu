@@ -1,0 +1,476 @@
+// HBM-bound kernels of the hot path: RMSNorm fwd/bwd
+// with fused residual add (the K15 epilogue once the TP partial sum is reduced), RoPE, SwiGLU,
+// embedding gather / scatter-add, vocab-parallel cross-entropy.  128-bit loads/stores, fp32
+// math, warp-shuffle reductions, deterministic column reductions (fixed order, no atomics) for
+// the norm-gain gradients.  bf16 rounding points follow reading R6.
+#include <cuda_bf16.h>
+#include "kernels.h"
+
+namespace mls {
+
+namespace {
+
+constexpr int NORM_THREADS = 128;
+constexpr int NORM_MAXV = 8;  // vectors of 8 bf16 per thread -> h <= 8 * 8 * 128 = 8192
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float r = 0.f;
+#pragma unroll
+  for (int i = 0; i < NT / 32; ++i) r += sh[i];
+  return r;
+}
+template <int NT>
+__device__ __forceinline__ float block_max(float v, float* sh) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float r = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NT / 32; ++i) r = fmaxf(r, sh[i]);
+  return r;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(b[i]);
+    f[2 * i] = t.x; f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+// ---------------------------------------------------------------- RMSNorm forward
+// y = x_new * r * g, r = rsqrt(mean(x_new^2) + eps), x_new = bf16(x + partial) if partial.
+__global__ void __launch_bounds__(NORM_THREADS)
+rmsnorm_fwd_kernel(int h, const uint4* __restrict__ x, const float4* __restrict__ partial,
+                   uint4* __restrict__ x_out, const uint4* __restrict__ g, float eps,
+                   uint4* __restrict__ y, float* __restrict__ rstd) {
+  __shared__ float sh[NORM_THREADS / 32];
+  const int row = blockIdx.x;
+  const int nv = h / 8;
+  const uint4* xr = x + (long long)row * nv;
+  float v[NORM_MAXV][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NORM_MAXV; ++i) {
+    const int c = threadIdx.x + i * NORM_THREADS;
+    if (c < nv) {
+      unpack8(xr[c], v[i]);
+      if (partial) {
+        const float4* pr = partial + ((long long)row * nv + c) * 2;
+        float4 p0 = pr[0], p1 = pr[1];
+        v[i][0] += p0.x; v[i][1] += p0.y; v[i][2] += p0.z; v[i][3] += p0.w;
+        v[i][4] += p1.x; v[i][5] += p1.y; v[i][6] += p1.z; v[i][7] += p1.w;
+        uint4 q = pack8(v[i]);          // residual stream is bf16 (reading R6)
+        x_out[(long long)row * nv + c] = q;
+        unpack8(q, v[i]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += v[i][j] * v[i][j];
+    }
+  }
+  ss = block_sum<NORM_THREADS>(ss, sh);
+  const float r = rsqrtf(ss / (float)h + eps);
+  if (threadIdx.x == 0) rstd[row] = r;
+#pragma unroll
+  for (int i = 0; i < NORM_MAXV; ++i) {
+    const int c = threadIdx.x + i * NORM_THREADS;
+    if (c < nv) {
+      float gg[8];
+      unpack8(g[c], gg);
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = v[i][j] * r * gg[j];
+      y[(long long)row * nv + c] = pack8(o);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- RMSNorm backward
+// dx = r*u - x*r^3*mean(x*u), u = g*dy; dx_out = bf16(dres + dx); dg partial per block.
+// Two passes over each row (the second re-reads x / dy / g from L1) so that only the dg
+// accumulators stay resident in registers.
+__device__ __forceinline__ void load_f8(const float4* p, float (&f)[8]) {
+  float4 a = p[0], b = p[1];
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+__global__ void __launch_bounds__(NORM_THREADS)
+rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x,
+                   const uint4* __restrict__ g, const float* __restrict__ rstd,
+                   const float4* __restrict__ dy, const uint4* __restrict__ dres,
+                   uint4* __restrict__ dx_out, float* __restrict__ dg_part) {
+  __shared__ float sh[NORM_THREADS / 32];
+  const int nv = h / 8;
+  float dg[NORM_MAXV][8];
+#pragma unroll
+  for (int i = 0; i < NORM_MAXV; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dg[i][j] = 0.f;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(T, r0 + rows_per_block);
+  for (int row = r0; row < r1; ++row) {
+    const float r = rstd[row];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < NORM_MAXV; ++i) {
+      const int c = threadIdx.x + i * NORM_THREADS;
+      if (c < nv) {
+        float xv[8], dv[8], gg[8];
+        unpack8(x[(long long)row * nv + c], xv);
+        load_f8(dy + ((long long)row * nv + c) * 2, dv);
+        unpack8(g[c], gg);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          dot += xv[j] * gg[j] * dv[j];
+          dg[i][j] += dv[j] * xv[j] * r;
+        }
+      }
+    }
+    dot = block_sum<NORM_THREADS>(dot, sh);
+    const float coef = r * r * r * dot / (float)h;
+#pragma unroll
+    for (int i = 0; i < NORM_MAXV; ++i) {
+      const int c = threadIdx.x + i * NORM_THREADS;
+      if (c < nv) {
+        float xv[8], dv[8], gg[8], o[8], rs[8];
+        unpack8(x[(long long)row * nv + c], xv);
+        load_f8(dy + ((long long)row * nv + c) * 2, dv);
+        unpack8(g[c], gg);
+        if (dres) unpack8(dres[(long long)row * nv + c], rs);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          o[j] = r * gg[j] * dv[j] - xv[j] * coef;
+          if (dres) o[j] += rs[j];
+        }
+        dx_out[(long long)row * nv + c] = pack8(o);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NORM_MAXV; ++i) {
+    const int c = threadIdx.x + i * NORM_THREADS;
+    if (c < nv) {
+      float4* out = reinterpret_cast<float4*>(dg_part + (long long)blockIdx.x * h + c * 8);
+      out[0] = make_float4(dg[i][0], dg[i][1], dg[i][2], dg[i][3]);
+      out[1] = make_float4(dg[i][4], dg[i][5], dg[i][6], dg[i][7]);
+    }
+  }
+}
+
+// dg[c] += sum_b part[b][c], b in fixed order (deterministic)
+__global__ void colsum_accum_kernel(int nb, int h, const float* __restrict__ part, float* __restrict__ dg) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= h) return;
+  float s = 0.f;
+  for (int b = 0; b < nb; ++b) s += part[(long long)b * h + c];
+  dg[c] += s;
+}
+
+constexpr int BWD_BLOCKS = 296;  // 2 per SM
+
+// ---------------------------------------------------------------- residual add
+__global__ void residual_add_kernel(long long nv, const uint4* __restrict__ x, const float4* __restrict__ p,
+                                    uint4* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+    float v[8];
+    unpack8(x[i], v);
+    float4 a = p[2 * i], b = p[2 * i + 1];
+    v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w; v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+    out[i] = pack8(v);
+  }
+}
+
+// ---------------------------------------------------------------- RoPE (half-split, reading R3)
+// buf row t: columns [col0 + j*d, col0 + (j+1)*d) is head j; pairs (i, i + d/2); pos = t % s.
+// Applied to q (col0 = 0) and k (col0 = n*d) by blockIdx.y.
+__global__ void rope_kernel(int T, int s, int n, int d, __nv_bfloat16* __restrict__ buf, long long ld,
+                            int col0, float log2_theta, float sign) {
+  const int half = d / 2;
+  const long long total = (long long)T * n * half;
+  const int which = blockIdx.y;  // 0: q block, 1: k block
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = idx % half;
+    const long long th = idx / half;
+    const int j = th % n;
+    const int t = th / n;
+    const int pos = t % s;
+    const float inv = exp2f(-(2.f * i / (float)d) * log2_theta);
+    float sn, cs;
+    sincosf((float)pos * inv, &sn, &cs);
+    sn *= sign;
+    __nv_bfloat16* p = buf + (long long)t * ld + col0 + which * n * d + j * d;
+    const float a = __bfloat162float(p[i]);
+    const float b = __bfloat162float(p[i + half]);
+    p[i] = __float2bfloat16_rn(a * cs - b * sn);
+    p[i + half] = __float2bfloat16_rn(b * cs + a * sn);
+  }
+}
+
+// ---------------------------------------------------------------- SwiGLU
+__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + __expf(-x)); }
+
+__global__ void swiglu_fwd_kernel(int T, int F, const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ u) {
+  const int fv = F / 8;
+  const long long total = (long long)T * fv;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long t = idx / fv;
+    const int c = idx % fv;
+    float G[8], U[8], o[8];
+    unpack8(reinterpret_cast<const uint4*>(gu + t * 2 * F)[c], G);
+    unpack8(reinterpret_cast<const uint4*>(gu + t * 2 * F + F)[c], U);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = G[j] * sigm(G[j]) * U[j];
+    reinterpret_cast<uint4*>(u + t * F)[c] = pack8(o);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(int T, int F, const __nv_bfloat16* __restrict__ gu,
+                                  const __nv_bfloat16* __restrict__ du, __nv_bfloat16* __restrict__ dgu) {
+  const int fv = F / 8;
+  const long long total = (long long)T * fv;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long t = idx / fv;
+    const int c = idx % fv;
+    float G[8], U[8], D[8], dG[8], dU[8];
+    unpack8(reinterpret_cast<const uint4*>(gu + t * 2 * F)[c], G);
+    unpack8(reinterpret_cast<const uint4*>(gu + t * 2 * F + F)[c], U);
+    unpack8(reinterpret_cast<const uint4*>(du + t * F)[c], D);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float sg = sigm(G[j]);
+      dU[j] = D[j] * G[j] * sg;
+      dG[j] = D[j] * U[j] * sg * (1.f + G[j] * (1.f - sg));
+    }
+    reinterpret_cast<uint4*>(dgu + t * 2 * F)[c] = pack8(dG);
+    reinterpret_cast<uint4*>(dgu + t * 2 * F + F)[c] = pack8(dU);
+  }
+}
+
+// ---------------------------------------------------------------- embedding
+__global__ void embed_fwd_kernel(int T, int h, const int32_t* __restrict__ tok, const uint4* __restrict__ E,
+                                 uint4* __restrict__ x) {
+  const int nv = h / 8;
+  const int t = blockIdx.x;
+  const long long src = (long long)tok[t] * nv;
+  for (int c = threadIdx.x; c < nv; c += blockDim.x) x[(long long)t * nv + c] = E[src + c];
+}
+
+__global__ void embed_bwd_kernel(int T, int h, const int32_t* __restrict__ tok, const uint4* __restrict__ dx,
+                                 float* __restrict__ dE) {
+  const int nv = h / 8;
+  const int t = blockIdx.x;
+  float* dst = dE + (long long)tok[t] * h;
+  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+    float v[8];
+    unpack8(dx[(long long)t * nv + c], v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) atomicAdd(dst + c * 8 + j, v[j]);
+  }
+}
+
+// ---------------------------------------------------------------- vocab-parallel cross-entropy
+constexpr int CE_THREADS = 256;
+
+// stats[t] = {local max, sum exp(z - local max), target logit or 0}
+__global__ void __launch_bounds__(CE_THREADS)
+ce_stats_kernel(int V, const float* __restrict__ z, const int32_t* __restrict__ tgt, int v0,
+                float* __restrict__ stats) {
+  __shared__ float sh[CE_THREADS / 32];
+  const int t = blockIdx.x;
+  const float* zr = z + (long long)t * V;
+  float m = -INFINITY;
+  for (int c = threadIdx.x; c < V; c += CE_THREADS) m = fmaxf(m, zr[c]);
+  m = block_max<CE_THREADS>(m, sh);
+  float s = 0.f;
+  for (int c = threadIdx.x; c < V; c += CE_THREADS) s += __expf(zr[c] - m);
+  s = block_sum<CE_THREADS>(s, sh);
+  if (threadIdx.x == 0) {
+    const int y = tgt[t] - v0;
+    stats[3 * t] = m;
+    stats[3 * t + 1] = s;
+    stats[3 * t + 2] = (y >= 0 && y < V) ? zr[y] : 0.f;
+  }
+}
+
+__global__ void ce_grad_kernel(int V, const float* __restrict__ z, const int32_t* __restrict__ tgt, int v0,
+                               const float* __restrict__ gmax, const float* __restrict__ gsum,
+                               const float* __restrict__ gtgt, float scale, __nv_bfloat16* __restrict__ dz,
+                               float* __restrict__ loss_rows) {
+  const int t = blockIdx.x;
+  const float lse = gmax[t] + logf(gsum[t]);
+  if (threadIdx.x == 0 && loss_rows) loss_rows[t] = lse - gtgt[t];
+  const float* zr = z + (long long)t * V;
+  __nv_bfloat16* dr = dz + (long long)t * V;
+  const int y = tgt[t] - v0;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    float p = __expf(zr[c] - lse);
+    if (c == y) p -= 1.f;
+    dr[c] = __float2bfloat16_rn(p * scale);
+  }
+}
+
+// gmax[t] = stats max (before TP all-reduce MAX)
+__global__ void ce_max_kernel(int T, const float* __restrict__ stats, float* __restrict__ gmax) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T) gmax[t] = stats[3 * t];
+}
+// sum_tgt[2t] = local sumexp rescaled to the global max, sum_tgt[2t+1] = target logit
+__global__ void ce_local_sum_kernel(int T, const float* __restrict__ stats, const float* __restrict__ gmax,
+                                    float* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T) {
+    out[t] = stats[3 * t + 1] * __expf(stats[3 * t] - gmax[t]);
+    out[T + t] = stats[3 * t + 2];
+  }
+}
+
+__global__ void reduce_loss_kernel(int T, const float* __restrict__ rows, float scale, float* __restrict__ out,
+                                   int accumulate) {
+  __shared__ float sh[1024 / 32];
+  float s = 0.f;
+  for (int t = threadIdx.x; t < T; t += 1024) s += rows[t];
+  s = block_sum<1024>(s, sh);
+  if (threadIdx.x == 0) *out = accumulate ? *out + s * scale : s * scale;
+}
+
+__global__ void cast_kernel(long long n, const float* __restrict__ in, __nv_bfloat16* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+__global__ void fill_kernel(long long n, float* __restrict__ p, float v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+inline int grid_for(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  return (int)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+}  // namespace
+
+cudaError_t rmsnorm_fwd(int T, int h, const void* x, const float* partial, void* x_out, const void* g,
+                        float eps, void* y, float* rstd, cudaStream_t st) {
+  if (h % 8 || h > 8 * NORM_MAXV * NORM_THREADS || T <= 0) return cudaErrorInvalidValue;
+  if (partial && !x_out) return cudaErrorInvalidValue;
+  rmsnorm_fwd_kernel<<<T, NORM_THREADS, 0, st>>>(h, (const uint4*)x, (const float4*)partial, (uint4*)x_out,
+                                                 (const uint4*)g, eps, (uint4*)y, rstd);
+  return cudaGetLastError();
+}
+
+size_t rmsnorm_bwd_scratch_floats(int T, int h) { return (size_t)BWD_BLOCKS * h; }
+
+cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float* rstd, const float* dy,
+                        const void* dres, void* dx_out, float* dg_accum, float* scratch, cudaStream_t st) {
+  if (h % 8 || h > 8 * NORM_MAXV * NORM_THREADS || T <= 0) return cudaErrorInvalidValue;
+  int rpb = (T + BWD_BLOCKS - 1) / BWD_BLOCKS;
+  int nb = (T + rpb - 1) / rpb;
+  rmsnorm_bwd_kernel<<<nb, NORM_THREADS, 0, st>>>(T, h, rpb, (const uint4*)x, (const uint4*)g, rstd,
+                                                  (const float4*)dy, (const uint4*)dres, (uint4*)dx_out, scratch);
+  colsum_accum_kernel<<<(h + 255) / 256, 256, 0, st>>>(nb, h, scratch, dg_accum);
+  return cudaGetLastError();
+}
+
+cudaError_t residual_add(long long n, const void* x, const float* partial, void* out, cudaStream_t st) {
+  if (n % 8) return cudaErrorInvalidValue;
+  residual_add_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>(n / 8, (const uint4*)x, (const float4*)partial, (uint4*)out);
+  return cudaGetLastError();
+}
+
+cudaError_t rope_inplace(int T, int s, int n, int d, void* buf, long long ld, int col0, float theta,
+                         bool inverse, cudaStream_t st) {
+  long long total = (long long)T * n * (d / 2);
+  dim3 grid(grid_for(total, 256), 2);
+  rope_kernel<<<grid, 256, 0, st>>>(T, s, n, d, (__nv_bfloat16*)buf, ld, col0, log2f(theta), inverse ? -1.f : 1.f);
+  return cudaGetLastError();
+}
+
+cudaError_t swiglu_fwd(int T, int F, const void* gu, void* u, cudaStream_t st) {
+  if (F % 8) return cudaErrorInvalidValue;
+  swiglu_fwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, st>>>(T, F, (const __nv_bfloat16*)gu, (__nv_bfloat16*)u);
+  return cudaGetLastError();
+}
+
+cudaError_t swiglu_bwd(int T, int F, const void* gu, const void* du, void* dgu, cudaStream_t st) {
+  if (F % 8) return cudaErrorInvalidValue;
+  swiglu_bwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, st>>>(T, F, (const __nv_bfloat16*)gu,
+                                                                       (const __nv_bfloat16*)du, (__nv_bfloat16*)dgu);
+  return cudaGetLastError();
+}
+
+cudaError_t embed_fwd(int T, int h, const int32_t* tok, const void* E, void* x, cudaStream_t st) {
+  embed_fwd_kernel<<<T, 128, 0, st>>>(T, h, tok, (const uint4*)E, (uint4*)x);
+  return cudaGetLastError();
+}
+
+cudaError_t embed_bwd(int T, int h, const int32_t* tok, const void* dx, float* dE, cudaStream_t st) {
+  embed_bwd_kernel<<<T, 128, 0, st>>>(T, h, tok, (const uint4*)dx, dE);
+  return cudaGetLastError();
+}
+
+cudaError_t ce_stats(int T, int V, const float* z, const int32_t* tgt, int v0, float* stats, cudaStream_t st) {
+  ce_stats_kernel<<<T, CE_THREADS, 0, st>>>(V, z, tgt, v0, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t ce_combine_max(int T, const float* stats, float* gmax, cudaStream_t st) {
+  ce_max_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, stats, gmax);
+  return cudaGetLastError();
+}
+
+cudaError_t ce_local_sum(int T, const float* stats, const float* gmax, float* sum_tgt, cudaStream_t st) {
+  ce_local_sum_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, stats, gmax, sum_tgt);
+  return cudaGetLastError();
+}
+
+cudaError_t ce_grad(int T, int V, const float* z, const int32_t* tgt, int v0, const float* gmax, const float* gsum,
+                    const float* gtgt, float scale, void* dz, float* loss_rows, cudaStream_t st) {
+  ce_grad_kernel<<<T, 256, 0, st>>>(V, z, tgt, v0, gmax, gsum, gtgt, scale, (__nv_bfloat16*)dz, loss_rows);
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_loss(int T, const float* rows, float scale, float* out, int accumulate, cudaStream_t st) {
+  reduce_loss_kernel<<<1, 1024, 0, st>>>(T, rows, scale, out, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t cast_f32_bf16(long long n, const float* in, void* out, cudaStream_t st) {
+  cast_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, in, (__nv_bfloat16*)out);
+  return cudaGetLastError();
+}
+
+cudaError_t fill_f32(long long n, float* p, float v, cudaStream_t st) {
+  fill_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, p, v);
+  return cudaGetLastError();
+}
+
+}  // namespace mls

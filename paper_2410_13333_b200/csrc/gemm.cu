@@ -1,0 +1,281 @@
+// tcgen05 / TMEM / TMA bf16 GEMM for sm_100a: the uneven-split sharded GEMMs of the hot path
+// (PAPER.md:262 Megatron TP column/row splits).
+//
+//   C[M,N] (op)= A[M,K] * B[K,N]      fp32 accumulation in TMEM, bf16 operands from HBM via TMA
+//
+// Operand storage (row-major in HBM):
+//   A K-major : A stored [M][K]          A MN-major : A stored [K][M]   (i.e. A^T row-major)
+//   B K-major : B stored [N][K] (Y=XW^T) B MN-major : B stored [K][N]
+// The three combinations used by a transformer layer:
+//   fwd / dgrad of K-major weights : (K, K)     x W^T
+//   fwd of [in,out]-stored weights, dgrad of [out,in]-stored weights : (K, MN)
+//   wgrad dW = dY^T X             : (MN, MN)
+//
+// Design: persistent, one CTA per SM, warp-specialised (warp 0 TMA producer, warp 1 MMA issuer +
+// TMEM owner, warps 2..5 epilogue), 4-stage smem ring of 128x64 A + 256x64 B bf16 tiles with
+// 128-byte swizzle, UMMA 128x256x16, double-buffered 2x256-column fp32 accumulators in TMEM so
+// the epilogue of tile i overlaps the main loop of tile i+1.  Ragged M/N/K tails are handled by
+// TMA out-of-bounds zero fill and masked epilogue stores (uneven TP shards produce ragged N).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include "ptx.cuh"
+#include "kernels.h"
+
+namespace mls {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_TILE_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_TILE_BYTES = BN * BK * 2;   // 32 KB
+constexpr int STAGE_BYTES = A_TILE_BYTES + B_TILE_BYTES;
+constexpr int GEMM_SMEM = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+constexpr int GEMM_THREADS = 192;
+
+struct GemmParams {
+  int M, N, K;
+  void* C;
+  long long ldc;
+  int mode;  // GEMM_STORE_BF16 / GEMM_STORE_F32 / GEMM_ACCUM_F32
+  int vec_ok;  // rows of C are 16-byte aligned -> 128-bit stores
+};
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
+  constexpr int G = 8;  // group 8 M-tiles so consecutive CTAs share B tiles in L2
+  int per_group = G * tiles_n;
+  int g = t / per_group;
+  int first_m = g * G;
+  int gsz = min(tiles_m - first_m, G);
+  int r = t % per_group;
+  tm = first_m + r % gsz;
+  tn = r / gsz;
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tiles_m = (p.M + BM - 1) / BM;
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int n_tiles = tiles_m * tiles_n;
+  const int n_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int tm, tn; tile_coords(t, tiles_m, tiles_n, tm, tn);
+        const int m0 = tm * BM, n0 = tn * BN;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_TILE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+          } else {
+            tma_load_2d(sa, &tmA, &full[stage], m0, k0);
+            tma_load_2d(sa + 8192, &tmA, &full[stage], m0 + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (single thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0; uint32_t phase = 0; int it = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_TILE_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad, bd;
+            if (!A_MN) ad = umma_desc_sw128(sa + k * 32, 16, 1024);
+            else       ad = umma_desc_sw128(sa + k * 2048, 8192, 1024);
+            if (!B_MN) bd = umma_desc_sw128(sb + k * 32, 16, 1024);
+            else       bd = umma_desc_sw128(sb + k * 2048, 8192, 1024);
+            umma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue: TMEM -> registers -> HBM
+    const int quarter = warp & 3;  // TMEM lane quarter accessible by this warp
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      int tm, tn; tile_coords(t, tiles_m, tiles_n, tm, tn);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * BM + quarter * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = tn * BN + c * 32;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, r);
+        tmem_wait_ld();
+        if (!row_ok || col0 >= p.N) continue;
+        const bool full_chunk = p.vec_ok && col0 + 32 <= p.N;
+        if (p.mode == GEMM_STORE_BF16) {
+          __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)row * p.ldc + col0;
+          if (full_chunk) {
+            uint4* dst = reinterpret_cast<uint4*>(C);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
+              w.y = pack_bf16(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
+              w.z = pack_bf16(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
+              w.w = pack_bf16(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+              dst[v] = w;
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) C[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+          }
+        } else {
+          float* C = reinterpret_cast<float*>(p.C) + (long long)row * p.ldc + col0;
+          const bool accum = p.mode == GEMM_ACCUM_F32;
+          if (full_chunk) {
+            float4* dst = reinterpret_cast<float4*>(C);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              float4 w = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                     __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+              if (accum) {
+                float4 o = dst[v];
+                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+              }
+              dst[v] = w;
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j)
+              C[j] = accum ? C[j] + __uint_as_float(r[j]) : __uint_as_float(r[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static cudaError_t get_encoder() {
+  if (g_encode) return cudaSuccess;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return cudaSuccess;
+}
+
+// 2-D bf16 row-major tensor [outer][inner] with row stride ld (elements); box = {64, box_outer}.
+static bool make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer, long long ld,
+                     int box_outer) {
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int g_num_sms = 0;
+
+template <bool A_MN, bool B_MN>
+static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                          cudaStream_t st) {
+  static bool attr_set = false;
+  auto kern = gemm_tcgen05_kernel<A_MN, B_MN>;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (!g_num_sms) {
+    int dev; cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  kern<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
+  cudaError_t e = get_encoder();
+  if (e != cudaSuccess) return e;
+  if ((g.lda % 8) || (g.ldb % 8) || (g.ldc % 4) ||
+      (reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15))
+    return cudaErrorInvalidValue;
+  CUtensorMap ta, tb;
+  bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.lda, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, BM);
+  ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, BN));
+  if (!ok) return cudaErrorInvalidValue;
+  const int esz = g.mode == GEMM_STORE_BF16 ? 2 : 4;
+  const int vec_ok = ((g.ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0);
+  GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok};
+  if (!g.a_mn && !g.b_mn) return launch<false, false>(ta, tb, p, st);
+  if (!g.a_mn && g.b_mn) return launch<false, true>(ta, tb, p, st);
+  if (g.a_mn && g.b_mn) return launch<true, true>(ta, tb, p, st);
+  return launch<true, false>(ta, tb, p, st);
+}
+
+}  // namespace mls

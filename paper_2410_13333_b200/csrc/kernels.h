@@ -1,0 +1,76 @@
+// Internal launcher interface between the C++ runtime and the sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mls {
+
+enum { GEMM_STORE_BF16 = 0, GEMM_STORE_F32 = 1, GEMM_ACCUM_F32 = 2 };
+
+struct GemmDesc {
+  int M, N, K;
+  const void* A; long long lda; bool a_mn;
+  const void* B; long long ldb; bool b_mn;
+  void* C; long long ldc;
+  int mode;
+};
+cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st);
+
+// ---- elementwise / normalisation (elementwise.cu)
+cudaError_t rmsnorm_fwd(int T, int h, const void* x, const float* partial, void* x_out,
+                        const void* g, float eps, void* y, float* rstd, cudaStream_t st);
+cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float* rstd,
+                        const float* dy, const void* dres, void* dx_out, float* dg_accum,
+                        float* scratch, cudaStream_t st);
+size_t rmsnorm_bwd_scratch_floats(int T, int h);
+cudaError_t residual_add(long long n, const void* x, const float* partial, void* out,
+                         cudaStream_t st);
+cudaError_t rope_inplace(int T, int s, int n, int d, void* buf, long long ld, int col0,
+                         float theta, bool inverse, cudaStream_t st);
+cudaError_t swiglu_fwd(int T, int F, const void* gu, void* u, cudaStream_t st);
+cudaError_t swiglu_bwd(int T, int F, const void* gu, const void* du, void* dgu, cudaStream_t st);
+cudaError_t embed_fwd(int T, int h, const int32_t* tok, const void* E, void* x, cudaStream_t st);
+cudaError_t embed_bwd(int T, int h, const int32_t* tok, const void* dx, float* dE, cudaStream_t st);
+// vocab-parallel CE, step 1: per-row local max, sum exp(z - max), target logit (0 if not local)
+cudaError_t ce_stats(int T, int V, const float* z, const int32_t* tgt, int v0, float* stats,
+                     cudaStream_t st);
+// step 2 (after TP reduction of stats): loss rows and dz = (softmax - onehot) * scale (bf16)
+cudaError_t ce_grad(int T, int V, const float* z, const int32_t* tgt, int v0, const float* gmax,
+                    const float* gsum, const float* gtgt, float scale, void* dz, float* loss_rows,
+                    cudaStream_t st);
+cudaError_t ce_combine_max(int T, const float* stats, float* gmax, cudaStream_t st);
+cudaError_t ce_local_sum(int T, const float* stats, const float* gmax, float* sum_tgt,
+                         cudaStream_t st);
+cudaError_t reduce_loss(int T, const float* loss_rows, float scale, float* out, int accumulate,
+                        cudaStream_t st);
+cudaError_t cast_f32_bf16(long long n, const float* in, void* out, cudaStream_t st);
+cudaError_t fill_f32(long long n, float* p, float v, cudaStream_t st);
+
+// ---- optimizer: fused batch-weighted reduce + AdamW on owned pieces (adam.cu)
+struct PieceDesc {
+  long long len;
+  long long state_off;   // offset (elements) into master/m/v/rgrad of the owner
+  long long param_off;   // offset (elements) into the owner's bf16 param buffer (its own copy)
+  int n_src;             // contributing pipelines (in pipeline order)
+  int decay;             // apply weight decay
+  long long src_off[8];  // offsets (elements, fp32) of each contribution in the gather buffer
+  float w[8];            // w_i
+};
+cudaError_t reduce_adam(int n_pieces, const PieceDesc* d_pieces, const float* gather,
+                        float* master, float* m, float* v, float* rgrad, uint16_t* param_base,
+                        float lr, float b1, float b2, float eps, float wd, int step, int apply,
+                        long long total_elems, cudaStream_t st);
+
+// ---- attention (attention.cu): qkv [T, 3*n*d] bf16 (rope already applied to q,k)
+cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o, float* lse,
+                          cudaStream_t st);
+cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const void* o,
+                          const float* lse, const void* dout, void* dqkv, float* dsum,
+                          cudaStream_t st);
+
+// ---- probe / straggler emulation (probe.cu)
+cudaError_t spin_ns(long long ns, cudaStream_t st);
+cudaError_t hog_start(int n_sms, volatile int* stop_flag, cudaStream_t st);
+cudaError_t probe_copy(long long n, const float* src, float* dst, cudaStream_t st);
+
+}  // namespace mls
