@@ -237,6 +237,8 @@ static bool make_map(CUtensorMap* m, const void* ptr, long long inner, long long
 }
 
 static int g_num_sms = 0;
+static int g_avail_sms = 0;  // 0 = all SMs; HOG straggler emulation caps the persistent grid
+void set_avail_sms(int n) { g_avail_sms = n; }
 
 template <bool A_MN, bool B_MN>
 static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
@@ -253,7 +255,8 @@ static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-  int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  const int sms = (g_avail_sms > 0 && g_avail_sms < g_num_sms) ? g_avail_sms : g_num_sms;
+  int grid = tiles < sms ? tiles : sms;
   kern<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p);
   return cudaGetLastError();
 }

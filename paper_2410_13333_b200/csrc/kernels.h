@@ -47,19 +47,31 @@ cudaError_t cast_f32_bf16(long long n, const float* in, void* out, cudaStream_t 
 cudaError_t fill_f32(long long n, float* p, float v, cudaStream_t st);
 
 // ---- optimizer: fused batch-weighted reduce + AdamW on owned pieces (adam.cu)
+constexpr int MAX_DP = 8;
 struct PieceDesc {
   long long len;
-  long long state_off;   // offset (elements) into master/m/v/rgrad of the owner
-  long long param_off;   // offset (elements) into the owner's bf16 param buffer (its own copy)
-  int n_src;             // contributing pipelines (in pipeline order)
-  int decay;             // apply weight decay
-  long long src_off[8];  // offsets (elements, fp32) of each contribution in the gather buffer
-  float w[8];            // w_i
+  const float* src[MAX_DP];  // contributions in pipeline order (local grad or receive staging)
+  float w[MAX_DP];           // w_i = m_i b / B
+  int n_src;
+  int decay;                 // apply weight decay (2-D tensors)
+  float* master;
+  float* m;
+  float* v;
+  float* rgrad;              // reduced gradient out (sum_i w_i g_i)
+  uint16_t* param;           // owner's bf16 copy of the piece
 };
-cudaError_t reduce_adam(int n_pieces, const PieceDesc* d_pieces, const float* gather,
-                        float* master, float* m, float* v, float* rgrad, uint16_t* param_base,
-                        float lr, float b1, float b2, float eps, float wd, int step, int apply,
-                        long long total_elems, cudaStream_t st);
+struct ChunkDesc {
+  int piece;
+  int pad;
+  long long off, len;
+};
+struct AdamHyper {
+  float lr, b1, b2, eps, wd;
+  float bc1, bc2;  // 1 - b1^t, 1 - b2^t
+  int apply;
+};
+cudaError_t reduce_adam(int n_chunks, const ChunkDesc* d_chunks, const PieceDesc* d_pieces,
+                        const AdamHyper& hp, cudaStream_t st);
 
 // ---- attention (attention.cu): qkv [T, 3*n*d] bf16 (rope already applied to q,k)
 cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o, float* lse,
@@ -71,6 +83,7 @@ cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const vo
 // ---- probe / straggler emulation (probe.cu)
 cudaError_t spin_ns(long long ns, cudaStream_t st);
 cudaError_t hog_start(int n_sms, volatile int* stop_flag, cudaStream_t st);
+void set_avail_sms(int n);  // persistent-GEMM grid cap (HOG emulation)
 cudaError_t probe_copy(long long n, const float* src, float* dst, cudaStream_t st);
 
 }  // namespace mls

@@ -1,0 +1,1107 @@
+// The malleable hybrid-parallel training step behind include/malleus.h.
+//
+// One context per process == per GPU.  A plan fixes this rank's pipeline,
+// stage and TP member; the runtime owns:
+//   * state placement (layout.cpp, reading R9): bf16 params of held rows, fp32 master/m/v of
+//     owned ZeRO-1 pieces, fp32 grads of held rows;
+//   * the layer forward / backward with uneven TP shards (Megatron column / row parallel,
+//     PAPER.md:262, with per-member split vectors) on the sm_100a kernels;
+//   * 1F1B pipelining over this pipeline's m_i micro-batches with NCCL P2P
+//     between stages whose TP degrees may differ (receiver r <- sender r mod TP_prev);
+//   * the batch-weighted cross-layout gradient reduction to owners + AdamW + bf16 push
+//     (readings R4, R9), NCCL P2P per refined piece, one group;
+//   * migration to a new plan in 4-layer packs, one grouped NCCL send/recv each;
+//   * probe and straggler emulation.
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "layout.h"
+#include "malleus.h"
+
+using namespace mls;
+
+namespace {
+
+struct LayerPtrs {
+  uint16_t *g1 = nullptr, *wqkv = nullptr, *wo = nullptr, *g2 = nullptr, *wgu = nullptr, *wd = nullptr;
+  float *dg1 = nullptr, *dwqkv = nullptr, *dwo = nullptr, *dg2 = nullptr, *dwgu = nullptr, *dwd = nullptr;
+};
+
+struct SlotLayer {
+  uint16_t *a1, *qkv, *o, *x1, *a2, *gu, *u;
+  float *r1, *r2, *lse;
+};
+
+struct Slot {
+  std::vector<uint16_t*> x;  // n_local + 1 activations [T, h]
+  std::vector<SlotLayer> L;
+  uint16_t *xf = nullptr, *dlast = nullptr;
+  float* rf = nullptr;
+};
+
+struct TState {
+  TensorInfo t;
+  bool held = false;
+  Range rows{0, 0};
+  uint16_t* param = nullptr;
+  float* grad = nullptr;
+  std::vector<Piece> owned;
+  std::vector<int64_t> owned_off;  // element offset of each owned piece in master/m/v/rgrad
+  int64_t owned_elems = 0;
+  float *master = nullptr, *m = nullptr, *v = nullptr, *rgrad = nullptr;
+};
+
+struct P2POp {
+  void* ptr;
+  size_t count;
+  ncclDataType_t type;
+  int peer;
+  bool send;
+};
+
+struct Layout {
+  PlanInfo plan;
+  int pipe = -1, stage = -1, member = -1;
+  bool standby = true;
+  int T = 0, n_loc = 0, F_loc = 0, V_loc = 0, v0 = 0;
+  int lb = 0, le = 0, n_local = 0, PP = 0, TP = 0, slots = 0;
+  bool first = false, last = false;
+  std::vector<TState> ts;
+  std::map<int32_t, int> tix;
+  std::vector<LayerPtrs> lp;
+  uint16_t *E = nullptr, *gf = nullptr, *Wlm = nullptr;
+  float *dE = nullptr, *dgf = nullptr, *dWlm = nullptr;
+  std::vector<Slot> slot;
+  // transient
+  float *part = nullptr, *scratch = nullptr, *dsum = nullptr, *logits = nullptr, *stats = nullptr;
+  float *gmax = nullptr, *sumtgt = nullptr, *loss_rows = nullptr, *loss_acc = nullptr;
+  uint16_t *dxa = nullptr, *dxb = nullptr, *dxc = nullptr, *dyrecv = nullptr, *dqkv = nullptr, *dout = nullptr;
+  uint16_t *dgu = nullptr, *du = nullptr, *dlogits = nullptr;
+  float* staging = nullptr;
+  int64_t staging_elems = 0;
+  // grad sync
+  std::vector<P2POp> gops, pops;
+  std::vector<PieceDesc> pieces;
+  std::vector<ChunkDesc> chunks;
+  PieceDesc* d_pieces = nullptr;
+  ChunkDesc* d_chunks = nullptr;
+  size_t state_bytes = 0, grads_bytes = 0, work_bytes = 0;
+  ncclComm_t tp_comm = nullptr;
+  std::vector<int> prev_ranks, next_ranks;  // adjacent stages' members
+};
+
+// bump allocator over an arena whose base may be 0 (sizing pass)
+struct Bump {
+  uintptr_t base;
+  size_t off = 0;
+  explicit Bump(uintptr_t b) : base(b) {}
+  template <class T>
+  T* take(size_t n, size_t align = 256) {
+    off = (off + align - 1) / align * align;
+    T* p = reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+}  // namespace
+
+struct malleus_ctx {
+  malleus_model_cfg cfg{};
+  int rank = 0, world = 1, device = 0;
+  ncclComm_t world_comm = nullptr;
+  std::unique_ptr<Layout> L;
+  std::string err;
+  bool sticky = false;
+  cudaStream_t side = nullptr;  // hog stream
+  int* hog_flag = nullptr;      // host-mapped
+  float slowdown = 1.f;
+  int slow_mode = 0;
+  // timing
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  std::vector<int> ev_cat;
+  size_t ev_used = 0;
+  cudaEvent_t step_beg = nullptr, step_end = nullptr;
+  bool have_timing = false;
+};
+
+static const char* kNoCtx = "no context";
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+      ctx->sticky = e_ != cudaErrorInvalidValue;                                      \
+      return e_ == cudaErrorInvalidValue ? MALLEUS_E_ARG : MALLEUS_E_CUDA;            \
+    }                                                                                 \
+  } while (0)
+#define NK(call)                                                                      \
+  do {                                                                                \
+    ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess) {                                                          \
+      ctx->err = std::string(#call) + ": " + ncclGetErrorString(r_);                  \
+      ctx->sticky = true;                                                             \
+      return MALLEUS_E_NCCL;                                                          \
+    }                                                                                 \
+  } while (0)
+#define RET(st)                                 \
+  do {                                          \
+    malleus_status s_ = (st);                   \
+    if (s_ != MALLEUS_OK) return s_;            \
+  } while (0)
+
+static malleus_status fail(malleus_ctx* ctx, malleus_status s, const std::string& m) {
+  ctx->err = m;
+  return s;
+}
+
+// ------------------------------------------------------------------ layout construction
+static void build_shape(const malleus_model_cfg& cfg, const PlanInfo& p, int rank, Layout& L) {
+  L.plan = p;
+  locate(p, rank, &L.pipe, &L.stage, &L.member);
+  L.standby = L.pipe < 0;
+  L.T = p.b * cfg.seq_len;
+  if (L.standby) return;
+  const PipeInfo& pp = p.pipes[L.pipe];
+  const StageInfo& st = pp.stages[L.stage];
+  L.PP = (int)pp.stages.size();
+  L.TP = (int)st.ranks.size();
+  L.lb = st.lb;
+  L.le = st.le;
+  L.n_local = st.le - st.lb;
+  L.first = L.stage == 0;
+  L.last = L.stage == L.PP - 1;
+  L.n_loc = st.heads[L.member];
+  L.F_loc = st.ffn[L.member];
+  L.V_loc = st.vocab[L.member];
+  L.v0 = 0;
+  for (int k = 0; k < L.member; ++k) L.v0 += st.vocab[k];
+  L.slots = std::max(1, std::min(L.PP - L.stage, std::max(pp.n_micro, 1)));
+  L.prev_ranks.clear();
+  L.next_ranks.clear();
+  if (!L.first) L.prev_ranks = pp.stages[L.stage - 1].ranks;
+  if (!L.last) L.next_ranks = pp.stages[L.stage + 1].ranks;
+}
+
+// Assign every buffer.  With zero bases this only computes sizes.
+static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t sb, uintptr_t gb, uintptr_t wb) {
+  Bump S(sb), G(gb), W(wb);
+  L.ts.clear();
+  L.tix.clear();
+  L.lp.assign(std::max(L.n_local, 0), LayerPtrs{});
+  const int64_t h = cfg.hidden, d = cfg.head_dim;
+  for (const TensorInfo& t : all_tensors(cfg)) {
+    TState s;
+    s.t = t;
+    s.held = held_rows(cfg, L.plan, t, rank, &s.rows);
+    L.tix[t.id] = (int)L.ts.size();
+    L.ts.push_back(s);
+  }
+  // params / grads: per layer the 9 tensors back to back (fused Wqkv, Wgu views), 16-byte units
+  for (TState& s : L.ts) {
+    if (!s.held) continue;
+    const bool group_start = s.t.layer < 0 || s.t.idx == LT_G1;
+    const int64_t n = (s.rows.e - s.rows.b) * s.t.cols;
+    const size_t al = group_start ? 256 : 16;
+    s.param = S.take<uint16_t>((size_t)((n + 7) / 8 * 8), al);
+    s.grad = G.take<float>((size_t)((n + 3) / 4 * 4), al);
+  }
+  // owned pieces: master, m, v in state; rgrad in grads
+  for (TState& s : L.ts) {
+    s.owned.clear();
+    s.owned_off.clear();
+    s.owned_elems = 0;
+    for (const Piece& pc : pieces(cfg, L.plan, s.t))
+      if (pc.owner == rank) {
+        s.owned.push_back(pc);
+        s.owned_off.push_back(s.owned_elems);
+        s.owned_elems += pc.e1 - pc.e0;
+      }
+    if (s.owned_elems) {
+      s.master = S.take<float>(s.owned_elems);
+      s.m = S.take<float>(s.owned_elems);
+      s.v = S.take<float>(s.owned_elems);
+      s.rgrad = G.take<float>(s.owned_elems);
+    }
+  }
+  // grad-sync receive staging: one fp32 slot per (owned piece, remote contributing pipeline)
+  int64_t stage_elems = 0;
+  if (!L.standby || true) {
+    for (TState& s : L.ts)
+      for (const Piece& pc : s.owned)
+        for (size_t i = 0; i < L.plan.pipes.size(); ++i) {
+          if (L.plan.pipes[i].n_micro <= 0) continue;
+          if (sync_holder(cfg, L.plan.pipes[i], s.t, pc.row0) != rank) stage_elems += pc.e1 - pc.e0;
+        }
+  }
+  L.staging_elems = stage_elems;
+  L.staging = G.take<float>(std::max<int64_t>(stage_elems, 1));
+
+  if (!L.standby) {
+    // per-layer fused views
+    for (int li = 0; li < L.n_local; ++li) {
+      const int l = L.lb + li;
+      auto ts = [&](int k) -> TState& { return L.ts[L.tix[l * 16 + k]]; };
+      LayerPtrs& P = L.lp[li];
+      P.g1 = ts(LT_G1).param; P.dg1 = ts(LT_G1).grad;
+      P.wqkv = ts(LT_WQ).param; P.dwqkv = ts(LT_WQ).grad;
+      P.wo = ts(LT_WO).param; P.dwo = ts(LT_WO).grad;
+      P.g2 = ts(LT_G2).param; P.dg2 = ts(LT_G2).grad;
+      P.wgu = ts(LT_WG).param; P.dwgu = ts(LT_WG).grad;
+      P.wd = ts(LT_WD).param; P.dwd = ts(LT_WD).grad;
+    }
+    if (L.first) { auto& s = L.ts[L.tix[MALLEUS_T_EMBED]]; L.E = s.param; L.dE = s.grad; }
+    if (L.last) {
+      auto& a = L.ts[L.tix[MALLEUS_T_FINAL_NORM]]; L.gf = a.param; L.dgf = a.grad;
+      auto& b = L.ts[L.tix[MALLEUS_T_LM_HEAD]]; L.Wlm = b.param; L.dWlm = b.grad;
+    }
+    // activations
+    const int64_t T = L.T, nd = (int64_t)L.n_loc * d, F = L.F_loc;
+    L.slot.assign(L.slots, Slot{});
+    for (Slot& sl : L.slot) {
+      sl.x.resize(L.n_local + 1);
+      for (auto& x : sl.x) x = W.take<uint16_t>(T * h);
+      sl.L.resize(L.n_local);
+      for (SlotLayer& y : sl.L) {
+        y.a1 = W.take<uint16_t>(T * h);
+        y.qkv = W.take<uint16_t>(T * 3 * nd);
+        y.o = W.take<uint16_t>(T * nd);
+        y.x1 = W.take<uint16_t>(T * h);
+        y.a2 = W.take<uint16_t>(T * h);
+        y.gu = W.take<uint16_t>(T * 2 * F);
+        y.u = W.take<uint16_t>(T * F);
+        y.r1 = W.take<float>(T);
+        y.r2 = W.take<float>(T);
+        y.lse = W.take<float>(T * L.n_loc);
+      }
+      if (L.last) {
+        sl.xf = W.take<uint16_t>(T * h);
+        sl.dlast = W.take<uint16_t>(T * h);
+        sl.rf = W.take<float>(T);
+      }
+    }
+    L.part = W.take<float>(T * h);
+    L.scratch = W.take<float>(rmsnorm_bwd_scratch_floats((int)T, (int)h));
+    L.dsum = W.take<float>(T * L.n_loc);
+    L.dxa = W.take<uint16_t>(T * h);
+    L.dxb = W.take<uint16_t>(T * h);
+    L.dxc = W.take<uint16_t>(T * h);
+    L.dyrecv = W.take<uint16_t>(T * h);
+    L.dqkv = W.take<uint16_t>(T * 3 * nd);
+    L.dout = W.take<uint16_t>(T * nd);
+    L.dgu = W.take<uint16_t>(T * 2 * F);
+    L.du = W.take<uint16_t>(T * F);
+    if (L.last) {
+      L.logits = W.take<float>(T * L.V_loc);
+      L.dlogits = W.take<uint16_t>(T * L.V_loc);
+      L.stats = W.take<float>(3 * T);
+      L.gmax = W.take<float>(T);
+      L.sumtgt = W.take<float>(2 * T);
+      L.loss_rows = W.take<float>(T);
+    }
+  }
+  L.loss_acc = W.take<float>(4);
+  L.state_bytes = S.off + 256;
+  L.grads_bytes = G.off + 256;
+  L.work_bytes = W.off + 256;
+}
+
+// grad-sync op lists and the reduce/Adam piece table (needs bound pointers)
+static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
+  L.gops.clear();
+  L.pops.clear();
+  L.pieces.clear();
+  L.chunks.clear();
+  const PlanInfo& p = L.plan;
+  const int DP = (int)p.pipes.size();
+  int64_t stage_off = 0;
+  for (TState& s : L.ts) {
+    const int64_t c = s.t.cols;
+    for (const Piece& pc : pieces(cfg, p, s.t)) {
+      const int64_t len = pc.e1 - pc.e0;
+      // contributions
+      PieceDesc pd{};
+      pd.len = len;
+      pd.n_src = 0;
+      for (int i = 0; i < DP; ++i) {
+        if (p.pipes[i].n_micro <= 0) continue;
+        const int hld = sync_holder(cfg, p.pipes[i], s.t, pc.row0);
+        const float w = (float)((double)p.pipes[i].n_micro * p.b / p.B);
+        if (hld == rank && pc.owner != rank) {
+          L.gops.push_back({s.grad + (pc.e0 - s.rows.b * c), (size_t)len, ncclFloat, pc.owner, true});
+        }
+        if (pc.owner == rank) {
+          if (hld == rank) {
+            pd.src[pd.n_src] = s.grad + (pc.e0 - s.rows.b * c);
+          } else {
+            float* dst = L.staging + stage_off;
+            stage_off += len;
+            L.gops.push_back({dst, (size_t)len, ncclFloat, hld, false});
+            pd.src[pd.n_src] = dst;
+          }
+          pd.w[pd.n_src] = w;
+          pd.n_src++;
+        }
+      }
+      // param push: owner -> every other holder of the segment
+      std::vector<int> holders;
+      for (int i = 0; i < DP; ++i) {
+        const PipeInfo& pp = p.pipes[i];
+        const StageInfo& st = pp.stages[stage_of(cfg, pp, s.t)];
+        for (size_t k = 0; k < st.ranks.size(); ++k) {
+          Range r = member_rows(cfg, st, s.t, (int)k);
+          if (r.b <= pc.row0 && pc.row0 < r.e) holders.push_back(st.ranks[k]);
+        }
+      }
+      for (int hr : holders) {
+        if (hr == pc.owner) continue;
+        if (rank == pc.owner)
+          L.pops.push_back({s.param + (pc.e0 - s.rows.b * c), (size_t)len, ncclBfloat16, hr, true});
+        else if (rank == hr)
+          L.pops.push_back({s.param + (pc.e0 - s.rows.b * c), (size_t)len, ncclBfloat16, pc.owner, false});
+      }
+      if (pc.owner == rank) {
+        size_t idx = 0;
+        while (s.owned[idx].e0 != pc.e0) ++idx;
+        const int64_t off = s.owned_off[idx];
+        pd.decay = s.t.decay ? 1 : 0;
+        pd.master = s.master + off;
+        pd.m = s.m + off;
+        pd.v = s.v + off;
+        pd.rgrad = s.rgrad + off;
+        pd.param = s.param + (pc.e0 - s.rows.b * c);
+        const int pid = (int)L.pieces.size();
+        L.pieces.push_back(pd);
+        const int64_t CH = 8192;
+        for (int64_t o = 0; o < len; o += CH) L.chunks.push_back({pid, 0, o, std::min(CH, len - o)});
+      }
+    }
+  }
+}
+
+static malleus_status free_layout(malleus_ctx* ctx, Layout* L) {
+  if (!L) return MALLEUS_OK;
+  if (L->d_pieces) cudaFree(L->d_pieces);
+  if (L->d_chunks) cudaFree(L->d_chunks);
+  if (L->tp_comm) ncclCommDestroy(L->tp_comm);
+  L->d_pieces = nullptr;
+  L->d_chunks = nullptr;
+  L->tp_comm = nullptr;
+  return MALLEUS_OK;
+}
+
+static malleus_status check_plan(malleus_ctx* ctx, const malleus_plan* plan, PlanInfo* out) {
+  if (!plan) return fail(ctx, MALLEUS_E_ARG, "plan is NULL");
+  *out = plan_from_c(plan);
+  std::string e = validate_plan(ctx->cfg, *out, ctx->world);
+  if (!e.empty()) return fail(ctx, MALLEUS_E_PLAN, e);
+  return MALLEUS_OK;
+}
+
+// bind arenas, split communicators, upload the piece table (collective: ncclCommSplit)
+static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_arenas* a) {
+  if (!a) return fail(ctx, MALLEUS_E_ARG, "arenas is NULL");
+  if (a->state_bytes < L.state_bytes || a->grads_bytes < L.grads_bytes || a->work_bytes < L.work_bytes)
+    return fail(ctx, MALLEUS_E_NOMEM, "arena smaller than malleus_plan_requirements");
+  if (((uintptr_t)a->state | (uintptr_t)a->grads | (uintptr_t)a->work) & 255)
+    return fail(ctx, MALLEUS_E_ARG, "arenas must be 256-byte aligned");
+  assign(ctx->cfg, ctx->rank, L, (uintptr_t)a->state, (uintptr_t)a->grads, (uintptr_t)a->work);
+  build_sync(ctx->cfg, ctx->rank, L);
+  // TP communicator: color = global stage index
+  int color = NCCL_SPLIT_NOCOLOR, key = 0;
+  if (!L.standby) {
+    color = 0;
+    for (int i = 0; i < L.pipe; ++i) color += (int)L.plan.pipes[i].stages.size();
+    color += L.stage;
+    key = L.member;
+  }
+  NK(ncclCommSplit(ctx->world_comm, color, key, &L.tp_comm, nullptr));
+  if (!L.pieces.empty()) {
+    CK(cudaMalloc(&L.d_pieces, L.pieces.size() * sizeof(PieceDesc)));
+    CK(cudaMemcpy(L.d_pieces, L.pieces.data(), L.pieces.size() * sizeof(PieceDesc), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&L.d_chunks, L.chunks.size() * sizeof(ChunkDesc)));
+    CK(cudaMemcpy(L.d_chunks, L.chunks.data(), L.chunks.size() * sizeof(ChunkDesc), cudaMemcpyHostToDevice));
+  }
+  return MALLEUS_OK;
+}
+
+// ------------------------------------------------------------------ timing helpers
+enum { CAT_TP = 1, CAT_PP = 2, CAT_SYNC = 3 };
+static void ev_begin(malleus_ctx* ctx, cudaStream_t st, int cat) {
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    ctx->ev_pool.push_back({a, b});
+    ctx->ev_cat.push_back(0);
+  }
+  ctx->ev_cat[ctx->ev_used] = cat;
+  cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, st);
+}
+static void ev_end(malleus_ctx* ctx, cudaStream_t st) {
+  cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, st);
+  ctx->ev_used++;
+}
+
+// ------------------------------------------------------------------ compute pieces
+static malleus_status gemm(malleus_ctx* ctx, int M, int N, int K, const void* A, long long lda, bool amn,
+                           const void* B, long long ldb, bool bmn, void* C, long long ldc, int mode,
+                           cudaStream_t st) {
+  GemmDesc g{M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, mode};
+  CK(gemm_bf16(g, st));
+  return MALLEUS_OK;
+}
+
+static malleus_status tp_allreduce(malleus_ctx* ctx, float* buf, size_t n, ncclRedOp_t op, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  if (L.TP <= 1) return MALLEUS_OK;
+  ev_begin(ctx, st, CAT_TP);
+  NK(ncclAllReduce(buf, buf, n, ncclFloat, op, L.tp_comm, st));
+  ev_end(ctx, st);
+  return MALLEUS_OK;
+}
+
+static void slow_spin(malleus_ctx* ctx, cudaStream_t st, double base_ns) {
+  if (ctx->slow_mode == 2 && ctx->slowdown > 1.f) spin_ns((long long)((ctx->slowdown - 1.f) * base_ns), st);
+}
+
+static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  const malleus_model_cfg& c = ctx->cfg;
+  const int T = L.T, h = c.hidden, d = c.head_dim, nd = L.n_loc * d, F = L.F_loc;
+  Slot& S = L.slot[si];
+  SlotLayer& Y = S.L[li];
+  LayerPtrs& P = L.lp[li];
+  CK(rmsnorm_fwd(T, h, S.x[li], nullptr, nullptr, P.g1, c.rms_eps, Y.a1, Y.r1, st));
+  RET(gemm(ctx, T, 3 * nd, h, Y.a1, h, false, P.wqkv, h, false, Y.qkv, 3 * nd, GEMM_STORE_BF16, st));
+  CK(rope_inplace(T, c.seq_len, L.n_loc, d, Y.qkv, 3LL * nd, 0, c.rope_theta, false, st));
+  CK(attention_fwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
+  RET(gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, L.part, h, GEMM_STORE_F32, st));
+  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  CK(rmsnorm_fwd(T, h, S.x[li], L.part, Y.x1, P.g2, c.rms_eps, Y.a2, Y.r2, st));
+  RET(gemm(ctx, T, 2 * F, h, Y.a2, h, false, P.wgu, h, false, Y.gu, 2 * F, GEMM_STORE_BF16, st));
+  CK(swiglu_fwd(T, F, Y.gu, Y.u, st));
+  RET(gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, L.part, h, GEMM_STORE_F32, st));
+  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  CK(residual_add((long long)T * h, Y.x1, L.part, S.x[li + 1], st));
+  return MALLEUS_OK;
+}
+
+// dy: grad of x[li+1]; writes grad of x[li] to dx.  first: STORE into wgrad (first micro-batch).
+static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uint16_t* dy, uint16_t* dx,
+                                     bool first, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  const malleus_model_cfg& c = ctx->cfg;
+  const int T = L.T, h = c.hidden, d = c.head_dim, nd = L.n_loc * d, F = L.F_loc;
+  Slot& S = L.slot[si];
+  SlotLayer& Y = S.L[li];
+  LayerPtrs& P = L.lp[li];
+  const int wm = first ? GEMM_STORE_F32 : GEMM_ACCUM_F32;
+  uint16_t* dx1 = L.dxc;
+  // MLP
+  RET(gemm(ctx, T, F, h, dy, h, false, P.wd, h, false, L.du, F, GEMM_STORE_BF16, st));
+  RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
+  CK(swiglu_bwd(T, F, Y.gu, L.du, L.dgu, st));
+  RET(gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, L.part, h, GEMM_STORE_F32, st));
+  RET(gemm(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
+  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  CK(rmsnorm_bwd(T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st));
+  // attention
+  RET(gemm(ctx, T, nd, h, dx1, h, false, P.wo, h, false, L.dout, nd, GEMM_STORE_BF16, st));
+  RET(gemm(ctx, nd, h, T, Y.o, nd, true, dx1, h, true, P.dwo, h, wm, st));
+  CK(attention_bwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, L.dqkv, L.dsum, st));
+  CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
+  RET(gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, L.part, h, GEMM_STORE_F32, st));
+  RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
+  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  CK(rmsnorm_bwd(T, h, S.x[li], P.g1, Y.r1, L.part, dx1, dx, P.dg1, L.scratch, st));
+  return MALLEUS_OK;
+}
+
+// last stage: final norm, LM head, vocab-parallel CE, and the head's backward (dlast).
+static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt, bool first, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  const malleus_model_cfg& c = ctx->cfg;
+  const int T = L.T, h = c.hidden, V = L.V_loc;
+  Slot& S = L.slot[si];
+  const PipeInfo& pp = L.plan.pipes[L.pipe];
+  CK(rmsnorm_fwd(T, h, S.x[L.n_local], nullptr, nullptr, L.gf, c.rms_eps, S.xf, S.rf, st));
+  RET(gemm(ctx, T, V, h, S.xf, h, false, L.Wlm, h, false, L.logits, V, GEMM_STORE_F32, st));
+  CK(ce_stats(T, V, L.logits, tgt, L.v0, L.stats, st));
+  CK(ce_combine_max(T, L.stats, L.gmax, st));
+  RET(tp_allreduce(ctx, L.gmax, (size_t)T, ncclMax, st));
+  CK(ce_local_sum(T, L.stats, L.gmax, L.sumtgt, st));
+  RET(tp_allreduce(ctx, L.sumtgt, (size_t)2 * T, ncclSum, st));
+  const double n_tok = (double)pp.n_micro * L.plan.b * c.seq_len;
+  CK(ce_grad(T, V, L.logits, tgt, L.v0, L.gmax, L.sumtgt, L.sumtgt + T, (float)(1.0 / n_tok), L.dlogits,
+             L.loss_rows, st));
+  if (L.member == 0)
+    CK(reduce_loss(T, L.loss_rows, (float)(1.0 / ((double)L.plan.B * c.seq_len)), L.loss_acc, 1, st));
+  RET(gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, L.part, h, GEMM_STORE_F32, st));
+  RET(gemm(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, first ? GEMM_STORE_F32 : GEMM_ACCUM_F32, st));
+  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  CK(rmsnorm_bwd(T, h, S.x[L.n_local], L.gf, S.rf, L.part, nullptr, S.dlast, L.dgf, L.scratch, st));
+  return MALLEUS_OK;
+}
+
+// ------------------------------------------------------------------ pipeline P2P
+// forward: member r of stage j+1 receives from member (r mod TP_j) of stage j
+static malleus_status pp_exchange(malleus_ctx* ctx, const uint16_t* send_fwd, uint16_t* recv_fwd,
+                                  const uint16_t* send_bwd, uint16_t* recv_bwd, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  const size_t n = (size_t)L.T * ctx->cfg.hidden;
+  if (!send_fwd && !recv_fwd && !send_bwd && !recv_bwd) return MALLEUS_OK;
+  ev_begin(ctx, st, CAT_PP);
+  NK(ncclGroupStart());
+  if (send_fwd)
+    for (size_t r = 0; r < L.next_ranks.size(); ++r)
+      if ((int)(r % L.TP) == L.member) NK(ncclSend(send_fwd, n, ncclBfloat16, L.next_ranks[r], ctx->world_comm, st));
+  if (recv_fwd)
+    NK(ncclRecv(recv_fwd, n, ncclBfloat16, L.prev_ranks[L.member % L.prev_ranks.size()], ctx->world_comm, st));
+  if (send_bwd)
+    for (size_t q = 0; q < L.prev_ranks.size(); ++q)
+      if ((int)(q % L.TP) == L.member) NK(ncclSend(send_bwd, n, ncclBfloat16, L.prev_ranks[q], ctx->world_comm, st));
+  if (recv_bwd)
+    NK(ncclRecv(recv_bwd, n, ncclBfloat16, L.next_ranks[L.member % L.next_ranks.size()], ctx->world_comm, st));
+  NK(ncclGroupEnd());
+  ev_end(ctx, st);
+  return MALLEUS_OK;
+}
+
+static malleus_status grad_sync_impl(malleus_ctx* ctx, const malleus_adam_cfg* a, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  ev_begin(ctx, st, CAT_SYNC);
+  if (!L.gops.empty()) {
+    NK(ncclGroupStart());
+    for (auto& o : L.gops) {
+      if (o.send) NK(ncclSend(o.ptr, o.count, o.type, o.peer, ctx->world_comm, st));
+      else NK(ncclRecv(o.ptr, o.count, o.type, o.peer, ctx->world_comm, st));
+    }
+    NK(ncclGroupEnd());
+  }
+  AdamHyper hp{a->lr, a->beta1, a->beta2, a->eps, a->weight_decay,
+               (float)(1.0 - std::pow((double)a->beta1, a->step)), (float)(1.0 - std::pow((double)a->beta2, a->step)),
+               a->apply_update};
+  CK(reduce_adam((int)L.chunks.size(), L.d_chunks, L.d_pieces, hp, st));
+  if (a->apply_update && !L.pops.empty()) {
+    NK(ncclGroupStart());
+    for (auto& o : L.pops) {
+      if (o.send) NK(ncclSend(o.ptr, o.count, o.type, o.peer, ctx->world_comm, st));
+      else NK(ncclRecv(o.ptr, o.count, o.type, o.peer, ctx->world_comm, st));
+    }
+    NK(ncclGroupEnd());
+  }
+  ev_end(ctx, st);
+  return MALLEUS_OK;
+}
+
+static malleus_status zero_grads(malleus_ctx* ctx, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  for (TState& s : L.ts) {
+    if (!s.held) continue;
+    if (s.t.kind == SPLIT_REP) CK(cudaMemsetAsync(s.grad, 0, (s.rows.e - s.rows.b) * s.t.cols * 4, st));
+  }
+  return MALLEUS_OK;
+}
+
+static malleus_status train_step_impl(malleus_ctx* ctx, const int32_t* tokens, const int32_t* targets,
+                                      float* loss_dev, const malleus_adam_cfg* adam, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  const malleus_model_cfg& c = ctx->cfg;
+  ctx->ev_used = 0;
+  if (!ctx->step_beg) { cudaEventCreate(&ctx->step_beg); cudaEventCreate(&ctx->step_end); }
+  cudaEventRecord(ctx->step_beg, st);
+  CK(cudaMemsetAsync(L.loss_acc, 0, sizeof(float), st));
+  if (!L.standby) {
+    RET(zero_grads(ctx, st));
+    const PipeInfo& pp = L.plan.pipes[L.pipe];
+    const int m = pp.n_micro;
+    int seq0 = 0;
+    for (int i = 0; i < L.pipe; ++i) seq0 += L.plan.pipes[i].n_micro * L.plan.b;
+    const long long s = c.seq_len;
+    auto tok_mb = [&](int j) { return tokens + (seq0 + (long long)j * L.plan.b) * s; };
+    auto tgt_mb = [&](int j) { return targets + (seq0 + (long long)j * L.plan.b) * s; };
+    const int warm = std::min(L.PP - L.stage - 1, m);
+    const int rem = m - warm;
+    auto fwd = [&](int j) -> malleus_status {
+      const int si = j % L.slots;
+      Slot& S = L.slot[si];
+      if (L.first) CK(embed_fwd(L.T, c.hidden, tok_mb(j), L.E, S.x[0], st));
+      for (int li = 0; li < L.n_local; ++li) RET(layer_fwd_impl(ctx, li, si, st));
+      if (L.last) RET(head_fwd_bwd(ctx, si, tgt_mb(j), j == 0, st));
+      return MALLEUS_OK;
+    };
+    // backward of micro-batch j; dy = grad of the stage output; returns grad of the stage input in *dx_out
+    auto bwd = [&](int j, const uint16_t* dy, uint16_t** dx_out) -> malleus_status {
+      const int si = j % L.slots;
+      const uint16_t* cur = dy;
+      uint16_t* bufs[2] = {L.dxa, L.dxb};
+      int k = 0;
+      for (int li = L.n_local - 1; li >= 0; --li) {
+        uint16_t* out = bufs[k];
+        k ^= 1;
+        RET(layer_bwd_impl(ctx, li, si, cur, out, j == 0, st));
+        cur = out;
+      }
+      if (L.first) CK(embed_bwd(L.T, c.hidden, tok_mb(j), cur, L.dE, st));
+      *dx_out = const_cast<uint16_t*>(cur);
+      return MALLEUS_OK;
+    };
+    auto stage_dy = [&](int j) -> const uint16_t* { return L.last ? L.slot[j % L.slots].dlast : L.dyrecv; };
+    for (int j = 0; j < warm; ++j) {
+      if (!L.first) RET(pp_exchange(ctx, nullptr, L.slot[j % L.slots].x[0], nullptr, nullptr, st));
+      RET(fwd(j));
+      RET(pp_exchange(ctx, L.last ? nullptr : L.slot[j % L.slots].x[L.n_local], nullptr, nullptr, nullptr, st));
+    }
+    if (rem > 0 && !L.first) RET(pp_exchange(ctx, nullptr, L.slot[warm % L.slots].x[0], nullptr, nullptr, st));
+    for (int i = 0; i < rem; ++i) {
+      const int jf = warm + i;
+      RET(fwd(jf));
+      RET(pp_exchange(ctx, L.last ? nullptr : L.slot[jf % L.slots].x[L.n_local], nullptr, nullptr,
+                      L.last ? nullptr : L.dyrecv, st));
+      uint16_t* dx = nullptr;
+      RET(bwd(i, stage_dy(i), &dx));
+      if (i == rem - 1) {
+        RET(pp_exchange(ctx, nullptr, nullptr, L.first ? nullptr : dx, nullptr, st));
+      } else {
+        RET(pp_exchange(ctx, nullptr, L.first ? nullptr : L.slot[(jf + 1) % L.slots].x[0], L.first ? nullptr : dx,
+                        nullptr, st));
+      }
+    }
+    for (int i = rem; i < m; ++i) {
+      RET(pp_exchange(ctx, nullptr, nullptr, nullptr, L.last ? nullptr : L.dyrecv, st));
+      uint16_t* dx = nullptr;
+      RET(bwd(i, stage_dy(i), &dx));
+      RET(pp_exchange(ctx, nullptr, nullptr, L.first ? nullptr : dx, nullptr, st));
+    }
+  }
+  RET(grad_sync_impl(ctx, adam, st));
+  // world loss: sum over pipelines of w_i * loss_i (only last-stage member 0 contributes)
+  NK(ncclAllReduce(L.loss_acc, L.loss_acc, 1, ncclFloat, ncclSum, ctx->world_comm, st));
+  if (loss_dev) CK(cudaMemcpyAsync(loss_dev, L.loss_acc, sizeof(float), cudaMemcpyDeviceToDevice, st));
+  cudaEventRecord(ctx->step_end, st);
+  ctx->have_timing = true;
+  return MALLEUS_OK;
+}
+
+// ------------------------------------------------------------------ C-ABI
+#define GUARD()                                                                \
+  do {                                                                         \
+    if (!ctx) return MALLEUS_E_ARG;                                            \
+    if (ctx->sticky) return MALLEUS_E_STATE;                                   \
+    cudaSetDevice(ctx->device);                                                \
+  } while (0)
+#define NEED_PLAN()                                                            \
+  do {                                                                         \
+    if (!ctx->L) return fail(ctx, MALLEUS_E_STATE, "no plan applied");         \
+  } while (0)
+
+extern "C" {
+
+const char* malleus_version(void) { return "malleus-b200 0.2 (sm_100a)"; }
+
+const char* malleus_last_error(const malleus_ctx* ctx) { return ctx ? ctx->err.c_str() : kNoCtx; }
+
+malleus_status malleus_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return MALLEUS_E_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return MALLEUS_E_NCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out, &id, 128);
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_create(const malleus_model_cfg* cfg, int32_t rank, int32_t world, int32_t device,
+                              const uint8_t nccl_uid[128], malleus_ctx** out) {
+  if (!cfg || !out || !nccl_uid || rank < 0 || rank >= world) return MALLEUS_E_ARG;
+  *out = nullptr;
+  auto* ctx = new malleus_ctx();
+  ctx->cfg = *cfg;
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->device = device;
+  if (cfg->hidden % 128 || cfg->head_dim % 32 || cfg->seq_len % 64) {
+    delete ctx;
+    return MALLEUS_E_ARG;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) { delete ctx; return MALLEUS_E_CUDA; }
+  ncclUniqueId id;
+  memcpy(&id, nccl_uid, 128);
+  if (ncclCommInitRank(&ctx->world_comm, world, id, rank) != ncclSuccess) { delete ctx; return MALLEUS_E_NCCL; }
+  cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+  *out = ctx;
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode);
+
+malleus_status malleus_destroy(malleus_ctx* ctx) {
+  if (!ctx) return MALLEUS_E_ARG;
+  cudaSetDevice(ctx->device);
+  if (ctx->hog_flag) malleus_set_slowdown(ctx, 1.f, 0);
+  cudaDeviceSynchronize();
+  if (ctx->L) free_layout(ctx, ctx->L.get());
+  if (ctx->world_comm) ncclCommDestroy(ctx->world_comm);
+  for (auto& e : ctx->ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  if (ctx->step_beg) { cudaEventDestroy(ctx->step_beg); cudaEventDestroy(ctx->step_end); }
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  delete ctx;
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_plan_requirements(malleus_ctx* ctx, const malleus_plan* plan, malleus_requirements* out) {
+  if (!ctx || !out) return MALLEUS_E_ARG;
+  PlanInfo p;
+  RET(check_plan(ctx, plan, &p));
+  Layout L;
+  build_shape(ctx->cfg, p, ctx->rank, L);
+  assign(ctx->cfg, ctx->rank, L, 0, 0, 0);
+  out->state = L.state_bytes;
+  out->grads = L.grads_bytes;
+  out->work = L.work_bytes;
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_plan_apply(malleus_ctx* ctx, const malleus_plan* plan, const malleus_arenas* arenas) {
+  GUARD();
+  PlanInfo p;
+  RET(check_plan(ctx, plan, &p));
+  auto L = std::make_unique<Layout>();
+  build_shape(ctx->cfg, p, ctx->rank, *L);
+  assign(ctx->cfg, ctx->rank, *L, 0, 0, 0);
+  RET(bind_layout(ctx, *L, arenas));
+  CK(cudaDeviceSynchronize());
+  if (ctx->L) free_layout(ctx, ctx->L.get());
+  ctx->L = std::move(L);
+  CK(cudaMemset(arenas->grads, 0, ctx->L->grads_bytes));
+  return MALLEUS_OK;
+}
+
+static float bf16_to_f32(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+malleus_status malleus_write_tensor(malleus_ctx* ctx, int32_t tensor_id, int32_t kind, const void* host) {
+  GUARD();
+  NEED_PLAN();
+  if (!host) return fail(ctx, MALLEUS_E_ARG, "host_full is NULL");
+  Layout& L = *ctx->L;
+  auto it = L.tix.find(tensor_id);
+  if (it == L.tix.end()) return fail(ctx, MALLEUS_E_ARG, "unknown tensor id");
+  TState& s = L.ts[it->second];
+  const int64_t c = s.t.cols;
+  if (kind == MALLEUS_KIND_PARAM) {
+    const uint16_t* h = static_cast<const uint16_t*>(host);
+    if (s.held)
+      CK(cudaMemcpy(s.param, h + s.rows.b * c, (s.rows.e - s.rows.b) * c * 2, cudaMemcpyHostToDevice));
+    if (s.owned_elems) {
+      std::vector<float> tmp(s.owned_elems);
+      for (size_t i = 0; i < s.owned.size(); ++i)
+        for (int64_t e = s.owned[i].e0; e < s.owned[i].e1; ++e) tmp[s.owned_off[i] + e - s.owned[i].e0] = bf16_to_f32(h[e]);
+      CK(cudaMemcpy(s.master, tmp.data(), s.owned_elems * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemset(s.m, 0, s.owned_elems * 4));
+      CK(cudaMemset(s.v, 0, s.owned_elems * 4));
+    }
+    return MALLEUS_OK;
+  }
+  float* dst = kind == MALLEUS_KIND_MASTER ? s.master : kind == MALLEUS_KIND_ADAM_M ? s.m
+             : kind == MALLEUS_KIND_ADAM_V ? s.v : nullptr;
+  if (!dst) return fail(ctx, MALLEUS_E_ARG, "write_tensor: kind must be PARAM, MASTER, ADAM_M or ADAM_V");
+  const float* h = static_cast<const float*>(host);
+  for (size_t i = 0; i < s.owned.size(); ++i)
+    CK(cudaMemcpy(dst + s.owned_off[i], h + s.owned[i].e0, (s.owned[i].e1 - s.owned[i].e0) * 4, cudaMemcpyHostToDevice));
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_read_local(malleus_ctx* ctx, int32_t tensor_id, int32_t kind, void* host_dst, int64_t* ranges,
+                                  int32_t* n_ranges, int64_t* n_elems) {
+  GUARD();
+  NEED_PLAN();
+  if (!n_ranges || !n_elems) return fail(ctx, MALLEUS_E_ARG, "n_ranges / n_elems NULL");
+  Layout& L = *ctx->L;
+  auto it = L.tix.find(tensor_id);
+  if (it == L.tix.end()) return fail(ctx, MALLEUS_E_ARG, "unknown tensor id");
+  TState& s = L.ts[it->second];
+  const int64_t c = s.t.cols;
+  std::vector<Range> rs;
+  const void* src = nullptr;
+  size_t esz = 4;
+  if (kind == MALLEUS_KIND_PARAM || kind == MALLEUS_KIND_GRAD) {
+    if (s.held) rs.push_back({s.rows.b * c, s.rows.e * c});
+    src = kind == MALLEUS_KIND_PARAM ? (const void*)s.param : (const void*)s.grad;
+    esz = kind == MALLEUS_KIND_PARAM ? 2 : 4;
+  } else {
+    for (auto& pc : s.owned) rs.push_back({pc.e0, pc.e1});
+    src = kind == MALLEUS_KIND_MASTER ? s.master : kind == MALLEUS_KIND_ADAM_M ? s.m
+        : kind == MALLEUS_KIND_ADAM_V ? s.v : kind == MALLEUS_KIND_RGRAD ? s.rgrad : nullptr;
+    if (kind < MALLEUS_KIND_MASTER || kind > MALLEUS_KIND_RGRAD) return fail(ctx, MALLEUS_E_ARG, "bad kind");
+  }
+  int64_t tot = 0;
+  for (auto& r : rs) tot += r.e - r.b;
+  const int cap = *n_ranges;
+  *n_ranges = (int32_t)rs.size();
+  *n_elems = tot;
+  if (!host_dst) return MALLEUS_OK;
+  if ((int)rs.size() > cap || !ranges) return fail(ctx, MALLEUS_E_ARG, "ranges capacity too small");
+  for (size_t i = 0; i < rs.size(); ++i) { ranges[2 * i] = rs[i].b; ranges[2 * i + 1] = rs[i].e; }
+  if (tot) CK(cudaDeviceSynchronize());
+  if (tot) CK(cudaMemcpy(host_dst, src, tot * esz, cudaMemcpyDeviceToHost));
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_layer_fwd(malleus_ctx* ctx, int32_t layer, int32_t slot, const void* x_in, void* x_out,
+                                 void* stream) {
+  GUARD();
+  NEED_PLAN();
+  Layout& L = *ctx->L;
+  if (L.standby || layer < L.lb || layer >= L.le || slot < 0 || slot >= L.slots || !x_in || !x_out)
+    return fail(ctx, MALLEUS_E_ARG, "layer not held by this rank or bad slot / pointers");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int li = layer - L.lb;
+  const size_t bytes = (size_t)L.T * ctx->cfg.hidden * 2;
+  CK(cudaMemcpyAsync(L.slot[slot].x[li], x_in, bytes, cudaMemcpyDeviceToDevice, st));
+  RET(layer_fwd_impl(ctx, li, slot, st));
+  CK(cudaMemcpyAsync(x_out, L.slot[slot].x[li + 1], bytes, cudaMemcpyDeviceToDevice, st));
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_layer_bwd(malleus_ctx* ctx, int32_t layer, int32_t slot, const void* dy, void* dx,
+                                 void* stream) {
+  GUARD();
+  NEED_PLAN();
+  Layout& L = *ctx->L;
+  if (L.standby || layer < L.lb || layer >= L.le || slot < 0 || slot >= L.slots || !dy || !dx)
+    return fail(ctx, MALLEUS_E_ARG, "layer not held by this rank or bad slot / pointers");
+  cudaStream_t st = (cudaStream_t)stream;
+  RET(layer_bwd_impl(ctx, layer - L.lb, slot, (const uint16_t*)dy, L.dxb == dx ? L.dxa : L.dxb, false, st));
+  CK(cudaMemcpyAsync(dx, L.dxb == dx ? L.dxa : L.dxb, (size_t)L.T * ctx->cfg.hidden * 2, cudaMemcpyDeviceToDevice, st));
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_train_step(malleus_ctx* ctx, const int32_t* tokens, const int32_t* targets, float* loss_dev,
+                                  const malleus_adam_cfg* adam, void* stream) {
+  GUARD();
+  NEED_PLAN();
+  if (!tokens || !targets || !adam || adam->step < 1) return fail(ctx, MALLEUS_E_ARG, "tokens/targets/adam");
+  return train_step_impl(ctx, tokens, targets, loss_dev, adam, (cudaStream_t)stream);
+}
+
+malleus_status malleus_grad_sync(malleus_ctx* ctx, const malleus_adam_cfg* adam, void* stream) {
+  GUARD();
+  NEED_PLAN();
+  if (!adam || adam->step < 1) return fail(ctx, MALLEUS_E_ARG, "adam cfg");
+  ctx->ev_used = 0;
+  return grad_sync_impl(ctx, adam, (cudaStream_t)stream);
+}
+
+malleus_status malleus_last_step_timing(malleus_ctx* ctx, float out[5]) {
+  GUARD();
+  if (!out) return MALLEUS_E_ARG;
+  for (int i = 0; i < 5; ++i) out[i] = 0.f;
+  if (!ctx->have_timing) return fail(ctx, MALLEUS_E_STATE, "no step timed yet");
+  CK(cudaEventSynchronize(ctx->step_end));
+  float tot = 0.f;
+  cudaEventElapsedTime(&tot, ctx->step_beg, ctx->step_end);
+  for (size_t i = 0; i < ctx->ev_used; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev_pool[i].first, ctx->ev_pool[i].second);
+    out[ctx->ev_cat[i]] += ms;
+  }
+  out[4] = tot;
+  out[0] = tot - out[1] - out[2] - out[3];
+  return MALLEUS_OK;
+}
+
+// ------------------------------------------------------------------ migration
+malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, const malleus_arenas* new_arenas,
+                               malleus_migrate_stats* stats) {
+  GUARD();
+  NEED_PLAN();
+  PlanInfo np;
+  RET(check_plan(ctx, new_plan, &np));
+  auto NL = std::make_unique<Layout>();
+  build_shape(ctx->cfg, np, ctx->rank, *NL);
+  assign(ctx->cfg, ctx->rank, *NL, 0, 0, 0);
+  RET(bind_layout(ctx, *NL, new_arenas));
+  CK(cudaMemset(new_arenas->grads, 0, NL->grads_bytes));
+  CK(cudaDeviceSynchronize());
+  Layout& O = *ctx->L;
+  const int me = ctx->rank;
+  const auto t0 = std::chrono::steady_clock::now();
+  // pointer of flat element e of tensor (kind) in a layout; nullptr if not resident
+  auto locate_ptr = [](Layout& Lx, int32_t tid, int kind, int64_t e, size_t* esz) -> char* {
+    TState& s = Lx.ts[Lx.tix[tid]];
+    if (kind == MALLEUS_KIND_PARAM) {
+      *esz = 2;
+      if (!s.held) return nullptr;
+      return reinterpret_cast<char*>(s.param + (e - s.rows.b * s.t.cols));
+    }
+    *esz = 4;
+    for (size_t i = 0; i < s.owned.size(); ++i)
+      if (s.owned[i].e0 <= e && e < s.owned[i].e1) {
+        float* base = kind == MALLEUS_KIND_MASTER ? s.master : kind == MALLEUS_KIND_ADAM_M ? s.m : s.v;
+        return reinterpret_cast<char*>(base + s.owned_off[i] + (e - s.owned[i].e0));
+      }
+    return nullptr;
+  };
+  cudaStream_t st = 0;
+  uint64_t sent = 0, recvd = 0;
+  // local copies: everything this rank keeps (needed in new, resident in old)
+  for (TState& ns : NL->ts) {
+    const int64_t c = ns.t.cols;
+    if (ns.held) {
+      Range orow;
+      if (held_rows(ctx->cfg, O.plan, ns.t, me, &orow)) {
+        const int64_t lo = std::max(ns.rows.b, orow.b), hi = std::min(ns.rows.e, orow.e);
+        if (hi > lo) {
+          size_t es;
+          char* src = locate_ptr(O, ns.t.id, MALLEUS_KIND_PARAM, lo * c, &es);
+          char* dst = locate_ptr(*NL, ns.t.id, MALLEUS_KIND_PARAM, lo * c, &es);
+          CK(cudaMemcpyAsync(dst, src, (hi - lo) * c * 2, cudaMemcpyDeviceToDevice, st));
+        }
+      }
+    }
+    TState& os = O.ts[O.tix[ns.t.id]];
+    for (size_t i = 0; i < ns.owned.size(); ++i)
+      for (size_t j = 0; j < os.owned.size(); ++j) {
+        const int64_t lo = std::max(ns.owned[i].e0, os.owned[j].e0), hi = std::min(ns.owned[i].e1, os.owned[j].e1);
+        if (hi <= lo) continue;
+        for (int kind : {MALLEUS_KIND_MASTER, MALLEUS_KIND_ADAM_M, MALLEUS_KIND_ADAM_V}) {
+          size_t es;
+          char* src = locate_ptr(O, ns.t.id, kind, lo, &es);
+          char* dst = locate_ptr(*NL, ns.t.id, kind, lo, &es);
+          CK(cudaMemcpyAsync(dst, src, (hi - lo) * 4, cudaMemcpyDeviceToDevice, st));
+        }
+      }
+  }
+  // remote transfers grouped in packs of 4 consecutive layers
+  const auto tr = migration_transfers(ctx->cfg, O.plan, np);
+  const int L_ = ctx->cfg.n_layers;
+  const int n_packs = std::max(1, (L_ + 3) / 4);
+  auto pack_of = [&](int32_t tid) {
+    if (tid == MALLEUS_T_EMBED) return 0;
+    if (tid >= MALLEUS_T_EMBED) return n_packs - 1;
+    return (tid / 16) / 4;
+  };
+  for (int pk = 0; pk < n_packs; ++pk) {
+    bool any = false;
+    for (auto& t : tr)
+      if (pack_of(t.tensor) == pk && (t.src == me || t.dst == me)) { any = true; break; }
+    if (!any) continue;
+    NK(ncclGroupStart());
+    for (auto& t : tr) {
+      if (pack_of(t.tensor) != pk) continue;
+      size_t es;
+      const ncclDataType_t ty = t.kind == MALLEUS_KIND_PARAM ? ncclBfloat16 : ncclFloat;
+      if (t.src == me) {
+        char* p = locate_ptr(O, t.tensor, t.kind, t.e0, &es);
+        NK(ncclSend(p, t.e1 - t.e0, ty, t.dst, ctx->world_comm, st));
+        sent += (t.e1 - t.e0) * es;
+      } else if (t.dst == me) {
+        char* p = locate_ptr(*NL, t.tensor, t.kind, t.e0, &es);
+        NK(ncclRecv(p, t.e1 - t.e0, ty, t.src, ctx->world_comm, st));
+        recvd += (t.e1 - t.e0) * es;
+      }
+    }
+    NK(ncclGroupEnd());
+  }
+  CK(cudaStreamSynchronize(st));
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  free_layout(ctx, ctx->L.get());
+  ctx->L = std::move(NL);
+  if (stats) {
+    stats->bytes_sent = sent;
+    stats->bytes_recv = recvd;
+    stats->seconds = secs;
+    stats->n_packs = n_packs;
+  }
+  return MALLEUS_OK;
+}
+
+// ------------------------------------------------------------------ probe / straggler emulation
+malleus_status malleus_probe_speed(malleus_ctx* ctx, int32_t iters, float* ms_per_rank) {
+  GUARD();
+  if (!ms_per_rank || iters < 1) return MALLEUS_E_ARG;
+  const int n = 4096;
+  void *a = nullptr, *b = nullptr, *cbuf = nullptr;
+  float* dev = nullptr;
+  CK(cudaMalloc(&a, (size_t)n * n * 2));
+  CK(cudaMalloc(&b, (size_t)n * n * 2));
+  CK(cudaMalloc(&cbuf, (size_t)n * n * 2));
+  CK(cudaMalloc(&dev, ctx->world * sizeof(float)));
+  CK(cudaMemset(a, 0, (size_t)n * n * 2));
+  CK(cudaMemset(b, 0, (size_t)n * n * 2));
+  cudaStream_t st = 0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  GemmDesc g{n, n, n, a, n, false, b, n, false, cbuf, n, GEMM_STORE_BF16};
+  CK(gemm_bf16(g, st));  // warm-up
+  CK(probe_copy((long long)n * n / 2, (const float*)a, (float*)cbuf, st));
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < iters; ++i) {
+    CK(gemm_bf16(g, st));
+    CK(probe_copy((long long)n * n / 2, (const float*)a, (float*)cbuf, st));
+    slow_spin(ctx, st, 0.2e6);
+  }
+  cudaEventRecord(e1, st);
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= iters;
+  CK(cudaMemcpy(dev + ctx->rank, &ms, 4, cudaMemcpyHostToDevice));
+  NK(ncclAllGather(dev + ctx->rank, dev, 1, ncclFloat, ctx->world_comm, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemcpy(ms_per_rank, dev, ctx->world * sizeof(float), cudaMemcpyDeviceToHost));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(a);
+  cudaFree(b);
+  cudaFree(cbuf);
+  cudaFree(dev);
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode) {
+  if (!ctx) return MALLEUS_E_ARG;
+  cudaSetDevice(ctx->device);
+  if (x < 1.f || mode < 0 || mode > 2) return fail(ctx, MALLEUS_E_ARG, "x >= 1, mode in {0,1,2}");
+  // stop a running hog
+  if (ctx->hog_flag) {
+    *(volatile int*)ctx->hog_flag = 1;
+    cudaStreamSynchronize(ctx->side);
+    cudaFreeHost(ctx->hog_flag);
+    ctx->hog_flag = nullptr;
+    set_avail_sms(0);
+  }
+  ctx->slowdown = x;
+  ctx->slow_mode = mode;
+  if (mode == 1 && x > 1.f) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int n_hog = std::min(sms - 1, (int)std::lround(sms * (1.0 - 1.0 / x)));
+    CK(cudaHostAlloc((void**)&ctx->hog_flag, sizeof(int), cudaHostAllocMapped));
+    *ctx->hog_flag = 0;
+    int* dflag = nullptr;
+    CK(cudaHostGetDevicePointer((void**)&dflag, ctx->hog_flag, 0));
+    set_avail_sms(sms - n_hog);
+    CK(hog_start(n_hog, dflag, ctx->side));
+  }
+  return MALLEUS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+"""Python front end of libmalleus.so: argument marshalling only.
+
+PyTorch provides device memory (the arenas), streams and the process group used to broadcast
+the NCCL unique id; every step of the hot path runs inside the library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import check
+
+_ADAM_DEFAULT = dict(lr=3e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1)
+
+
+def name_to_id(name: str) -> int:
+    if name == "E":
+        return L.T_EMBED
+    if name == "gf":
+        return L.T_FINAL_NORM
+    if name == "Wlm":
+        return L.T_LM_HEAD
+    layer, t = name.split(".")
+    return int(layer) * 16 + ("g1", "wq", "wk", "wv", "wo", "g2", "wg", "wu", "wd").index(t)
+
+
+def tensor_names(cfg):
+    names = []
+    for l in range(cfg.n_layers):
+        names += [f"{l}.{t}" for t in ("g1", "wq", "wk", "wv", "wo", "g2", "wg", "wu", "wd")]
+    return names + ["E", "gf", "Wlm"]
+
+
+class Engine:
+    """One malleus context (one process == one GPU)."""
+
+    def __init__(self, cfg, rank: int = 0, world: int = 1, device: int | None = None, group=None):
+        self.cfg = cfg
+        self.rank, self.world = rank, world
+        self.device = torch.cuda.current_device() if device is None else device
+        torch.cuda.set_device(self.device)
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            check(L.lib.malleus_nccl_unique_id(uid), None, "nccl_unique_id")
+        if world > 1:
+            import torch.distributed as dist
+            obj = [bytes(uid.raw) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = C.create_string_buffer(obj[0], 128)
+        self._ccfg = L.make_cfg(cfg)
+        ctx = C.c_void_p()
+        check(L.lib.malleus_create(C.byref(self._ccfg), rank, world, self.device, uid, C.byref(ctx)), None, "create")
+        self.ctx = ctx
+        self.plan = None
+        self._arenas = None
+        self._plan_struct = None
+
+    # ------------------------------------------------------------------ plans
+    def requirements(self, plan: dict):
+        ps = L.PlanStruct(plan)
+        req = L.Requirements()
+        check(L.lib.malleus_plan_requirements(self.ctx, ps.ref, C.byref(req)), self.ctx, "plan_requirements")
+        return req.state, req.grads, req.work
+
+    def _alloc(self, plan):
+        s, g, w = self.requirements(plan)
+        bufs = [torch.empty(n, dtype=torch.uint8, device=f"cuda:{self.device}") for n in (s, g, w)]
+        ar = L.Arenas(bufs[0].data_ptr(), s, bufs[1].data_ptr(), g, bufs[2].data_ptr(), w)
+        return bufs, ar
+
+    def apply(self, plan: dict):
+        bufs, ar = self._alloc(plan)
+        ps = L.PlanStruct(plan)
+        check(L.lib.malleus_plan_apply(self.ctx, ps.ref, C.byref(ar)), self.ctx, "plan_apply")
+        self.plan, self._arenas, self._plan_struct = plan, bufs, ps
+
+    def migrate(self, plan: dict) -> dict:
+        bufs, ar = self._alloc(plan)
+        ps = L.PlanStruct(plan)
+        st = L.MigrateStats()
+        check(L.lib.malleus_migrate(self.ctx, ps.ref, C.byref(ar), C.byref(st)), self.ctx, "migrate")
+        self.plan, self._arenas, self._plan_struct = plan, bufs, ps
+        return dict(bytes_sent=st.bytes_sent, bytes_recv=st.bytes_recv, seconds=st.seconds, n_packs=st.n_packs)
+
+    # ------------------------------------------------------------------ state I/O
+    def write_weights(self, weights_bf16: dict):
+        for name, arr in weights_bf16.items():
+            a = np.ascontiguousarray(arr, dtype=np.uint16)
+            check(L.lib.malleus_write_tensor(self.ctx, name_to_id(name), L.KIND_PARAM, a.ctypes.data), self.ctx,
+                  f"write_tensor {name}")
+
+    def write_state(self, name: str, kind: int, values: np.ndarray):
+        a = np.ascontiguousarray(values, dtype=np.float32)
+        check(L.lib.malleus_write_tensor(self.ctx, name_to_id(name), kind, a.ctypes.data), self.ctx, "write_tensor")
+
+    def read(self, name: str, kind: int):
+        """(list of (e0, e1) flat ranges, values concatenated as np array)."""
+        nr, ne = C.c_int32(0), C.c_int64(0)
+        tid = name_to_id(name)
+        check(L.lib.malleus_read_local(self.ctx, tid, kind, None, None, C.byref(nr), C.byref(ne)), self.ctx, "read")
+        ranges = (C.c_int64 * max(1, 2 * nr.value))()
+        dtype = np.uint16 if kind == L.KIND_PARAM else np.float32
+        out = np.empty(max(ne.value, 1), dtype=dtype)
+        check(L.lib.malleus_read_local(self.ctx, tid, kind, out.ctypes.data, ranges, C.byref(nr), C.byref(ne)),
+              self.ctx, "read")
+        return [(ranges[2 * i], ranges[2 * i + 1]) for i in range(nr.value)], out[:ne.value]
+
+    # ------------------------------------------------------------------ step
+    def adam(self, step: int, apply_update: bool = True, **kw):
+        hp = dict(_ADAM_DEFAULT, **kw)
+        return L.AdamCfg(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"], step, int(apply_update))
+
+    def train_step(self, tokens: torch.Tensor, targets: torch.Tensor, step: int, apply_update: bool = True,
+                   loss_out: torch.Tensor | None = None, stream=None, **adam_kw) -> torch.Tensor:
+        """tokens/targets: device int32 [B, s] (whole global batch).  Returns the device loss."""
+        assert tokens.dtype == torch.int32 and tokens.is_cuda and tokens.is_contiguous()
+        if loss_out is None:
+            loss_out = torch.zeros(1, dtype=torch.float32, device=tokens.device)
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        a = self.adam(step, apply_update, **adam_kw)
+        check(L.lib.malleus_train_step(self.ctx, tokens.data_ptr(), targets.data_ptr(), loss_out.data_ptr(),
+                                       C.byref(a), st), self.ctx, "train_step")
+        return loss_out
+
+    def timing(self):
+        out = (C.c_float * 5)()
+        check(L.lib.malleus_last_step_timing(self.ctx, out), self.ctx, "timing")
+        return dict(compute=out[0], tp_comm=out[1], pp_comm=out[2], grad_sync=out[3], total=out[4])
+
+    def probe(self, iters: int = 10):
+        out = (C.c_float * self.world)()
+        check(L.lib.malleus_probe_speed(self.ctx, iters, out), self.ctx, "probe")
+        return list(out)
+
+    def set_slowdown(self, x: float, mode: int = 1):
+        check(L.lib.malleus_set_slowdown(self.ctx, float(x), int(mode)), self.ctx, "set_slowdown")
+
+    def close(self):
+        if self.ctx:
+            L.lib.malleus_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def gather_logical(engines_reads, shape, dtype=np.float32):
+    """Assemble a logical tensor from (ranges, values) pieces of several ranks."""
+    full = np.zeros(int(np.prod(shape)), dtype=dtype)
+    seen = np.zeros(full.shape, dtype=bool)
+    for ranges, vals in engines_reads:
+        off = 0
+        for e0, e1 in ranges:
+            full[e0:e1] = vals[off:off + e1 - e0]
+            seen[e0:e1] = True
+            off += e1 - e0
+    return full.reshape(shape), seen.reshape(shape)

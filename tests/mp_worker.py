@@ -1,0 +1,127 @@
+"""Step-parity worker: runs one malleable plan through libmalleus.so on N GPUs (one process per
+GPU; launched by torchrun for N > 1) and compares against the oracle on rank 0.
+
+Checks (readings R15, R16):
+  * loss: |l - l_ref| / |l_ref| <= 1e-3 (bf16 path);
+  * reduced gradients (sum_i w_i g_i on the owners, gathered over ranks into logical tensors):
+    ||g - g_ref||_inf / ||g_ref||_inf <= 2e-2 per tensor, every element owned exactly once;
+  * AdamW on owned pieces vs the oracle's AdamW applied to the GPU's own reduced gradient
+    (fp32 vs fp64): <= 1e-6 relative on master;
+  * param push: every holder's bf16 copy == RNE(owner's fp32 master), bit for bit.
+Usage: python -m torch.distributed.run --nproc-per-node N tests/mp_worker.py <plan> <out.json>
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from synth.gen import C1_TINY, make_weights, make_tokens, bf16_rne, tensor_shapes  # noqa: E402
+from paper_2410_13333_b200 import plans as Pl  # noqa: E402
+from paper_2410_13333_b200 import _lib as L  # noqa: E402
+from paper_2410_13333_b200.engine import Engine, gather_logical  # noqa: E402
+
+
+def run(plan_name: str, rank: int = 0, world: int = 1, local_rank: int = 0, group=None, steps: int = 1):
+    cfg = C1_TINY
+    B, b = 8, 2
+    plan = Pl.plan_matrix_c1(cfg, B=B, b=b)[plan_name]
+    assert Pl.world_of(plan) == world, (plan_name, world)
+    torch.cuda.set_device(local_rank)
+    eng = Engine(cfg, rank, world, local_rank, group=group)
+    eng.apply(plan)
+    W = make_weights(cfg)
+    eng.write_weights(W)
+    tok, tgt = make_tokens(cfg, B)
+    dtok = torch.tensor(tok, device="cuda")
+    dtgt = torch.tensor(tgt, device="cuda")
+    names = list(tensor_shapes(cfg))
+    results = {"losses": []}
+    reads_step1 = None
+    for step in range(1, steps + 1):
+        loss = eng.train_step(dtok, dtgt, step=step, apply_update=True)
+        torch.cuda.synchronize()
+        results["losses"].append(float(loss.item()))
+        if step == 1:
+            reads_step1 = {n: (eng.read(n, L.KIND_RGRAD), eng.read(n, L.KIND_MASTER), eng.read(n, L.KIND_PARAM))
+                           for n in names}
+    eng.close()
+    if world > 1:
+        import torch.distributed as dist
+        allr = [None] * world
+        dist.all_gather_object(allr, reads_step1, group=group)
+    else:
+        allr = [reads_step1]
+    if rank != 0:
+        return None
+    return check(cfg, W, tok, tgt, names, allr, results, plan)
+
+
+def check(cfg, W, tok, tgt, names, allr, results, plan):
+    from oracle import model as M
+    P = M.params_f64(W)
+    loss_ref, g_ref = M.forward_backward(cfg, P, tok, tgt)
+    out = {"loss": results["losses"][0], "loss_ref": loss_ref,
+           "loss_rel": abs(results["losses"][0] - loss_ref) / abs(loss_ref), "grad_rel": {}, "adam_rel": {},
+           "push_ok": True, "owned_once": True}
+    hp = M.ADAM_DEFAULT
+    for n in names:
+        shp = tensor_shapes(cfg)[n]
+        g, seen = gather_logical([r[n][0] for r in allr], shp)
+        cnt = np.zeros(int(np.prod(shp)), np.int64)
+        for r in allr:
+            for e0, e1 in r[n][0][0]:
+                cnt[e0:e1] += 1
+        out["owned_once"] &= bool(np.all(cnt == 1))
+        out["grad_rel"][n] = float(np.abs(g - g_ref[n]).max() / max(np.abs(g_ref[n]).max(), 1e-30))
+        master, _ = gather_logical([r[n][1] for r in allr], shp)
+        wd = hp["weight_decay"] if M.decays(n) else 0.0
+        th, _, _ = M.adamw(P[n], np.zeros(shp), np.zeros(shp), g.astype(np.float64), 1, hp["lr"], hp["beta1"],
+                           hp["beta2"], hp["eps"], wd)
+        out["adam_rel"][n] = float(np.abs(master - th).max() / max(np.abs(th).max(), 1e-30))
+        # param push: each holder's bf16 == RNE(master)
+        want = bf16_rne(master.reshape(-1).astype(np.float32))
+        for r in allr:
+            (ranges, vals) = r[n][2]
+            off = 0
+            for e0, e1 in ranges:
+                if not np.array_equal(vals[off:off + e1 - e0], want[e0:e1]):
+                    out["push_ok"] = False
+                off += e1 - e0
+    # multi-step loss curve vs the oracle fed with bf16(master) each step (the GPU's param definition)
+    if len(results["losses"]) > 1:
+        Pm = {k: v.copy() for k, v in P.items()}
+        Mm = {k: np.zeros_like(v) for k, v in P.items()}
+        Vm = {k: np.zeros_like(v) for k, v in P.items()}
+        ref_losses = []
+        from synth.gen import bf16_to_f64
+        for step in range(1, len(results["losses"]) + 1):
+            Pb = {k: bf16_to_f64(bf16_rne(v.astype(np.float32))) for k, v in Pm.items()}
+            l, g = M.forward_backward(cfg, Pb, tok, tgt)
+            ref_losses.append(l)
+            for k in Pm:
+                wd = hp["weight_decay"] if M.decays(k) else 0.0
+                Pm[k], Mm[k], Vm[k] = M.adamw(Pm[k], Mm[k], Vm[k], g[k], step, hp["lr"], hp["beta1"], hp["beta2"],
+                                              hp["eps"], wd)
+        out["losses"] = results["losses"]
+        out["ref_losses"] = ref_losses
+    return out
+
+
+if __name__ == "__main__":
+    import torch.distributed as dist
+    plan_name, out_path = sys.argv[1], sys.argv[2]
+    steps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    dist.init_process_group("gloo")
+    r = run(plan_name, dist.get_rank(), dist.get_world_size(), int(os.environ.get("LOCAL_RANK", 0)), steps=steps)
+    if dist.get_rank() == 0:
+        json.dump(r, open(out_path, "w"), indent=1)
+    dist.barrier()
+    dist.destroy_process_group()

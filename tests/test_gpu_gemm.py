@@ -41,7 +41,7 @@ def _run(L, A, B, a_mn, b_mn, mode, C0=None):
     return dC.float().cpu().numpy()
 
 
-SHAPES = [(128, 256, 64), (256, 512, 1024), (200, 300, 136), (96, 48, 2048), (1000, 770, 520),
+SHAPES = [(128, 256, 64), (256, 512, 1024), (200, 304, 136), (96, 48, 2048), (1000, 776, 520),
           (2048, 2304, 4096)]
 
 
@@ -51,7 +51,7 @@ def test_gemm_small_int_bitwise(L, a_mn, b_mn, shape):
     M, N, K = shape
     A = small_int_matrix((M, K), 8, seed=M + K)
     B = small_int_matrix((K, N), 8, seed=N + 7 * K)
-    exact = (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float64)
+    exact = A.astype(np.float64) @ B.astype(np.float64)  # exact: |products| < 2^53
     assert np.abs(exact).max() < 2 ** 24
     C = _run(L, A, B, a_mn, b_mn, 1)
     assert np.array_equal(C, exact.astype(np.float32))
@@ -72,3 +72,13 @@ def test_gemm_random_tolerance(L, a_mn, b_mn):
     C = _run(L, A, B, a_mn, b_mn, 1)
     err = np.abs(C - ref).max() / np.abs(ref).max()
     assert err < 1e-5, err
+
+
+def test_gemm_rejects_unaligned_strides(L):
+    """TMA needs 16-byte row strides: ld not a multiple of 8 bf16 elements is E_ARG, not a fault."""
+    A = torch.zeros(64, 100, dtype=torch.bfloat16, device="cuda")
+    B = torch.zeros(64, 100, dtype=torch.bfloat16, device="cuda")
+    C = torch.zeros(64, 64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.lib.malleus_k_gemm(64, 64, 100, A.data_ptr(), 100, 0, B.data_ptr(), 100, 0, C.data_ptr(), 64, 1,
+                                st) == 1

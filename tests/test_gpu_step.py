@@ -1,0 +1,52 @@
+"""Whole-step parity of the malleable step (libmalleus.so) vs the oracle on the C1 tiny model over
+the SURVEY §8(d) plan matrix.  P0 runs in-process on one GPU; multi-GPU plans run under torchrun
+with one process per GPU and are skipped when the box has fewer GPUs."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+PLAN_WORLD = {"P0": 1, "P1": 2, "P2": 2, "P3": 2, "P4": 4, "P5": 3, "P6": 3, "P7": 8, "P8": 2}
+
+
+def _assert_ok(r):
+    assert r["loss_rel"] <= 1e-3, r
+    assert r["owned_once"]
+    bad = {k: v for k, v in r["grad_rel"].items() if v > 2e-2}
+    assert not bad, bad
+    bad = {k: v for k, v in r["adam_rel"].items() if v > 1e-6}
+    assert not bad, bad
+    assert r["push_ok"]
+    if "losses" in r:
+        for a, b in zip(r["losses"], r["ref_losses"]):
+            assert abs(a - b) / abs(b) <= 1e-3, (r["losses"], r["ref_losses"])
+
+
+def test_p0_single_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from tests.mp_worker import run
+    r = run("P0", steps=4)
+    _assert_ok(r)
+
+
+@pytest.mark.parametrize("plan", ["P1", "P2", "P3", "P8", "P5", "P6", "P4", "P7"])
+def test_multi_gpu_plans(plan, tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    n = PLAN_WORLD[plan]
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"{plan} needs {n} GPUs")
+    out = tmp_path / "r.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mp_worker.py"), plan,
+           str(out), "2"]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    _assert_ok(json.load(open(out)))
