@@ -1,0 +1,295 @@
+"""Benchmark of the malleable hybrid-parallel training step (BASELINE.json metric: tokens/s under
+injected stragglers at 1/2/4/8 B200; migration GB/s reported separately by tools/bench_migrate.py).
+
+  python bench.py --gpus N --steps K --warmup W [--impl malleus|reference]
+
+Workload (config.workload): the LLaMA-7B-shaped 4-layer slice (BASELINE.json configs[1]; h 4096,
+32 heads, ffn 11008, vocab 32000, seq 2048, global batch 16 sequences, b = 1), synthetic tokens
+and random-init weights (synth/gen.py, seeds 1234 / 5678).  Plans: SURVEY §8(d) ladder —
+N=1: TP1 (a straggler is degenerate on one GPU, none injected);
+N=2: TP2 with rank 1 slowed 2x (HOG), heads 22/10;
+N=4: the C2 plan, DP2 x TP2, rank 1 slowed 1.5x, heads 19/13, m = (7, 9);
+N=8: DP2 x TP4, rank 3 slowed 2x, m = (7, 9).
+One step = the whole malleable step: embedding, 4 layers fwd+bwd for every micro-batch, LM head +
+CE, cross-layout weighted grad reduction, AdamW on owned pieces, bf16 param push.
+Timing: W untimed warm-up steps, then K steps between barrier + synchronize, CUDA events on the
+launching stream, max over ranks.  The step's working set (2.1 GB of bf16 weights, 4.3 GB fp32
+grads, 13 GB optimizer state) is far larger than the 126 MB L2, so no explicit flush is done.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+STRAGGLER = {1: None, 2: (1, 2.0), 4: (1, 1.5), 8: (3, 2.0)}  # rank, x
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def flops_per_token(cfg):
+    """Algorithmic FLOPs per token: fwd+bwd = 3x fwd, causal attention at
+    (s+1)/2 keys, LM head included, embedding excluded."""
+    h, F, V, L, s = cfg.hidden, cfg.ffn, cfg.vocab, cfg.n_layers, cfg.seq_len
+    return 3 * (L * (2 * (4 * h * h + 3 * h * F) + 4 * ((s + 1) / 2) * h) + 2 * h * V)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/malleus_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        rows = [[x.strip() for x in r] for r in rows if len(r) >= 7]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def oracle_sample(cfg, seconds_hint=20.0):
+    """CPU baseline: the oracle (numpy fp64) as it stands, on a bounded sample of the workload: one
+    sequence (2048 tokens) through embedding, ONE layer and the LM head, fwd + bwd.  Scaled to the
+    full 4-layer model by the algorithmic FLOP ratio."""
+    import dataclasses
+    from synth.gen import make_weights, make_tokens
+    from oracle import model as M
+    small = dataclasses.replace(cfg, n_layers=1)
+    P = M.params_f64(make_weights(small))
+    tok, tgt = make_tokens(small, 1)
+    t0 = time.perf_counter()
+    M.forward_backward(small, P, tok, tgt)
+    t = time.perf_counter() - t0
+    tok_s_small = tok.size / t
+    ratio = flops_per_token(small) / flops_per_token(cfg)
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        threads = max(i.get("num_threads", 1) for i in info) if info else len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        threads = len(os.sched_getaffinity(0))
+    return {"value": tok_s_small * ratio, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+            "sample": f"1 sequence x {cfg.seq_len} tokens through embedding + 1 of {cfg.n_layers} layers + LM head, "
+                      f"fwd+bwd in numpy fp64 ({t:.1f} s), scaled by the algorithmic FLOP ratio {ratio:.3f}"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.warmup + args.steps):
+        vals.append(oracle_sample(cfg))
+    vals = vals[args.warmup:]
+    v = statistics.median(x["value"] for x in vals)
+    cpu = dict(vals[0])
+    cpu["value"] = v
+    line = {"impl": "reference", "metric": "tokens/s", "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2 LLaMA-7B-shaped 4-layer slice, seq 2048, B=16 (oracle sample)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="malleus", choices=["malleus", "reference"])
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--no-straggler", action="store_true")
+    ap.add_argument("--uniform", action="store_true", help="non-malleable even plan (T_u / T0 runs)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    from synth.gen import C2_7B_SLICE
+    cfg = C2_7B_SLICE
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from synth.gen import make_weights, make_tokens
+    from paper_2410_13333_b200 import plans as Pl
+    from paper_2410_13333_b200 import _lib as L
+    from paper_2410_13333_b200.engine import Engine
+    import ctypes as C
+
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("gloo")
+    B = args.batch
+    straggle = STRAGGLER[world] if not args.no_straggler else None
+    plan = Pl.ladder_plan(cfg, world, B, b=1, straggle=not args.uniform)
+    eng = Engine(cfg, rank, world, local)
+    eng.apply(plan)
+    eng.write_weights(make_weights(cfg, parity=False))
+    tok, tgt = make_tokens(cfg, B)
+    dtok = torch.tensor(tok, device="cuda")
+    dtgt = torch.tensor(tgt, device="cuda")
+    if straggle and straggle[0] == rank:
+        eng.set_slowdown(straggle[1], 1)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    step = 1
+    for _ in range(max(args.warmup, 3)):
+        eng.train_step(dtok, dtgt, step=step)
+        step += 1
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    L.lib.malleus_gemm_profile(1, None, None, None)
+    n0 = L.lib.malleus_kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        eng.train_step(dtok, dtgt, step=step)
+        step += 1
+    e1.record(stream)
+    barrier()
+    n_launch = (L.lib.malleus_kernel_launches() - n0) // args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    gl, gf, gms = C.c_int64(0), C.c_double(0), C.c_double(0)
+    L.lib.malleus_gemm_profile(-1, C.byref(gl), C.byref(gf), C.byref(gms))
+    L.lib.malleus_gemm_profile(0, None, None, None)
+    clk = clocks.stop()
+    timing = eng.timing()
+    t_ms = torch.tensor([ms], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms_max = float(t_ms.item())
+    tokens_per_step = B * cfg.seq_len
+    value = tokens_per_step / (ms_max / 1e3)
+
+    # e2e: the public API call with the step's inputs copied from pinned host memory and the loss read back
+    htok = torch.tensor(tok).pin_memory()
+    htgt = torch.tensor(tgt).pin_memory()
+    hloss = torch.zeros(1).pin_memory()
+    barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    n_e2e = max(3, args.steps // 2)
+    e2.record(stream)
+    for _ in range(n_e2e):
+        dtok.copy_(htok, non_blocking=True)
+        dtgt.copy_(htgt, non_blocking=True)
+        loss = eng.train_step(dtok, dtgt, step=step)
+        step += 1
+        hloss.copy_(loss, non_blocking=True)
+    e3.record(stream)
+    barrier()
+    e2e_ms = torch.tensor([e2.elapsed_time(e3) / n_e2e], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_val = tokens_per_step / (float(e2e_ms.item()) / 1e3)
+
+    pk, pk_kind = peaks()
+    gemm_tf = (gf.value / (gms.value / 1e3)) / 1e12 if gms.value > 0 else None
+    gemm_share = (gms.value / args.steps) / ms if ms > 0 else None
+    roof = {"bound": "tensor", "kernel": "gemm_tcgen05_kernel (all layer/head GEMMs)",
+            "achieved": gemm_tf, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+            "frac": (gemm_tf / pk["bf16_tflops_sustained"]) if gemm_tf else None,
+            "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside a long step)",
+            "traffic": None, "gemm_launches_per_step": gl.value // max(1, args.steps),
+            "gemm_share_of_step": gemm_share}
+    prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(prof):
+        roof["traffic"] = json.load(open(prof)).get("bytes_per_launch")
+    step_tf = flops_per_token(cfg) * value / 1e12
+    line = None
+    if rank == 0:
+        line = {"metric": "tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights (seeds 1234/5678)",
+                "config": {"workload": "C2: LLaMA-7B-shaped 4-layer slice (h 4096, 32 heads, ffn 11008, V 32000)",
+                           "global_batch": B, "seq_len": cfg.seq_len, "micro_batch": 1,
+                           "plan": plan_summary(plan), "straggler": (
+                               {"rank": straggle[0], "x": straggle[1], "mode": "HOG"} if straggle else None),
+                           "l2": "working set >> 126 MB L2 (no flush needed)"},
+                "step_tflops": step_tf,
+                "roofline": roof,
+                "model_flops_frac": step_tf / (pk["bf16_tflops_sustained"] * world),
+                "breakdown_ms_rank0": timing,
+                "clocks": clk,
+                "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": int(2 * tok.nbytes),
+                        "d2h_bytes_per_step": 4},
+                "gpu_launches": int(n_launch)}
+    eng.close()
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_sample(cfg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def plan_summary(p):
+    out = []
+    for pp in p["pipes"]:
+        out.append({"m": pp["n_micro"], "stages": [{"ranks": st["ranks"], "heads": st["heads"],
+                                                    "layers": st["layers"]} for st in pp["stages"]]})
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -219,6 +219,16 @@ malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode);
  * out[0] compute, out[1] tp_comm, out[2] pp_comm, out[3] grad_sync, out[4] total. */
 malleus_status malleus_last_step_timing(malleus_ctx* ctx, float out[5]);
 
+/* ---------------------------------------------------------------- instrumentation
+ * kernel_launches (local): number of kernels this library has launched since it was loaded
+ * (all entry points), for the bench's gpu_launches count.
+ * gemm_profile (local): enable = 1 starts recording CUDA events around every tcgen05 GEMM launch
+ * (resetting totals), enable = 0 stops; enable = -1 queries (synchronising on the recorded
+ * events): number of recorded launches, their algorithmic FLOPs (sum of 2*M*N*K) and summed
+ * device milliseconds.  Used for the roofline of the dominant kernel. */
+int64_t malleus_kernel_launches(void);
+malleus_status malleus_gemm_profile(int32_t enable, int64_t* launches, double* flops, double* ms);
+
 /* ---------------------------------------------------------------- kernel-level entry points
  * Single-GPU building blocks of the hot path, exposed for parity tests and roofline
  * measurement.  All pointers are device pointers; all calls enqueue on `stream` and return

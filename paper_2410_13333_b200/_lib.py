@@ -93,6 +93,8 @@ _SIGS = {
     "malleus_probe_speed": ([vp, i32, P_f32], i32),
     "malleus_set_slowdown": ([vp, f32, i32], i32),
     "malleus_last_step_timing": ([vp, P_f32], i32),
+    "malleus_kernel_launches": ([], i64),
+    "malleus_gemm_profile": ([i32, P_i64, C.POINTER(C.c_double), C.POINTER(C.c_double)], i32),
     "malleus_k_gemm": ([i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, i32, vp], i32),
     "malleus_k_rmsnorm_fwd": ([i32, i32, vp, vp, vp, vp, f32, vp, vp, vp], i32),
     "malleus_k_rmsnorm_bwd": ([i32, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) reduce_adam_kernel(const ChunkDesc* __res
 cudaError_t reduce_adam(int n_chunks, const ChunkDesc* d_chunks, const PieceDesc* d_pieces, const AdamHyper& hp,
                         cudaStream_t st) {
   if (n_chunks <= 0) return cudaSuccess;
-  reduce_adam_kernel<<<n_chunks, 256, 0, st>>>(d_chunks, d_pieces, hp);
+  reduce_adam_kernel<<<n_chunks, 256, 0, st>>>(d_chunks, d_pieces, hp); count_launch();
   return cudaGetLastError();
 }
 

@@ -56,3 +56,17 @@ extern "C" malleus_status malleus_k_attention_bwd(int32_t nb, int32_t s, int32_t
   cudaFreeAsync(dsum, st);
   return cu(e);
 }
+
+extern "C" int64_t malleus_kernel_launches(void) { return (int64_t)launches_total(); }
+
+extern "C" malleus_status malleus_gemm_profile(int32_t enable, int64_t* launches, double* flops, double* ms) {
+  if (enable >= 0) {
+    gemm_profile_enable(enable != 0);
+    return MALLEUS_OK;
+  }
+  if (!launches || !flops || !ms) return MALLEUS_E_ARG;
+  long long l = 0;
+  cudaError_t e = gemm_profile_query(&l, flops, ms);
+  *launches = l;
+  return cu(e);
+}

@@ -412,7 +412,7 @@ cudaError_t fwd_impl(int nb, int s, int n, const void* qkv, void* o, float* lse,
   auto k = attn_fwd_kernel<D>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid(s / BQ, n, nb);
-  k<<<grid, 128, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse, rsqrtf((float)D));
+  k<<<grid, 128, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse, rsqrtf((float)D)); count_launch();
   return cudaGetLastError();
 }
 
@@ -422,7 +422,7 @@ cudaError_t bwd_impl(int nb, int s, int n, const void* qkv, const void* o, const
   const long long T = (long long)nb * s;
   dim3 pblk(32, 8);
   attn_dsum_kernel<D><<<(unsigned)((T * n + 7) / 8), pblk, 0, st>>>(s, n, (const __nv_bfloat16*)o,
-                                                                     (const __nv_bfloat16*)dout, dsum, T);
+                                                                     (const __nv_bfloat16*)dout, dsum, T); count_launch();
   const int smem = (BQ + BKV) * 2 * Tile<D>::LD * 2 + 2 * BQ * 4;
   auto k1 = attn_bwd_dkv_kernel<D>;
   auto k2 = attn_bwd_dq_kernel<D>;
@@ -431,9 +431,9 @@ cudaError_t bwd_impl(int nb, int s, int n, const void* qkv, const void* o, const
   dim3 grid(s / BQ, n, nb);
   const float scale = rsqrtf((float)D);
   k1<<<grid, 128, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse, dsum,
-                              (__nv_bfloat16*)dqkv, scale);
+                              (__nv_bfloat16*)dqkv, scale); count_launch();
   k2<<<grid, 128, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse, dsum,
-                              (__nv_bfloat16*)dqkv, scale);
+                              (__nv_bfloat16*)dqkv, scale); count_launch();
   return cudaGetLastError();
 }
 

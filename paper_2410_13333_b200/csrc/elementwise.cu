@@ -383,7 +383,7 @@ cudaError_t rmsnorm_fwd(int T, int h, const void* x, const float* partial, void*
   if (h % 8 || h > 8 * NORM_MAXV * NORM_THREADS || T <= 0) return cudaErrorInvalidValue;
   if (partial && !x_out) return cudaErrorInvalidValue;
   rmsnorm_fwd_kernel<<<T, NORM_THREADS, 0, st>>>(h, (const uint4*)x, (const float4*)partial, (uint4*)x_out,
-                                                 (const uint4*)g, eps, (uint4*)y, rstd);
+                                                 (const uint4*)g, eps, (uint4*)y, rstd); count_launch();
   return cudaGetLastError();
 }
 
@@ -395,14 +395,14 @@ cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float*
   int rpb = (T + BWD_BLOCKS - 1) / BWD_BLOCKS;
   int nb = (T + rpb - 1) / rpb;
   rmsnorm_bwd_kernel<<<nb, NORM_THREADS, 0, st>>>(T, h, rpb, (const uint4*)x, (const uint4*)g, rstd,
-                                                  (const float4*)dy, (const uint4*)dres, (uint4*)dx_out, scratch);
-  colsum_accum_kernel<<<(h + 255) / 256, 256, 0, st>>>(nb, h, scratch, dg_accum);
+                                                  (const float4*)dy, (const uint4*)dres, (uint4*)dx_out, scratch); count_launch();
+  colsum_accum_kernel<<<(h + 255) / 256, 256, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t residual_add(long long n, const void* x, const float* partial, void* out, cudaStream_t st) {
   if (n % 8) return cudaErrorInvalidValue;
-  residual_add_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>(n / 8, (const uint4*)x, (const float4*)partial, (uint4*)out);
+  residual_add_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>(n / 8, (const uint4*)x, (const float4*)partial, (uint4*)out); count_launch();
   return cudaGetLastError();
 }
 
@@ -410,66 +410,66 @@ cudaError_t rope_inplace(int T, int s, int n, int d, void* buf, long long ld, in
                          bool inverse, cudaStream_t st) {
   long long total = (long long)T * n * (d / 2);
   dim3 grid(grid_for(total, 256), 2);
-  rope_kernel<<<grid, 256, 0, st>>>(T, s, n, d, (__nv_bfloat16*)buf, ld, col0, log2f(theta), inverse ? -1.f : 1.f);
+  rope_kernel<<<grid, 256, 0, st>>>(T, s, n, d, (__nv_bfloat16*)buf, ld, col0, log2f(theta), inverse ? -1.f : 1.f); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t swiglu_fwd(int T, int F, const void* gu, void* u, cudaStream_t st) {
   if (F % 8) return cudaErrorInvalidValue;
-  swiglu_fwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, st>>>(T, F, (const __nv_bfloat16*)gu, (__nv_bfloat16*)u);
+  swiglu_fwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, st>>>(T, F, (const __nv_bfloat16*)gu, (__nv_bfloat16*)u); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t swiglu_bwd(int T, int F, const void* gu, const void* du, void* dgu, cudaStream_t st) {
   if (F % 8) return cudaErrorInvalidValue;
   swiglu_bwd_kernel<<<grid_for((long long)T * F / 8, 256), 256, 0, st>>>(T, F, (const __nv_bfloat16*)gu,
-                                                                       (const __nv_bfloat16*)du, (__nv_bfloat16*)dgu);
+                                                                       (const __nv_bfloat16*)du, (__nv_bfloat16*)dgu); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t embed_fwd(int T, int h, const int32_t* tok, const void* E, void* x, cudaStream_t st) {
-  embed_fwd_kernel<<<T, 128, 0, st>>>(T, h, tok, (const uint4*)E, (uint4*)x);
+  embed_fwd_kernel<<<T, 128, 0, st>>>(T, h, tok, (const uint4*)E, (uint4*)x); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t embed_bwd(int T, int h, const int32_t* tok, const void* dx, float* dE, cudaStream_t st) {
-  embed_bwd_kernel<<<T, 128, 0, st>>>(T, h, tok, (const uint4*)dx, dE);
+  embed_bwd_kernel<<<T, 128, 0, st>>>(T, h, tok, (const uint4*)dx, dE); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t ce_stats(int T, int V, const float* z, const int32_t* tgt, int v0, float* stats, cudaStream_t st) {
-  ce_stats_kernel<<<T, CE_THREADS, 0, st>>>(V, z, tgt, v0, stats);
+  ce_stats_kernel<<<T, CE_THREADS, 0, st>>>(V, z, tgt, v0, stats); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t ce_combine_max(int T, const float* stats, float* gmax, cudaStream_t st) {
-  ce_max_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, stats, gmax);
+  ce_max_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, stats, gmax); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t ce_local_sum(int T, const float* stats, const float* gmax, float* sum_tgt, cudaStream_t st) {
-  ce_local_sum_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, stats, gmax, sum_tgt);
+  ce_local_sum_kernel<<<(T + 255) / 256, 256, 0, st>>>(T, stats, gmax, sum_tgt); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t ce_grad(int T, int V, const float* z, const int32_t* tgt, int v0, const float* gmax, const float* gsum,
                     const float* gtgt, float scale, void* dz, float* loss_rows, cudaStream_t st) {
-  ce_grad_kernel<<<T, 256, 0, st>>>(V, z, tgt, v0, gmax, gsum, gtgt, scale, (__nv_bfloat16*)dz, loss_rows);
+  ce_grad_kernel<<<T, 256, 0, st>>>(V, z, tgt, v0, gmax, gsum, gtgt, scale, (__nv_bfloat16*)dz, loss_rows); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t reduce_loss(int T, const float* rows, float scale, float* out, int accumulate, cudaStream_t st) {
-  reduce_loss_kernel<<<1, 1024, 0, st>>>(T, rows, scale, out, accumulate);
+  reduce_loss_kernel<<<1, 1024, 0, st>>>(T, rows, scale, out, accumulate); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t cast_f32_bf16(long long n, const float* in, void* out, cudaStream_t st) {
-  cast_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, in, (__nv_bfloat16*)out);
+  cast_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, in, (__nv_bfloat16*)out); count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t fill_f32(long long n, float* p, float v, cudaStream_t st) {
-  fill_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, p, v);
+  fill_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, p, v); count_launch();
   return cudaGetLastError();
 }
 

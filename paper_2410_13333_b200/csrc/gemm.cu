@@ -18,6 +18,9 @@
 // TMA out-of-bounds zero fill and masked epilogue stores (uneven TP shards produce ragged N).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <atomic>
+#include <utility>
+#include <vector>
 #include "ptx.cuh"
 #include "kernels.h"
 
@@ -240,6 +243,40 @@ static int g_num_sms = 0;
 static int g_avail_sms = 0;  // 0 = all SMs; HOG straggler emulation caps the persistent grid
 void set_avail_sms(int n) { g_avail_sms = n; }
 
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches += n; }
+long long launches_total() { return g_launches.load(); }
+
+// Optional per-launch CUDA-event timing of this GEMM (bench.py roofline of the dominant kernel).
+struct GemmProf {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<double> flops;
+  size_t used = 0;
+};
+static GemmProf g_prof;
+
+void gemm_profile_enable(bool on) {
+  g_prof.on = on;
+  g_prof.used = 0;
+  g_prof.flops.clear();
+}
+cudaError_t gemm_profile_query(long long* launches, double* flops, double* ms) {
+  double f = 0, t = 0;
+  for (size_t i = 0; i < g_prof.used; ++i) {
+    cudaError_t e = cudaEventSynchronize(g_prof.ev[i].second);
+    if (e != cudaSuccess) return e;
+    float x = 0.f;
+    cudaEventElapsedTime(&x, g_prof.ev[i].first, g_prof.ev[i].second);
+    t += x;
+    f += g_prof.flops[i];
+  }
+  *launches = (long long)g_prof.used;
+  *flops = f;
+  *ms = t;
+  return cudaSuccess;
+}
+
 template <bool A_MN, bool B_MN>
 static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                           cudaStream_t st) {
@@ -257,7 +294,22 @@ static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
   int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   const int sms = (g_avail_sms > 0 && g_avail_sms < g_num_sms) ? g_avail_sms : g_num_sms;
   int grid = tiles < sms ? tiles : sms;
-  kern<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p);
+  if (g_prof.on) {
+    if (g_prof.used == g_prof.ev.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      g_prof.ev.push_back({a, b});
+    }
+    cudaEventRecord(g_prof.ev[g_prof.used].first, st);
+    kern<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p);
+    count_launch();
+    cudaEventRecord(g_prof.ev[g_prof.used].second, st);
+    g_prof.flops.push_back(2.0 * p.M * (double)p.N * p.K);
+    g_prof.used++;
+    return cudaGetLastError();
+  }
+  kern<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(ta, tb, p); count_launch();
   return cudaGetLastError();
 }
 

@@ -5,6 +5,12 @@
 
 namespace mls {
 
+// instrumentation: library-wide kernel launch counter (gpu_launches in bench.py)
+void count_launch(int n = 1);
+long long launches_total();
+void gemm_profile_enable(bool on);
+cudaError_t gemm_profile_query(long long* launches, double* flops, double* ms);
+
 enum { GEMM_STORE_BF16 = 0, GEMM_STORE_F32 = 1, GEMM_ACCUM_F32 = 2 };
 
 struct GemmDesc {

@@ -15,7 +15,7 @@ __global__ void probe_copy_kernel(long long n, const float4* __restrict__ src, f
 }
 
 cudaError_t probe_copy(long long n, const float* src, float* dst, cudaStream_t st) {
-  probe_copy_kernel<<<148 * 8, 256, 0, st>>>(n / 4, (const float4*)src, (float4*)dst);
+  probe_copy_kernel<<<148 * 8, 256, 0, st>>>(n / 4, (const float4*)src, (float4*)dst); count_launch();
   return cudaGetLastError();
 }
 
@@ -29,7 +29,7 @@ __global__ void spin_kernel(long long ns) {
 
 cudaError_t spin_ns(long long ns, cudaStream_t st) {
   if (ns <= 0) return cudaSuccess;
-  spin_kernel<<<1, 32, 0, st>>>(ns);
+  spin_kernel<<<1, 32, 0, st>>>(ns); count_launch();
   return cudaGetLastError();
 }
 
@@ -68,7 +68,7 @@ cudaError_t hog_start(int n_sms, volatile int* stop_flag, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   }
   *(volatile int*)started = 0;
-  hog_kernel<<<n_sms, 1024, HOG_SMEM, st>>>(stop_flag, dstarted, 1.0f);
+  hog_kernel<<<n_sms, 1024, HOG_SMEM, st>>>(stop_flag, dstarted, 1.0f); count_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // wait (bounded, ~1 s) until every hog block is resident
