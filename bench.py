@@ -91,15 +91,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def oracle_sample(cfg, seconds_hint=20.0):
+_ORACLE_CACHE = {}
+
+
+def oracle_sample(cfg, seq=256):
     """CPU baseline: the oracle (numpy fp64) as it stands, on a bounded sample of the workload: one
-    sequence (2048 tokens) through embedding, ONE layer and the LM head, fwd + bwd.  Scaled to the
-    full 4-layer model by the algorithmic FLOP ratio."""
+    `seq`-token sequence through embedding, ONE layer of the C2 shape and the LM head, fwd + bwd.
+    Scaled to the full workload (4 layers, seq 2048) by the algorithmic FLOP-per-token ratio."""
     import dataclasses
     from synth.gen import make_weights, make_tokens
     from oracle import model as M
-    small = dataclasses.replace(cfg, n_layers=1)
-    P = M.params_f64(make_weights(small))
+    small = dataclasses.replace(cfg, n_layers=1, seq_len=seq)
+    if small not in _ORACLE_CACHE:
+        _ORACLE_CACHE[small] = M.params_f64(make_weights(small))
+    P = _ORACLE_CACHE[small]
     tok, tgt = make_tokens(small, 1)
     t0 = time.perf_counter()
     M.forward_backward(small, P, tok, tgt)
@@ -113,7 +118,7 @@ def oracle_sample(cfg, seconds_hint=20.0):
     except Exception:  # noqa: BLE001
         threads = len(os.sched_getaffinity(0))
     return {"value": tok_s_small * ratio, "unit": "tokens/s", "cores": threads, "kind": "oracle",
-            "sample": f"1 sequence x {cfg.seq_len} tokens through embedding + 1 of {cfg.n_layers} layers + LM head, "
+            "sample": f"1 sequence x {small.seq_len} tokens through embedding + 1 of {cfg.n_layers} layers + LM head, "
                       f"fwd+bwd in numpy fp64 ({t:.1f} s), scaled by the algorithmic FLOP ratio {ratio:.3f}"}
 
 

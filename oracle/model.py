@@ -73,25 +73,25 @@ def attention_fwd(q, k, v):
     """q,k,v [B, n, s, d].  S = q k^T/sqrt(d) + causal; P = softmax(S); o = P v."""
     d = q.shape[-1]
     s = q.shape[-2]
-    S = np.einsum("bnid,bnjd->bnij", q, k) / np.sqrt(d)
+    S = (q @ np.swapaxes(k, -1, -2)) / np.sqrt(d)          # [B, n, s, s]
     mask = np.triu(np.ones((s, s), dtype=bool), k=1)
     S = np.where(mask, -np.inf, S)
     S = S - S.max(axis=-1, keepdims=True)
     P = np.exp(S)
     P = P / P.sum(axis=-1, keepdims=True)
-    o = np.einsum("bnij,bnjd->bnid", P, v)
+    o = P @ v
     return o, P
 
 
 def attention_bwd(q, k, v, o, P, do):
     """dV = P^T dO; dP = dO V^T; dS = P*(dP - rowsum(dO*O)); dQ = dS K/sqrt(d); dK = dS^T Q/sqrt(d)."""
     d = q.shape[-1]
-    dv = np.einsum("bnij,bnid->bnjd", P, do)
-    dP = np.einsum("bnid,bnjd->bnij", do, v)
+    dv = np.swapaxes(P, -1, -2) @ do
+    dP = do @ np.swapaxes(v, -1, -2)
     D = np.sum(do * o, axis=-1, keepdims=True)
     dS = P * (dP - D)
-    dq = np.einsum("bnij,bnjd->bnid", dS, k) / np.sqrt(d)
-    dk = np.einsum("bnij,bnid->bnjd", dS, q) / np.sqrt(d)
+    dq = (dS @ k) / np.sqrt(d)
+    dk = (np.swapaxes(dS, -1, -2) @ q) / np.sqrt(d)
     return dq, dk, dv
 
 
