@@ -196,7 +196,7 @@ def main():
 
     step = 1
     for _ in range(max(args.warmup, 3)):
-        eng.train_step(dtok, dtgt, step=step)
+        eng.train_step(dtok, dtgt, step=step, apply_update=2)
         step += 1
     barrier()
     clocks = ClockSampler(local)
@@ -207,7 +207,7 @@ def main():
     barrier()
     e0.record(stream)
     for _ in range(args.steps):
-        eng.train_step(dtok, dtgt, step=step)
+        eng.train_step(dtok, dtgt, step=step, apply_update=2)
         step += 1
     e1.record(stream)
     barrier()
@@ -237,7 +237,7 @@ def main():
     for _ in range(n_e2e):
         dtok.copy_(htok, non_blocking=True)
         dtgt.copy_(htgt, non_blocking=True)
-        loss = eng.train_step(dtok, dtgt, step=step)
+        loss = eng.train_step(dtok, dtgt, step=step, apply_update=2)
         step += 1
         hloss.copy_(loss, non_blocking=True)
     e3.record(stream)

@@ -2,31 +2,71 @@
 // (§5.1; readings R4, R5, R9).
 //
 // For every owned piece: G = sum_i w_i g_i over contributing pipelines in fixed pipeline order
-// (w_i = m_i b / B), written to rgrad; then torch.optim.AdamW semantics:
+// (w_i = m_i b / B); optionally written to rgrad; then torch.optim.AdamW semantics:
 //   theta *= 1 - lr*wd;  m = b1 m + (1-b1) G;  v = b2 v + (1-b2) G^2;
 //   theta -= lr * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
-// and the owner's bf16 param copy = RNE(theta).  HBM-bound: (4 n_src + 16 read, 4 + 12 + 2 write)
-// bytes per element.
+// and the owner's bf16 param copy = RNE(theta).  HBM-bound: per element (4 n_src + 12) B read and
+// (12 + 2 [+ 4 rgrad]) B written; 128-bit accesses when the piece is 16-byte aligned.
 #include <cuda_bf16.h>
 #include "kernels.h"
 
 namespace mls {
+
+struct AdamEl {
+  float th, m, v, g;
+};
+
+__device__ __forceinline__ float adam_one(float g, float& th, float& m, float& v, const AdamHyper& hp, int decay) {
+  if (decay) th *= 1.f - hp.lr * hp.wd;
+  m = hp.b1 * m + (1.f - hp.b1) * g;
+  v = hp.b2 * v + (1.f - hp.b2) * g * g;
+  th -= hp.lr * (m / hp.bc1) / (sqrtf(v / hp.bc2) + hp.eps);
+  return th;
+}
 
 __global__ void __launch_bounds__(256) reduce_adam_kernel(const ChunkDesc* __restrict__ chunks,
                                                           const PieceDesc* __restrict__ pieces, AdamHyper hp) {
   const ChunkDesc ch = chunks[blockIdx.x];
   const PieceDesc& pd = pieces[ch.piece];
   const int ns = pd.n_src;
+  const bool keep_rgrad = hp.apply != 2;
+  if (pd.vec) {
+    // 4 elements per thread per iteration
+    for (long long i = ch.off + 4 * threadIdx.x; i < ch.off + ch.len; i += 4 * blockDim.x) {
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < ns; ++s) {
+        const float4 x = *reinterpret_cast<const float4*>(pd.src[s] + i);
+        const float w = pd.w[s];
+        g.x += w * x.x; g.y += w * x.y; g.z += w * x.z; g.w += w * x.w;
+      }
+      if (keep_rgrad) *reinterpret_cast<float4*>(pd.rgrad + i) = g;
+      if (hp.apply) {
+        float4 th = *reinterpret_cast<const float4*>(pd.master + i);
+        float4 m = *reinterpret_cast<const float4*>(pd.m + i);
+        float4 v = *reinterpret_cast<const float4*>(pd.v + i);
+        adam_one(g.x, th.x, m.x, v.x, hp, pd.decay);
+        adam_one(g.y, th.y, m.y, v.y, hp, pd.decay);
+        adam_one(g.z, th.z, m.z, v.z, hp, pd.decay);
+        adam_one(g.w, th.w, m.w, v.w, hp, pd.decay);
+        *reinterpret_cast<float4*>(pd.master + i) = th;
+        *reinterpret_cast<float4*>(pd.m + i) = m;
+        *reinterpret_cast<float4*>(pd.v + i) = v;
+        __nv_bfloat162 lo = __floats2bfloat162_rn(th.x, th.y), hi = __floats2bfloat162_rn(th.z, th.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(pd.param + i) = pk;
+      }
+    }
+    return;
+  }
   for (long long i = ch.off + threadIdx.x; i < ch.off + ch.len; i += blockDim.x) {
     float g = 0.f;
     for (int s = 0; s < ns; ++s) g += pd.w[s] * pd.src[s][i];
-    pd.rgrad[i] = g;
+    if (keep_rgrad) pd.rgrad[i] = g;
     if (hp.apply) {
-      float th = pd.master[i];
-      if (pd.decay) th *= 1.f - hp.lr * hp.wd;
-      const float m = hp.b1 * pd.m[i] + (1.f - hp.b1) * g;
-      const float v = hp.b2 * pd.v[i] + (1.f - hp.b2) * g * g;
-      th -= hp.lr * (m / hp.bc1) / (sqrtf(v / hp.bc2) + hp.eps);
+      float th = pd.master[i], m = pd.m[i], v = pd.v[i];
+      adam_one(g, th, m, v, hp, pd.decay);
       pd.m[i] = m;
       pd.v[i] = v;
       pd.master[i] = th;

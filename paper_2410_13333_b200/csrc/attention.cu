@@ -1,21 +1,22 @@
 // Causal multi-head attention, forward and backward (PAPER.md:780 names
 // FlashAttention).  FlashAttention-2-style tiling with warp-level mma.sync m16n8k16 bf16 tensor
-// ops (fp32 accumulate), online softmax in registers, causal tile skipping.  Backward is split
+// ops (fp32 accumulate), online softmax in registers, causal tile skipping, cp.async double
+// buffering of the streamed tiles, heaviest causal blocks scheduled first.  Backward is split
 // into a dK/dV kernel (one CTA per key block) and a dQ kernel (one CTA per query block) so that
 // no atomics are needed and results are bitwise reproducible run to run.
 //
 // Layout: qkv [T, 3*n*d] bf16, T = nb * s; q | k | v column blocks, head j at columns j*d.
 // RoPE has already been applied to q and k (elementwise.cu).  o [T, n*d]; lse [nb, n, s] fp32.
 // Attention is 2-5% of step FLOPs; a tcgen05 version is future work
-// (DESIGN.md §Attention).
+// (DESIGN.md §Kernels).
 #include <cuda_bf16.h>
 #include "kernels.h"
 
 namespace mls {
 namespace {
 
-constexpr int BQ = 64;   // queries per CTA (16 per warp)
-constexpr int BKV = 64;  // keys per tile
+constexpr int BKV = 64;  // keys per streamed tile / per dK-dV CTA
+constexpr int BQB = 64;  // queries per streamed tile in the dK/dV kernel
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -40,32 +41,37 @@ __device__ __forceinline__ uint32_t pk(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Tile in smem: rows x D bf16, row stride D + 8 elements (conflict-free ldmatrix).
+// smem tile: rows x D bf16, row stride D + 8 elements (conflict-free ldmatrix)
 template <int D>
 struct Tile {
   static constexpr int LD = D + 8;
+  static constexpr int BYTES = LD * 2;
 };
 
-// Copy `rows` x D bf16 from global (row stride ld elements) to smem tile; zero rows >= valid.
+// async copy of `rows` x D bf16 (global row stride ld elements) into a smem tile
 template <int D>
-__device__ __forceinline__ void load_tile(__nv_bfloat16* sm, const __nv_bfloat16* g, long long ld, int rows) {
-  constexpr int CH = D / 8;  // 16-byte chunks per row
+__device__ __forceinline__ void load_tile_async(__nv_bfloat16* sm, const __nv_bfloat16* g, long long ld, int rows) {
+  constexpr int CH = D / 8;
   for (int i = threadIdx.x; i < rows * CH; i += blockDim.x) {
     const int r = i / CH, c = i % CH;
-    *reinterpret_cast<uint4*>(sm + r * Tile<D>::LD + c * 8) =
-        *reinterpret_cast<const uint4*>(g + (long long)r * ld + c * 8);
+    cp_async16(sm + r * Tile<D>::LD + c * 8, g + (long long)r * ld + c * 8);
   }
 }
 
-// A fragment (16x16) at (r0, c0) of a row-major smem tile.
 template <int D>
 __device__ __forceinline__ void frag_a(const __nv_bfloat16* sm, int r0, int c0, uint32_t (&a)[4]) {
   const int l = threadIdx.x & 31, mi = l >> 3;
   const int r = r0 + (mi & 1) * 8 + (l & 7), c = c0 + (mi >> 1) * 8;
   ldsm_x4(smem_addr(sm + r * Tile<D>::LD + c), a[0], a[1], a[2], a[3]);
 }
-// B fragments for two n-tiles [n0, n0+16) and k-step [k0, k0+16) from smem stored [n][k].
+// B fragments for two n-tiles [n0, n0+16) and k-step [k0, k0+16) from smem stored [n][k]
 template <int D>
 __device__ __forceinline__ void frag_b_nk(const __nv_bfloat16* sm, int n0, int k0, uint32_t& b00, uint32_t& b01,
                                           uint32_t& b10, uint32_t& b11) {
@@ -73,7 +79,7 @@ __device__ __forceinline__ void frag_b_nk(const __nv_bfloat16* sm, int n0, int k
   const int n = n0 + (mi >> 1) * 8 + (l & 7), k = k0 + (mi & 1) * 8;
   ldsm_x4(smem_addr(sm + n * Tile<D>::LD + k), b00, b01, b10, b11);
 }
-// B fragments for k-step [k0, k0+16) and two n-tiles [n0, n0+16) from smem stored [k][n].
+// B fragments for k-step [k0, k0+16) and two n-tiles [n0, n0+16) from smem stored [k][n]
 template <int D>
 __device__ __forceinline__ void frag_b_kn(const __nv_bfloat16* sm, int k0, int n0, uint32_t& b00, uint32_t& b01,
                                           uint32_t& b10, uint32_t& b11) {
@@ -83,97 +89,117 @@ __device__ __forceinline__ void frag_b_kn(const __nv_bfloat16* sm, int k0, int n
 }
 
 // ------------------------------------------------------------------ forward
-template <int D>
-__global__ void __launch_bounds__(128)
+// CTA = NW warps x 16 queries; K/V tiles of 64 keys streamed with a 2-deep cp.async ring.
+template <int D, int NW>
+__global__ void __launch_bounds__(NW * 32)
 attn_fwd_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ o,
                 float* __restrict__ lse, float scale) {
+  constexpr int BQ = NW * 16;
   extern __shared__ __align__(16) uint8_t sraw[];
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(sraw);
-  __nv_bfloat16* sK = sQ + BQ * Tile<D>::LD;
-  __nv_bfloat16* sV = sK + BKV * Tile<D>::LD;
-  const int qb = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
+  __nv_bfloat16* sKV = sQ + BQ * Tile<D>::LD;  // [2 stages][K | V][64][LD]
+  const int nqb = s / BQ;
+  const int qb = nqb - 1 - blockIdx.x;  // heaviest (most keys) first
+  const int head = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const long long ld = 3LL * n * D;
   const __nv_bfloat16* Qg = qkv + ((long long)b * s + qb * BQ) * ld + head * D;
   const __nv_bfloat16* Kg = qkv + (long long)b * s * ld + n * D + head * D;
-  const __nv_bfloat16* Vg = qkv + (long long)b * s * ld + 2 * n * D + head * D;
+  const __nv_bfloat16* Vg = Kg + n * D;
+  const int last_kb = ((qb + 1) * BQ - 1) / BKV;
+  auto kv = [&](int stage, int which) { return sKV + (stage * 2 + which) * BKV * Tile<D>::LD; };
 
-  load_tile<D>(sQ, Qg, ld, BQ);
-  __syncthreads();
-  uint32_t qf[D / 16][4];
-#pragma unroll
-  for (int kk = 0; kk < D / 16; ++kk) frag_a<D>(sQ, warp * 16, kk * 16, qf[kk]);
+  load_tile_async<D>(sQ, Qg, ld, BQ);
+  load_tile_async<D>(kv(0, 0), Kg, ld, BKV);
+  load_tile_async<D>(kv(0, 1), Vg, ld, BKV);
+  cp_commit();
 
   float acc[D / 8][4];
 #pragma unroll
   for (int j = 0; j < D / 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   const float sl2 = scale * LOG2E;
-  const int qrow0 = qb * BQ + warp * 16 + g;  // query index of rows g / g+8
+  const int qrow0 = qb * BQ + warp * 16 + g;
+  uint32_t qf[D / 16][4];
 
-  for (int kb = 0; kb <= qb; ++kb) {
+  for (int kb = 0; kb <= last_kb; ++kb) {
+    const int stg = kb & 1;
+    if (kb + 1 <= last_kb) {
+      load_tile_async<D>(kv(stg ^ 1, 0), Kg + (long long)(kb + 1) * BKV * ld, ld, BKV);
+      load_tile_async<D>(kv(stg ^ 1, 1), Vg + (long long)(kb + 1) * BKV * ld, ld, BKV);
+    }
+    cp_commit();
+    cp_wait<1>();
     __syncthreads();
-    load_tile<D>(sK, Kg + (long long)kb * BKV * ld, ld, BKV);
-    load_tile<D>(sV, Vg + (long long)kb * BKV * ld, ld, BKV);
-    __syncthreads();
-    float S[BKV / 8][4];
+    if (kb == 0) {
 #pragma unroll
-    for (int j = 0; j < BKV / 8; ++j) S[j][0] = S[j][1] = S[j][2] = S[j][3] = 0.f;
+      for (int kk = 0; kk < D / 16; ++kk) frag_a<D>(sQ, warp * 16, kk * 16, qf[kk]);
+    }
+    const __nv_bfloat16* sK = kv(stg, 0);
+    const __nv_bfloat16* sV = kv(stg, 1);
+    // warps whose 16 rows all precede this key tile skip it (causal)
+    const bool active = kb * BKV <= qb * BQ + warp * 16 + 15;
+    if (active) {
+      float S[BKV / 8][4];
 #pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
+      for (int j = 0; j < BKV / 8; ++j) S[j][0] = S[j][1] = S[j][2] = S[j][3] = 0.f;
 #pragma unroll
-      for (int jj = 0; jj < BKV / 16; ++jj) {
-        uint32_t b00, b01, b10, b11;
-        frag_b_nk<D>(sK, jj * 16, kk * 16, b00, b01, b10, b11);
-        mma16816(S[2 * jj], qf[kk], b00, b01);
-        mma16816(S[2 * jj + 1], qf[kk], b10, b11);
+      for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+        for (int jj = 0; jj < BKV / 16; ++jj) {
+          uint32_t b00, b01, b10, b11;
+          frag_b_nk<D>(sK, jj * 16, kk * 16, b00, b01, b10, b11);
+          mma16816(S[2 * jj], qf[kk], b00, b01);
+          mma16816(S[2 * jj + 1], qf[kk], b10, b11);
+        }
+      }
+      const bool diag = (kb + 1) * BKV - 1 > qb * BQ + warp * 16;
+      float mx0 = m0, mx1 = m1;
+#pragma unroll
+      for (int j = 0; j < BKV / 8; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = kb * BKV + j * 8 + 2 * tq + (e & 1);
+          const int q = qrow0 + (e >> 1) * 8;
+          float v = S[j][e] * sl2;
+          if (diag && key > q) v = -INFINITY;
+          S[j][e] = v;
+        }
+        mx0 = fmaxf(mx0, fmaxf(S[j][0], S[j][1]));
+        mx1 = fmaxf(mx1, fmaxf(S[j][2], S[j][3]));
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float c0 = exp2f(m0 - mx0), c1 = exp2f(m1 - mx1);
+      m0 = mx0; m1 = mx1;
+      float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < BKV / 8; ++j) {
+        S[j][0] = exp2f(S[j][0] - m0); S[j][1] = exp2f(S[j][1] - m0);
+        S[j][2] = exp2f(S[j][2] - m1); S[j][3] = exp2f(S[j][3] - m1);
+        rs0 += S[j][0] + S[j][1];
+        rs1 += S[j][2] + S[j][3];
+      }
+      l0 = l0 * c0 + rs0;
+      l1 = l1 * c1 + rs1;
+#pragma unroll
+      for (int j = 0; j < D / 8; ++j) { acc[j][0] *= c0; acc[j][1] *= c0; acc[j][2] *= c1; acc[j][3] *= c1; }
+#pragma unroll
+      for (int kk = 0; kk < BKV / 16; ++kk) {
+        uint32_t pa[4] = {pk(S[2 * kk][0], S[2 * kk][1]), pk(S[2 * kk][2], S[2 * kk][3]),
+                          pk(S[2 * kk + 1][0], S[2 * kk + 1][1]), pk(S[2 * kk + 1][2], S[2 * kk + 1][3])};
+#pragma unroll
+        for (int jj = 0; jj < D / 16; ++jj) {
+          uint32_t b00, b01, b10, b11;
+          frag_b_kn<D>(sV, kk * 16, jj * 16, b00, b01, b10, b11);
+          mma16816(acc[2 * jj], pa, b00, b01);
+          mma16816(acc[2 * jj + 1], pa, b10, b11);
+        }
       }
     }
-    // causal mask on the diagonal tile, scaled row max
-    float mx0 = m0, mx1 = m1;
-#pragma unroll
-    for (int j = 0; j < BKV / 8; ++j) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = kb * BKV + j * 8 + 2 * tq + (e & 1);
-        const int q = qrow0 + (e >> 1) * 8;
-        float v = S[j][e] * sl2;
-        if (kb == qb && key > q) v = -INFINITY;
-        S[j][e] = v;
-      }
-      mx0 = fmaxf(mx0, fmaxf(S[j][0], S[j][1]));
-      mx1 = fmaxf(mx1, fmaxf(S[j][2], S[j][3]));
-    }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float c0 = exp2f(m0 - mx0), c1 = exp2f(m1 - mx1);
-    m0 = mx0; m1 = mx1;
-    float rs0 = 0.f, rs1 = 0.f;
-#pragma unroll
-    for (int j = 0; j < BKV / 8; ++j) {
-      S[j][0] = exp2f(S[j][0] - m0); S[j][1] = exp2f(S[j][1] - m0);
-      S[j][2] = exp2f(S[j][2] - m1); S[j][3] = exp2f(S[j][3] - m1);
-      rs0 += S[j][0] + S[j][1];
-      rs1 += S[j][2] + S[j][3];
-    }
-    l0 = l0 * c0 + rs0;
-    l1 = l1 * c1 + rs1;
-#pragma unroll
-    for (int j = 0; j < D / 8; ++j) { acc[j][0] *= c0; acc[j][1] *= c0; acc[j][2] *= c1; acc[j][3] *= c1; }
-#pragma unroll
-    for (int kk = 0; kk < BKV / 16; ++kk) {
-      uint32_t pa[4] = {pk(S[2 * kk][0], S[2 * kk][1]), pk(S[2 * kk][2], S[2 * kk][3]),
-                        pk(S[2 * kk + 1][0], S[2 * kk + 1][1]), pk(S[2 * kk + 1][2], S[2 * kk + 1][3])};
-#pragma unroll
-      for (int jj = 0; jj < D / 16; ++jj) {
-        uint32_t b00, b01, b10, b11;
-        frag_b_kn<D>(sV, kk * 16, jj * 16, b00, b01, b10, b11);
-        mma16816(acc[2 * jj], pa, b00, b01);
-        mma16816(acc[2 * jj + 1], pa, b10, b11);
-      }
-    }
+    __syncthreads();  // stage stg is refilled in the next iteration
   }
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
@@ -189,9 +215,9 @@ attn_fwd_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat
     *reinterpret_cast<uint32_t*>(O1 + j * 8 + 2 * tq) = pk(acc[j][2] * inv1, acc[j][3] * inv1);
   }
   if (tq == 0) {
-    float* L = lse + ((long long)b * n + head) * s;
-    L[qrow0] = (m0 + log2f(l0)) / LOG2E;       // natural-log LSE of the scaled scores
-    L[qrow0 + 8] = (m1 + log2f(l1)) / LOG2E;
+    float* Lr = lse + ((long long)b * n + head) * s;
+    Lr[qrow0] = (m0 + log2f(l0)) / LOG2E;  // natural-log LSE of the scaled scores
+    Lr[qrow0 + 8] = (m1 + log2f(l1)) / LOG2E;
   }
 }
 
@@ -221,6 +247,8 @@ __global__ void attn_dsum_kernel(int s, int n, const __nv_bfloat16* __restrict__
 }
 
 // ------------------------------------------------------------------ backward dK, dV
+// CTA = 4 warps x 16 keys (one 64-key block); Q / dO / lse / D tiles of 64 queries streamed with a
+// 2-deep cp.async ring.
 template <int D>
 __global__ void __launch_bounds__(128)
 attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ dout,
@@ -230,16 +258,31 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
   constexpr int LDT = Tile<D>::LD;
   __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(sraw);
   __nv_bfloat16* sV = sK + BKV * LDT;
-  __nv_bfloat16* sQ = sV + BKV * LDT;
-  __nv_bfloat16* sO = sQ + BQ * LDT;  // dO tile
-  float* sL = reinterpret_cast<float*>(sO + BQ * LDT);
-  float* sD = sL + BQ;
-  const int kb = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
+  __nv_bfloat16* sQO = sV + BKV * LDT;  // [2 stages][Q | dO][64][LDT]
+  float* sLD = reinterpret_cast<float*>(sQO + 4 * BQB * LDT);  // [2 stages][lse | D][64]
+  const int nkb = s / BKV;
+  const int kb = blockIdx.x;  // light blocks last: kb = 0 has the most query blocks
+  const int head = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const long long ld = 3LL * n * D, ldo = (long long)n * D;
   const __nv_bfloat16* base = qkv + (long long)b * s * ld;
-  load_tile<D>(sK, base + (long long)kb * BKV * ld + n * D + head * D, ld, BKV);
-  load_tile<D>(sV, base + (long long)kb * BKV * ld + 2 * n * D + head * D, ld, BKV);
+  const float* Lrow = lse + ((long long)b * n + head) * s;
+  const float* Drow = dsum + ((long long)b * n + head) * s;
+  auto qo = [&](int stage, int which) { return sQO + (stage * 2 + which) * BQB * LDT; };
+  auto ldv = [&](int stage, int which) { return sLD + (stage * 2 + which) * BQB; };
+  auto issue = [&](int qb, int stage) {
+    load_tile_async<D>(qo(stage, 0), base + (long long)qb * BQB * ld + head * D, ld, BQB);
+    load_tile_async<D>(qo(stage, 1), dout + ((long long)b * s + qb * BQB) * ldo + head * D, ldo, BQB);
+    for (int i = threadIdx.x; i < BQB / 4; i += blockDim.x) {
+      cp_async16(ldv(stage, 0) + 4 * i, Lrow + qb * BQB + 4 * i);
+      cp_async16(ldv(stage, 1) + 4 * i, Drow + qb * BQB + 4 * i);
+    }
+  };
+  load_tile_async<D>(sK, base + (long long)kb * BKV * ld + n * D + head * D, ld, BKV);
+  load_tile_async<D>(sV, base + (long long)kb * BKV * ld + 2 * n * D + head * D, ld, BKV);
+  const int qb0 = (kb * BKV) / BQB;
+  issue(qb0, 0);
+  cp_commit();
 
   float dK[D / 8][4], dV[D / 8][4];
 #pragma unroll
@@ -247,19 +290,23 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
 #pragma unroll
     for (int e = 0; e < 4; ++e) dK[j][e] = dV[j][e] = 0.f;
   const float sl2 = scale * LOG2E;
-  const int key0 = kb * BKV + warp * 16 + g;  // key index of rows g / g+8
-  const float* Lrow = lse + ((long long)b * n + head) * s;
-  const float* Drow = dsum + ((long long)b * n + head) * s;
+  const int key0 = kb * BKV + warp * 16 + g;
+  const int nqb = s / BQB;
+  (void)nkb;
 
-  for (int qb = kb; qb < s / BQ; ++qb) {
+  for (int qb = qb0; qb < nqb; ++qb) {
+    const int stg = (qb - qb0) & 1;
+    if (qb + 1 < nqb) issue(qb + 1, stg ^ 1);
+    cp_commit();
+    cp_wait<1>();
     __syncthreads();
-    load_tile<D>(sQ, base + (long long)qb * BQ * ld + head * D, ld, BQ);
-    load_tile<D>(sO, dout + ((long long)b * s + qb * BQ) * ldo + head * D, ldo, BQ);
-    for (int i = threadIdx.x; i < BQ; i += blockDim.x) { sL[i] = Lrow[qb * BQ + i] * LOG2E; sD[i] = Drow[qb * BQ + i]; }
-    __syncthreads();
-    float S[BQ / 8][4], dP[BQ / 8][4];
+    const __nv_bfloat16* sQ = qo(stg, 0);
+    const __nv_bfloat16* sO = qo(stg, 1);
+    const float* sL = ldv(stg, 0);
+    const float* sD = ldv(stg, 1);
+    float S[BQB / 8][4], dP[BQB / 8][4];
 #pragma unroll
-    for (int j = 0; j < BQ / 8; ++j)
+    for (int j = 0; j < BQB / 8; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) S[j][e] = dP[j][e] = 0.f;
 #pragma unroll
@@ -268,7 +315,7 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
       frag_a<D>(sK, warp * 16, kk * 16, ka);
       frag_a<D>(sV, warp * 16, kk * 16, va);
 #pragma unroll
-      for (int jj = 0; jj < BQ / 16; ++jj) {
+      for (int jj = 0; jj < BQB / 16; ++jj) {
         uint32_t b00, b01, b10, b11;
         frag_b_nk<D>(sQ, jj * 16, kk * 16, b00, b01, b10, b11);
         mma16816(S[2 * jj], ka, b00, b01);
@@ -278,21 +325,21 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
         mma16816(dP[2 * jj + 1], va, b10, b11);
       }
     }
-    // P^T = exp(S^T * scale - lse[q]); dS^T = P^T * (dP^T - D[q])
+    const bool diag = qb * BQB < kb * BKV + BKV;
 #pragma unroll
-    for (int j = 0; j < BQ / 8; ++j) {
+    for (int j = 0; j < BQB / 8; ++j) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int qi = j * 8 + 2 * tq + (e & 1);
         const int key = key0 + (e >> 1) * 8;
-        float p = exp2f(S[j][e] * sl2 - sL[qi]);
-        if (qb == kb && key > qb * BQ + qi) p = 0.f;
+        float p = exp2f(S[j][e] * sl2 - sL[qi] * LOG2E);
+        if (diag && key > qb * BQB + qi) p = 0.f;
         S[j][e] = p;
         dP[j][e] = p * (dP[j][e] - sD[qi]);
       }
     }
 #pragma unroll
-    for (int kk = 0; kk < BQ / 16; ++kk) {
+    for (int kk = 0; kk < BQB / 16; ++kk) {
       uint32_t pa[4] = {pk(S[2 * kk][0], S[2 * kk][1]), pk(S[2 * kk][2], S[2 * kk][3]),
                         pk(S[2 * kk + 1][0], S[2 * kk + 1][1]), pk(S[2 * kk + 1][2], S[2 * kk + 1][3])};
       uint32_t da[4] = {pk(dP[2 * kk][0], dP[2 * kk][1]), pk(dP[2 * kk][2], dP[2 * kk][3]),
@@ -308,6 +355,7 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
         mma16816(dK[2 * jj + 1], da, b10, b11);
       }
     }
+    __syncthreads();
   }
   __nv_bfloat16* dK0 = dqkv + ((long long)b * s + key0) * ld + n * D + head * D;
   __nv_bfloat16* dV0 = dK0 + n * D;
@@ -321,23 +369,32 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
 }
 
 // ------------------------------------------------------------------ backward dQ
+// CTA = 4 warps x 16 queries; K/V tiles streamed with a 2-deep cp.async ring.
 template <int D>
 __global__ void __launch_bounds__(128)
 attn_bwd_dq_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ dout,
                    const float* __restrict__ lse, const float* __restrict__ dsum,
                    __nv_bfloat16* __restrict__ dqkv, float scale) {
+  constexpr int BQ = 64;
   extern __shared__ __align__(16) uint8_t sraw[];
   constexpr int LDT = Tile<D>::LD;
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(sraw);
   __nv_bfloat16* sO = sQ + BQ * LDT;
-  __nv_bfloat16* sK = sO + BQ * LDT;
-  __nv_bfloat16* sV = sK + BKV * LDT;
-  const int qb = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
+  __nv_bfloat16* sKV = sO + BQ * LDT;  // [2 stages][K | V][64][LDT]
+  const int nqb = s / BQ;
+  const int qb = nqb - 1 - blockIdx.x;  // heaviest first
+  const int head = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const long long ld = 3LL * n * D, ldo = (long long)n * D;
   const __nv_bfloat16* base = qkv + (long long)b * s * ld;
-  load_tile<D>(sQ, base + (long long)qb * BQ * ld + head * D, ld, BQ);
-  load_tile<D>(sO, dout + ((long long)b * s + qb * BQ) * ldo + head * D, ldo, BQ);
+  const __nv_bfloat16* Kg = base + n * D + head * D;
+  const __nv_bfloat16* Vg = Kg + n * D;
+  auto kv = [&](int stage, int which) { return sKV + (stage * 2 + which) * BKV * LDT; };
+  load_tile_async<D>(sQ, base + (long long)qb * BQ * ld + head * D, ld, BQ);
+  load_tile_async<D>(sO, dout + ((long long)b * s + qb * BQ) * ldo + head * D, ldo, BQ);
+  load_tile_async<D>(kv(0, 0), Kg, ld, BKV);
+  load_tile_async<D>(kv(0, 1), Vg, ld, BKV);
+  cp_commit();
   const float sl2 = scale * LOG2E;
   const int q0 = qb * BQ + warp * 16 + g;
   const float* Lrow = lse + ((long long)b * n + head) * s;
@@ -347,12 +404,19 @@ attn_bwd_dq_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __
   float dQ[D / 8][4];
 #pragma unroll
   for (int j = 0; j < D / 8; ++j) dQ[j][0] = dQ[j][1] = dQ[j][2] = dQ[j][3] = 0.f;
+  const int last_kb = ((qb + 1) * BQ - 1) / BKV;
 
-  for (int kb = 0; kb <= qb; ++kb) {
+  for (int kb = 0; kb <= last_kb; ++kb) {
+    const int stg = kb & 1;
+    if (kb + 1 <= last_kb) {
+      load_tile_async<D>(kv(stg ^ 1, 0), Kg + (long long)(kb + 1) * BKV * ld, ld, BKV);
+      load_tile_async<D>(kv(stg ^ 1, 1), Vg + (long long)(kb + 1) * BKV * ld, ld, BKV);
+    }
+    cp_commit();
+    cp_wait<1>();
     __syncthreads();
-    load_tile<D>(sK, base + (long long)kb * BKV * ld + n * D + head * D, ld, BKV);
-    load_tile<D>(sV, base + (long long)kb * BKV * ld + 2 * n * D + head * D, ld, BKV);
-    __syncthreads();
+    const __nv_bfloat16* sK = kv(stg, 0);
+    const __nv_bfloat16* sV = kv(stg, 1);
     float S[BKV / 8][4], dP[BKV / 8][4];
 #pragma unroll
     for (int j = 0; j < BKV / 8; ++j)
@@ -374,6 +438,7 @@ attn_bwd_dq_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __
         mma16816(dP[2 * jj + 1], oa, b10, b11);
       }
     }
+    const bool diag = kb == last_kb;
 #pragma unroll
     for (int j = 0; j < BKV / 8; ++j) {
 #pragma unroll
@@ -381,7 +446,7 @@ attn_bwd_dq_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __
         const int key = kb * BKV + j * 8 + 2 * tq + (e & 1);
         const int q = q0 + (e >> 1) * 8;
         float p = exp2f(S[j][e] * sl2 - ((e >> 1) ? L1 : L0));
-        if (kb == qb && key > q) p = 0.f;
+        if (diag && key > q) p = 0.f;
         dP[j][e] = p * (dP[j][e] - ((e >> 1) ? D1 : D0));
       }
     }
@@ -397,6 +462,7 @@ attn_bwd_dq_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __
         mma16816(dQ[2 * jj + 1], da, b10, b11);
       }
     }
+    __syncthreads();
   }
   __nv_bfloat16* dQ0 = dqkv + ((long long)b * s + q0) * ld + head * D;
 #pragma unroll
@@ -406,13 +472,25 @@ attn_bwd_dq_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __
   }
 }
 
+constexpr int FWD_NW = 8;  // 128 queries per forward CTA
+
 template <int D>
 cudaError_t fwd_impl(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st) {
-  const int smem = (BQ + 2 * BKV) * Tile<D>::LD * 2;
-  auto k = attn_fwd_kernel<D>;
+  constexpr int BQ = FWD_NW * 16;
+  if (s % BQ) {
+    // short sequences: 64-query CTAs
+    constexpr int smem = (64 + 4 * BKV) * Tile<D>::BYTES;
+    auto k = attn_fwd_kernel<D, 4>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k<<<dim3(s / 64, n, nb), 128, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse,
+                                              rsqrtf((float)D)); count_launch();
+    return cudaGetLastError();
+  }
+  constexpr int smem = (BQ + 4 * BKV) * Tile<D>::BYTES;
+  auto k = attn_fwd_kernel<D, FWD_NW>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  dim3 grid(s / BQ, n, nb);
-  k<<<grid, 128, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse, rsqrtf((float)D)); count_launch();
+  k<<<dim3(s / BQ, n, nb), FWD_NW * 32, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse,
+                                                    rsqrtf((float)D)); count_launch();
   return cudaGetLastError();
 }
 
@@ -423,24 +501,24 @@ cudaError_t bwd_impl(int nb, int s, int n, const void* qkv, const void* o, const
   dim3 pblk(32, 8);
   attn_dsum_kernel<D><<<(unsigned)((T * n + 7) / 8), pblk, 0, st>>>(s, n, (const __nv_bfloat16*)o,
                                                                      (const __nv_bfloat16*)dout, dsum, T); count_launch();
-  const int smem = (BQ + BKV) * 2 * Tile<D>::LD * 2 + 2 * BQ * 4;
+  const int smem1 = (2 * BKV + 4 * BQB) * Tile<D>::BYTES + 4 * BQB * 4;
+  const int smem2 = (2 * 64 + 4 * BKV) * Tile<D>::BYTES;
   auto k1 = attn_bwd_dkv_kernel<D>;
   auto k2 = attn_bwd_dq_kernel<D>;
-  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  dim3 grid(s / BQ, n, nb);
+  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
+  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
   const float scale = rsqrtf((float)D);
-  k1<<<grid, 128, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse, dsum,
-                              (__nv_bfloat16*)dqkv, scale); count_launch();
-  k2<<<grid, 128, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse, dsum,
-                              (__nv_bfloat16*)dqkv, scale); count_launch();
+  k1<<<dim3(s / BKV, n, nb), 128, smem1, st>>>(s, n, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse,
+                                               dsum, (__nv_bfloat16*)dqkv, scale); count_launch();
+  k2<<<dim3(s / 64, n, nb), 128, smem2, st>>>(s, n, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse,
+                                              dsum, (__nv_bfloat16*)dqkv, scale); count_launch();
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o, float* lse, cudaStream_t st) {
-  if (s % BQ) return cudaErrorInvalidValue;
+  if (s % 64) return cudaErrorInvalidValue;
   switch (d) {
     case 32: return fwd_impl<32>(nb, s, n, qkv, o, lse, st);
     case 64: return fwd_impl<64>(nb, s, n, qkv, o, lse, st);
@@ -451,7 +529,7 @@ cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o,
 
 cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const void* o, const float* lse,
                           const void* dout, void* dqkv, float* dsum, cudaStream_t st) {
-  if (s % BQ) return cudaErrorInvalidValue;
+  if (s % 64) return cudaErrorInvalidValue;
   switch (d) {
     case 32: return bwd_impl<32>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);
     case 64: return bwd_impl<64>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);

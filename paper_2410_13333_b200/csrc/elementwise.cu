@@ -183,13 +183,24 @@ rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x
   }
 }
 
-// dg[c] += sum_b part[b][c], b in fixed order (deterministic)
-__global__ void colsum_accum_kernel(int nb, int h, const float* __restrict__ part, float* __restrict__ dg) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= h) return;
+// dg[c] += sum_b part[b][c] in a fixed order (deterministic): block = 32 columns x 8 warps, warp w
+// sums rows w, w+8, ... (lane = column, coalesced), then the 8 warp sums are added in warp order.
+__global__ void __launch_bounds__(256) colsum_accum_kernel(int nb, int h, const float* __restrict__ part,
+                                                           float* __restrict__ dg) {
+  __shared__ float sh[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int b = 0; b < nb; ++b) s += part[(long long)b * h + c];
-  dg[c] += s;
+  if (c < h)
+    for (int b = w; b < nb; b += 8) s += part[(long long)b * h + c];
+  sh[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < h) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += sh[i][lane];
+    dg[c] += t;
+  }
 }
 
 constexpr int BWD_BLOCKS = 296;  // 2 per SM
@@ -209,27 +220,41 @@ __global__ void residual_add_kernel(long long nv, const uint4* __restrict__ x, c
 // ---------------------------------------------------------------- RoPE (half-split, reading R3)
 // buf row t: columns [col0 + j*d, col0 + (j+1)*d) is head j; pairs (i, i + d/2); pos = t % s.
 // Applied to q (col0 = 0) and k (col0 = n*d) by blockIdx.y.
+// One thread per (token, group of 8 consecutive pair indices i): the 8 angles are computed once and
+// reused for every head of q and k (2n heads); 128-bit loads of both halves of each head.
 __global__ void rope_kernel(int T, int s, int n, int d, __nv_bfloat16* __restrict__ buf, long long ld,
                             int col0, float log2_theta, float sign) {
   const int half = d / 2;
-  const long long total = (long long)T * n * half;
-  const int which = blockIdx.y;  // 0: q block, 1: k block
+  const int groups = half / 8;
+  const long long total = (long long)T * groups;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = idx % half;
-    const long long th = idx / half;
-    const int j = th % n;
-    const int t = th / n;
-    const int pos = t % s;
-    const float inv = exp2f(-(2.f * i / (float)d) * log2_theta);
-    float sn, cs;
-    sincosf((float)pos * inv, &sn, &cs);
-    sn *= sign;
-    __nv_bfloat16* p = buf + (long long)t * ld + col0 + which * n * d + j * d;
-    const float a = __bfloat162float(p[i]);
-    const float b = __bfloat162float(p[i + half]);
-    p[i] = __float2bfloat16_rn(a * cs - b * sn);
-    p[i + half] = __float2bfloat16_rn(b * cs + a * sn);
+    const int gi = idx % groups;
+    const long long t = idx / groups;
+    const int pos = (int)(t % s);
+    float cs[8], sn[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = gi * 8 + u;
+      const float inv = exp2f(-(2.f * i / (float)d) * log2_theta);
+      sincosf((float)pos * inv, &sn[u], &cs[u]);
+      sn[u] *= sign;
+    }
+    __nv_bfloat16* row = buf + t * ld + col0;
+    for (int j = 0; j < 2 * n; ++j) {  // q heads then k heads
+      uint4* p1 = reinterpret_cast<uint4*>(row + j * d + gi * 8);
+      uint4* p2 = reinterpret_cast<uint4*>(row + j * d + half + gi * 8);
+      float a[8], b[8], o1[8], o2[8];
+      unpack8(*p1, a);
+      unpack8(*p2, b);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        o1[u] = a[u] * cs[u] - b[u] * sn[u];
+        o2[u] = b[u] * cs[u] + a[u] * sn[u];
+      }
+      *p1 = pack8(o1);
+      *p2 = pack8(o2);
+    }
   }
 }
 
@@ -396,7 +421,7 @@ cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float*
   int nb = (T + rpb - 1) / rpb;
   rmsnorm_bwd_kernel<<<nb, NORM_THREADS, 0, st>>>(T, h, rpb, (const uint4*)x, (const uint4*)g, rstd,
                                                   (const float4*)dy, (const uint4*)dres, (uint4*)dx_out, scratch); count_launch();
-  colsum_accum_kernel<<<(h + 255) / 256, 256, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
+  colsum_accum_kernel<<<(h + 31) / 32, 256, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
   return cudaGetLastError();
 }
 
@@ -408,9 +433,10 @@ cudaError_t residual_add(long long n, const void* x, const float* partial, void*
 
 cudaError_t rope_inplace(int T, int s, int n, int d, void* buf, long long ld, int col0, float theta,
                          bool inverse, cudaStream_t st) {
-  long long total = (long long)T * n * (d / 2);
-  dim3 grid(grid_for(total, 256), 2);
-  rope_kernel<<<grid, 256, 0, st>>>(T, s, n, d, (__nv_bfloat16*)buf, ld, col0, log2f(theta), inverse ? -1.f : 1.f); count_launch();
+  if (d % 16 || ld % 8 || col0 % 8) return cudaErrorInvalidValue;
+  long long total = (long long)T * (d / 16);
+  rope_kernel<<<grid_for(total, 128), 128, 0, st>>>(T, s, n, d, (__nv_bfloat16*)buf, ld, col0, log2f(theta),
+                                                    inverse ? -1.f : 1.f); count_launch();
   return cudaGetLastError();
 }
 

@@ -60,6 +60,8 @@ struct PieceDesc {
   float w[MAX_DP];           // w_i = m_i b / B
   int n_src;
   int decay;                 // apply weight decay (2-D tensors)
+  int vec;                   // all pointers 16-byte aligned (param 8-byte), len % 4 == 0
+  int pad_;
   float* master;
   float* m;
   float* v;
@@ -74,7 +76,7 @@ struct ChunkDesc {
 struct AdamHyper {
   float lr, b1, b2, eps, wd;
   float bc1, bc2;  // 1 - b1^t, 1 - b2^t
-  int apply;
+  int apply;       // 0 reduce only, 1 reduce + AdamW (+ rgrad), 2 AdamW without storing rgrad
 };
 cudaError_t reduce_adam(int n_chunks, const ChunkDesc* d_chunks, const PieceDesc* d_pieces,
                         const AdamHyper& hp, cudaStream_t st);

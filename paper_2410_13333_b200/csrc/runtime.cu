@@ -242,7 +242,7 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
       for (const Piece& pc : s.owned)
         for (size_t i = 0; i < L.plan.pipes.size(); ++i) {
           if (L.plan.pipes[i].n_micro <= 0) continue;
-          if (sync_holder(cfg, L.plan.pipes[i], s.t, pc.row0) != rank) stage_elems += pc.e1 - pc.e0;
+          if (sync_holder(cfg, L.plan.pipes[i], s.t, pc.row0) != rank) stage_elems += (pc.e1 - pc.e0 + 3) / 4 * 4;
         }
   }
   L.staging_elems = stage_elems;
@@ -346,7 +346,7 @@ static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
             pd.src[pd.n_src] = s.grad + (pc.e0 - s.rows.b * c);
           } else {
             float* dst = L.staging + stage_off;
-            stage_off += len;
+            stage_off += (len + 3) / 4 * 4;  // keep every slot 16-byte aligned
             L.gops.push_back({dst, (size_t)len, ncclFloat, hld, false});
             pd.src[pd.n_src] = dst;
           }
@@ -381,6 +381,10 @@ static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
         pd.v = s.v + off;
         pd.rgrad = s.rgrad + off;
         pd.param = s.param + (pc.e0 - s.rows.b * c);
+        bool vec = (len % 4 == 0) && ((uintptr_t)pd.param % 8 == 0);
+        for (uintptr_t q : {(uintptr_t)pd.master, (uintptr_t)pd.m, (uintptr_t)pd.v, (uintptr_t)pd.rgrad}) vec &= q % 16 == 0;
+        for (int k = 0; k < pd.n_src; ++k) vec &= (uintptr_t)pd.src[k] % 16 == 0;
+        pd.vec = vec ? 1 : 0;
         const int pid = (int)L.pieces.size();
         L.pieces.push_back(pd);
         const int64_t CH = 8192;
