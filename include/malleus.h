@@ -244,6 +244,11 @@ malleus_status malleus_k_gemm(int32_t M, int32_t N, int32_t K, const void* A, in
                               int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, void* C,
                               int64_t ldc, int32_t mode, void* stream);
 
+/* GEMM kernel selection for all subsequent GEMMs (tests / benchmarks): 0 = automatic (CTA pair,
+ * tcgen05.mma.cta_group::2 with 256x256 tiles, when M >= 256; single CTA 128x256 otherwise),
+ * 1 = always single CTA, 2 = always CTA pair. */
+malleus_status malleus_k_gemm_variant(int32_t variant);
+
 /* y = x * rsqrt(mean(x^2) + eps) * g; optional fused residual: if partial != NULL then
  * x_new = bf16(x + partial) is written to x_out and normalised.  x, x_out, y: bf16 [T, h];
  * partial: fp32 [T, h] or NULL; g: bf16 [h]; rstd: fp32 [T]. */

@@ -52,6 +52,57 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   tn = r / gsz;
 }
 
+// Epilogue of one 256-column accumulator for one row per thread: TMEM (32 lanes x 32 columns per
+// tcgen05.ld) -> registers -> bf16 / fp32 store or fp32 read-add-write (wgrad accumulation).
+__device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t taddr, int row, int col_base) {
+  const bool row_ok = row < p.M;
+#pragma unroll 1
+  for (int c = 0; c < 256 / 32; ++c) {
+    const int col0 = col_base + c * 32;
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+    if (!row_ok || col0 >= p.N) continue;
+    const bool full_chunk = p.vec_ok && col0 + 32 <= p.N;
+    if (p.mode == GEMM_STORE_BF16) {
+      __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)row * p.ldc + col0;
+      if (full_chunk) {
+        uint4* dst = reinterpret_cast<uint4*>(C);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
+          w.y = pack_bf16(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
+          w.z = pack_bf16(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
+          w.w = pack_bf16(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+          dst[v] = w;
+        }
+      } else {
+        for (int j = 0; j < 32 && col0 + j < p.N; ++j) C[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+      }
+    } else {
+      float* C = reinterpret_cast<float*>(p.C) + (long long)row * p.ldc + col0;
+      const bool accum = p.mode == GEMM_ACCUM_F32;
+      if (full_chunk) {
+        float4* dst = reinterpret_cast<float4*>(C);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          float4 w = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                 __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+          if (accum) {
+            float4 o = dst[v];
+            w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+          }
+          dst[v] = w;
+        }
+      } else {
+        for (int j = 0; j < 32 && col0 + j < p.N; ++j)
+          C[j] = accum ? C[j] + __uint_as_float(r[j]) : __uint_as_float(r[j]);
+      }
+    }
+  }
+}
+
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -155,52 +206,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = tm * BM + quarter * 32 + lane;
-      const bool row_ok = row < p.M;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        const int col0 = tn * BN + c * 32;
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, r);
-        tmem_wait_ld();
-        if (!row_ok || col0 >= p.N) continue;
-        const bool full_chunk = p.vec_ok && col0 + 32 <= p.N;
-        if (p.mode == GEMM_STORE_BF16) {
-          __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)row * p.ldc + col0;
-          if (full_chunk) {
-            uint4* dst = reinterpret_cast<uint4*>(C);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 w;
-              w.x = pack_bf16(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
-              w.y = pack_bf16(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
-              w.z = pack_bf16(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
-              w.w = pack_bf16(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
-              dst[v] = w;
-            }
-          } else {
-            for (int j = 0; j < 32 && col0 + j < p.N; ++j) C[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
-          }
-        } else {
-          float* C = reinterpret_cast<float*>(p.C) + (long long)row * p.ldc + col0;
-          const bool accum = p.mode == GEMM_ACCUM_F32;
-          if (full_chunk) {
-            float4* dst = reinterpret_cast<float4*>(C);
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              float4 w = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                     __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-              if (accum) {
-                float4 o = dst[v];
-                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
-              }
-              dst[v] = w;
-            }
-          } else {
-            for (int j = 0; j < 32 && col0 + j < p.N; ++j)
-              C[j] = accum ? C[j] + __uint_as_float(r[j]) : __uint_as_float(r[j]);
-          }
-        }
-      }
+      epilogue_tile(p, tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN, row, tn * BN);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -210,6 +216,135 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ------------------------------------------------------------------ CTA-pair variant (cta_group::2)
+// A cluster of 2 CTAs on one TPC computes a 256 x 256 tile with UMMA M=256 (tcgen05.mma.cta_group::2
+// issued by the even CTA): each CTA stages its own 128 rows of A and 128 rows (N) of B, so per SM the
+// smem operand traffic per MMA drops by a third and each B tile is fetched from L2 once per pair.
+// Both CTAs' TMA loads complete on the leader's full barrier; the leader's commits multicast to
+// both CTAs' empty / TMEM-full barriers; both epilogues arrive on the leader's TMEM-empty barrier.
+constexpr int BM2 = 128, BN2 = 256, STAGES2 = 6;
+constexpr int A2_BYTES = BM2 * BK * 2;            // 16 KB
+constexpr int B2_BYTES = (BN2 / 2) * BK * 2;      // 16 KB (this CTA's half of N)
+constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 1024;
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2] (leader's copy is the one used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int tiles_m = (p.M + 2 * BM2 - 1) / (2 * BM2);
+  const int tiles_n = (p.N + BN2 - 1) / BN2;
+  const int n_tiles = tiles_m * tiles_n;
+  const int n_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0; uint32_t phase = 0;
+      for (int t = cid; t < n_tiles; t += ncl) {
+        int tm, tn; tile_coords(t, tiles_m, tiles_n, tm, tn);
+        const int m0 = tm * 2 * BM2 + rank * BM2, n0 = tn * BN2 + rank * (BN2 / 2);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE2_BYTES;
+          uint8_t* sb = sa + A2_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE2_BYTES);
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d_2sm(sa, &tmA, &full[stage], k0, m0);
+          } else {
+            tma_load_2d_2sm(sa, &tmA, &full[stage], m0, k0);
+            tma_load_2d_2sm(sa + 8192, &tmA, &full[stage], m0 + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d_2sm(sb, &tmB, &full[stage], k0, n0);
+          } else {
+            tma_load_2d_2sm(sb, &tmB, &full[stage], n0, k0);
+            tma_load_2d_2sm(sb + 8192, &tmB, &full[stage], n0 + 64, k0);
+          }
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM2, BN2, A_MN, B_MN);
+      int stage = 0; uint32_t phase = 0; int it = 0;
+      for (int t = cid; t < n_tiles; t += ncl, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN2;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE2_BYTES);
+          const uint32_t sb = sa + A2_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad, bd;
+            if (!A_MN) ad = umma_desc_sw128(sa + k * 32, 16, 1024);
+            else       ad = umma_desc_sw128(sa + k * 2048, 8192, 1024);
+            if (!B_MN) bd = umma_desc_sw128(sb + k * 32, 16, 1024);
+            else       bd = umma_desc_sw128(sb + k * 2048, 8192, 1024);
+            umma_f16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit_2sm_mc(&empty[stage]);
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_2sm_mc(&tfull[acc]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    int it = 0;
+    for (int t = cid; t < n_tiles; t += ncl, ++it) {
+      int tm, tn; tile_coords(t, tiles_m, tiles_n, tm, tn);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * 2 * BM2 + rank * BM2 + quarter * 32 + lane;
+      epilogue_tile(p, tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN2, row, tn * BN2);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem_base, 512);
   }
 }
 
@@ -313,6 +448,45 @@ static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
   return cudaGetLastError();
 }
 
+static int g_variant = 0;  // 0 auto, 1 single-CTA, 2 CTA pair
+void gemm_set_variant(int v) { g_variant = v; }
+
+template <bool A_MN, bool B_MN>
+static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
+  static bool attr_set = false;
+  auto kern = gemm_tcgen05_2sm_kernel<A_MN, B_MN>;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM2_SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (!g_num_sms) {
+    int dev; cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = ((p.M + 2 * BM2 - 1) / (2 * BM2)) * ((p.N + BN2 - 1) / BN2);
+  const int sms = (g_avail_sms > 0 && g_avail_sms < g_num_sms) ? g_avail_sms : g_num_sms;
+  const int clusters = tiles < sms / 2 ? tiles : sms / 2;
+  const int grid = 2 * (clusters > 0 ? clusters : 1);
+  const bool prof = g_prof.on;
+  if (prof) {
+    if (g_prof.used == g_prof.ev.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      g_prof.ev.push_back({a, b});
+    }
+    cudaEventRecord(g_prof.ev[g_prof.used].first, st);
+  }
+  kern<<<grid, GEMM_THREADS, GEMM2_SMEM, st>>>(ta, tb, p); count_launch();
+  if (prof) {
+    cudaEventRecord(g_prof.ev[g_prof.used].second, st);
+    g_prof.flops.push_back(2.0 * p.M * (double)p.N * p.K);
+    g_prof.used++;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
   cudaError_t e = get_encoder();
@@ -320,6 +494,20 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
   if ((g.lda % 8) || (g.ldb % 8) || (g.ldc % 4) ||
       (reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15))
     return cudaErrorInvalidValue;
+  const bool pair = g_variant == 2 || (g_variant == 0 && g.M >= 256);
+  if (pair) {
+    CUtensorMap ta, tb;
+    bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.lda, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, BM2);
+    ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, BN2 / 2));
+    if (!ok) return cudaErrorInvalidValue;
+    const int esz = g.mode == GEMM_STORE_BF16 ? 2 : 4;
+    const int vec_ok = ((g.ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0);
+    GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok};
+    if (!g.a_mn && !g.b_mn) return launch2<false, false>(ta, tb, p, st);
+    if (!g.a_mn && g.b_mn) return launch2<false, true>(ta, tb, p, st);
+    if (g.a_mn && g.b_mn) return launch2<true, true>(ta, tb, p, st);
+    return launch2<true, false>(ta, tb, p, st);
+  }
   CUtensorMap ta, tb;
   bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.lda, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, BM);
   ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, BN));

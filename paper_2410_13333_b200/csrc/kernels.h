@@ -9,6 +9,7 @@ namespace mls {
 void count_launch(int n = 1);
 long long launches_total();
 void gemm_profile_enable(bool on);
+void gemm_set_variant(int v);
 cudaError_t gemm_profile_query(long long* launches, double* flops, double* ms);
 
 enum { GEMM_STORE_BF16 = 0, GEMM_STORE_F32 = 1, GEMM_ACCUM_F32 = 2 };

@@ -139,6 +139,33 @@ class Engine:
     def set_slowdown(self, x: float, mode: int = 1):
         check(L.lib.malleus_set_slowdown(self.ctx, float(x), int(mode)), self.ctx, "set_slowdown")
 
+    def calibrate_slowdown(self, slow_rank: int, x_target: float, mode: int = 1, iters: int = 10, tol: float = 0.05,
+                           max_rounds: int = 8):
+        """Collective.  Reading R13: inject on `slow_rank` until the probe measures
+        x = t_slow / t_ref within `tol` of x_target; t_ref = median probe of the other ranks (or the
+        rank's own uninjected probe on one GPU).  Returns (nominal x used, measured x)."""
+        if self.rank == slow_rank:
+            self.set_slowdown(1.0, 0)
+        base = self.probe(iters)
+        t_ref_self = base[slow_rank]
+        lo, hi, nominal = 1.0, max(2.0, 4.0 * x_target), x_target
+        measured = 1.0
+        for _ in range(max_rounds):
+            if self.rank == slow_rank:
+                self.set_slowdown(nominal, mode)
+            t = self.probe(iters)
+            others = [v for i, v in enumerate(t) if i != slow_rank]
+            t_ref = sorted(others)[len(others) // 2] if others else t_ref_self
+            measured = t[slow_rank] / t_ref
+            if abs(measured / x_target - 1.0) <= tol:
+                break
+            if measured < x_target:
+                lo = nominal
+            else:
+                hi = nominal
+            nominal = 0.5 * (lo + hi)
+        return nominal, measured
+
     def close(self):
         if self.ctx:
             L.lib.malleus_destroy(self.ctx)

@@ -45,9 +45,17 @@ SHAPES = [(128, 256, 64), (256, 512, 1024), (200, 304, 136), (96, 48, 2048), (10
           (2048, 2304, 4096)]
 
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+def variant(request, L):
+    """1: single-CTA 128x256 tiles; 2: CTA pair (tcgen05.mma.cta_group::2) 256x256 tiles."""
+    assert L.lib.malleus_k_gemm_variant(request.param) == 0
+    yield request.param
+    L.lib.malleus_k_gemm_variant(0)
+
+
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_gemm_small_int_bitwise(L, a_mn, b_mn, shape):
+def test_gemm_small_int_bitwise(L, variant, a_mn, b_mn, shape):
     M, N, K = shape
     A = small_int_matrix((M, K), 8, seed=M + K)
     B = small_int_matrix((K, N), 8, seed=N + 7 * K)
@@ -64,7 +72,7 @@ def test_gemm_small_int_bitwise(L, a_mn, b_mn, shape):
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
-def test_gemm_random_tolerance(L, a_mn, b_mn):
+def test_gemm_random_tolerance(L, variant, a_mn, b_mn):
     M, N, K = 1536, 1000, 4096
     A = torch.tensor(normal_matrix((M, K), 1)).to(torch.bfloat16).float().numpy()
     B = torch.tensor(normal_matrix((K, N), 2)).to(torch.bfloat16).float().numpy()

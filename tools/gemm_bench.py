@@ -27,3 +27,15 @@ for name, M, N, K, amn, bmn in shapes:
     ref = bench(lambda: torch.matmul(At, Bt))
     err = (C.float() - torch.matmul(At, Bt).float()).abs().max().item()
     print(f"{name:10s} M={M} N={N} K={K}: malleus {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:7.1f} TF | cublas {ref*1e3:8.1f} us {2*M*N*K/ref/1e9:7.1f} TF | maxdiff {err:.3g}", flush=True)
+
+# CTA-pair vs single-CTA on the same shapes
+for var in (1, 2):
+    L.lib.malleus_k_gemm_variant(var)
+    for name, M, N, K, amn, bmn in shapes:
+        A = torch.randn(K, M, device="cuda").to(torch.bfloat16) if amn else torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        B = torch.randn(K, N, device="cuda").to(torch.bfloat16) if bmn else torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        f = lambda: L.lib.malleus_k_gemm(M, N, K, A.data_ptr(), A.shape[1], amn, B.data_ptr(), B.shape[1], bmn, C.data_ptr(), N, 0, st)
+        ms = bench(f)
+        print(f"variant {var} {name:10s}: {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:7.1f} TF", flush=True)
+L.lib.malleus_k_gemm_variant(0)
