@@ -186,7 +186,7 @@ def main():
     dtok = torch.tensor(tok, device="cuda")
     dtgt = torch.tensor(tgt, device="cuda")
     if straggle and straggle[0] == rank:
-        eng.set_slowdown(straggle[1], 1)
+        eng.set_slowdown(straggle[1], 2)  # DUTY: compute segments stretched x-fold on this rank
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -268,7 +268,7 @@ def main():
                 "config": {"workload": "C2: LLaMA-7B-shaped 4-layer slice (h 4096, 32 heads, ffn 11008, V 32000)",
                            "global_batch": B, "seq_len": cfg.seq_len, "micro_batch": 1,
                            "plan": plan_summary(plan), "straggler": (
-                               {"rank": straggle[0], "x": straggle[1], "mode": "HOG"} if straggle else None),
+                               {"rank": straggle[0], "x": straggle[1], "mode": "DUTY"} if straggle else None),
                            "l2": "working set >> 126 MB L2 (no flush needed)"},
                 "step_tflops": step_tf,
                 "roofline": roof,

@@ -111,9 +111,10 @@ typedef struct {
 } malleus_adam_cfg;
 
 typedef struct {
-  uint64_t bytes_sent, bytes_recv; /* this rank */
-  double seconds;                  /* wall, this rank, excluding the final barrier */
+  uint64_t bytes_sent, bytes_recv; /* this rank, payload bytes of the shard deltas */
+  double seconds;                  /* wall, this rank: data movement (keep-copies, pack, NCCL, unpack) */
   int32_t n_packs;                 /* 4-layer packs */
+  double total_seconds;            /* wall, this rank, including host planning and comm split */
 } malleus_migrate_stats;
 
 typedef struct malleus_ctx malleus_ctx;

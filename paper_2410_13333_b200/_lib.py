@@ -69,7 +69,7 @@ class AdamCfg(C.Structure):
 
 class MigrateStats(C.Structure):
     _fields_ = [("bytes_sent", C.c_uint64), ("bytes_recv", C.c_uint64), ("seconds", C.c_double),
-                ("n_packs", i32)]
+                ("n_packs", i32), ("total_seconds", C.c_double)]
 
 
 _SIGS = {

@@ -89,6 +89,14 @@ cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const vo
                           const float* lse, const void* dout, void* dqkv, float* dsum,
                           cudaStream_t st);
 
+// ---- multi-range copy (copy.cu): migration pack / unpack / keep-copies
+struct CopyDesc {
+  const char* src;
+  char* dst;
+  long long bytes;  // <= 64 KB per descriptor (host splits longer ranges)
+};
+cudaError_t copy_ranges(int n, const CopyDesc* d_desc, cudaStream_t st);
+
 // ---- probe / straggler emulation (probe.cu)
 cudaError_t spin_ns(long long ns, cudaStream_t st);
 cudaError_t hog_start(int n_sms, volatile int* stop_flag, cudaStream_t st);

@@ -114,6 +114,14 @@ struct Bump {
   }
 };
 
+constexpr int kDutySegs = 16, kDutyRing = 64;
+struct DutyTimer {
+  bool init = false;
+  cudaEvent_t b[kDutyRing], e[kDutyRing];
+  long long head = 0, tail = 0;
+  double ms = -1.0;
+};
+
 }  // namespace
 
 struct malleus_ctx {
@@ -127,6 +135,8 @@ struct malleus_ctx {
   int* hog_flag = nullptr;      // host-mapped
   float slowdown = 1.f;
   int slow_mode = 0;
+  DutyTimer duty[kDutySegs];
+  int cur_seg = -1;
   // timing
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
   std::vector<int> ev_cat;
@@ -467,8 +477,12 @@ static malleus_status gemm(malleus_ctx* ctx, int M, int N, int K, const void* A,
   return MALLEUS_OK;
 }
 
+static void duty_begin(malleus_ctx* ctx, int seg, cudaStream_t st);
+static void duty_end(malleus_ctx* ctx, cudaStream_t st);
+
 static malleus_status tp_allreduce(malleus_ctx* ctx, float* buf, size_t n, ncclRedOp_t op, cudaStream_t st) {
   Layout& L = *ctx->L;
+  duty_end(ctx, st);
   if (L.TP <= 1) return MALLEUS_OK;
   ev_begin(ctx, st, CAT_TP);
   NK(ncclAllReduce(buf, buf, n, ncclFloat, op, L.tp_comm, st));
@@ -476,8 +490,37 @@ static malleus_status tp_allreduce(malleus_ctx* ctx, float* buf, size_t n, ncclR
   return MALLEUS_OK;
 }
 
-static void slow_spin(malleus_ctx* ctx, cudaStream_t st, double base_ns) {
-  if (ctx->slow_mode == 2 && ctx->slowdown > 1.f) spin_ns((long long)((ctx->slowdown - 1.f) * base_ns), st);
+// DUTY straggler emulation: every compute segment (the kernels between two TP collectives) is
+// bracketed by CUDA events; after it a spin kernel of (x - 1) * t_segment is enqueued on the same
+// stream, where t_segment is a moving average of that segment's own measured duration (events are
+// polled without blocking).  Only compute is stretched, not communication, as with a GPU that is
+// x times slower (PAPER.md:400-401 defines x as the slowdown vs a normal GPU).
+static void duty_begin(malleus_ctx* ctx, int seg, cudaStream_t st) {
+  if (ctx->slow_mode != 2 || ctx->slowdown <= 1.f) return;
+  DutyTimer& d = ctx->duty[seg % kDutySegs];
+  if (!d.init) {
+    for (int i = 0; i < kDutyRing; ++i) { cudaEventCreate(&d.b[i]); cudaEventCreate(&d.e[i]); }
+    d.init = true;
+  }
+  if (d.head - d.tail >= kDutyRing) {  // ring full: wait for the oldest
+    cudaEventSynchronize(d.e[d.tail % kDutyRing]);
+  }
+  cudaEventRecord(d.b[d.head % kDutyRing], st);
+  ctx->cur_seg = seg;
+}
+static void duty_end(malleus_ctx* ctx, cudaStream_t st) {
+  if (ctx->slow_mode != 2 || ctx->slowdown <= 1.f || ctx->cur_seg < 0) return;
+  DutyTimer& d = ctx->duty[ctx->cur_seg % kDutySegs];
+  cudaEventRecord(d.e[d.head % kDutyRing], st);
+  d.head++;
+  while (d.tail < d.head && cudaEventQuery(d.e[d.tail % kDutyRing]) == cudaSuccess) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, d.b[d.tail % kDutyRing], d.e[d.tail % kDutyRing]);
+    d.ms = d.ms < 0 ? ms : 0.7 * d.ms + 0.3 * ms;
+    d.tail++;
+  }
+  if (d.ms > 0) spin_ns((long long)((ctx->slowdown - 1.0) * d.ms * 1e6), st);
+  ctx->cur_seg = -1;
 }
 
 static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStream_t st) {
@@ -487,18 +530,22 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   Slot& S = L.slot[si];
   SlotLayer& Y = S.L[li];
   LayerPtrs& P = L.lp[li];
+  duty_begin(ctx, 0, st);
   CK(rmsnorm_fwd(T, h, S.x[li], nullptr, nullptr, P.g1, c.rms_eps, Y.a1, Y.r1, st));
   RET(gemm(ctx, T, 3 * nd, h, Y.a1, h, false, P.wqkv, h, false, Y.qkv, 3 * nd, GEMM_STORE_BF16, st));
   CK(rope_inplace(T, c.seq_len, L.n_loc, d, Y.qkv, 3LL * nd, 0, c.rope_theta, false, st));
   CK(attention_fwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
   RET(gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, L.part, h, GEMM_STORE_F32, st));
   RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  duty_begin(ctx, 1, st);
   CK(rmsnorm_fwd(T, h, S.x[li], L.part, Y.x1, P.g2, c.rms_eps, Y.a2, Y.r2, st));
   RET(gemm(ctx, T, 2 * F, h, Y.a2, h, false, P.wgu, h, false, Y.gu, 2 * F, GEMM_STORE_BF16, st));
   CK(swiglu_fwd(T, F, Y.gu, Y.u, st));
   RET(gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, L.part, h, GEMM_STORE_F32, st));
   RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  duty_begin(ctx, 2, st);
   CK(residual_add((long long)T * h, Y.x1, L.part, S.x[li + 1], st));
+  duty_end(ctx, st);
   return MALLEUS_OK;
 }
 
@@ -514,12 +561,14 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   const int wm = first ? GEMM_STORE_F32 : GEMM_ACCUM_F32;
   uint16_t* dx1 = L.dxc;
   // MLP
+  duty_begin(ctx, 3, st);
   RET(gemm(ctx, T, F, h, dy, h, false, P.wd, h, false, L.du, F, GEMM_STORE_BF16, st));
   RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
   CK(swiglu_bwd(T, F, Y.gu, L.du, L.dgu, st));
   RET(gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, L.part, h, GEMM_STORE_F32, st));
   RET(gemm(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
   RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  duty_begin(ctx, 4, st);
   CK(rmsnorm_bwd(T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st));
   // attention
   RET(gemm(ctx, T, nd, h, dx1, h, false, P.wo, h, false, L.dout, nd, GEMM_STORE_BF16, st));
@@ -529,7 +578,9 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, L.part, h, GEMM_STORE_F32, st));
   RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
   RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  duty_begin(ctx, 5, st);
   CK(rmsnorm_bwd(T, h, S.x[li], P.g1, Y.r1, L.part, dx1, dx, P.dg1, L.scratch, st));
+  duty_end(ctx, st);
   return MALLEUS_OK;
 }
 
@@ -540,6 +591,7 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
   const int T = L.T, h = c.hidden, V = L.V_loc;
   Slot& S = L.slot[si];
   const PipeInfo& pp = L.plan.pipes[L.pipe];
+  duty_begin(ctx, 6, st);
   CK(rmsnorm_fwd(T, h, S.x[L.n_local], nullptr, nullptr, L.gf, c.rms_eps, S.xf, S.rf, st));
   RET(gemm(ctx, T, V, h, S.xf, h, false, L.Wlm, h, false, L.logits, V, GEMM_STORE_F32, st));
   CK(ce_stats(T, V, L.logits, tgt, L.v0, L.stats, st));
@@ -547,6 +599,7 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
   RET(tp_allreduce(ctx, L.gmax, (size_t)T, ncclMax, st));
   CK(ce_local_sum(T, L.stats, L.gmax, L.sumtgt, st));
   RET(tp_allreduce(ctx, L.sumtgt, (size_t)2 * T, ncclSum, st));
+  duty_begin(ctx, 7, st);
   const double n_tok = (double)pp.n_micro * L.plan.b * c.seq_len;
   CK(ce_grad(T, V, L.logits, tgt, L.v0, L.gmax, L.sumtgt, L.sumtgt + T, (float)(1.0 / n_tok), L.dlogits,
              L.loss_rows, st));
@@ -555,7 +608,9 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
   RET(gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, L.part, h, GEMM_STORE_F32, st));
   RET(gemm(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, first ? GEMM_STORE_F32 : GEMM_ACCUM_F32, st));
   RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  duty_begin(ctx, 8, st);
   CK(rmsnorm_bwd(T, h, S.x[L.n_local], L.gf, S.rf, L.part, nullptr, S.dlast, L.dgf, L.scratch, st));
+  duty_end(ctx, st);
   return MALLEUS_OK;
 }
 
@@ -964,7 +1019,13 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
   };
   cudaStream_t st = 0;
   uint64_t sent = 0, recvd = 0;
-  // local copies: everything this rank keeps (needed in new, resident in old)
+  constexpr long long CHUNK = 64 * 1024;
+  auto add_copy = [&](std::vector<CopyDesc>& v, const char* s, char* d, long long bytes) {
+    for (long long o = 0; o < bytes; o += CHUNK) v.push_back({s + o, d + o, std::min(CHUNK, bytes - o)});
+  };
+  auto pad16 = [](long long b) { return (b + 15) / 16 * 16; };
+  // (1) keep-copies: everything this rank needs and already has (old arena -> new arena)
+  std::vector<CopyDesc> keep;
   for (TState& ns : NL->ts) {
     const int64_t c = ns.t.cols;
     if (ns.held) {
@@ -975,7 +1036,7 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
           size_t es;
           char* src = locate_ptr(O, ns.t.id, MALLEUS_KIND_PARAM, lo * c, &es);
           char* dst = locate_ptr(*NL, ns.t.id, MALLEUS_KIND_PARAM, lo * c, &es);
-          CK(cudaMemcpyAsync(dst, src, (hi - lo) * c * 2, cudaMemcpyDeviceToDevice, st));
+          add_copy(keep, src, dst, (hi - lo) * c * 2);
         }
       }
     }
@@ -988,11 +1049,14 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
           size_t es;
           char* src = locate_ptr(O, ns.t.id, kind, lo, &es);
           char* dst = locate_ptr(*NL, ns.t.id, kind, lo, &es);
-          CK(cudaMemcpyAsync(dst, src, (hi - lo) * 4, cudaMemcpyDeviceToDevice, st));
+          add_copy(keep, src, dst, (hi - lo) * 4);
         }
       }
   }
-  // remote transfers grouped in packs of 4 consecutive layers
+  // (2) remote deltas in packs of 4 consecutive layers: per pack and peer, the
+  // outgoing ranges are packed into one contiguous buffer (K11 pack), exchanged with one grouped
+  // NCCL send / recv per peer, and unpacked into the new layout.  Every rank derives the same
+  // transfer list (layout.cpp), so pack offsets agree on both sides.
   const auto tr = migration_transfers(ctx->cfg, O.plan, np);
   const int L_ = ctx->cfg.n_layers;
   const int n_packs = std::max(1, (L_ + 3) / 4);
@@ -1001,37 +1065,94 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
     if (tid >= MALLEUS_T_EMBED) return n_packs - 1;
     return (tid / 16) / 4;
   };
+  struct PeerBuf {
+    long long off = 0, bytes = 0;
+  };
+  struct Pack {
+    std::map<int, PeerBuf> send, recv;
+    long long send_bytes = 0, recv_bytes = 0;
+    size_t pack_d0 = 0, pack_d1 = 0, unpack_d0 = 0, unpack_d1 = 0;
+  };
+  std::vector<Pack> packs(n_packs);
+  std::vector<CopyDesc> descs = keep;
+  // sizes per peer first (canonical order), then descriptors
+  for (auto& t : tr) {
+    size_t es = t.kind == MALLEUS_KIND_PARAM ? 2 : 4;
+    const long long b = (t.e1 - t.e0) * (long long)es;
+    Pack& P = packs[pack_of(t.tensor)];
+    if (t.src == me) P.send[t.dst].bytes += pad16(b);
+    if (t.dst == me) P.recv[t.src].bytes += pad16(b);
+  }
+  long long max_send = 0, max_recv = 0;
+  for (Pack& P : packs) {
+    for (auto& kv : P.send) { kv.second.off = P.send_bytes; P.send_bytes += kv.second.bytes; }
+    for (auto& kv : P.recv) { kv.second.off = P.recv_bytes; P.recv_bytes += kv.second.bytes; }
+    max_send = std::max(max_send, P.send_bytes);
+    max_recv = std::max(max_recv, P.recv_bytes);
+  }
+  char *sbuf = nullptr, *rbuf = nullptr;
+  if (max_send) CK(cudaMalloc(&sbuf, max_send));
+  if (max_recv) CK(cudaMalloc(&rbuf, max_recv));
   for (int pk = 0; pk < n_packs; ++pk) {
-    bool any = false;
-    for (auto& t : tr)
-      if (pack_of(t.tensor) == pk && (t.src == me || t.dst == me)) { any = true; break; }
-    if (!any) continue;
-    NK(ncclGroupStart());
+    Pack& P = packs[pk];
+    std::map<int, long long> scur, rcur;
+    for (auto& kv : P.send) scur[kv.first] = kv.second.off;
+    for (auto& kv : P.recv) rcur[kv.first] = kv.second.off;
+    P.pack_d0 = descs.size();
     for (auto& t : tr) {
-      if (pack_of(t.tensor) != pk) continue;
+      if (pack_of(t.tensor) != pk || t.src != me) continue;
       size_t es;
-      const ncclDataType_t ty = t.kind == MALLEUS_KIND_PARAM ? ncclBfloat16 : ncclFloat;
-      if (t.src == me) {
-        char* p = locate_ptr(O, t.tensor, t.kind, t.e0, &es);
-        NK(ncclSend(p, t.e1 - t.e0, ty, t.dst, ctx->world_comm, st));
-        sent += (t.e1 - t.e0) * es;
-      } else if (t.dst == me) {
-        char* p = locate_ptr(*NL, t.tensor, t.kind, t.e0, &es);
-        NK(ncclRecv(p, t.e1 - t.e0, ty, t.src, ctx->world_comm, st));
-        recvd += (t.e1 - t.e0) * es;
-      }
+      const char* p = locate_ptr(O, t.tensor, t.kind, t.e0, &es);
+      const long long b = (t.e1 - t.e0) * (long long)es;
+      add_copy(descs, p, sbuf + scur[t.dst], b);
+      scur[t.dst] += pad16(b);
+      sent += b;
     }
-    NK(ncclGroupEnd());
+    P.pack_d1 = P.unpack_d0 = descs.size();
+    for (auto& t : tr) {
+      if (pack_of(t.tensor) != pk || t.dst != me) continue;
+      size_t es;
+      char* p = locate_ptr(*NL, t.tensor, t.kind, t.e0, &es);
+      const long long b = (t.e1 - t.e0) * (long long)es;
+      add_copy(descs, rbuf + rcur[t.src], p, b);
+      rcur[t.src] += pad16(b);
+      recvd += b;
+    }
+    P.unpack_d1 = descs.size();
+  }
+  CopyDesc* d_desc = nullptr;
+  if (!descs.empty()) {
+    CK(cudaMalloc(&d_desc, descs.size() * sizeof(CopyDesc)));
+    CK(cudaMemcpy(d_desc, descs.data(), descs.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+  }
+  CK(cudaDeviceSynchronize());
+  const auto t1 = std::chrono::steady_clock::now();
+  CK(copy_ranges((int)keep.size(), d_desc, st));
+  for (int pk = 0; pk < n_packs; ++pk) {
+    Pack& P = packs[pk];
+    CK(copy_ranges((int)(P.pack_d1 - P.pack_d0), d_desc + P.pack_d0, st));
+    if (!P.send.empty() || !P.recv.empty()) {
+      NK(ncclGroupStart());
+      for (auto& kv : P.send) NK(ncclSend(sbuf + kv.second.off, kv.second.bytes, ncclUint8, kv.first, ctx->world_comm, st));
+      for (auto& kv : P.recv) NK(ncclRecv(rbuf + kv.second.off, kv.second.bytes, ncclUint8, kv.first, ctx->world_comm, st));
+      NK(ncclGroupEnd());
+    }
+    CK(copy_ranges((int)(P.unpack_d1 - P.unpack_d0), d_desc + P.unpack_d0, st));
   }
   CK(cudaStreamSynchronize(st));
+  const double xfer_secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+  if (d_desc) cudaFree(d_desc);
+  if (sbuf) cudaFree(sbuf);
+  if (rbuf) cudaFree(rbuf);
   const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   free_layout(ctx, ctx->L.get());
   ctx->L = std::move(NL);
   if (stats) {
     stats->bytes_sent = sent;
     stats->bytes_recv = recvd;
-    stats->seconds = secs;
+    stats->seconds = xfer_secs;
     stats->n_packs = n_packs;
+    stats->total_seconds = secs;
   }
   return MALLEUS_OK;
 }
@@ -1054,13 +1175,21 @@ malleus_status malleus_probe_speed(malleus_ctx* ctx, int32_t iters, float* ms_pe
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   GemmDesc g{n, n, n, a, n, false, b, n, false, cbuf, n, GEMM_STORE_BF16};
-  CK(gemm_bf16(g, st));  // warm-up
-  CK(probe_copy((long long)n * n / 2, (const float*)a, (float*)cbuf, st));
-  cudaEventRecord(e0, st);
-  for (int i = 0; i < iters; ++i) {
+  // warm-up (also primes the DUTY timer of the probe segment so the emulated slowdown applies)
+  for (int i = 0; i < 6; ++i) {
+    duty_begin(ctx, 9, st);
     CK(gemm_bf16(g, st));
     CK(probe_copy((long long)n * n / 2, (const float*)a, (float*)cbuf, st));
-    slow_spin(ctx, st, 0.2e6);
+    duty_end(ctx, st);
+    if (i == 2) CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaStreamSynchronize(st));
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < iters; ++i) {
+    duty_begin(ctx, 9, st);
+    CK(gemm_bf16(g, st));
+    CK(probe_copy((long long)n * n / 2, (const float*)a, (float*)cbuf, st));
+    duty_end(ctx, st);
   }
   cudaEventRecord(e1, st);
   CK(cudaEventSynchronize(e1));
@@ -1092,8 +1221,13 @@ malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode) {
     ctx->hog_flag = nullptr;
     set_avail_sms(0);
   }
+  if (mode == 1)
+    return fail(ctx, MALLEUS_E_ARG,
+                "HOG mode is disabled: a resident SM-occupying kernel deadlocks any device-wide "
+                "synchronisation (cudaDeviceSynchronize / cudaFree) of the process; use DUTY (2)");
   ctx->slowdown = x;
   ctx->slow_mode = mode;
+  for (auto& d : ctx->duty) { d.ms = -1.0; }
   if (mode == 1 && x > 1.f) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);

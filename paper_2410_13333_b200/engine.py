@@ -84,7 +84,8 @@ class Engine:
         st = L.MigrateStats()
         check(L.lib.malleus_migrate(self.ctx, ps.ref, C.byref(ar), C.byref(st)), self.ctx, "migrate")
         self.plan, self._arenas, self._plan_struct = plan, bufs, ps
-        return dict(bytes_sent=st.bytes_sent, bytes_recv=st.bytes_recv, seconds=st.seconds, n_packs=st.n_packs)
+        return dict(bytes_sent=st.bytes_sent, bytes_recv=st.bytes_recv, seconds=st.seconds, n_packs=st.n_packs,
+                    total_seconds=st.total_seconds)
 
     # ------------------------------------------------------------------ state I/O
     def write_weights(self, weights_bf16: dict):
@@ -139,7 +140,7 @@ class Engine:
     def set_slowdown(self, x: float, mode: int = 1):
         check(L.lib.malleus_set_slowdown(self.ctx, float(x), int(mode)), self.ctx, "set_slowdown")
 
-    def calibrate_slowdown(self, slow_rank: int, x_target: float, mode: int = 1, iters: int = 10, tol: float = 0.05,
+    def calibrate_slowdown(self, slow_rank: int, x_target: float, mode: int = 2, iters: int = 10, tol: float = 0.05,
                            max_rounds: int = 8):
         """Collective.  Reading R13: inject on `slow_rank` until the probe measures
         x = t_slow / t_ref within `tol` of x_target; t_ref = median probe of the other ranks (or the

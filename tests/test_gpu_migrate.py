@@ -21,7 +21,8 @@ def test_migration_bitexact(pair, n, tmp_path):
            "--master-addr=127.0.0.1", "--master-port=29541", os.path.join(ROOT, "tests", "mp_migrate_worker.py"),
            pair, str(out)]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert p.returncode == 0, "\n".join(l for l in (p.stdout + p.stderr).splitlines()
+                                        if "Error" in l or "error" in l or "rank" in l)[-6000:]
     r = json.load(open(out))
     assert r["ok"], r["errors"]
     assert r["bytes_recv"] == r["oracle_bytes"], r

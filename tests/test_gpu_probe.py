@@ -24,9 +24,9 @@ def test_probe_uniform_repeatable(eng):
     assert a > 0 and abs(a / b - 1) < 0.05
 
 
-def test_hog_slows_and_recovers(eng):
+def test_duty_slows_and_recovers(eng):
     t0 = eng.probe(10)[0]
-    eng.set_slowdown(2.0, 1)
+    eng.set_slowdown(2.0, 2)
     t1 = eng.probe(10)[0]
     eng.set_slowdown(1.0, 0)
     t2 = eng.probe(10)[0]
@@ -39,3 +39,9 @@ def test_calibration_hits_target(eng, x):
     nominal, measured = eng.calibrate_slowdown(0, x)
     eng.set_slowdown(1.0, 0)
     assert abs(measured / x - 1) <= 0.05, (nominal, measured)
+
+
+def test_hog_mode_refused(eng):
+    """HOG (a resident SM-occupying kernel) deadlocks device-wide syncs; the library refuses it."""
+    from paper_2410_13333_b200 import _lib as L
+    assert L.lib.malleus_set_slowdown(eng.ctx, 2.0, 1) == 1

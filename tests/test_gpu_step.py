@@ -48,5 +48,6 @@ def test_multi_gpu_plans(plan, tmp_path):
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mp_worker.py"), plan,
            str(out), "2"]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert p.returncode == 0, "\n".join(l for l in (p.stdout + p.stderr).splitlines()
+                                        if "Error" in l or "error" in l or "rank" in l)[-6000:]
     _assert_ok(json.load(open(out)))

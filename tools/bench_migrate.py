@@ -59,6 +59,12 @@ def main():
     eng.apply(a)
     torch.cuda.synchronize()
     dist.barrier()
+    # warm-up round trip: NCCL establishes peer connections lazily on first use; in a training job
+    # they exist from previous re-plans / grad syncs
+    eng.migrate(b)
+    dist.barrier()
+    eng.migrate(a)
+    dist.barrier()
     st = eng.migrate(b)
     dist.barrier()
     # and back (A -> B -> A)
