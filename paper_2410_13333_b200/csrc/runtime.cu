@@ -877,9 +877,10 @@ malleus_status malleus_write_tensor(malleus_ctx* ctx, int32_t tensor_id, int32_t
     }
     return MALLEUS_OK;
   }
-  float* dst = kind == MALLEUS_KIND_MASTER ? s.master : kind == MALLEUS_KIND_ADAM_M ? s.m
-             : kind == MALLEUS_KIND_ADAM_V ? s.v : nullptr;
-  if (!dst) return fail(ctx, MALLEUS_E_ARG, "write_tensor: kind must be PARAM, MASTER, ADAM_M or ADAM_V");
+  if (kind != MALLEUS_KIND_MASTER && kind != MALLEUS_KIND_ADAM_M && kind != MALLEUS_KIND_ADAM_V)
+    return fail(ctx, MALLEUS_E_ARG, "write_tensor: kind must be PARAM, MASTER, ADAM_M or ADAM_V");
+  float* dst = kind == MALLEUS_KIND_MASTER ? s.master : kind == MALLEUS_KIND_ADAM_M ? s.m : s.v;
+  if (s.owned.empty()) return MALLEUS_OK;  // this rank owns no piece of the tensor
   const float* h = static_cast<const float*>(host);
   for (size_t i = 0; i < s.owned.size(); ++i)
     CK(cudaMemcpy(dst + s.owned_off[i], h + s.owned[i].e0, (s.owned[i].e1 - s.owned[i].e0) * 4, cudaMemcpyHostToDevice));
