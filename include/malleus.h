@@ -249,6 +249,9 @@ malleus_status malleus_k_gemm(int32_t M, int32_t N, int32_t K, const void* A, in
  * tcgen05.mma.cta_group::2 with 256x256 tiles, when M >= 256; single CTA 128x256 otherwise),
  * 1 = always single CTA, 2 = always CTA pair. */
 malleus_status malleus_k_gemm_variant(int32_t variant);
+/* Attention forward kernel selection: 0 = automatic (tcgen05/TMEM/TMA kernel when head_dim == 128
+ * and s % 128 == 0, warp-level mma.sync kernel otherwise), 1 = always mma.sync. */
+malleus_status malleus_k_attention_variant(int32_t variant);
 
 /* y = x * rsqrt(mean(x^2) + eps) * g; optional fused residual: if partial != NULL then
  * x_new = bf16(x + partial) is written to x_out and normalised.  x, x_out, y: bf16 [T, h];

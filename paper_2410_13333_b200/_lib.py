@@ -97,6 +97,7 @@ _SIGS = {
     "malleus_gemm_profile": ([i32, P_i64, C.POINTER(C.c_double), C.POINTER(C.c_double)], i32),
     "malleus_k_gemm": ([i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, i32, vp], i32),
     "malleus_k_gemm_variant": ([i32], i32),
+    "malleus_k_attention_variant": ([i32], i32),
     "malleus_k_rmsnorm_fwd": ([i32, i32, vp, vp, vp, vp, f32, vp, vp, vp], i32),
     "malleus_k_rmsnorm_bwd": ([i32, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),
     "malleus_k_attention_fwd": ([i32, i32, i32, i32, vp, vp, vp, f32, vp], i32),

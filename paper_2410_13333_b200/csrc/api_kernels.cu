@@ -76,3 +76,9 @@ extern "C" malleus_status malleus_k_gemm_variant(int32_t variant) {
   gemm_set_variant(variant);
   return MALLEUS_OK;
 }
+
+extern "C" malleus_status malleus_k_attention_variant(int32_t variant) {
+  if (variant < 0 || variant > 1) return MALLEUS_E_ARG;
+  attention_set_variant(variant);
+  return MALLEUS_OK;
+}

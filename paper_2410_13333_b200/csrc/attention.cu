@@ -517,8 +517,12 @@ cudaError_t bwd_impl(int nb, int s, int n, const void* qkv, const void* o, const
 
 }  // namespace
 
+static int g_attn_variant = 0;  // 0 auto (tcgen05 when supported), 1 mma.sync only
+void attention_set_variant(int v) { g_attn_variant = v; }
+
 cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o, float* lse, cudaStream_t st) {
   if (s % 64) return cudaErrorInvalidValue;
+  if (g_attn_variant == 0 && attention_fwd_tc_supported(s, d)) return attention_fwd_tc(nb, s, n, qkv, o, lse, st);
   switch (d) {
     case 32: return fwd_impl<32>(nb, s, n, qkv, o, lse, st);
     case 64: return fwd_impl<64>(nb, s, n, qkv, o, lse, st);

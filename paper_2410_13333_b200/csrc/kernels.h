@@ -89,6 +89,11 @@ cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const vo
                           const float* lse, const void* dout, void* dqkv, float* dsum,
                           cudaStream_t st);
 
+// tcgen05/TMEM/TMA forward for d = 128, s % 128 == 0 (attention_tc.cu)
+bool attention_fwd_tc_supported(int s, int d);
+cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st);
+void attention_set_variant(int v);
+
 // ---- multi-range copy (copy.cu): migration pack / unpack / keep-copies
 struct CopyDesc {
   const char* src;

@@ -131,3 +131,25 @@ def test_attention_fwd_bwd(L, nb, s, n, d):
     for i, ref in enumerate((dq4, dk4, dv4)):
         got = hd(gd[:, i * n * d:(i + 1) * n * d])
         assert rel(got, ref) < 2e-2, (i, rel(got, ref))
+
+
+@pytest.mark.parametrize("nb,s,n", [(1, 128, 2), (2, 512, 3), (1, 2048, 4)])
+def test_attention_tc_matches_mma(L, nb, s, n):
+    """The tcgen05 forward and the mma.sync forward agree (both vs the oracle above); here on the
+    same rotated qkv, element by element within bf16 rounding, and LSE within 1e-3."""
+    d = 128
+    T = nb * s
+    qkv = bf(normal_matrix((T, 3 * n * d), 21))
+    outs = []
+    for var in (0, 1):
+        assert L.lib.malleus_k_attention_variant(var) == 0
+        q = qkv.clone()
+        o = torch.empty(T, n * d, dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty(nb, n, s, device="cuda")
+        assert L.lib.malleus_k_attention_fwd(nb, s, n, d, q.data_ptr(), o.data_ptr(), lse.data_ptr(), 1e4,
+                                             stream()) == 0
+        torch.cuda.synchronize()
+        outs.append((f64(o), lse.double().cpu().numpy(), q))
+    L.lib.malleus_k_attention_variant(0)
+    assert rel(outs[0][0], outs[1][0]) < 2e-2
+    assert np.abs(outs[0][1] - outs[1][1]).max() < 1e-3
