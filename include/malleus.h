@@ -247,7 +247,8 @@ malleus_status malleus_k_gemm(int32_t M, int32_t N, int32_t K, const void* A, in
 
 /* GEMM kernel selection for all subsequent GEMMs (tests / benchmarks): 0 = automatic (CTA pair,
  * tcgen05.mma.cta_group::2 with 256x256 tiles, when M >= 256; single CTA 128x256 otherwise),
- * 1 = always single CTA, 2 = always CTA pair. */
+ * 1 = always single CTA, 2 = always CTA pair (TMA-store / TMA-reduce-add epilogue), 3 = always CTA
+ * pair with direct register-to-global epilogue stores. */
 malleus_status malleus_k_gemm_variant(int32_t variant);
 /* Attention forward kernel selection: 0 = automatic (tcgen05/TMEM/TMA kernel when head_dim == 128
  * and s % 128 == 0, warp-level mma.sync kernel otherwise), 1 = always mma.sync. */

@@ -72,7 +72,7 @@ extern "C" malleus_status malleus_gemm_profile(int32_t enable, int64_t* launches
 }
 
 extern "C" malleus_status malleus_k_gemm_variant(int32_t variant) {
-  if (variant < 0 || variant > 2) return MALLEUS_E_ARG;
+  if (variant < 0 || variant > 3) return MALLEUS_E_ARG;
   gemm_set_variant(variant);
   return MALLEUS_OK;
 }

@@ -21,6 +21,7 @@
 #include <atomic>
 #include <utility>
 #include <vector>
+#include <cstring>
 #include "ptx.cuh"
 #include "kernels.h"
 
@@ -39,6 +40,7 @@ struct GemmParams {
   long long ldc;
   int mode;  // GEMM_STORE_BF16 / GEMM_STORE_F32 / GEMM_ACCUM_F32
   int vec_ok;  // rows of C are 16-byte aligned -> 128-bit stores
+  int tma_epi; // C written by TMA store / reduce-add (CTA-pair kernel)
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
@@ -99,6 +101,73 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
         for (int j = 0; j < 32 && col0 + j < p.N; ++j)
           C[j] = accum ? C[j] + __uint_as_float(r[j]) : __uint_as_float(r[j]);
       }
+    }
+  }
+}
+
+// TMA epilogue: per warp, 32 rows x 128 bytes (32 fp32 or 64 bf16 columns) are staged in a
+// 128B-swizzled smem box (double buffered) and written with one TMA store, or, for the fp32
+// wgrad accumulation, with one TMA reduce-add (the add happens in L2; the SM never reads C).
+// Out-of-bounds rows / columns are clipped by TMA, so ragged uneven-split shapes need no masks.
+__device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC, uint32_t taddr,
+                                                  int row_box0, int col_base, uint8_t* stg, int& sbuf) {
+  const int lane = threadIdx.x & 31;
+  if (row_box0 >= p.M) return;
+  if (p.mode == GEMM_STORE_BF16) {
+#pragma unroll 1
+    for (int c = 0; c < 256 / 64; ++c) {
+      const int col0 = col_base + c * 64;
+      uint32_t r0[32], r1[32];
+      tmem_ld32(taddr + c * 64, r0);
+      tmem_ld32(taddr + c * 64 + 32, r1);
+      tmem_wait_ld();
+      if (col0 >= p.N) continue;
+      uint8_t* buf = stg + sbuf * 4096;
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const uint32_t* r = ch < 4 ? r0 : r1;
+        const int o = (ch & 3) * 8;
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(r[o + 0]), __uint_as_float(r[o + 1]));
+        w.y = pack_bf16(__uint_as_float(r[o + 2]), __uint_as_float(r[o + 3]));
+        w.z = pack_bf16(__uint_as_float(r[o + 4]), __uint_as_float(r[o + 5]));
+        w.w = pack_bf16(__uint_as_float(r[o + 6]), __uint_as_float(r[o + 7]));
+        *reinterpret_cast<uint4*>(buf + lane * 128 + ((ch ^ (lane & 7)) << 4)) = w;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmC, buf, col0, row_box0);
+        bulk_commit();
+      }
+      sbuf ^= 1;
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < 256 / 32; ++c) {
+      const int col0 = col_base + c * 32;
+      uint32_t r[32];
+      tmem_ld32(taddr + c * 32, r);
+      tmem_wait_ld();
+      if (col0 >= p.N) continue;
+      uint8_t* buf = stg + sbuf * 4096;
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        uint4 w = make_uint4(r[4 * ch], r[4 * ch + 1], r[4 * ch + 2], r[4 * ch + 3]);
+        *reinterpret_cast<uint4*>(buf + lane * 128 + ((ch ^ (lane & 7)) << 4)) = w;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        if (p.mode == GEMM_ACCUM_F32) tma_reduce_add_2d(tmC, buf, col0, row_box0);
+        else tma_store_2d(tmC, buf, col0, row_box0);
+        bulk_commit();
+      }
+      sbuf ^= 1;
     }
   }
 }
@@ -229,15 +298,17 @@ constexpr int BM2 = 128, BN2 = 256, STAGES2 = 6;
 constexpr int A2_BYTES = BM2 * BK * 2;            // 16 KB
 constexpr int B2_BYTES = (BN2 / 2) * BK * 2;      // 16 KB (this CTA's half of N)
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
-constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + 1024 + 1024;
+constexpr int EPI_STAGE_BYTES = 4 * 2 * 4096;  // 4 epilogue warps x 2 swizzled 4 KB boxes
+constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + EPI_STAGE_BYTES + 1024 + 1024;
 
 template <bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmC, GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  uint8_t* epi_stage = smem + STAGES2 * STAGE2_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + EPI_STAGE_BYTES);
   uint64_t* empty = full + STAGES2;
   uint64_t* tfull = empty + STAGES2;  // [2]
   uint64_t* tempty = tfull + 2;       // [2] (leader's copy is the one used)
@@ -326,6 +397,8 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
     }
   } else {
     const int quarter = warp & 3;
+    uint8_t* stg = epi_stage + (warp - 2) * 2 * 4096;
+    int sbuf = 0;
     int it = 0;
     for (int t = cid; t < n_tiles; t += ncl, ++it) {
       int tm, tn; tile_coords(t, tiles_m, tiles_n, tm, tn);
@@ -333,12 +406,16 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = tm * 2 * BM2 + rank * BM2 + quarter * 32 + lane;
-      epilogue_tile(p, tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN2, row, tn * BN2);
+      const int row_box0 = tm * 2 * BM2 + rank * BM2 + quarter * 32;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN2;
+      if (p.tma_epi) epilogue_tile_tma(p, &tmC, taddr, row_box0, tn * BN2, stg, sbuf);
+      else epilogue_tile(p, taddr, row_box0 + lane, tn * BN2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   }
   tc_fence_before();
   cluster_sync();
@@ -370,6 +447,18 @@ static bool make_map(CUtensorMap* m, const void* ptr, long long inner, long long
   cuuint32_t es[2] = {1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
                         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// C map for the TMA epilogue: [M][N] row stride ldc, box {128 bytes, 32 rows}, 128B swizzle.
+static bool make_map_c(CUtensorMap* m, void* ptr, long long N, long long M, long long ldc, bool f32) {
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)ldc * (f32 ? 4 : 2)};
+  cuuint32_t box[2] = {f32 ? 32u : 64u, 32u};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims,
+                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -448,11 +537,16 @@ static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
   return cudaGetLastError();
 }
 
-static int g_variant = 0;  // 0 auto, 1 single-CTA, 2 CTA pair
-void gemm_set_variant(int v) { g_variant = v; }
+static int g_variant = 0;  // 0 auto, 1 single-CTA, 2 CTA pair (TMA epilogue), 3 CTA pair (direct stores)
+static int g_tma_epi = 1;
+void gemm_set_variant(int v) {
+  g_variant = v == 3 ? 2 : v;
+  g_tma_epi = v == 3 ? 0 : 1;
+}
 
 template <bool A_MN, bool B_MN>
-static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
+static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmParams& p,
+                           cudaStream_t st) {
   static bool attr_set = false;
   auto kern = gemm_tcgen05_2sm_kernel<A_MN, B_MN>;
   if (!attr_set) {
@@ -478,7 +572,7 @@ static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const G
     }
     cudaEventRecord(g_prof.ev[g_prof.used].first, st);
   }
-  kern<<<grid, GEMM_THREADS, GEMM2_SMEM, st>>>(ta, tb, p); count_launch();
+  kern<<<grid, GEMM_THREADS, GEMM2_SMEM, st>>>(ta, tb, tc, p); count_launch();
   if (prof) {
     cudaEventRecord(g_prof.ev[g_prof.used].second, st);
     g_prof.flops.push_back(2.0 * p.M * (double)p.N * p.K);
@@ -502,11 +596,14 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
     if (!ok) return cudaErrorInvalidValue;
     const int esz = g.mode == GEMM_STORE_BF16 ? 2 : 4;
     const int vec_ok = ((g.ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0);
-    GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok};
-    if (!g.a_mn && !g.b_mn) return launch2<false, false>(ta, tb, p, st);
-    if (!g.a_mn && g.b_mn) return launch2<false, true>(ta, tb, p, st);
-    if (g.a_mn && g.b_mn) return launch2<true, true>(ta, tb, p, st);
-    return launch2<true, false>(ta, tb, p, st);
+    CUtensorMap tc;
+    int tma_epi = vec_ok && g_tma_epi && make_map_c(&tc, g.C, g.N, g.M, g.ldc, g.mode != GEMM_STORE_BF16);
+    if (!tma_epi) memset(&tc, 0, sizeof(tc));
+    GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, tma_epi};
+    if (!g.a_mn && !g.b_mn) return launch2<false, false>(ta, tb, tc, p, st);
+    if (!g.a_mn && g.b_mn) return launch2<false, true>(ta, tb, tc, p, st);
+    if (g.a_mn && g.b_mn) return launch2<true, true>(ta, tb, tc, p, st);
+    return launch2<true, false>(ta, tb, tc, p, st);
   }
   CUtensorMap ta, tb;
   bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.lda, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, BM);
@@ -514,7 +611,7 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
   if (!ok) return cudaErrorInvalidValue;
   const int esz = g.mode == GEMM_STORE_BF16 ? 2 : 4;
   const int vec_ok = ((g.ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0);
-  GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok};
+  GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, 0};
   if (!g.a_mn && !g.b_mn) return launch<false, false>(ta, tb, p, st);
   if (!g.a_mn && g.b_mn) return launch<false, true>(ta, tb, p, st);
   if (g.a_mn && g.b_mn) return launch<true, true>(ta, tb, p, st);

@@ -45,9 +45,10 @@ SHAPES = [(128, 256, 64), (256, 512, 1024), (200, 304, 136), (96, 48, 2048), (10
           (2048, 2304, 4096)]
 
 
-@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+@pytest.fixture(params=[1, 2, 3], ids=["cta1", "cta2_tma_epi", "cta2_direct_epi"])
 def variant(request, L):
-    """1: single-CTA 128x256 tiles; 2: CTA pair (tcgen05.mma.cta_group::2) 256x256 tiles."""
+    """1: single-CTA 128x256 tiles; 2: CTA pair (tcgen05.mma.cta_group::2) 256x256 tiles with TMA
+    store / reduce-add epilogue; 3: CTA pair with direct stores."""
     assert L.lib.malleus_k_gemm_variant(request.param) == 0
     yield request.param
     L.lib.malleus_k_gemm_variant(0)

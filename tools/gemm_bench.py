@@ -29,7 +29,7 @@ for name, M, N, K, amn, bmn in shapes:
     print(f"{name:10s} M={M} N={N} K={K}: malleus {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:7.1f} TF | cublas {ref*1e3:8.1f} us {2*M*N*K/ref/1e9:7.1f} TF | maxdiff {err:.3g}", flush=True)
 
 # CTA-pair vs single-CTA on the same shapes
-for var in (1, 2):
+for var in (1, 3, 2):
     L.lib.malleus_k_gemm_variant(var)
     for name, M, N, K, amn, bmn in shapes:
         A = torch.randn(K, M, device="cuda").to(torch.bfloat16) if amn else torch.randn(M, K, device="cuda").to(torch.bfloat16)
