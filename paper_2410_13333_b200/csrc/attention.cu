@@ -534,6 +534,12 @@ cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o,
 cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const void* o, const float* lse,
                           const void* dout, void* dqkv, float* dsum, cudaStream_t st) {
   if (s % 64) return cudaErrorInvalidValue;
+  if (g_attn_variant == 0 && attention_fwd_tc_supported(s, d)) {
+    const long long T = (long long)nb * s;
+    attn_dsum_kernel<128><<<(unsigned)((T * n + 7) / 8), dim3(32, 8), 0, st>>>(
+        s, n, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dsum, T); count_launch();
+    return attention_bwd_tc(nb, s, n, qkv, lse, dout, dqkv, dsum, st);
+  }
   switch (d) {
     case 32: return bwd_impl<32>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);
     case 64: return bwd_impl<64>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);

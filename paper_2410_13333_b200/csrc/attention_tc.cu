@@ -246,6 +246,372 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
   }
 }
 
+// ------------------------------------------------------------------ backward (tcgen05)
+// 1-D bulk copy global -> shared completing on an mbarrier (lse / D rows of a query tile)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// write 32 consecutive bf16 (cols c0..c0+31 of row r) into a 2-panel K-major 128B-swizzled tile
+__device__ __forceinline__ void st_sw128_32(uint8_t* tile, int r, int c0, const float (&v)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int col = c0 + q * 8;
+    const int panel = col >> 6, c16 = (col & 63) >> 3;
+    uint4 w;
+    w.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]); w.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+    w.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]); w.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+    *reinterpret_cast<uint4*>(tile + panel * PANEL + r * 128 + ((c16 ^ (r & 7)) << 4)) = w;
+  }
+}
+
+// dK / dV: CTA = 128 keys of one (sequence, head); loop over query tiles j >= key tile.
+//   TMEM: S^T [0,128), dP^T [128,256), dV [256,384), dK [384,512)
+//   S^T = K Q_j^T, dP^T = V dO_j^T (M = keys); P^T, dS^T -> smem; dV += P^T dO_j; dK += dS^T Q_j
+//   (Q_j / dO_j tiles serve as K-major B for S^T / dP^T and, same bytes, as MN-major B for dK / dV).
+constexpr int BWD1_SMEM = 7 * Q_BYTES + 1024 + 1024 + 1024;
+
+__global__ void __launch_bounds__(192, 1)
+attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s,
+                       int n, const float* __restrict__ lse, const float* __restrict__ dsum,
+                       __nv_bfloat16* __restrict__ dqkv, float scale) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + Q_BYTES;
+  uint8_t* sQ = sV + Q_BYTES;
+  uint8_t* sO = sQ + Q_BYTES;   // dO tile
+  uint8_t* sP = sO + Q_BYTES;   // P^T
+  uint8_t* sS = sP + Q_BYTES;   // dS^T
+  float* sL = reinterpret_cast<float*>(sS + Q_BYTES);  // lse * log2e [128], D [128]
+  float* sD = sL + 128;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sL + 256);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;
+  uint64_t* qd_empty = bars + 2;
+  uint64_t* sd_full = bars + 3;
+  uint64_t* sd_empty = bars + 4;
+  uint64_t* pd_full = bars + 5;
+  uint64_t* pd_empty = bars + 6;
+  uint64_t* done = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x;  // kb = 0 has the most query tiles: scheduled first
+  const int head = blockIdx.y, b = blockIdx.z;
+  const int nq = s / TQ;
+  const int nd = n * DH;
+  const long long lrow = ((long long)b * n + head) * s;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm);
+    tma_prefetch(&tmo);
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], (i == 4 || i == 5) ? 4 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int krow = b * s + kb * TK;
+      mbar_arrive_expect_tx(kv_full, 2 * Q_BYTES);
+      tma_load_2d(sK, &tm, kv_full, nd + head * DH, krow);
+      tma_load_2d(sK + PANEL, &tm, kv_full, nd + head * DH + 64, krow);
+      tma_load_2d(sV, &tm, kv_full, 2 * nd + head * DH, krow);
+      tma_load_2d(sV + PANEL, &tm, kv_full, 2 * nd + head * DH + 64, krow);
+      for (int j = kb; j < nq; ++j) {
+        const int it = j - kb;
+        mbar_wait(qd_empty, (it & 1) ^ 1);
+        const int qrow = b * s + j * TQ;
+        mbar_arrive_expect_tx(qd_full, 2 * Q_BYTES + 1024);
+        tma_load_2d(sQ, &tm, qd_full, head * DH, qrow);
+        tma_load_2d(sQ + PANEL, &tm, qd_full, head * DH + 64, qrow);
+        tma_load_2d(sO, &tmo, qd_full, head * DH, qrow);
+        tma_load_2d(sO + PANEL, &tmo, qd_full, head * DH + 64, qrow);
+        bulk_load(sL, lse + lrow + j * TQ, 512, qd_full);
+        bulk_load(sD, dsum + lrow + j * TQ, 512, qd_full);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_kk = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_km = umma_idesc_bf16(128, 128, false, true);
+      const uint32_t ak = smem_u32(sK), av = smem_u32(sV), bq = smem_u32(sQ), bo = smem_u32(sO);
+      const uint32_t ap = smem_u32(sP), as = smem_u32(sS);
+      mbar_wait(kv_full, 0);
+      for (int j = kb; j < nq; ++j) {
+        const int it = j - kb;
+        mbar_wait(qd_full, it & 1);
+        mbar_wait(sd_empty, (it & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
+          umma_f16(tbase + 0, umma_desc_sw128(ak + off, 16, 1024), umma_desc_sw128(bq + off, 16, 1024), id_kk,
+                   kk > 0 ? 1u : 0u);
+          umma_f16(tbase + 128, umma_desc_sw128(av + off, 16, 1024), umma_desc_sw128(bo + off, 16, 1024), id_kk,
+                   kk > 0 ? 1u : 0u);
+        }
+        umma_commit(sd_full);
+        mbar_wait(pd_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < TQ / 16; ++kk) {
+          const uint32_t aoff = (kk >> 2) * PANEL + (kk & 3) * 32;
+          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+          umma_f16(tbase + 256, umma_desc_sw128(ap + aoff, 16, 1024), umma_desc_sw128(bo + kk * 2048, PANEL, 1024),
+                   id_km, acc);
+          umma_f16(tbase + 384, umma_desc_sw128(as + aoff, 16, 1024), umma_desc_sw128(bq + kk * 2048, PANEL, 1024),
+                   id_km, acc);
+        }
+        umma_commit(pd_empty);
+        umma_commit(qd_empty);
+      }
+      umma_commit(done);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // key row within the tile
+    const int key = kb * TK + r;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float sl2 = scale * LOG2E;
+    for (int j = kb; j < nq; ++j) {
+      const int it = j - kb;
+      mbar_wait(sd_full, it & 1);
+      tc_fence_after();
+      if (it > 0) mbar_wait(pd_empty, (it - 1) & 1);  // P^T / dS^T smem free
+      const bool diag = j == kb;
+#pragma unroll 1
+      for (int c = 0; c < TQ / 32; ++c) {
+        uint32_t us[32], ud[32];
+        tmem_ld32(tbase + lane_off + c * 32, us);
+        tmem_ld32(tbase + lane_off + 128 + c * 32, ud);
+        tmem_wait_ld();
+        float p[32], ds[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int qi = c * 32 + t;
+          float pv = exp2f(__uint_as_float(us[t]) * sl2 - sL[qi] * LOG2E);
+          if (diag && key > j * TQ + qi) pv = 0.f;
+          p[t] = pv;
+          ds[t] = pv * (__uint_as_float(ud[t]) - sD[qi]);
+        }
+        st_sw128_32(sP, r, c * 32, p);
+        st_sw128_32(sS, r, c * 32, ds);
+      }
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(sd_empty);
+        mbar_arrive(pd_full);
+      }
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    __nv_bfloat16* dk = dqkv + (long long)(b * s + key) * 3 * nd + nd + head * DH;
+    __nv_bfloat16* dv = dk + nd;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t uk[32], uv[32];
+      tmem_ld32(tbase + lane_off + 384 + c * 32, uk);
+      tmem_ld32(tbase + lane_off + 256 + c * 32, uv);
+      tmem_wait_ld();
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 wk, wv;
+        wk.x = pack_bf16(__uint_as_float(uk[8 * v]) * scale, __uint_as_float(uk[8 * v + 1]) * scale);
+        wk.y = pack_bf16(__uint_as_float(uk[8 * v + 2]) * scale, __uint_as_float(uk[8 * v + 3]) * scale);
+        wk.z = pack_bf16(__uint_as_float(uk[8 * v + 4]) * scale, __uint_as_float(uk[8 * v + 5]) * scale);
+        wk.w = pack_bf16(__uint_as_float(uk[8 * v + 6]) * scale, __uint_as_float(uk[8 * v + 7]) * scale);
+        wv.x = pack_bf16(__uint_as_float(uv[8 * v]), __uint_as_float(uv[8 * v + 1]));
+        wv.y = pack_bf16(__uint_as_float(uv[8 * v + 2]), __uint_as_float(uv[8 * v + 3]));
+        wv.z = pack_bf16(__uint_as_float(uv[8 * v + 4]), __uint_as_float(uv[8 * v + 5]));
+        wv.w = pack_bf16(__uint_as_float(uv[8 * v + 6]), __uint_as_float(uv[8 * v + 7]));
+        reinterpret_cast<uint4*>(dk + c * 32)[v] = wk;
+        reinterpret_cast<uint4*>(dv + c * 32)[v] = wv;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+// dQ: CTA = 128 queries; loop over key tiles i <= query tile (2-stage K / V ring).
+//   TMEM: S [0,128), dP [128,256), dQ [256,384)
+//   S = Q K_i^T, dP = dO V_i^T (M = queries); dS -> smem; dQ += dS K_i (K_i as MN-major B)
+constexpr int BWD2_SMEM = 3 * Q_BYTES + 2 * 2 * Q_BYTES + 1024 + 1024;
+
+__global__ void __launch_bounds__(192, 1)
+attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s, int n,
+                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
+                      float scale) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sO = sQ + Q_BYTES;
+  uint8_t* sS = sO + Q_BYTES;   // dS
+  uint8_t* sKV = sS + Q_BYTES;  // [2 stages][K | V]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + 4 * Q_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* sd_full = bars + 5;
+  uint64_t* sd_empty = bars + 6;
+  uint64_t* ds_full = bars + 7;
+  uint64_t* ds_empty = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = s / TQ;
+  const int qb = nqb - 1 - blockIdx.x;  // heaviest first
+  const int head = blockIdx.y, b = blockIdx.z;
+  const int n_tiles = qb + 1;
+  const int nd = n * DH;
+  const int row0 = b * s + qb * TQ;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm);
+    tma_prefetch(&tmo);
+    for (int i = 0; i < 9; ++i) mbar_init(&bars[i], (i == 6 || i == 7) ? 4 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * Q_BYTES);
+      tma_load_2d(sQ, &tm, q_full, head * DH, row0);
+      tma_load_2d(sQ + PANEL, &tm, q_full, head * DH + 64, row0);
+      tma_load_2d(sO, &tmo, q_full, head * DH, row0);
+      tma_load_2d(sO + PANEL, &tmo, q_full, head * DH + 64, row0);
+      for (int i = 0; i < n_tiles; ++i) {
+        const int st = i & 1;
+        mbar_wait(&kv_empty[st], ((i >> 1) & 1) ^ 1);
+        uint8_t* k = sKV + st * 2 * Q_BYTES;
+        uint8_t* v = k + Q_BYTES;
+        const int krow = b * s + i * TK;
+        mbar_arrive_expect_tx(&kv_full[st], 2 * Q_BYTES);
+        tma_load_2d(k, &tm, &kv_full[st], nd + head * DH, krow);
+        tma_load_2d(k + PANEL, &tm, &kv_full[st], nd + head * DH + 64, krow);
+        tma_load_2d(v, &tm, &kv_full[st], 2 * nd + head * DH, krow);
+        tma_load_2d(v + PANEL, &tm, &kv_full[st], 2 * nd + head * DH + 64, krow);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_kk = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_km = umma_idesc_bf16(128, 128, false, true);
+      const uint32_t aq = smem_u32(sQ), ao = smem_u32(sO), as = smem_u32(sS);
+      auto issue_dq = [&](int i) {
+        const int st = i & 1;
+        mbar_wait(ds_full, i & 1);
+        tc_fence_after();
+        const uint32_t k = smem_u32(sKV + st * 2 * Q_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < TK / 16; ++kk)
+          umma_f16(tbase + 256, umma_desc_sw128(as + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024),
+                   umma_desc_sw128(k + kk * 2048, PANEL, 1024), id_km, (i > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(ds_empty);
+        umma_commit(&kv_empty[st]);
+      };
+      mbar_wait(q_full, 0);
+      for (int i = 0; i < n_tiles; ++i) {
+        const int st = i & 1;
+        mbar_wait(&kv_full[st], (i >> 1) & 1);
+        mbar_wait(sd_empty, (i & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k = smem_u32(sKV + st * 2 * Q_BYTES), v = k + Q_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
+          umma_f16(tbase + 0, umma_desc_sw128(aq + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024), id_kk,
+                   kk > 0 ? 1u : 0u);
+          umma_f16(tbase + 128, umma_desc_sw128(ao + off, 16, 1024), umma_desc_sw128(v + off, 16, 1024), id_kk,
+                   kk > 0 ? 1u : 0u);
+        }
+        umma_commit(sd_full);
+        if (i > 0) issue_dq(i - 1);
+      }
+      issue_dq(n_tiles - 1);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int q = qb * TQ + r;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float sl2 = scale * LOG2E;
+    const long long lrow = ((long long)b * n + head) * s;
+    const float L2 = lse[lrow + q] * LOG2E, Dq = dsum[lrow + q];
+    for (int i = 0; i < n_tiles; ++i) {
+      mbar_wait(sd_full, i & 1);
+      tc_fence_after();
+      if (i > 0) mbar_wait(ds_empty, (i - 1) & 1);
+      const bool diag = i == n_tiles - 1;
+#pragma unroll 1
+      for (int c = 0; c < TK / 32; ++c) {
+        uint32_t us[32], ud[32];
+        tmem_ld32(tbase + lane_off + c * 32, us);
+        tmem_ld32(tbase + lane_off + 128 + c * 32, ud);
+        tmem_wait_ld();
+        float ds[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          float pv = exp2f(__uint_as_float(us[t]) * sl2 - L2);
+          if (diag && i * TK + c * 32 + t > q) pv = 0.f;
+          ds[t] = pv * (__uint_as_float(ud[t]) - Dq);
+        }
+        st_sw128_32(sS, r, c * 32, ds);
+      }
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(sd_empty);
+        mbar_arrive(ds_full);
+      }
+    }
+    mbar_wait(ds_empty, (n_tiles - 1) & 1);  // last dQ MMA done
+    tc_fence_after();
+    __nv_bfloat16* dq = dqkv + (long long)(b * s + q) * 3 * nd + head * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tbase + lane_off + 256 + c * 32, u);
+      tmem_wait_ld();
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(u[8 * v]) * scale, __uint_as_float(u[8 * v + 1]) * scale);
+        w.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * scale, __uint_as_float(u[8 * v + 3]) * scale);
+        w.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * scale, __uint_as_float(u[8 * v + 5]) * scale);
+        w.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * scale, __uint_as_float(u[8 * v + 7]) * scale);
+        reinterpret_cast<uint4*>(dq + c * 32)[v] = w;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
   if (!f) {
@@ -261,6 +627,40 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 }  // namespace
 
 bool attention_fwd_tc_supported(int s, int d) { return d == DH && s % TQ == 0; }
+
+static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long rows) {
+  auto enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// dsum (= rowsum(dO * O)) must already be in `dsum`; writes dq, dk, dv column blocks of dqkv.
+cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float* lse, const void* dout,
+                             void* dqkv, const float* dsum, cudaStream_t st) {
+  CUtensorMap tm, tmo;
+  const long long T = (long long)nb * s;
+  if (!map_rows(&tm, qkv, 3LL * n * DH, T) || !map_rows(&tmo, dout, (long long)n * DH, T)) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD1_SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD2_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const float scale = rsqrtf((float)DH);
+  attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 192, BWD1_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
+                                                                      (__nv_bfloat16*)dqkv, scale); count_launch();
+  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 192, BWD2_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
+                                                                     (__nv_bfloat16*)dqkv, scale); count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st) {
   auto enc = encoder();

@@ -93,6 +93,8 @@ cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const vo
 bool attention_fwd_tc_supported(int s, int d);
 cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st);
 void attention_set_variant(int v);
+cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float* lse, const void* dout,
+                             void* dqkv, const float* dsum, cudaStream_t st);
 
 // ---- multi-range copy (copy.cu): migration pack / unpack / keep-copies
 struct CopyDesc {

@@ -140,6 +140,7 @@ def test_attention_tc_matches_mma(L, nb, s, n):
     d = 128
     T = nb * s
     qkv = bf(normal_matrix((T, 3 * n * d), 21))
+    dout = bf(normal_matrix((T, n * d), 22))
     outs = []
     for var in (0, 1):
         assert L.lib.malleus_k_attention_variant(var) == 0
@@ -148,8 +149,15 @@ def test_attention_tc_matches_mma(L, nb, s, n):
         lse = torch.empty(nb, n, s, device="cuda")
         assert L.lib.malleus_k_attention_fwd(nb, s, n, d, q.data_ptr(), o.data_ptr(), lse.data_ptr(), 1e4,
                                              stream()) == 0
+        dq = torch.empty_like(qkv)
+        assert L.lib.malleus_k_attention_bwd(nb, s, n, d, q.data_ptr(), o.data_ptr(), lse.data_ptr(),
+                                             dout.data_ptr(), dq.data_ptr(), 1e4, stream()) == 0
         torch.cuda.synchronize()
-        outs.append((f64(o), lse.double().cpu().numpy(), q))
+        outs.append((f64(o), lse.double().cpu().numpy(), f64(dq)))
     L.lib.malleus_k_attention_variant(0)
     assert rel(outs[0][0], outs[1][0]) < 2e-2
     assert np.abs(outs[0][1] - outs[1][1]).max() < 1e-3
+    for i in range(3):  # dq, dk, dv blocks
+        a = outs[0][2][:, i * n * d:(i + 1) * n * d]
+        b = outs[1][2][:, i * n * d:(i + 1) * n * d]
+        assert rel(a, b) < 2e-2, (i, rel(a, b))
