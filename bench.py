@@ -153,6 +153,9 @@ def main():
     ap.add_argument("--uniform", action="store_true", help="non-malleable even plan (T_u / T0 runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if os.environ.get("MALLEUS_WATCHDOG"):  # debugging aid: dump all stacks if the run hangs
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["MALLEUS_WATCHDOG"]), exit=True)
 
     from synth.gen import C2_7B_SLICE
     cfg = C2_7B_SLICE

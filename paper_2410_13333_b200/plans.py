@@ -51,7 +51,9 @@ def plan_matrix_c1(cfg, B=8, b=2):
     """SURVEY §8(d) parity plan matrix P0-P8 on the tiny C1 model (4 heads, F 512, V 256, L 2)."""
     L = cfg.n_layers
     m = B // b
-    s31 = lambda ranks, layers: stage(ranks, [3, 1], [384, 128], [192, 64], layers)
+    H, F, V = cfg.n_heads, cfg.ffn, cfg.vocab
+    s31 = lambda ranks, layers: stage(ranks, [3 * H // 4, H // 4], [3 * F // 4, F // 4], [3 * V // 4, V // 4],
+                                      layers)
     ev = lambda ranks, layers: even_stage(cfg, ranks, layers)
     P = {}
     P["P0"] = plan([pipe([ev([0], [0, L])], m)], b, B)

@@ -59,6 +59,8 @@ C4_70B_SLICE = ModelCfg(n_layers=4, hidden=8192, n_heads=64, head_dim=128, ffn=2
                         seq_len=4096)
 C5_110B_SLICE = ModelCfg(n_layers=4, hidden=8192, n_heads=64, head_dim=128, ffn=49152, vocab=32000,
                          seq_len=4096)
+# C1 with d = 128 and 256-token sequences: exercises the tcgen05 attention and CTA-pair GEMM paths
+C1_MED = ModelCfg(n_layers=2, hidden=512, n_heads=4, head_dim=128, ffn=1536, vocab=2048, seq_len=256)
 MICRO = ModelCfg(n_layers=2, hidden=16, n_heads=2, head_dim=8, ffn=32, vocab=16, seq_len=8)
 
 

@@ -23,14 +23,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-from synth.gen import C1_TINY, make_weights, make_tokens, bf16_rne, tensor_shapes  # noqa: E402
+from synth.gen import C1_TINY, C1_MED, make_weights, make_tokens, bf16_rne, tensor_shapes  # noqa: E402
 from paper_2410_13333_b200 import plans as Pl  # noqa: E402
 from paper_2410_13333_b200 import _lib as L  # noqa: E402
 from paper_2410_13333_b200.engine import Engine, gather_logical  # noqa: E402
 
+CONFIGS = {"c1": C1_TINY, "c1m": C1_MED}
 
-def run(plan_name: str, rank: int = 0, world: int = 1, local_rank: int = 0, group=None, steps: int = 1):
-    cfg = C1_TINY
+
+def run(plan_name: str, rank: int = 0, world: int = 1, local_rank: int = 0, group=None, steps: int = 1,
+        cfg_name: str = "c1"):
+    cfg = CONFIGS[cfg_name]
     B, b = 8, 2
     plan = Pl.plan_matrix_c1(cfg, B=B, b=b)[plan_name]
     assert Pl.world_of(plan) == world, (plan_name, world)
@@ -120,7 +123,9 @@ if __name__ == "__main__":
     plan_name, out_path = sys.argv[1], sys.argv[2]
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     dist.init_process_group("gloo")
-    r = run(plan_name, dist.get_rank(), dist.get_world_size(), int(os.environ.get("LOCAL_RANK", 0)), steps=steps)
+    cfg_name = sys.argv[4] if len(sys.argv) > 4 else "c1"
+    r = run(plan_name, dist.get_rank(), dist.get_world_size(), int(os.environ.get("LOCAL_RANK", 0)), steps=steps,
+            cfg_name=cfg_name)
     if dist.get_rank() == 0:
         json.dump(r, open(out_path, "w"), indent=1)
     dist.barrier()

@@ -36,6 +36,33 @@ def test_p0_single_gpu():
     _assert_ok(r)
 
 
+def test_p0_single_gpu_d128():
+    """C1_MED (d = 128, s = 256, 512-token micro-batches): the tcgen05 attention kernels and the
+    CTA-pair GEMM with TMA-store / TMA-reduce-add epilogues run inside the step."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from tests.mp_worker import run
+    r = run("P0", steps=3, cfg_name="c1m")
+    _assert_ok(r)
+
+
+@pytest.mark.parametrize("plan", ["P2", "P4"])
+def test_multi_gpu_plans_d128(plan, tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    n = PLAN_WORLD[plan]
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"{plan} needs {n} GPUs")
+    out = tmp_path / "r.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(ROOT, "tests", "mp_worker.py"), plan,
+           str(out), "2", "c1m"]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, "\n".join(l for l in (p.stdout + p.stderr).splitlines()
+                                        if "Error" in l or "error" in l or "rank" in l)[-6000:]
+    _assert_ok(json.load(open(out)))
+
+
 @pytest.mark.parametrize("plan", ["P1", "P2", "P3", "P8", "P5", "P6", "P4", "P7"])
 def test_multi_gpu_plans(plan, tmp_path):
     if not torch.cuda.is_available():
