@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(256) reduce_adam_kernel(const ChunkDesc* __res
         pk.x = *reinterpret_cast<uint32_t*>(&lo);
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
         *reinterpret_cast<uint2*>(pd.param + i) = pk;
+        for (int q = 0; q < pd.n_push; ++q) *reinterpret_cast<uint2*>(pd.push[q] + i) = pk;  // NVLink stores
       }
     }
     return;
@@ -72,6 +73,7 @@ __global__ void __launch_bounds__(256) reduce_adam_kernel(const ChunkDesc* __res
       pd.master[i] = th;
       __nv_bfloat16 b = __float2bfloat16_rn(th);
       pd.param[i] = *reinterpret_cast<uint16_t*>(&b);
+      for (int q = 0; q < pd.n_push; ++q) pd.push[q][i] = *reinterpret_cast<uint16_t*>(&b);
     }
   }
 }

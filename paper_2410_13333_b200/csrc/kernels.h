@@ -68,6 +68,9 @@ struct PieceDesc {
   float* v;
   float* rgrad;              // reduced gradient out (sum_i w_i g_i)
   uint16_t* param;           // owner's bf16 copy of the piece
+  int n_push;                // peer-memory param push (fused ZeRO-1 all-gather): other holders' copies
+  int pad2_;
+  uint16_t* push[15];
 };
 struct ChunkDesc {
   int piece;

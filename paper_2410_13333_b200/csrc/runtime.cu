@@ -12,6 +12,7 @@
 //     (readings R4, R9), NCCL P2P per refined piece, one group;
 //   * migration to a new plan in 4-layer packs, one grouped NCCL send/recv each;
 //   * probe and straggler emulation.
+#include <cuda.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -98,6 +99,11 @@ struct Layout {
   size_t state_bytes = 0, grads_bytes = 0, work_bytes = 0;
   ncclComm_t tp_comm = nullptr;
   std::vector<int> prev_ranks, next_ranks;  // adjacent stages' members
+  // peer memory (CUDA IPC over NVLink): every other rank's layout with its state / grads arena
+  // pointers mapped into this process; p2p == true when every rank mapped every peer.
+  std::vector<std::unique_ptr<Layout>> peer;
+  std::vector<void*> ipc_opened;
+  bool p2p = false;
 };
 
 // bump allocator over an arena whose base may be 0 (sizing pass)
@@ -338,6 +344,16 @@ static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
   int64_t stage_off = 0;
   for (TState& s : L.ts) {
     const int64_t c = s.t.cols;
+    const size_t ti = &s - &L.ts[0];
+    // pointer to element e of tensor ti in rank r's grad / param buffer (own or peer-mapped)
+    auto peer_grad = [&](int r, int64_t e) {
+      TState& q = r == rank ? s : L.peer[r]->ts[ti];
+      return q.grad + (e - q.rows.b * c);
+    };
+    auto peer_param = [&](int r, int64_t e) {
+      TState& q = r == rank ? s : L.peer[r]->ts[ti];
+      return q.param + (e - q.rows.b * c);
+    };
     for (const Piece& pc : pieces(cfg, p, s.t)) {
       const int64_t len = pc.e1 - pc.e0;
       // contributions
@@ -348,12 +364,14 @@ static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
         if (p.pipes[i].n_micro <= 0) continue;
         const int hld = sync_holder(cfg, p.pipes[i], s.t, pc.row0);
         const float w = (float)((double)p.pipes[i].n_micro * p.b / p.B);
-        if (hld == rank && pc.owner != rank) {
+        if (hld == rank && pc.owner != rank && !L.p2p) {
           L.gops.push_back({s.grad + (pc.e0 - s.rows.b * c), (size_t)len, ncclFloat, pc.owner, true});
         }
         if (pc.owner == rank) {
           if (hld == rank) {
             pd.src[pd.n_src] = s.grad + (pc.e0 - s.rows.b * c);
+          } else if (L.p2p) {
+            pd.src[pd.n_src] = peer_grad(hld, pc.e0);  // read the holder's gradient over NVLink
           } else {
             float* dst = L.staging + stage_off;
             stage_off += (len + 3) / 4 * 4;  // keep every slot 16-byte aligned
@@ -376,10 +394,13 @@ static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
       }
       for (int hr : holders) {
         if (hr == pc.owner) continue;
-        if (rank == pc.owner)
+        if (L.p2p) {
+          if (rank == pc.owner) pd.push[pd.n_push++] = peer_param(hr, pc.e0);  // NVLink store in the Adam kernel
+        } else if (rank == pc.owner) {
           L.pops.push_back({s.param + (pc.e0 - s.rows.b * c), (size_t)len, ncclBfloat16, hr, true});
-        else if (rank == hr)
+        } else if (rank == hr) {
           L.pops.push_back({s.param + (pc.e0 - s.rows.b * c), (size_t)len, ncclBfloat16, pc.owner, false});
+        }
       }
       if (pc.owner == rank) {
         size_t idx = 0;
@@ -394,6 +415,7 @@ static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
         bool vec = (len % 4 == 0) && ((uintptr_t)pd.param % 8 == 0);
         for (uintptr_t q : {(uintptr_t)pd.master, (uintptr_t)pd.m, (uintptr_t)pd.v, (uintptr_t)pd.rgrad}) vec &= q % 16 == 0;
         for (int k = 0; k < pd.n_src; ++k) vec &= (uintptr_t)pd.src[k] % 16 == 0;
+        for (int k = 0; k < pd.n_push; ++k) vec &= (uintptr_t)pd.push[k] % 8 == 0;
         pd.vec = vec ? 1 : 0;
         const int pid = (int)L.pieces.size();
         L.pieces.push_back(pd);
@@ -406,12 +428,106 @@ static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
 
 static malleus_status free_layout(malleus_ctx* ctx, Layout* L) {
   if (!L) return MALLEUS_OK;
+  for (void* p : L->ipc_opened) cudaIpcCloseMemHandle(p);
+  L->ipc_opened.clear();
+  L->peer.clear();
+  L->p2p = false;
   if (L->d_pieces) cudaFree(L->d_pieces);
   if (L->d_chunks) cudaFree(L->d_chunks);
   if (L->tp_comm) ncclCommDestroy(L->tp_comm);
   L->d_pieces = nullptr;
   L->d_chunks = nullptr;
   L->tp_comm = nullptr;
+  return MALLEUS_OK;
+}
+
+// CUDA IPC exchange of the state and grads arenas (collective).  Each rank publishes, per arena,
+// an IPC handle of the enclosing allocation and the arena's offset in it; every rank opens the
+// others' handles and rebuilds their layouts (the bump-allocator arithmetic is deterministic) so
+// it can address any peer's parameter / gradient rows directly over NVLink.  If any rank fails
+// to map any peer, all ranks fall back to the NCCL point-to-point path (p2p = false).
+struct IpcInfo {
+  cudaIpcMemHandle_t h[2];
+  unsigned long long off[2];
+  int ok, pad;
+};
+typedef CUresult (*PFN_getAddrRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+static malleus_status map_peers(malleus_ctx* ctx, Layout& L, const malleus_arenas* a) {
+  L.peer.clear();
+  L.peer.resize(ctx->world);
+  L.p2p = false;
+  if (ctx->world == 1 || getenv("MALLEUS_NO_P2P")) return MALLEUS_OK;
+  static PFN_getAddrRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      get_range = reinterpret_cast<PFN_getAddrRange>(fn);
+  }
+  IpcInfo mine{};
+  mine.ok = get_range != nullptr;
+  void* bases[2] = {a->state, a->grads};
+  for (int i = 0; i < 2 && mine.ok; ++i) {
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, (CUdeviceptr)bases[i]) != CUDA_SUCCESS ||
+        cudaIpcGetMemHandle(&mine.h[i], (void*)base) != cudaSuccess) {
+      mine.ok = 0;
+      cudaGetLastError();
+      break;
+    }
+    mine.off[i] = (unsigned long long)((uintptr_t)bases[i] - (uintptr_t)base);
+  }
+  IpcInfo* dbuf = nullptr;
+  CK(cudaMalloc(&dbuf, sizeof(IpcInfo) * ctx->world));
+  CK(cudaMemcpy(dbuf + ctx->rank, &mine, sizeof(IpcInfo), cudaMemcpyHostToDevice));
+  NK(ncclAllGather(dbuf + ctx->rank, dbuf, sizeof(IpcInfo), ncclUint8, ctx->world_comm, 0));
+  std::vector<IpcInfo> all(ctx->world);
+  CK(cudaMemcpy(all.data(), dbuf, sizeof(IpcInfo) * ctx->world, cudaMemcpyDeviceToHost));
+  cudaFree(dbuf);
+  bool ok = true;
+  for (auto& x : all) ok &= x.ok != 0;
+  for (int r = 0; r < ctx->world && ok; ++r) {
+    if (r == ctx->rank) continue;
+    char* ptrs[2] = {nullptr, nullptr};
+    for (int i = 0; i < 2; ++i) {
+      if (i == 1 && memcmp(&all[r].h[1], &all[r].h[0], sizeof(cudaIpcMemHandle_t)) == 0) {
+        ptrs[1] = ptrs[0] - all[r].off[0];  // both arenas inside one allocation
+      } else {
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, all[r].h[i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          ok = false;
+          break;
+        }
+        L.ipc_opened.push_back(p);
+        ptrs[i] = static_cast<char*>(p);
+      }
+      ptrs[i] += all[r].off[i];
+    }
+    if (!ok) break;
+    auto P = std::make_unique<Layout>();
+    build_shape(ctx->cfg, L.plan, r, *P);
+    assign(ctx->cfg, r, *P, (uintptr_t)ptrs[0], (uintptr_t)ptrs[1], 0);
+    L.peer[r] = std::move(P);
+  }
+  // every rank must agree on the path
+  int* dok = nullptr;
+  int flag = ok ? 1 : 0;
+  CK(cudaMalloc(&dok, sizeof(int)));
+  CK(cudaMemcpy(dok, &flag, sizeof(int), cudaMemcpyHostToDevice));
+  NK(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, ctx->world_comm, 0));
+  CK(cudaMemcpy(&flag, dok, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(dok);
+  L.p2p = flag == 1;
+  if (!L.p2p) {
+    for (void* p : L.ipc_opened) cudaIpcCloseMemHandle(p);
+    L.ipc_opened.clear();
+    L.peer.clear();
+    L.peer.resize(ctx->world);
+  }
   return MALLEUS_OK;
 }
 
@@ -431,6 +547,7 @@ static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_are
   if (((uintptr_t)a->state | (uintptr_t)a->grads | (uintptr_t)a->work) & 255)
     return fail(ctx, MALLEUS_E_ARG, "arenas must be 256-byte aligned");
   assign(ctx->cfg, ctx->rank, L, (uintptr_t)a->state, (uintptr_t)a->grads, (uintptr_t)a->work);
+  RET(map_peers(ctx, L, a));
   build_sync(ctx->cfg, ctx->rank, L);
   // TP communicator: color = global stage index
   int color = NCCL_SPLIT_NOCOLOR, key = 0;
@@ -641,6 +758,20 @@ static malleus_status pp_exchange(malleus_ctx* ctx, const uint16_t* send_fwd, ui
 static malleus_status grad_sync_impl(malleus_ctx* ctx, const malleus_adam_cfg* a, cudaStream_t st) {
   Layout& L = *ctx->L;
   ev_begin(ctx, st, CAT_SYNC);
+  if (L.p2p) {
+    // peer-memory path: barrier (every rank's gradients final), fused reduce + AdamW reading the
+    // other pipelines' gradient rows and storing the updated bf16 rows into every holder over
+    // NVLink, barrier (all pushes landed; nobody still reads a gradient that the next step overwrites)
+    float* bar = L.loss_acc + 2;
+    NK(ncclAllReduce(bar, bar, 1, ncclFloat, ncclSum, ctx->world_comm, st));
+    AdamHyper hp{a->lr, a->beta1, a->beta2, a->eps, a->weight_decay,
+                 (float)(1.0 - std::pow((double)a->beta1, a->step)),
+                 (float)(1.0 - std::pow((double)a->beta2, a->step)), a->apply_update};
+    CK(reduce_adam((int)L.chunks.size(), L.d_chunks, L.d_pieces, hp, st));
+    NK(ncclAllReduce(bar, bar, 1, ncclFloat, ncclSum, ctx->world_comm, st));
+    ev_end(ctx, st);
+    return MALLEUS_OK;
+  }
   if (!L.gops.empty()) {
     NK(ncclGroupStart());
     for (auto& o : L.gops) {
@@ -1053,6 +1184,50 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
           add_copy(keep, src, dst, (hi - lo) * 4);
         }
       }
+  }
+  if (O.p2p) {
+    // peer-memory path: every rank pulls its deltas straight from the sources' old arenas over
+    // NVLink (no packing, no staging), in the same launch as its keep-copies, then a barrier so
+    // no rank frees an old arena that a peer is still reading.
+    const auto trp = migration_transfers(ctx->cfg, O.plan, np);
+    std::vector<CopyDesc> descs = keep;
+    for (auto& t : trp) {
+      if (t.dst != me) {
+        if (t.src == me) sent += (t.e1 - t.e0) * (t.kind == MALLEUS_KIND_PARAM ? 2 : 4);
+        continue;
+      }
+      size_t es;
+      const char* src = locate_ptr(*O.peer[t.src], t.tensor, t.kind, t.e0, &es);
+      char* dst = locate_ptr(*NL, t.tensor, t.kind, t.e0, &es);
+      add_copy(descs, src, dst, (t.e1 - t.e0) * (long long)es);
+      recvd += (t.e1 - t.e0) * es;
+    }
+    CopyDesc* d_desc = nullptr;
+    if (!descs.empty()) {
+      CK(cudaMalloc(&d_desc, descs.size() * sizeof(CopyDesc)));
+      CK(cudaMemcpy(d_desc, descs.data(), descs.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    }
+    float* bar = NL->loss_acc + 2;
+    CK(cudaMemsetAsync(bar, 0, sizeof(float), st));
+    NK(ncclAllReduce(bar, bar, 1, ncclFloat, ncclSum, ctx->world_comm, st));  // everyone ready
+    CK(cudaStreamSynchronize(st));
+    const auto t1 = std::chrono::steady_clock::now();
+    CK(copy_ranges((int)descs.size(), d_desc, st));
+    NK(ncclAllReduce(bar, bar, 1, ncclFloat, ncclSum, ctx->world_comm, st));  // everyone done reading
+    CK(cudaStreamSynchronize(st));
+    const double xfer = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    if (d_desc) cudaFree(d_desc);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    free_layout(ctx, ctx->L.get());
+    ctx->L = std::move(NL);
+    if (stats) {
+      stats->bytes_sent = sent;
+      stats->bytes_recv = recvd;
+      stats->seconds = xfer;
+      stats->n_packs = std::max(1, (ctx->cfg.n_layers + 3) / 4);
+      stats->total_seconds = secs;
+    }
+    return MALLEUS_OK;
   }
   // (2) remote deltas in packs of 4 consecutive layers: per pack and peer, the
   // outgoing ranges are packed into one contiguous buffer (K11 pack), exchanged with one grouped
