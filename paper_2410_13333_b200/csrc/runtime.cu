@@ -591,6 +591,12 @@ static malleus_status gemm(malleus_ctx* ctx, int M, int N, int K, const void* A,
                            cudaStream_t st) {
   GemmDesc g{M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, mode};
   CK(gemm_bf16(g, st));
+  static const bool dbg = getenv("MALLEUS_DEBUG_SYNC") != nullptr;  // debugging aid: serialize + trace
+  if (dbg) {
+    fprintf(stderr, "[malleus] gemm M=%d N=%d K=%d amn=%d bmn=%d mode=%d ...", M, N, K, amn, bmn, mode);
+    CK(cudaStreamSynchronize(st));
+    fprintf(stderr, " ok\n");
+  }
   return MALLEUS_OK;
 }
 
@@ -652,6 +658,7 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   RET(gemm(ctx, T, 3 * nd, h, Y.a1, h, false, P.wqkv, h, false, Y.qkv, 3 * nd, GEMM_STORE_BF16, st));
   CK(rope_inplace(T, c.seq_len, L.n_loc, d, Y.qkv, 3LL * nd, 0, c.rope_theta, false, st));
   CK(attention_fwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
+  if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   RET(gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, L.part, h, GEMM_STORE_F32, st));
   RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
   duty_begin(ctx, 1, st);
@@ -691,6 +698,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, T, nd, h, dx1, h, false, P.wo, h, false, L.dout, nd, GEMM_STORE_BF16, st));
   RET(gemm(ctx, nd, h, T, Y.o, nd, true, dx1, h, true, P.dwo, h, wm, st));
   CK(attention_bwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, L.dqkv, L.dsum, st));
+  if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
   RET(gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, L.part, h, GEMM_STORE_F32, st));
   RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
