@@ -178,9 +178,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         mbar_wait(o_done, (i - 1) & 1);
         tc_fence_after();
       }
-      if (mt > m_used + 8.f) {
+      // tcgen05.ld / st are warp-collective (.sync.aligned): the rescale decision must be
+      // warp-uniform; lanes whose max did not grow scale by exactly 1
+      if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
+        const float m_new = fmaxf(m_used, mt);
         if (i > 0) {
-          const float f = exp2f(m_used - mt);
+          const float f = exp2f(m_used - m_new);
           l *= f;
 #pragma unroll 1
           for (int c = 0; c < DH / 32; ++c) {
@@ -193,7 +196,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
           }
           tmem_wait_st();
         }
-        m_used = mt;
+        m_used = m_new;
       }
       // P = exp2(s - m_used) -> bf16 into the swizzled A tile (2 panels of 64 keys)
 #pragma unroll
