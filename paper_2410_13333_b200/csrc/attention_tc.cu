@@ -25,7 +25,7 @@ constexpr int Q_BYTES = 2 * PANEL;             // 32 KB
 constexpr int KV_STAGE = 4 * PANEL;            // K (2 panels) + V (2 panels)
 constexpr int P_BYTES = 2 * PANEL;
 constexpr int KV_STAGES = 2;
-constexpr int SMEM_TC = Q_BYTES + KV_STAGES * KV_STAGE + P_BYTES + 1024 + 1024;
+constexpr int SMEM_TC = Q_BYTES + KV_STAGES * KV_STAGE + 2 * P_BYTES + 1024 + 1024;  // P double-buffered
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -49,15 +49,15 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + Q_BYTES;
   uint8_t* sP = sKV + KV_STAGES * KV_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;              // [2]
   uint64_t* kv_empty = bars + 3;             // [2]
   uint64_t* s_full = bars + 5;               // [2]
   uint64_t* s_empty = bars + 7;              // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* o_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* p_full = bars + 9;   // [2] (P buffer j & 1)
+  uint64_t* o_done = bars + 11;  // [2] (PV of tile j completes on o_done[j & 1])
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;
@@ -74,8 +74,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4);
     }
-    mbar_init(p_full, 4);
-    mbar_init(o_done, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -110,16 +109,17 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       const uint32_t aq = smem_u32(sQ), ap = smem_u32(sP);
       auto issue_pv = [&](int j) {
         const int st = j & 1;
-        mbar_wait(p_full, j & 1);
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t v = smem_u32(sKV + st * KV_STAGE + 2 * PANEL);
+        const uint32_t apj = ap + (j & 1) * P_BYTES;
 #pragma unroll
         for (int kk = 0; kk < TK / 16; ++kk) {
-          const uint64_t ad = umma_desc_sw128(ap + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024);
+          const uint64_t ad = umma_desc_sw128(apj + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = umma_desc_sw128(v + kk * 2048, PANEL, 1024);
           umma_f16(tbase + 256, ad, bd, id_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(o_done);
+        umma_commit(&o_done[j & 1]);
         umma_commit(&kv_empty[st]);
       };
       mbar_wait(q_full, 0);
@@ -173,9 +173,9 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       }
 #pragma unroll
       for (int j = 0; j < TK; ++j) mt = fmaxf(mt, sv[j]);
-      // previous PV must be done before O may be rescaled and before P is overwritten
-      if (i > 0) {
-        mbar_wait(o_done, (i - 1) & 1);
+      // P buffer i & 1 is free once PV_{i-2} is done
+      if (i > 1) {
+        mbar_wait(&o_done[i & 1], ((i - 2) >> 1) & 1);
         tc_fence_after();
       }
       // tcgen05.ld / st are warp-collective (.sync.aligned): the rescale decision must be
@@ -183,6 +183,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
         const float m_new = fmaxf(m_used, mt);
         if (i > 0) {
+          mbar_wait(&o_done[(i - 1) & 1], ((i - 1) >> 1) & 1);  // O stable: PV_{i-1} done
+          tc_fence_after();
           const float f = exp2f(m_used - m_new);
           l *= f;
 #pragma unroll 1
@@ -211,15 +213,15 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         w.x = pack_bf16(p[0], p[1]); w.y = pack_bf16(p[2], p[3]);
         w.z = pack_bf16(p[4], p[5]); w.w = pack_bf16(p[6], p[7]);
         const int panel = ch >> 3, c16 = ch & 7;
-        *reinterpret_cast<uint4*>(prow + panel * PANEL + ((c16 ^ (r & 7)) << 4)) = w;
+        *reinterpret_cast<uint4*>(prow + (i & 1) * P_BYTES + panel * PANEL + ((c16 ^ (r & 7)) << 4)) = w;
       }
       fence_proxy_async();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[i & 1]);
     }
-    // epilogue: O / l
-    mbar_wait(o_done, (n_tiles - 1) & 1);
+    // epilogue: O / l (MMAs complete in issue order: the last PV implies all)
+    mbar_wait(&o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l;
     __nv_bfloat16* orow = o + (long long)(b * s + q) * nd + head * DH;
