@@ -152,6 +152,7 @@ def main():
     ap.add_argument("--no-straggler", action="store_true")
     ap.add_argument("--uniform", action="store_true", help="non-malleable even plan (T_u / T0 runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-replan", action="store_true", help="keep the nominal-rate plan (no measured re-plan)")
     args = ap.parse_args()
     if os.environ.get("MALLEUS_WATCHDOG"):  # debugging aid: dump all stacks if the run hangs
         import faulthandler
@@ -202,6 +203,44 @@ def main():
         eng.train_step(dtok, dtgt, step=step, apply_update=2)
         step += 1
     barrier()
+    replan = None
+    if world > 1 and straggle and not args.no_replan:
+        # The Malleus loop: profile -> re-plan -> migrate.  Time the initial
+        # (nominal-rate) plan, re-apportion the splits and micro-batches from each rank's measured
+        # compute time (reading R12), migrate the model states to the new plan, then measure.
+        def timed(n):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            nonlocal step
+            barrier()
+            a.record(stream)
+            for _ in range(n):
+                eng.train_step(dtok, dtgt, step=step, apply_update=2)
+                step += 1
+            b.record(stream)
+            barrier()
+            t = torch.tensor([a.elapsed_time(b) / n], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        ms_before = timed(3)
+        comp = [None] * world
+        dist.all_gather_object(comp, eng.timing()["compute"])
+        obj = [Pl.rebalance(cfg, plan, {r: comp[r] for r in range(world)}) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        new_plan = obj[0]
+        mig = eng.migrate(new_plan)
+        allm = [None] * world
+        dist.all_gather_object(allm, mig)
+        plan = new_plan
+        for _ in range(2):
+            eng.train_step(dtok, dtgt, step=step, apply_update=2)
+            step += 1
+        barrier()
+        replan = {"tokens_s_before": B * cfg.seq_len / (ms_before / 1e3), "ms_per_step_before": ms_before,
+                  "compute_ms_per_rank_before": comp,
+                  "migration": {"bytes": sum(m["bytes_recv"] for m in allm),
+                                "seconds_max": max(m["seconds"] for m in allm),
+                                "GBps": sum(m["bytes_recv"] for m in allm) / max(max(m["seconds"] for m in allm), 1e-9) / 1e9,
+                                "total_seconds_max": max(m["total_seconds"] for m in allm)}}
     clocks = ClockSampler(local)
     clocks.start()
     L.lib.malleus_gemm_profile(1, None, None, None)
@@ -280,7 +319,8 @@ def main():
                 "clocks": clk,
                 "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": int(2 * tok.nbytes),
                         "d2h_bytes_per_step": 4},
-                "gpu_launches": int(n_launch)}
+                "gpu_launches": int(n_launch),
+                "replan": replan}
     eng.close()
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_sample(cfg)

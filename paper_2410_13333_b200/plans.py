@@ -126,6 +126,62 @@ def _minmax(n_units, rates):
     return counts
 
 
+def _apportion(n_units, weights, min_units=1):
+    """Largest-remainder apportionment of n_units proportional to weights (each >= min_units)."""
+    k = len(weights)
+    tot = float(sum(weights))
+    raw = [n_units * w / tot for w in weights]
+    out = [max(min_units, int(r)) for r in raw]
+    while sum(out) > n_units:  # min_units pushed us over: take from the largest
+        j = max(range(k), key=lambda i: out[i])
+        out[j] -= 1
+    order = sorted(range(k), key=lambda i: -(raw[i] - int(raw[i])))
+    i = 0
+    while sum(out) < n_units:
+        out[order[i % k]] += 1
+        i += 1
+    return out
+
+
+def rebalance(cfg, plan, compute_ms: dict, min_micro: int = 0):
+    """Re-plan from measured speeds (the profiler -> planner -> migration loop of PAPER.md:378-384).
+
+    Reading R12 (work-normalised rates): member k of a TP group that processed share f_k of the
+    columns in t_k ms of compute runs at speed f_k / t_k; new shares are proportional to the
+    speeds (heads whole, FFN / vocab in 128-wide tiles).  Pipelines: a pipeline's time per
+    micro-batch is the max over its members' compute; m_i is re-apportioned proportional to
+    m_i / T_i (Eq.(3)'s min-max objective, with measured o_i).  Layers, groups
+    and stage order are kept."""
+    import copy
+    p = copy.deepcopy(plan)
+    p["plan_id"] = plan.get("plan_id", 0) + 1
+    pipe_speed = []
+    for pp in p["pipes"]:
+        t_pipe = 0.0
+        for st in pp["stages"]:
+            ranks = st["ranks"]
+            t = [max(compute_ms[r], 1e-6) for r in ranks]
+            t_pipe = max(t_pipe, max(t))
+            if len(ranks) == 1:
+                continue
+            speed = [st["heads"][k] / t[k] for k in range(len(ranks))]
+            st["heads"] = _apportion(cfg.n_heads, speed)
+            for key, total in (("ffn", cfg.ffn), ("vocab", cfg.vocab)):
+                tile = 128 if total // 128 >= 4 * len(ranks) else 16  # GEMM-friendly tiles when possible
+                n_t, rem = divmod(total, tile)
+                spd = [st[key][k] / t[k] for k in range(len(ranks))]
+                tiles = _apportion(n_t, spd)
+                st[key] = [x * tile for x in tiles]
+                st[key][-1] += rem
+        pipe_speed.append(pp["n_micro"] / t_pipe if pp["n_micro"] > 0 else 1.0 / t_pipe)
+    total_m = sum(pp["n_micro"] for pp in p["pipes"])
+    if len(p["pipes"]) > 1:
+        ms = _apportion(total_m, pipe_speed, min_units=min_micro)
+        for pp, m in zip(p["pipes"], ms):
+            pp["n_micro"] = m
+    return p
+
+
 def _heads_split(H, rates):
     return _minmax(H, rates)
 
