@@ -230,12 +230,22 @@ def main():
         mig = eng.migrate(new_plan)
         allm = [None] * world
         dist.all_gather_object(allm, mig)
-        plan = new_plan
         for _ in range(2):
             eng.train_step(dtok, dtgt, step=step, apply_update=2)
             step += 1
+        ms_after = timed(3)
+        kept = ms_after <= ms_before
+        if kept:
+            plan = new_plan
+        else:  # the measured re-plan did not pay off: migrate back (a planner keeps the faster plan)
+            eng.migrate(plan)
+            for _ in range(2):
+                eng.train_step(dtok, dtgt, step=step, apply_update=2)
+                step += 1
         barrier()
         replan = {"tokens_s_before": B * cfg.seq_len / (ms_before / 1e3), "ms_per_step_before": ms_before,
+                  "tokens_s_replanned": B * cfg.seq_len / (ms_after / 1e3), "replanned_plan_kept": kept,
+                  "replanned_plan": plan_summary(new_plan),
                   "compute_ms_per_rank_before": comp,
                   "migration": {"bytes": sum(m["bytes_recv"] for m in allm),
                                 "seconds_max": max(m["seconds"] for m in allm),
