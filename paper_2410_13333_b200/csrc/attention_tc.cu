@@ -40,6 +40,12 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// MUFU exp2 without the non-ftz fix-up sequence (inputs are <= 0 after max subtraction; ex2(-inf) = 0)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __global__ void __launch_bounds__(192, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bfloat16* __restrict__ o,
@@ -206,7 +212,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         float p[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          p[j] = exp2f(sv[ch * 8 + j] - m_used);
+          p[j] = ex2(sv[ch * 8 + j] - m_used);
           l += p[j];
         }
         uint4 w;
@@ -402,7 +408,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           const int qi = c * 32 + t;
-          float pv = exp2f(__uint_as_float(us[t]) * sl2 - sL[qi] * LOG2E);
+          float pv = ex2(fmaf(__uint_as_float(us[t]), sl2, -sL[qi] * LOG2E));
           if (diag && key > j * TQ + qi) pv = 0.f;
           p[t] = pv;
           ds[t] = pv * (__uint_as_float(ud[t]) - sD[qi]);
@@ -576,7 +582,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
         float ds[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
-          float pv = exp2f(__uint_as_float(us[t]) * sl2 - L2);
+          float pv = ex2(fmaf(__uint_as_float(us[t]), sl2, -L2));
           if (diag && i * TK + c * 32 + t > q) pv = 0.f;
           ds[t] = pv * (__uint_as_float(ud[t]) - Dq);
         }
