@@ -531,14 +531,16 @@ cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o,
   }
 }
 
+bool attention_bwd_fuses_rope(int s, int d) { return g_attn_variant == 0 && attention_fwd_tc_supported(s, d); }
+
 cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const void* o, const float* lse,
-                          const void* dout, void* dqkv, float* dsum, cudaStream_t st) {
+                          const void* dout, void* dqkv, float* dsum, cudaStream_t st, const float2* rope_cs) {
   if (s % 64) return cudaErrorInvalidValue;
   if (g_attn_variant == 0 && attention_fwd_tc_supported(s, d)) {
     const long long T = (long long)nb * s;
     attn_dsum_kernel<128><<<(unsigned)((T * n + 7) / 8), dim3(32, 8), 0, st>>>(
         s, n, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dsum, T); count_launch();
-    return attention_bwd_tc(nb, s, n, qkv, lse, dout, dqkv, dsum, st);
+    return attention_bwd_tc(nb, s, n, qkv, lse, dout, dqkv, dsum, rope_cs, st);
   }
   switch (d) {
     case 32: return bwd_impl<32>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);

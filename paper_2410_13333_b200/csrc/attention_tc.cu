@@ -47,7 +47,7 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bfloat16* __restrict__ o,
                    float* __restrict__ lse, float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -78,9 +78,9 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4);
+      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
     }
-    for (int i = 0; i < 2; ++i) { mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&p_full[i], 8); mbar_init(&o_done[i], 1); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -147,23 +147,42 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       issue_pv(n_tiles - 1);
     }
   } else {
-    // ---------------- softmax warps: thread = one query row
+    // ---------------- softmax: 8 warps, two per TMEM lane quarter; thread = half a query row
+    // (64 of the 128 keys of a tile).  The pair exchanges its partial row maxima through two
+    // spare TMEM columns (same lane) and a named barrier; each half writes its own P panel and
+    // owns half of the O columns for rescaling and the epilogue.
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;            // row within the 128-query block
     const int q = qb * TQ + r;                    // query position in the sequence
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = scale * LOG2E;
     float m_used = -INFINITY, l = 0.f;
-    uint8_t* prow = sP + r * 128;  // this row inside each 64-col panel (128 B per row)
+    uint8_t* prow = sP + half * PANEL + r * 128;  // this row of this half's 64-key panel
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory"); };
+    auto exchange = [&](float mine, int slot) -> float {  // returns the partner's value
+      uint32_t v = __float_as_uint(mine);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tbase + lane_off + 384 + slot * 2 + half),
+                   "r"(v) : "memory");
+      tmem_wait_st();
+      tc_fence_before();
+      pair_sync();
+      tc_fence_after();
+      uint32_t o;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(o)
+                   : "r"(tbase + lane_off + 384 + slot * 2 + (half ^ 1)) : "memory");
+      tmem_wait_ld();
+      return __uint_as_float(o);
+    };
     for (int i = 0; i < n_tiles; ++i) {
       const int sb = i & 1;
       mbar_wait(&s_full[sb], (i >> 1) & 1);
       tc_fence_after();
-      float sv[TK];
+      float sv[TK / 2];
 #pragma unroll
-      for (int c = 0; c < TK / 32; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t u[32];
-        tmem_ld32(tbase + lane_off + 128 * sb + c * 32, u);
+        tmem_ld32(tbase + lane_off + 128 * sb + half * 64 + c * 32, u);
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 32; ++j) sv[c * 32 + j] = __uint_as_float(u[j]) * sl2;
@@ -174,41 +193,42 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       float mt = -INFINITY;
       if (i == n_tiles - 1) {  // diagonal tile: keys > query masked
 #pragma unroll
-        for (int j = 0; j < TK; ++j)
-          if (i * TK + j > q) sv[j] = -INFINITY;
+        for (int j = 0; j < TK / 2; ++j)
+          if (i * TK + half * 64 + j > q) sv[j] = -INFINITY;
       }
 #pragma unroll
-      for (int j = 0; j < TK; ++j) mt = fmaxf(mt, sv[j]);
+      for (int j = 0; j < TK / 2; ++j) mt = fmaxf(mt, sv[j]);
+      mt = fmaxf(mt, exchange(mt, i & 1));  // full-row max of this tile
       // P buffer i & 1 is free once PV_{i-2} is done
       if (i > 1) {
         mbar_wait(&o_done[i & 1], ((i - 2) >> 1) & 1);
         tc_fence_after();
       }
-      // tcgen05.ld / st are warp-collective (.sync.aligned): the rescale decision must be
-      // warp-uniform; lanes whose max did not grow scale by exactly 1
+      // tcgen05.ld / st are warp-collective: the rescale decision is warp-uniform (and identical
+      // in both warps of the pair: same rows, same maxima); lanes whose max did not grow scale by 1
       if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
         const float m_new = fmaxf(m_used, mt);
         if (i > 0) {
           mbar_wait(&o_done[(i - 1) & 1], ((i - 1) >> 1) & 1);  // O stable: PV_{i-1} done
           tc_fence_after();
-          const float f = exp2f(m_used - m_new);
+          const float f = ex2(m_used - m_new);
           l *= f;
 #pragma unroll 1
-          for (int c = 0; c < DH / 32; ++c) {
+          for (int c = 0; c < 2; ++c) {
             uint32_t u[32];
-            tmem_ld32(tbase + lane_off + 256 + c * 32, u);
+            tmem_ld32(tbase + lane_off + 256 + half * 64 + c * 32, u);
             tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 32; ++j) u[j] = __float_as_uint(__uint_as_float(u[j]) * f);
-            tmem_st32(tbase + lane_off + 256 + c * 32, u);
+            tmem_st32(tbase + lane_off + 256 + half * 64 + c * 32, u);
           }
           tmem_wait_st();
         }
         m_used = m_new;
       }
-      // P = exp2(s - m_used) -> bf16 into the swizzled A tile (2 panels of 64 keys)
+      // P = exp2(s - m_used) -> bf16 into this half's swizzled 64-key panel
 #pragma unroll
-      for (int ch = 0; ch < TK / 8; ++ch) {
+      for (int ch = 0; ch < 8; ++ch) {
         float p[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -218,8 +238,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         uint4 w;
         w.x = pack_bf16(p[0], p[1]); w.y = pack_bf16(p[2], p[3]);
         w.z = pack_bf16(p[4], p[5]); w.w = pack_bf16(p[6], p[7]);
-        const int panel = ch >> 3, c16 = ch & 7;
-        *reinterpret_cast<uint4*>(prow + (i & 1) * P_BYTES + panel * PANEL + ((c16 ^ (r & 7)) << 4)) = w;
+        *reinterpret_cast<uint4*>(prow + (i & 1) * P_BYTES + ((ch ^ (r & 7)) << 4)) = w;
       }
       fence_proxy_async();
       tc_fence_before();
@@ -229,12 +248,13 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
     // epilogue: O / l (MMAs complete in issue order: the last PV implies all)
     mbar_wait(&o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
     tc_fence_after();
+    l += exchange(l, n_tiles & 1);  // the slot the last tile did not use
     const float inv = 1.f / l;
-    __nv_bfloat16* orow = o + (long long)(b * s + q) * nd + head * DH;
+    __nv_bfloat16* orow = o + (long long)(b * s + q) * nd + head * DH + half * 64;
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
+    for (int c = 0; c < 2; ++c) {
       uint32_t u[32];
-      tmem_ld32(tbase + lane_off + 256 + c * 32, u);
+      tmem_ld32(tbase + lane_off + 256 + half * 64 + c * 32, u);
       tmem_wait_ld();
       uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
@@ -247,7 +267,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         dst[v] = w;
       }
     }
-    lse[((long long)b * n + head) * s + q] = (m_used + log2f(l)) / LOG2E;
+    if (half == 0) lse[((long long)b * n + head) * s + q] = (m_used + log2f(l)) / LOG2E;
   }
   tc_fence_before();
   __syncthreads();
@@ -263,6 +283,41 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// One 128-wide fp32 TMEM row (this thread's lane) * scale -> bf16 global row, optionally rotated
+// by -phi (RoPE backward, half-split pairs (i, i+64); cs = this position's (cos, sin) row).
+__device__ __forceinline__ void store_row_rope(__nv_bfloat16* dst, uint32_t taddr, float scale, const float2* cs) {
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    uint32_t ua[32], ub[32];
+    tmem_ld32(taddr + c * 32, ua);       // cols 32c ..      (i)
+    tmem_ld32(taddr + 64 + c * 32, ub);  // cols 64 + 32c .. (i + 64)
+    tmem_wait_ld();
+    float a[32], bb[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float x = __uint_as_float(ua[j]) * scale, y = __uint_as_float(ub[j]) * scale;
+      if (cs) {
+        const float2 t = cs[c * 32 + j];
+        const float x2 = x * t.x + y * t.y;
+        y = y * t.x - x * t.y;
+        x = x2;
+      }
+      a[j] = x;
+      bb[j] = y;
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      uint4 wa, wb;
+      wa.x = pack_bf16(a[8 * v], a[8 * v + 1]); wa.y = pack_bf16(a[8 * v + 2], a[8 * v + 3]);
+      wa.z = pack_bf16(a[8 * v + 4], a[8 * v + 5]); wa.w = pack_bf16(a[8 * v + 6], a[8 * v + 7]);
+      wb.x = pack_bf16(bb[8 * v], bb[8 * v + 1]); wb.y = pack_bf16(bb[8 * v + 2], bb[8 * v + 3]);
+      wb.z = pack_bf16(bb[8 * v + 4], bb[8 * v + 5]); wb.w = pack_bf16(bb[8 * v + 6], bb[8 * v + 7]);
+      reinterpret_cast<uint4*>(dst + c * 32)[v] = wa;
+      reinterpret_cast<uint4*>(dst + 64 + c * 32)[v] = wb;
+    }
+  }
 }
 
 // write 32 consecutive bf16 (cols c0..c0+31 of row r) into a 2-panel K-major 128B-swizzled tile
@@ -287,7 +342,7 @@ constexpr int BWD1_SMEM = 7 * Q_BYTES + 1024 + 1024 + 1024;
 __global__ void __launch_bounds__(192, 1)
 attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s,
                        int n, const float* __restrict__ lse, const float* __restrict__ dsum,
-                       __nv_bfloat16* __restrict__ dqkv, float scale) {
+                       __nv_bfloat16* __restrict__ dqkv, float scale, const float2* __restrict__ rope_cs) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
@@ -428,27 +483,8 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
     tc_fence_after();
     __nv_bfloat16* dk = dqkv + (long long)(b * s + key) * 3 * nd + nd + head * DH;
     __nv_bfloat16* dv = dk + nd;
-#pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t uk[32], uv[32];
-      tmem_ld32(tbase + lane_off + 384 + c * 32, uk);
-      tmem_ld32(tbase + lane_off + 256 + c * 32, uv);
-      tmem_wait_ld();
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 wk, wv;
-        wk.x = pack_bf16(__uint_as_float(uk[8 * v]) * scale, __uint_as_float(uk[8 * v + 1]) * scale);
-        wk.y = pack_bf16(__uint_as_float(uk[8 * v + 2]) * scale, __uint_as_float(uk[8 * v + 3]) * scale);
-        wk.z = pack_bf16(__uint_as_float(uk[8 * v + 4]) * scale, __uint_as_float(uk[8 * v + 5]) * scale);
-        wk.w = pack_bf16(__uint_as_float(uk[8 * v + 6]) * scale, __uint_as_float(uk[8 * v + 7]) * scale);
-        wv.x = pack_bf16(__uint_as_float(uv[8 * v]), __uint_as_float(uv[8 * v + 1]));
-        wv.y = pack_bf16(__uint_as_float(uv[8 * v + 2]), __uint_as_float(uv[8 * v + 3]));
-        wv.z = pack_bf16(__uint_as_float(uv[8 * v + 4]), __uint_as_float(uv[8 * v + 5]));
-        wv.w = pack_bf16(__uint_as_float(uv[8 * v + 6]), __uint_as_float(uv[8 * v + 7]));
-        reinterpret_cast<uint4*>(dk + c * 32)[v] = wk;
-        reinterpret_cast<uint4*>(dv + c * 32)[v] = wv;
-      }
-    }
+    store_row_rope(dk, tbase + lane_off + 384, scale, rope_cs ? rope_cs + (long long)key * 64 : nullptr);
+    store_row_rope(dv, tbase + lane_off + 256, 1.f, nullptr);
   }
   tc_fence_before();
   __syncthreads();
@@ -466,7 +502,7 @@ constexpr int BWD2_SMEM = 3 * Q_BYTES + 2 * 2 * Q_BYTES + 1024 + 1024;
 __global__ void __launch_bounds__(192, 1)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s, int n,
                       const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                      float scale) {
+                      float scale, const float2* __restrict__ rope_cs) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -599,21 +635,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
     mbar_wait(ds_empty, (n_tiles - 1) & 1);  // last dQ MMA done
     tc_fence_after();
     __nv_bfloat16* dq = dqkv + (long long)(b * s + q) * 3 * nd + head * DH;
-#pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t u[32];
-      tmem_ld32(tbase + lane_off + 256 + c * 32, u);
-      tmem_wait_ld();
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(u[8 * v]) * scale, __uint_as_float(u[8 * v + 1]) * scale);
-        w.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * scale, __uint_as_float(u[8 * v + 3]) * scale);
-        w.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * scale, __uint_as_float(u[8 * v + 5]) * scale);
-        w.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * scale, __uint_as_float(u[8 * v + 7]) * scale);
-        reinterpret_cast<uint4*>(dq + c * 32)[v] = w;
-      }
-    }
+    store_row_rope(dq, tbase + lane_off + 256, scale, rope_cs ? rope_cs + (long long)q * 64 : nullptr);
   }
   tc_fence_before();
   __syncthreads();
@@ -653,7 +675,7 @@ static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long
 
 // dsum (= rowsum(dO * O)) must already be in `dsum`; writes dq, dk, dv column blocks of dqkv.
 cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float* lse, const void* dout,
-                             void* dqkv, const float* dsum, cudaStream_t st) {
+                             void* dqkv, const float* dsum, const float2* rope_cs, cudaStream_t st) {
   CUtensorMap tm, tmo;
   const long long T = (long long)nb * s;
   if (!map_rows(&tm, qkv, 3LL * n * DH, T) || !map_rows(&tmo, dout, (long long)n * DH, T)) return cudaErrorInvalidValue;
@@ -667,9 +689,9 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
   }
   const float scale = rsqrtf((float)DH);
   attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 192, BWD1_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
-                                                                      (__nv_bfloat16*)dqkv, scale); count_launch();
+                                                                      (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
   attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 192, BWD2_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
-                                                                     (__nv_bfloat16*)dqkv, scale); count_launch();
+                                                                     (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
   return cudaGetLastError();
 }
 
@@ -692,7 +714,7 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  attn_fwd_tc_kernel<<<dim3(s / TQ, n, nb), 192, SMEM_TC, st>>>(tm, s, n, (__nv_bfloat16*)o, lse,
+  attn_fwd_tc_kernel<<<dim3(s / TQ, n, nb), 320, SMEM_TC, st>>>(tm, s, n, (__nv_bfloat16*)o, lse,
                                                                 rsqrtf((float)DH)); count_launch();
   return cudaGetLastError();
 }

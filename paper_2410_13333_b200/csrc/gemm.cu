@@ -41,6 +41,8 @@ struct GemmParams {
   int mode;  // GEMM_STORE_BF16 / GEMM_STORE_F32 / GEMM_ACCUM_F32
   int vec_ok;  // rows of C are 16-byte aligned -> 128-bit stores
   int tma_epi; // C written by TMA store / reduce-add (CTA-pair kernel)
+  const float2* rope_cs;  // fused RoPE (bf16 TMA epilogue only), see GemmDesc
+  int rope_cols, rope_s;
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
@@ -113,6 +115,62 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
                                                   int row_box0, int col_base, uint8_t* stg, int& sbuf) {
   const int lane = threadIdx.x & 31;
   if (row_box0 >= p.M) return;
+  if (p.mode == GEMM_STORE_BF16 && p.rope_cs != nullptr && col_base < p.rope_cols) {
+    // QKV projection with RoPE fused (half-split pairs (i, i+64) of each 128-column head, reading
+    // R3): the two heads of this 256-column tile are rotated in registers before the bf16 store.
+    const int row = min(row_box0 + lane, p.M - 1);
+    const float2* cs = p.rope_cs + (long long)(row % p.rope_s) * 64;
+#pragma unroll 1
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int hc0 = col_base + h2 * 128;
+      uint32_t r0[32], r1[32], r2[32], r3[32];
+      tmem_ld32(taddr + h2 * 128, r0);
+      tmem_ld32(taddr + h2 * 128 + 32, r1);
+      tmem_ld32(taddr + h2 * 128 + 64, r2);
+      tmem_ld32(taddr + h2 * 128 + 96, r3);
+      tmem_wait_ld();
+      if (hc0 >= p.N) continue;
+      if (hc0 < p.rope_cols) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float2 c0 = cs[j], c1 = cs[32 + j];
+          const float a0 = __uint_as_float(r0[j]), b0 = __uint_as_float(r2[j]);
+          const float a1 = __uint_as_float(r1[j]), b1 = __uint_as_float(r3[j]);
+          r0[j] = __float_as_uint(a0 * c0.x - b0 * c0.y);
+          r2[j] = __float_as_uint(b0 * c0.x + a0 * c0.y);
+          r1[j] = __float_as_uint(a1 * c1.x - b1 * c1.y);
+          r3[j] = __float_as_uint(b1 * c1.x + a1 * c1.y);
+        }
+      }
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {  // unrolled: register arrays are selected statically
+        const uint32_t* ra = half ? r2 : r0;
+        const uint32_t* rb = half ? r3 : r1;
+        uint8_t* buf = stg + sbuf * 4096;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          const uint32_t* r = ch < 4 ? ra : rb;
+          const int o = (ch & 3) * 8;
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(r[o + 0]), __uint_as_float(r[o + 1]));
+          w.y = pack_bf16(__uint_as_float(r[o + 2]), __uint_as_float(r[o + 3]));
+          w.z = pack_bf16(__uint_as_float(r[o + 4]), __uint_as_float(r[o + 5]));
+          w.w = pack_bf16(__uint_as_float(r[o + 6]), __uint_as_float(r[o + 7]));
+          *reinterpret_cast<uint4*>(buf + lane * 128 + ((ch ^ (lane & 7)) << 4)) = w;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(tmC, buf, hc0 + half * 64, row_box0);
+          bulk_commit();
+        }
+        sbuf ^= 1;
+      }
+    }
+    return;
+  }
   if (p.mode == GEMM_STORE_BF16) {
 #pragma unroll 1
     for (int c = 0; c < 256 / 64; ++c) {
@@ -599,7 +657,10 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
     CUtensorMap tc;
     int tma_epi = vec_ok && g_tma_epi && make_map_c(&tc, g.C, g.N, g.M, g.ldc, g.mode != GEMM_STORE_BF16);
     if (!tma_epi) memset(&tc, 0, sizeof(tc));
-    GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, tma_epi};
+    const bool rope = tma_epi && g.rope_cs && g.mode == GEMM_STORE_BF16 && g.rope_cols % 128 == 0;
+    if (g.rope_done) *g.rope_done = rope;
+    GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, tma_epi, rope ? g.rope_cs : nullptr, g.rope_cols,
+                 g.rope_s};
     if (!g.a_mn && !g.b_mn) return launch2<false, false>(ta, tb, tc, p, st);
     if (!g.a_mn && g.b_mn) return launch2<false, true>(ta, tb, tc, p, st);
     if (g.a_mn && g.b_mn) return launch2<true, true>(ta, tb, tc, p, st);
@@ -611,7 +672,8 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
   if (!ok) return cudaErrorInvalidValue;
   const int esz = g.mode == GEMM_STORE_BF16 ? 2 : 4;
   const int vec_ok = ((g.ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0);
-  GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, 0};
+  if (g.rope_done) *g.rope_done = false;
+  GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, 0, nullptr, 0, 0};
   if (!g.a_mn && !g.b_mn) return launch<false, false>(ta, tb, p, st);
   if (!g.a_mn && g.b_mn) return launch<false, true>(ta, tb, p, st);
   if (g.a_mn && g.b_mn) return launch<true, true>(ta, tb, p, st);

@@ -20,6 +20,12 @@ struct GemmDesc {
   const void* B; long long ldb; bool b_mn;
   void* C; long long ldc;
   int mode;
+  // optional RoPE fused into the bf16 epilogue (QKV projection): columns [0, rope_cols) are heads
+  // of 128; row r is position r % rope_s; rope_cs = [rope_s][64] (cos, sin).  *rope_done tells the
+  // caller whether the kernel applied it (only the CTA-pair TMA epilogue does).
+  const float2* rope_cs = nullptr;
+  int rope_cols = 0, rope_s = 0;
+  bool* rope_done = nullptr;
 };
 cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st);
 
@@ -90,14 +96,17 @@ cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o,
                           cudaStream_t st);
 cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const void* o,
                           const float* lse, const void* dout, void* dqkv, float* dsum,
-                          cudaStream_t st);
+                          cudaStream_t st, const float2* rope_cs = nullptr);
 
 // tcgen05/TMEM/TMA forward for d = 128, s % 128 == 0 (attention_tc.cu)
 bool attention_fwd_tc_supported(int s, int d);
 cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st);
 void attention_set_variant(int v);
 cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float* lse, const void* dout,
-                             void* dqkv, const float* dsum, cudaStream_t st);
+                             void* dqkv, const float* dsum, const float2* rope_cs, cudaStream_t st);
+// true when attention_bwd with this (s, d) runs the tcgen05 kernels, which apply the RoPE backward
+// rotation to dq / dk in their epilogues when given a (cos, sin) table
+bool attention_bwd_fuses_rope(int s, int d);
 
 // ---- multi-range copy (copy.cu): migration pack / unpack / keep-copies
 struct CopyDesc {

@@ -85,6 +85,7 @@ struct Layout {
   std::vector<Slot> slot;
   // transient
   float *part = nullptr, *scratch = nullptr, *dsum = nullptr, *logits = nullptr, *stats = nullptr;
+  float2* rope_cs = nullptr;  // [seq_len][64] (cos, sin) for the fused RoPE (head_dim 128)
   float *gmax = nullptr, *sumtgt = nullptr, *loss_rows = nullptr, *loss_acc = nullptr;
   uint16_t *dxa = nullptr, *dxb = nullptr, *dxc = nullptr, *dyrecv = nullptr, *dqkv = nullptr, *dout = nullptr;
   uint16_t *dgu = nullptr, *du = nullptr, *dlogits = nullptr;
@@ -310,6 +311,7 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
     L.part = W.take<float>(T * h);
     L.scratch = W.take<float>(rmsnorm_bwd_scratch_floats((int)T, (int)h));
     L.dsum = W.take<float>(T * L.n_loc);
+    if (cfg.head_dim == 128) L.rope_cs = W.take<float2>((size_t)cfg.seq_len * 64);
     L.dxa = W.take<uint16_t>(T * h);
     L.dxb = W.take<uint16_t>(T * h);
     L.dxc = W.take<uint16_t>(T * h);
@@ -548,6 +550,16 @@ static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_are
     return fail(ctx, MALLEUS_E_ARG, "arenas must be 256-byte aligned");
   assign(ctx->cfg, ctx->rank, L, (uintptr_t)a->state, (uintptr_t)a->grads, (uintptr_t)a->work);
   RET(map_peers(ctx, L, a));
+  if (L.rope_cs) {  // (cos, sin)(pos * theta^(-2i/d)) in double precision (readings R2/R3)
+    const int d = ctx->cfg.head_dim, S = ctx->cfg.seq_len;
+    std::vector<float2> cs((size_t)S * 64);
+    for (int pos = 0; pos < S; ++pos)
+      for (int i = 0; i < 64; ++i) {
+        const double ang = pos * std::pow((double)ctx->cfg.rope_theta, -2.0 * i / d);
+        cs[(size_t)pos * 64 + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+      }
+    CK(cudaMemcpy(L.rope_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
   build_sync(ctx->cfg, ctx->rank, L);
   // TP communicator: color = global stage index
   int color = NCCL_SPLIT_NOCOLOR, key = 0;
@@ -655,8 +667,16 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   LayerPtrs& P = L.lp[li];
   duty_begin(ctx, 0, st);
   CK(rmsnorm_fwd(T, h, S.x[li], nullptr, nullptr, P.g1, c.rms_eps, Y.a1, Y.r1, st));
-  RET(gemm(ctx, T, 3 * nd, h, Y.a1, h, false, P.wqkv, h, false, Y.qkv, 3 * nd, GEMM_STORE_BF16, st));
-  CK(rope_inplace(T, c.seq_len, L.n_loc, d, Y.qkv, 3LL * nd, 0, c.rope_theta, false, st));
+  {  // QKV projection; RoPE fused into the epilogue when the kernel supports it
+    bool rope_done = false;
+    GemmDesc g{T, 3 * nd, h, Y.a1, h, false, P.wqkv, h, false, Y.qkv, 3 * nd, GEMM_STORE_BF16};
+    g.rope_cs = L.rope_cs;
+    g.rope_cols = 2 * nd;
+    g.rope_s = c.seq_len;
+    g.rope_done = &rope_done;
+    CK(gemm_bf16(g, st));
+    if (!rope_done) CK(rope_inplace(T, c.seq_len, L.n_loc, d, Y.qkv, 3LL * nd, 0, c.rope_theta, false, st));
+  }
   CK(attention_fwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
   if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   RET(gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, L.part, h, GEMM_STORE_F32, st));
@@ -697,9 +717,10 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   // attention
   RET(gemm(ctx, T, nd, h, dx1, h, false, P.wo, h, false, L.dout, nd, GEMM_STORE_BF16, st));
   RET(gemm(ctx, nd, h, T, Y.o, nd, true, dx1, h, true, P.dwo, h, wm, st));
-  CK(attention_bwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, L.dqkv, L.dsum, st));
+  CK(attention_bwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, L.dqkv, L.dsum, st, L.rope_cs));
   if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
-  CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
+  if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
+    CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
   RET(gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, L.part, h, GEMM_STORE_F32, st));
   RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
   RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
