@@ -2,14 +2,16 @@
 // and sequence lengths that are multiples of 128 (PAPER.md:780 FlashAttention).
 //
 // One CTA = 128 queries of one (sequence, head).  Warp roles:
-//   warp 0      TMA producer: Q once; K and V tiles of 128 keys through a 2-stage ring;
+//   warp 0      TMA producer: Q once; K and V tiles of 128 keys through separate 2-stage rings
+//               (K_i is released when S_i is done, a full tile before V_i, so its reload is hidden);
 //   warp 1      MMA issuer (one thread) + TMEM owner: S_i = Q K_i^T into one of two TMEM S buffers,
 //               then O += P_{i-1} V_{i-1} once the softmax warps have written P_{i-1};
-//   warps 2..5  softmax (one query row per thread): S row from TMEM, online max with lazy
+//   warps 2..9  softmax (two warps per query row, 64 keys each): S row from TMEM, online max with lazy
 //               rescaling (O in TMEM is rescaled only when the running max grows by > 2^8, FA4
 //               style; exact since numerator and denominator share the stale max), P (bf16) into
 //               a 128B-swizzled smem tile that is the A operand of the PV MMA; final O / l, LSE.
-// TMEM: S0 cols [0,128), S1 [128,256), O [256,384).  smem: Q 32 KB, 2 x (K 32 KB + V 32 KB), P 32 KB.
+// TMEM: S0 cols [0,128), S1 [128,256), O [256,384), row-max exchange [384,388).
+// smem: Q 32 KB, 2 x K 32 KB, 2 x V 32 KB, 2 x P 32 KB.
 // Output identical in layout to attention.cu: o [T, n*d] bf16, lse [nb, n, s] (natural log).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -26,6 +28,7 @@ constexpr int KV_STAGE = 4 * PANEL;            // K (2 panels) + V (2 panels)
 constexpr int P_BYTES = 2 * PANEL;
 constexpr int KV_STAGES = 2;
 constexpr int SMEM_TC = Q_BYTES + KV_STAGES * KV_STAGE + 2 * P_BYTES + 1024 + 1024;  // P double-buffered
+constexpr int K_BYTES = 2 * PANEL;             // one K (or V) tile of 128 keys
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -53,17 +56,20 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sKV = sQ + Q_BYTES;
-  uint8_t* sP = sKV + KV_STAGES * KV_STAGE;
+  uint8_t* sK = sQ + Q_BYTES;                // [2 stages] K tiles
+  uint8_t* sV = sK + KV_STAGES * K_BYTES;    // [2 stages] V tiles
+  uint8_t* sP = sV + KV_STAGES * K_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;              // [2]
-  uint64_t* kv_empty = bars + 3;             // [2]
+  uint64_t* k_full = bars + 1;               // [2]
+  uint64_t* k_empty = bars + 3;              // [2] K_i free once S_i = Q K_i^T is done
   uint64_t* s_full = bars + 5;               // [2]
   uint64_t* s_empty = bars + 7;              // [2]
   uint64_t* p_full = bars + 9;   // [2] (P buffer j & 1)
   uint64_t* o_done = bars + 11;  // [2] (PV of tile j completes on o_done[j & 1])
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* v_full = bars + 13;  // [2]
+  uint64_t* v_empty = bars + 15; // [2] V_j free once O += P_j V_j is done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;
@@ -77,7 +83,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
     tma_prefetch(&tm);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
     }
     for (int i = 0; i < 2; ++i) { mbar_init(&p_full[i], 8); mbar_init(&o_done[i], 1); }
@@ -97,15 +104,17 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       for (int i = 0; i < n_tiles; ++i) {
         const int st = i & 1;
         const uint32_t ph = (i >> 1) & 1;
-        mbar_wait(&kv_empty[st], ph ^ 1);
-        uint8_t* k = sKV + st * KV_STAGE;
-        uint8_t* v = k + 2 * PANEL;
+        uint8_t* k = sK + st * K_BYTES;
+        uint8_t* v = sV + st * K_BYTES;
         const int krow = b * s + i * TK;
-        mbar_arrive_expect_tx(&kv_full[st], KV_STAGE);
-        tma_load_2d(k, &tm, &kv_full[st], nd + head * DH, krow);
-        tma_load_2d(k + PANEL, &tm, &kv_full[st], nd + head * DH + 64, krow);
-        tma_load_2d(v, &tm, &kv_full[st], 2 * nd + head * DH, krow);
-        tma_load_2d(v + PANEL, &tm, &kv_full[st], 2 * nd + head * DH + 64, krow);
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], K_BYTES);
+        tma_load_2d(k, &tm, &k_full[st], nd + head * DH, krow);
+        tma_load_2d(k + PANEL, &tm, &k_full[st], nd + head * DH + 64, krow);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&v_full[st], K_BYTES);
+        tma_load_2d(v, &tm, &v_full[st], 2 * nd + head * DH, krow);
+        tma_load_2d(v + PANEL, &tm, &v_full[st], 2 * nd + head * DH + 64, krow);
       }
     }
   } else if (warp == 1) {
@@ -115,9 +124,10 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       const uint32_t aq = smem_u32(sQ), ap = smem_u32(sP);
       auto issue_pv = [&](int j) {
         const int st = j & 1;
+        mbar_wait(&v_full[st], (j >> 1) & 1);
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t v = smem_u32(sKV + st * KV_STAGE + 2 * PANEL);
+        const uint32_t v = smem_u32(sV + st * K_BYTES);
         const uint32_t apj = ap + (j & 1) * P_BYTES;
 #pragma unroll
         for (int kk = 0; kk < TK / 16; ++kk) {
@@ -126,15 +136,15 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
           umma_f16(tbase + 256, ad, bd, id_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&o_done[j & 1]);
-        umma_commit(&kv_empty[st]);
+        umma_commit(&v_empty[st]);
       };
       mbar_wait(q_full, 0);
       for (int i = 0; i < n_tiles; ++i) {
         const int st = i & 1, sb = i & 1;
-        mbar_wait(&kv_full[st], (i >> 1) & 1);
+        mbar_wait(&k_full[st], (i >> 1) & 1);
         mbar_wait(&s_empty[sb], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t k = smem_u32(sKV + st * KV_STAGE);
+        const uint32_t k = smem_u32(sK + st * K_BYTES);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint64_t ad = umma_desc_sw128(aq + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024);
@@ -142,6 +152,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
           umma_f16(tbase + 128 * sb, ad, bd, id_qk, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[sb]);
+        umma_commit(&k_empty[st]);
         if (i > 0) issue_pv(i - 1);
       }
       issue_pv(n_tiles - 1);
@@ -287,9 +298,10 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 
 // One 128-wide fp32 TMEM row (this thread's lane) * scale -> bf16 global row, optionally rotated
 // by -phi (RoPE backward, half-split pairs (i, i+64); cs = this position's (cos, sin) row).
-__device__ __forceinline__ void store_row_rope(__nv_bfloat16* dst, uint32_t taddr, float scale, const float2* cs) {
+__device__ __forceinline__ void store_row_rope(__nv_bfloat16* dst, uint32_t taddr, float scale, const float2* cs,
+                                               int c0 = 0, int c1 = 2) {
 #pragma unroll 1
-  for (int c = 0; c < 2; ++c) {
+  for (int c = c0; c < c1; ++c) {
     uint32_t ua[32], ub[32];
     tmem_ld32(taddr + c * 32, ua);       // cols 32c ..      (i)
     tmem_ld32(taddr + 64 + c * 32, ub);  // cols 64 + 32c .. (i + 64)
@@ -339,7 +351,7 @@ __device__ __forceinline__ void st_sw128_32(uint8_t* tile, int r, int c0, const 
 //   (Q_j / dO_j tiles serve as K-major B for S^T / dP^T and, same bytes, as MN-major B for dK / dV).
 constexpr int BWD1_SMEM = 7 * Q_BYTES + 1024 + 1024 + 1024;
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
 attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s,
                        int n, const float* __restrict__ lse, const float* __restrict__ dsum,
                        __nv_bfloat16* __restrict__ dqkv, float scale, const float2* __restrict__ rope_cs) {
@@ -374,7 +386,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
     tma_prefetch(&tmo);
-    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], (i == 4 || i == 5) ? 4 : 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], (i == 4 || i == 5) ? 8 : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -443,6 +455,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
     }
   } else {
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;  // 8 compute warps: two per TMEM lane quarter
     const int r = quarter * 32 + lane;  // key row within the tile
     const int key = kb * TK + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
@@ -451,40 +464,43 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       const int it = j - kb;
       mbar_wait(sd_full, it & 1);
       tc_fence_after();
+      uint32_t us[2][32], ud[2][32];  // this warp's 64 query columns of S^T and dP^T
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tmem_ld32(tbase + lane_off + (2 * half + c) * 32, us[c]);
+        tmem_ld32(tbase + lane_off + 128 + (2 * half + c) * 32, ud[c]);
+      }
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sd_empty);
       if (it > 0) mbar_wait(pd_empty, (it - 1) & 1);  // P^T / dS^T smem free
       const bool diag = j == kb;
-#pragma unroll 1
-      for (int c = 0; c < TQ / 32; ++c) {
-        uint32_t us[32], ud[32];
-        tmem_ld32(tbase + lane_off + c * 32, us);
-        tmem_ld32(tbase + lane_off + 128 + c * 32, ud);
-        tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col = (2 * half + c) * 32;
         float p[32], ds[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
-          const int qi = c * 32 + t;
-          float pv = ex2(fmaf(__uint_as_float(us[t]), sl2, -sL[qi] * LOG2E));
+          const int qi = col + t;
+          float pv = ex2(fmaf(__uint_as_float(us[c][t]), sl2, -sL[qi] * LOG2E));
           if (diag && key > j * TQ + qi) pv = 0.f;
           p[t] = pv;
-          ds[t] = pv * (__uint_as_float(ud[t]) - sD[qi]);
+          ds[t] = pv * (__uint_as_float(ud[c][t]) - sD[qi]);
         }
-        st_sw128_32(sP, r, c * 32, p);
-        st_sw128_32(sS, r, c * 32, ds);
+        st_sw128_32(sP, r, col, p);
+        st_sw128_32(sS, r, col, ds);
       }
-      tc_fence_before();
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(sd_empty);
-        mbar_arrive(pd_full);
-      }
+      if (lane == 0) mbar_arrive(pd_full);
     }
     mbar_wait(done, 0);
     tc_fence_after();
     __nv_bfloat16* dk = dqkv + (long long)(b * s + key) * 3 * nd + nd + head * DH;
     __nv_bfloat16* dv = dk + nd;
-    store_row_rope(dk, tbase + lane_off + 384, scale, rope_cs ? rope_cs + (long long)key * 64 : nullptr);
-    store_row_rope(dv, tbase + lane_off + 256, 1.f, nullptr);
+    store_row_rope(dk, tbase + lane_off + 384, scale, rope_cs ? rope_cs + (long long)key * 64 : nullptr, half, half + 1);
+    store_row_rope(dv, tbase + lane_off + 256, 1.f, nullptr, half, half + 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -499,7 +515,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
 //   S = Q K_i^T, dP = dO V_i^T (M = queries); dS -> smem; dQ += dS K_i (K_i as MN-major B)
 constexpr int BWD2_SMEM = 3 * Q_BYTES + 2 * 2 * Q_BYTES + 1024 + 1024;
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s, int n,
                       const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
                       float scale, const float2* __restrict__ rope_cs) {
@@ -530,7 +546,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
     tma_prefetch(&tmo);
-    for (int i = 0; i < 9; ++i) mbar_init(&bars[i], (i == 6 || i == 7) ? 4 : 1);
+    for (int i = 0; i < 9; ++i) mbar_init(&bars[i], (i == 6 || i == 7) ? 8 : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -598,6 +614,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
     }
   } else {
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;
     const int q = qb * TQ + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
@@ -607,35 +624,40 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
     for (int i = 0; i < n_tiles; ++i) {
       mbar_wait(sd_full, i & 1);
       tc_fence_after();
-      if (i > 0) mbar_wait(ds_empty, (i - 1) & 1);
+      // this warp's 64 key columns of S and dP into registers, then hand the TMEM back at once so
+      // the next tile's S / dP MMAs overlap this tile's arithmetic
+      uint32_t us[2][32], ud[2][32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tmem_ld32(tbase + lane_off + (2 * half + c) * 32, us[c]);
+        tmem_ld32(tbase + lane_off + 128 + (2 * half + c) * 32, ud[c]);
+      }
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sd_empty);
+      if (i > 0) mbar_wait(ds_empty, (i - 1) & 1);  // dS smem free: dQ MMA of tile i-1 done
       const bool diag = i == n_tiles - 1;
-#pragma unroll 1
-      for (int c = 0; c < TK / 32; ++c) {
-        uint32_t us[32], ud[32];
-        tmem_ld32(tbase + lane_off + c * 32, us);
-        tmem_ld32(tbase + lane_off + 128 + c * 32, ud);
-        tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col = (2 * half + c) * 32;
         float ds[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
-          float pv = ex2(fmaf(__uint_as_float(us[t]), sl2, -L2));
-          if (diag && i * TK + c * 32 + t > q) pv = 0.f;
-          ds[t] = pv * (__uint_as_float(ud[t]) - Dq);
+          float pv = ex2(fmaf(__uint_as_float(us[c][t]), sl2, -L2));
+          if (diag && i * TK + col + t > q) pv = 0.f;
+          ds[t] = pv * (__uint_as_float(ud[c][t]) - Dq);
         }
-        st_sw128_32(sS, r, c * 32, ds);
+        st_sw128_32(sS, r, col, ds);
       }
-      tc_fence_before();
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(sd_empty);
-        mbar_arrive(ds_full);
-      }
+      if (lane == 0) mbar_arrive(ds_full);
     }
     mbar_wait(ds_empty, (n_tiles - 1) & 1);  // last dQ MMA done
     tc_fence_after();
     __nv_bfloat16* dq = dqkv + (long long)(b * s + q) * 3 * nd + head * DH;
-    store_row_rope(dq, tbase + lane_off + 256, scale, rope_cs ? rope_cs + (long long)q * 64 : nullptr);
+    store_row_rope(dq, tbase + lane_off + 256, scale, rope_cs ? rope_cs + (long long)q * 64 : nullptr, half, half + 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -688,9 +710,9 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
     attr = true;
   }
   const float scale = rsqrtf((float)DH);
-  attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 192, BWD1_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
+  attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 320, BWD1_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
                                                                       (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
-  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 192, BWD2_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
+  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
                                                                      (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
   return cudaGetLastError();
 }

@@ -105,6 +105,10 @@ struct Layout {
   std::vector<std::unique_ptr<Layout>> peer;
   std::vector<void*> ipc_opened;
   bool p2p = false;
+  // TP reduction over peer memory (tp_reduce.cu): double-buffered fp32 partials + flag block
+  float* tpp[2] = {nullptr, nullptr};
+  unsigned long long* tpflags = nullptr;
+  unsigned long long tp_epoch = 0;
 };
 
 // bump allocator over an arena whose base may be 0 (sizing pass)
@@ -309,6 +313,11 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
       }
     }
     L.part = W.take<float>(T * h);
+    if (L.TP > 1) {
+      L.tpp[0] = W.take<float>(T * h);
+      L.tpp[1] = W.take<float>(T * h);
+      L.tpflags = W.take<unsigned long long>(TPF_WORDS);
+    }
     L.scratch = W.take<float>(rmsnorm_bwd_scratch_floats((int)T, (int)h));
     L.dsum = W.take<float>(T * L.n_loc);
     if (cfg.head_dim == 128) L.rope_cs = W.take<float2>((size_t)cfg.seq_len * 64);
@@ -449,8 +458,8 @@ static malleus_status free_layout(malleus_ctx* ctx, Layout* L) {
 // it can address any peer's parameter / gradient rows directly over NVLink.  If any rank fails
 // to map any peer, all ranks fall back to the NCCL point-to-point path (p2p = false).
 struct IpcInfo {
-  cudaIpcMemHandle_t h[2];
-  unsigned long long off[2];
+  cudaIpcMemHandle_t h[3];
+  unsigned long long off[3];
   int ok, pad;
 };
 typedef CUresult (*PFN_getAddrRange)(CUdeviceptr*, size_t*, CUdeviceptr);
@@ -470,8 +479,8 @@ static malleus_status map_peers(malleus_ctx* ctx, Layout& L, const malleus_arena
   }
   IpcInfo mine{};
   mine.ok = get_range != nullptr;
-  void* bases[2] = {a->state, a->grads};
-  for (int i = 0; i < 2 && mine.ok; ++i) {
+  void* bases[3] = {a->state, a->grads, a->work};
+  for (int i = 0; i < 3 && mine.ok; ++i) {
     CUdeviceptr base = 0;
     size_t size = 0;
     if (get_range(&base, &size, (CUdeviceptr)bases[i]) != CUDA_SUCCESS ||
@@ -493,10 +502,13 @@ static malleus_status map_peers(malleus_ctx* ctx, Layout& L, const malleus_arena
   for (auto& x : all) ok &= x.ok != 0;
   for (int r = 0; r < ctx->world && ok; ++r) {
     if (r == ctx->rank) continue;
-    char* ptrs[2] = {nullptr, nullptr};
-    for (int i = 0; i < 2; ++i) {
-      if (i == 1 && memcmp(&all[r].h[1], &all[r].h[0], sizeof(cudaIpcMemHandle_t)) == 0) {
-        ptrs[1] = ptrs[0] - all[r].off[0];  // both arenas inside one allocation
+    char* ptrs[3] = {nullptr, nullptr, nullptr};
+    for (int i = 0; i < 3; ++i) {
+      int same = -1;  // arenas inside one allocation share its mapping
+      for (int q = 0; q < i; ++q)
+        if (memcmp(&all[r].h[i], &all[r].h[q], sizeof(cudaIpcMemHandle_t)) == 0) same = q;
+      if (same >= 0) {
+        ptrs[i] = ptrs[same] - all[r].off[same];
       } else {
         void* p = nullptr;
         if (cudaIpcOpenMemHandle(&p, all[r].h[i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
@@ -512,7 +524,7 @@ static malleus_status map_peers(malleus_ctx* ctx, Layout& L, const malleus_arena
     if (!ok) break;
     auto P = std::make_unique<Layout>();
     build_shape(ctx->cfg, L.plan, r, *P);
-    assign(ctx->cfg, r, *P, (uintptr_t)ptrs[0], (uintptr_t)ptrs[1], 0);
+    assign(ctx->cfg, r, *P, (uintptr_t)ptrs[0], (uintptr_t)ptrs[1], (uintptr_t)ptrs[2]);
     L.peer[r] = std::move(P);
   }
   // every rank must agree on the path
@@ -549,6 +561,11 @@ static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_are
   if (((uintptr_t)a->state | (uintptr_t)a->grads | (uintptr_t)a->work) & 255)
     return fail(ctx, MALLEUS_E_ARG, "arenas must be 256-byte aligned");
   assign(ctx->cfg, ctx->rank, L, (uintptr_t)a->state, (uintptr_t)a->grads, (uintptr_t)a->work);
+  // TP flag blocks start at zero on every member before any peer can signal (map_peers ends
+  // with a world all-reduce, which orders this memset before every later kernel of every rank)
+  L.tp_epoch = 0;
+  if (L.tpflags) CK(cudaMemset(L.tpflags, 0, TPF_WORDS * sizeof(unsigned long long)));
+  CK(cudaDeviceSynchronize());
   RET(map_peers(ctx, L, a));
   if (L.rope_cs) {  // (cos, sin)(pos * theta^(-2i/d)) in double precision (readings R2/R3)
     const int d = ctx->cfg.head_dim, S = ctx->cfg.seq_len;
@@ -625,6 +642,50 @@ static malleus_status tp_allreduce(malleus_ctx* ctx, float* buf, size_t n, ncclR
   return MALLEUS_OK;
 }
 
+// ---- TP reduction over NVLink peer memory (tp_reduce.cu), fused with residual / RMSNorm
+static bool tp_peer(const Layout& L) { return L.TP > 1 && L.p2p && L.tpflags != nullptr; }
+// where the next row-parallel GEMM writes its fp32 partial
+static float* tp_part(Layout& L) { return tp_peer(L) ? L.tpp[(L.tp_epoch + 1) & 1] : L.part; }
+static Layout& member_layout(Layout& L, int j) {
+  const int r = L.plan.pipes[L.pipe].stages[L.stage].ranks[j];
+  return L.peer[r] ? *L.peer[r] : L;
+}
+// sel(M, a, j) fills member j's destinations a.d0/d1/d2[j] from its layout M
+template <class Sel>
+static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const float* part, const void* x, const void* g,
+                                     Sel sel, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  duty_end(ctx, st);
+  ev_begin(ctx, st, CAT_TP);
+  TpArgs a{};
+  a.k = L.TP;
+  a.me = L.member;
+  a.T = L.T;
+  a.h = ctx->cfg.hidden;
+  a.mode = mode;
+  a.eps = ctx->cfg.rms_eps;
+  a.epoch = ++L.tp_epoch;
+  a.x = x;
+  a.g = g;
+  const int buf = (int)(a.epoch & 1);
+  for (int j = 0; j < L.TP; ++j) {
+    Layout& M = member_layout(L, j);
+    a.part[j] = j == L.member ? part : M.tpp[buf];
+    a.flags[j] = M.tpflags;
+    sel(M, a, j);
+  }
+  CK(tp_reduce(a, st));
+  ev_end(ctx, st);
+  return MALLEUS_OK;
+}
+
+// backward input gradients: L.part = sum_j P_j on every member (peer kernel, else NCCL in place)
+static malleus_status tp_sum(malleus_ctx* ctx, float* pb, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  if (!tp_peer(L)) return tp_allreduce(ctx, L.part, (size_t)L.T * ctx->cfg.hidden, ncclSum, st);
+  return tp_reduce_peer(ctx, TP_SUM, pb, nullptr, nullptr, [&](Layout& M, TpArgs& a, int j) { a.d0[j] = M.part; }, st);
+}
+
 // DUTY straggler emulation: every compute segment (the kernels between two TP collectives) is
 // bracketed by CUDA events; after it a spin kernel of (x - 1) * t_segment is enqueued on the same
 // stream, where t_segment is a moving average of that segment's own measured duration (events are
@@ -679,17 +740,33 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   }
   CK(attention_fwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
   if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
-  RET(gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, L.part, h, GEMM_STORE_F32, st));
-  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
-  duty_begin(ctx, 1, st);
-  CK(rmsnorm_fwd(T, h, S.x[li], L.part, Y.x1, P.g2, c.rms_eps, Y.a2, Y.r2, st));
+  float* pb = tp_part(L);
+  RET(gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, pb, h, GEMM_STORE_F32, st));
+  if (tp_peer(L)) {  // x1 = x + sum P, a2 = RMSNorm(x1) in one peer-memory kernel
+    RET(tp_reduce_peer(ctx, TP_RESID_NORM, pb, S.x[li], P.g2, [&](Layout& M, TpArgs& a, int j) {
+      const SlotLayer& Z = M.slot[si].L[li];
+      a.d0[j] = Z.x1; a.d1[j] = Z.a2; a.d2[j] = Z.r2;
+    }, st));
+    duty_begin(ctx, 1, st);
+  } else {
+    RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+    duty_begin(ctx, 1, st);
+    CK(rmsnorm_fwd(T, h, S.x[li], L.part, Y.x1, P.g2, c.rms_eps, Y.a2, Y.r2, st));
+  }
   RET(gemm(ctx, T, 2 * F, h, Y.a2, h, false, P.wgu, h, false, Y.gu, 2 * F, GEMM_STORE_BF16, st));
   CK(swiglu_fwd(T, F, Y.gu, Y.u, st));
-  RET(gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, L.part, h, GEMM_STORE_F32, st));
-  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
-  duty_begin(ctx, 2, st);
-  CK(residual_add((long long)T * h, Y.x1, L.part, S.x[li + 1], st));
-  duty_end(ctx, st);
+  pb = tp_part(L);
+  RET(gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, pb, h, GEMM_STORE_F32, st));
+  if (tp_peer(L)) {  // x[l+1] = x1 + sum P
+    RET(tp_reduce_peer(ctx, TP_RESID, pb, Y.x1, nullptr, [&](Layout& M, TpArgs& a, int j) {
+      a.d0[j] = M.slot[si].x[li + 1];
+    }, st));
+  } else {
+    RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+    duty_begin(ctx, 2, st);
+    CK(residual_add((long long)T * h, Y.x1, L.part, S.x[li + 1], st));
+    duty_end(ctx, st);
+  }
   return MALLEUS_OK;
 }
 
@@ -709,9 +786,10 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, T, F, h, dy, h, false, P.wd, h, false, L.du, F, GEMM_STORE_BF16, st));
   RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
   CK(swiglu_bwd(T, F, Y.gu, L.du, L.dgu, st));
-  RET(gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, L.part, h, GEMM_STORE_F32, st));
+  float* pb = tp_part(L);
+  RET(gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, pb, h, GEMM_STORE_F32, st));
   RET(gemm(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
-  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  RET(tp_sum(ctx, pb, st));
   duty_begin(ctx, 4, st);
   CK(rmsnorm_bwd(T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st));
   // attention
@@ -721,9 +799,10 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
     CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
-  RET(gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, L.part, h, GEMM_STORE_F32, st));
+  pb = tp_part(L);
+  RET(gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, pb, h, GEMM_STORE_F32, st));
   RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
-  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  RET(tp_sum(ctx, pb, st));
   duty_begin(ctx, 5, st);
   CK(rmsnorm_bwd(T, h, S.x[li], P.g1, Y.r1, L.part, dx1, dx, P.dg1, L.scratch, st));
   duty_end(ctx, st);
@@ -751,9 +830,10 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
              L.loss_rows, st));
   if (L.member == 0)
     CK(reduce_loss(T, L.loss_rows, (float)(1.0 / ((double)L.plan.B * c.seq_len)), L.loss_acc, 1, st));
-  RET(gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, L.part, h, GEMM_STORE_F32, st));
+  float* pb = tp_part(L);
+  RET(gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, pb, h, GEMM_STORE_F32, st));
   RET(gemm(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, first ? GEMM_STORE_F32 : GEMM_ACCUM_F32, st));
-  RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+  RET(tp_sum(ctx, pb, st));
   duty_begin(ctx, 8, st);
   CK(rmsnorm_bwd(T, h, S.x[L.n_local], L.gf, S.rf, L.part, nullptr, S.dlast, L.dgf, L.scratch, st));
   duty_end(ctx, st);

@@ -78,3 +78,25 @@ def test_multi_gpu_plans(plan, tmp_path):
     assert p.returncode == 0, "\n".join(l for l in (p.stdout + p.stderr).splitlines()
                                         if "Error" in l or "error" in l or "rank" in l)[-6000:]
     _assert_ok(json.load(open(out)))
+
+
+def test_tp_peer_reduce_matches_nccl(tmp_path):
+    """The fused peer-memory TP reduction (tp_reduce.cu: reduce-scatter + push, fused residual and
+    RMSNorm) against the NCCL all-reduce path (MALLEUS_NO_P2P=1) on P2 (TP 2, uneven heads), C1_MED:
+    with two members every row sum is one fp32 addition on both paths and the norm arithmetic is
+    the same, so the losses of a 3-step run must agree bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = {}
+    for tag, extra in (("peer", {}), ("nccl", {"MALLEUS_NO_P2P": "1"})):
+        out = tmp_path / f"{tag}.json"
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+               "--master-addr=127.0.0.1", "--master-port=29535", os.path.join(ROOT, "tests", "mp_worker.py"), "P2",
+               str(out), "3", "c1m"]
+        p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env={**os.environ, **extra})
+        assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+        res[tag] = json.load(open(out))
+        _assert_ok(res[tag])
+    assert res["peer"]["losses"] == res["nccl"]["losses"], (res["peer"]["losses"], res["nccl"]["losses"])

@@ -37,5 +37,11 @@ for nb, s, n, d in [(1, 2048, 32, 128), (1, 4096, 16, 128), (2, 2048, 16, 128)]:
     # reference: torch SDPA (flash) for context
     q = torch.randn(nb, n, s, d, device="cuda", dtype=torch.bfloat16)
     ref = bench(lambda: torch.nn.functional.scaled_dot_product_attention(q, q, q, is_causal=True))
+    qg = q.clone().requires_grad_(True)
+    out = torch.nn.functional.scaled_dot_product_attention(qg, qg, qg, is_causal=True)
+    g = torch.randn_like(out)
+    refb = bench(lambda: torch.autograd.grad(out, qg, g, retain_graph=True))
+    tb2 = bench(b)  # re-time ours after the others (first-call effects)
     print(f"nb={nb} s={s} n={n} d={d}: fwd {tf*1e3:.0f} us {flops/tf/1e9:.0f} TF | bwd {tb*1e3:.0f} us "
-          f"{2.5*flops/tb/1e9:.0f} TF | torch sdpa fwd {ref*1e3:.0f} us {flops/ref/1e9:.0f} TF", flush=True)
+          f"{2.5*flops/tb/1e9:.0f} TF (again {tb2*1e3:.0f} us) | torch sdpa fwd {ref*1e3:.0f} us "
+          f"{flops/ref/1e9:.0f} TF bwd {refb*1e3:.0f} us {2.5*flops/refb/1e9:.0f} TF", flush=True)
