@@ -82,3 +82,23 @@ extern "C" malleus_status malleus_k_attention_variant(int32_t variant) {
   attention_set_variant(variant);
   return MALLEUS_OK;
 }
+
+extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, int32_t h, int32_t mode, float eps,
+                                              uint64_t epoch, const float* const* part, uint64_t* const* flags,
+                                              void* const* d0, void* const* d1, float* const* d2, const void* x,
+                                              const void* g, void* stream) {
+  if (k < 2 || k > MAX_TP || !part || !flags || !d0) return MALLEUS_E_ARG;
+  if (mode == TP_RESID_NORM && (!d1 || !d2 || !g)) return MALLEUS_E_ARG;
+  if (mode != TP_SUM && !x) return MALLEUS_E_ARG;
+  TpArgs a{};
+  a.k = k; a.me = me; a.T = T; a.h = h; a.mode = mode; a.eps = eps; a.epoch = epoch;
+  a.x = x; a.g = g;
+  for (int j = 0; j < k; ++j) {
+    if (!part[j] || !flags[j] || !d0[j]) return MALLEUS_E_ARG;
+    a.part[j] = part[j];
+    a.flags[j] = reinterpret_cast<unsigned long long*>(flags[j]);
+    a.d0[j] = d0[j];
+    if (mode == TP_RESID_NORM) { a.d1[j] = d1[j]; a.d2[j] = d2[j]; }
+  }
+  return cu(tp_reduce(a, (cudaStream_t)stream));
+}

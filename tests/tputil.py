@@ -1,0 +1,73 @@
+"""Single-process, multi-device driver of malleus_k_tp_reduce (one member per visible GPU, peer
+access enabled between them) for the TP-reduction parity test and tools/tp_bench.py."""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from paper_2410_13333_b200 import _lib as L
+
+TPF_WORDS = 64
+
+
+def enable_peer_access(k: int) -> None:
+    from cuda.bindings import runtime as rt  # cuda-python
+    for i in range(k):
+        rt.cudaSetDevice(i)
+        for j in range(k):
+            if i != j:
+                err, = rt.cudaDeviceEnablePeerAccess(j, 0)
+                if err not in (rt.cudaError_t.cudaSuccess, rt.cudaError_t.cudaErrorPeerAccessAlreadyEnabled):
+                    raise RuntimeError(f"peer access {i}->{j}: {err}")
+    rt.cudaGetLastError()
+
+
+def _ptrs(ts):
+    arr = (C.c_void_p * len(ts))(*[t.data_ptr() if t is not None else None for t in ts])
+    return arr
+
+
+class Group:
+    """k members, member j on cuda:j: double-buffered partials, flag blocks, destinations."""
+
+    def __init__(self, k: int, T: int, h: int):
+        self.k, self.T, self.h = k, T, h
+        dev = [torch.device("cuda", j) for j in range(k)]
+        self.part = [[torch.zeros(T, h, device=d) for d in dev] for _ in range(2)]
+        self.flags = [torch.zeros(TPF_WORDS, dtype=torch.int64, device=d) for d in dev]
+        self.out32 = [torch.zeros(T, h, device=d) for d in dev]
+        self.x1 = [torch.zeros(T, h, dtype=torch.bfloat16, device=d) for d in dev]
+        self.a = [torch.zeros(T, h, dtype=torch.bfloat16, device=d) for d in dev]
+        self.rstd = [torch.zeros(T, device=d) for d in dev]
+        self.epoch = 0
+        for d in dev:
+            torch.cuda.synchronize(d)
+
+    def launch(self, mode: int, x=None, g=None, eps: float = 1e-5) -> None:
+        """One reduction of the partials in buffer (epoch + 1) & 1; all members launched
+        asynchronously on their devices' current streams."""
+        self.epoch += 1
+        buf = self.epoch & 1
+        parts = _ptrs(self.part[buf])
+        flags = _ptrs(self.flags)
+        if mode == 0:
+            d0, d1, d2 = _ptrs(self.out32), None, None
+        elif mode == 1:
+            d0, d1, d2 = _ptrs(self.x1), _ptrs(self.a), _ptrs(self.rstd)
+        else:
+            d0, d1, d2 = _ptrs(self.x1), None, None
+        for j in range(self.k):
+            with torch.cuda.device(j):
+                st = torch.cuda.current_stream().cuda_stream
+                r = L.lib.malleus_k_tp_reduce(self.k, j, self.T, self.h, mode, eps, self.epoch,
+                                              C.cast(parts, C.c_void_p), C.cast(flags, C.c_void_p),
+                                              C.cast(d0, C.c_void_p), C.cast(d1, C.c_void_p) if d1 else None,
+                                              C.cast(d2, C.c_void_p) if d2 else None,
+                                              x[j].data_ptr() if x is not None else None,
+                                              g[j].data_ptr() if g is not None else None, st)
+                assert r == 0, r
+
+    def sync(self) -> None:
+        for j in range(self.k):
+            torch.cuda.synchronize(j)
