@@ -14,24 +14,26 @@
 //
 // Synchronisation (one flag block of 64 u64 per member, in its work arena; epochs count the TP
 // reductions of the current plan, identical on every member because they run the same schedule):
-//   ready[j]  = epoch: member j's partial for this epoch is complete (written by every CTA of j's
-//               kernel before it reads anything; the partial came from an earlier kernel on j's stream)
-//   done[j]  += 1 per CTA of member j that finished pushing its rows into this member's buffers
-//   ticket    local CTA counter: the last CTA to finish waits until done[j] == epoch * grid for all j,
-//             so the kernel completes only when every row of this member's output has landed.
+//   ready[j]  = epoch: member j's partial for this epoch is complete (written by CTA 0 of j's
+//               kernel; the partial came from an earlier kernel on j's stream)
+//   ticket    local CTA counter (each CTA fences its stores system-wide, then takes a ticket)
+//   done[j]   = epoch: every CTA of member j finished pushing its rows (written by j's last CTA);
+//             this member's last CTA waits for done[j] == epoch for all j, so the kernel completes
+//             only when every row of this member's output has landed.
 // Partials are double-buffered by epoch parity: member j overwrites P_j[e & 1] in epoch e + 2, after
 // it has seen ready(e + 1) from every member, i.e. after every member finished reading epoch e.
 // A member's output buffers (activations, or the fp32 sum) are written by peers in epoch e only
 // after this member's ready(e), i.e. after all its earlier stream work (readers of the previous
 // contents) completed.  A wait that exceeds 20 s traps (sticky CUDA error) instead of hanging.
 #include <cuda_bf16.h>
+#include <type_traits>
 #include "kernels.h"
 
 namespace mls {
 namespace {
 
-constexpr int TPR_THREADS = 128;
-constexpr int TPR_MAXV = 8;  // 8 vectors of 8 elements per thread: h <= 8192
+constexpr int TPR_THREADS = 256;
+constexpr int TPR_MAXV = 4;  // 4 vectors of 8 elements per thread: h <= 8192
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
@@ -87,66 +89,89 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
   return r;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(TPR_THREADS) tp_reduce_kernel(const __grid_constant__ TpArgs a) {
+// K > 0: member count known at compile time, V = vectors of 8 per thread (h <= 8 * V * TPR_THREADS):
+// the loads of up to KC members are issued before their adds.  K == 0: generic runtime k.
+template <int MODE, int K, int V>
+__global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_constant__ TpArgs a) {
+  constexpr int KC = V >= 4 ? 2 : 3;
   __shared__ float sh[TPR_THREADS / 32];
   __shared__ bool last;
-  const int k = a.k, me = a.me, h = a.h, nv = h / 8;
+  const int k = K > 0 ? K : a.k;
+  const int me = a.me, h = a.h, nv = h / 8;
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int j = 0; j < k; ++j) st_release_sys(a.flags[j] + TPF_READY + me, a.epoch);
+    // ready: only CTA 0 publishes (dispatched first, so it is resident whenever any CTA waits)
+    if (blockIdx.x == 0) {
+      __threadfence_system();
+      for (int j = 0; j < k; ++j) st_release_sys(a.flags[j] + TPF_READY + me, a.epoch);
+    }
     for (int j = 0; j < k; ++j) wait_geq(a.flags[me] + TPF_READY + j, a.epoch);
   }
   __syncthreads();
   const int r0 = (int)((long long)me * a.T / k), r1 = (int)((long long)(me + 1) * a.T / k);
   for (int row = r0 + blockIdx.x; row < r1; row += gridDim.x) {
     const long long rb = (long long)row * h;
-    float v[TPR_MAXV][8];
+    float4 acc[V][2];
+    float4 t[KC][V][2];
+    auto load = [&](float4 (&dst)[V][2], const float* base) {
 #pragma unroll
-    for (int i = 0; i < TPR_MAXV; ++i) {
-      const int c = threadIdx.x + i * TPR_THREADS;
-      if (c < nv) {
-        float s[8];
-        {
-          const float4 p0 = ldcg4(a.part[0] + rb + 8 * c), p1 = ldcg4(a.part[0] + rb + 8 * c + 4);
-          s[0] = p0.x; s[1] = p0.y; s[2] = p0.z; s[3] = p0.w; s[4] = p1.x; s[5] = p1.y; s[6] = p1.z; s[7] = p1.w;
+      for (int i = 0; i < V; ++i) {
+        const int c = threadIdx.x + i * TPR_THREADS;
+        if (c < nv) {
+          dst[i][0] = ldcg4(base + rb + 8 * c);
+          dst[i][1] = ldcg4(base + rb + 8 * c + 4);
         }
-        for (int j = 1; j < k; ++j) {
-          const float4 p0 = ldcg4(a.part[j] + rb + 8 * c), p1 = ldcg4(a.part[j] + rb + 8 * c + 4);
-          s[0] += p0.x; s[1] += p0.y; s[2] += p0.z; s[3] += p0.w;
-          s[4] += p1.x; s[5] += p1.y; s[6] += p1.z; s[7] += p1.w;
-        }
-        if (MODE == TP_SUM) {
+      }
+    };
+    auto add = [&](const float4 (&src)[V][2]) {
 #pragma unroll
-          for (int t = 0; t < 8; ++t) v[i][t] = s[t];
-        } else {
-          float xv[8];
-          unpack8(reinterpret_cast<const uint4*>(a.x)[(long long)row * nv + c], xv);
+      for (int i = 0; i < V; ++i)
 #pragma unroll
-          for (int t = 0; t < 8; ++t) v[i][t] = xv[t] + s[t];
+        for (int q = 0; q < 2; ++q) {
+          acc[i][q].x += src[i][q].x; acc[i][q].y += src[i][q].y;
+          acc[i][q].z += src[i][q].z; acc[i][q].w += src[i][q].w;
         }
+    };
+    load(acc, a.part[0]);
+    if (K > 0) {
+#pragma unroll
+      for (int j0 = 1; j0 < (K > 0 ? K : 1); j0 += KC) {  // members j0 .. j0+KC-1: loads, then adds in order
+#pragma unroll
+        for (int u = 0; u < KC; ++u)
+          if (j0 + u < K) load(t[u], a.part[j0 + u]);
+#pragma unroll
+        for (int u = 0; u < KC; ++u)
+          if (j0 + u < K) add(t[u]);
+      }
+    } else {
+      for (int j = 1; j < k; ++j) {
+        load(t[0], a.part[j]);
+        add(t[0]);
       }
     }
     if (MODE == TP_SUM) {
 #pragma unroll
-      for (int i = 0; i < TPR_MAXV; ++i) {
+      for (int i = 0; i < V; ++i) {
         const int c = threadIdx.x + i * TPR_THREADS;
-        if (c < nv) {
-          const float4 o0 = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
-          const float4 o1 = make_float4(v[i][4], v[i][5], v[i][6], v[i][7]);
+        if (c < nv)
           for (int j = 0; j < k; ++j) {
             float4* d = reinterpret_cast<float4*>(static_cast<float*>(a.d0[j]) + rb + 8 * c);
-            __stcg(d, o0);
-            __stcg(d + 1, o1);
+            __stcg(d, acc[i][0]);
+            __stcg(d + 1, acc[i][1]);
           }
-        }
       }
     } else {
+      float v[V][8];
       float ss = 0.f;
 #pragma unroll
-      for (int i = 0; i < TPR_MAXV; ++i) {
+      for (int i = 0; i < V; ++i) {
         const int c = threadIdx.x + i * TPR_THREADS;
         if (c < nv) {
+          float xv[8];
+          unpack8(reinterpret_cast<const uint4*>(a.x)[(long long)row * nv + c], xv);
+          const float sv[8] = {acc[i][0].x, acc[i][0].y, acc[i][0].z, acc[i][0].w,
+                               acc[i][1].x, acc[i][1].y, acc[i][1].z, acc[i][1].w};
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v[i][t] = xv[t] + sv[t];
           const uint4 q = pack8(v[i]);  // residual stream is bf16 (reading R6)
           for (int j = 0; j < k; ++j) __stcg(static_cast<uint4*>(a.d0[j]) + (long long)row * nv + c, q);
           if (MODE == TP_RESID_NORM) {
@@ -162,7 +187,7 @@ __global__ void __launch_bounds__(TPR_THREADS) tp_reduce_kernel(const __grid_con
         if (threadIdx.x == 0)
           for (int j = 0; j < k; ++j) __stcg(a.d2[j] + row, r);
 #pragma unroll
-        for (int i = 0; i < TPR_MAXV; ++i) {
+        for (int i = 0; i < V; ++i) {
           const int c = threadIdx.x + i * TPR_THREADS;
           if (c < nv) {
             float gg[8], o[8];
@@ -176,18 +201,19 @@ __global__ void __launch_bounds__(TPR_THREADS) tp_reduce_kernel(const __grid_con
       }
     }
   }
-  // completion: this CTA's pushes -> every member's done counter; the last local CTA waits for all
+  // completion: each CTA makes its stores visible system-wide and takes a local ticket; the last
+  // CTA of this member tells every member "done" and waits for every member's "done"
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    for (int j = 0; j < k; ++j) red_release_sys(a.flags[j] + TPF_DONE + me, 1ull);
     const unsigned long long t = atomicAdd(a.flags[me] + TPF_TICKET, 1ull);
     last = t + 1 == a.epoch * (unsigned long long)gridDim.x;
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
-    const unsigned long long target = a.epoch * (unsigned long long)gridDim.x;
-    for (int j = 0; j < k; ++j) wait_geq(a.flags[me] + TPF_DONE + j, target);
+    __threadfence_system();
+    for (int j = 0; j < k; ++j) st_release_sys(a.flags[j] + TPF_DONE + me, a.epoch);
+    for (int j = 0; j < k; ++j) wait_geq(a.flags[me] + TPF_DONE + j, a.epoch);
     __threadfence_system();
   }
 }
@@ -198,10 +224,26 @@ cudaError_t tp_reduce(const TpArgs& a, cudaStream_t st) {
   if (a.k < 2 || a.k > MAX_TP || a.me < 0 || a.me >= a.k || a.h % 8 || a.h > 8 * TPR_MAXV * TPR_THREADS ||
       a.T <= 0 || a.epoch == 0)
     return cudaErrorInvalidValue;
+  const int vpt = (a.h / 8 + TPR_THREADS - 1) / TPR_THREADS;
+  auto launch_kv = [&](auto mode_c, auto k_c) {
+    constexpr int M = decltype(mode_c)::value, K = decltype(k_c)::value;
+    if (vpt <= 1) tp_reduce_kernel<M, K, 1><<<TP_GRID, TPR_THREADS, 0, st>>>(a);
+    else if (vpt == 2) tp_reduce_kernel<M, K, 2><<<TP_GRID, TPR_THREADS, 0, st>>>(a);
+    else tp_reduce_kernel<M, K, TPR_MAXV><<<TP_GRID, TPR_THREADS, 0, st>>>(a);
+  };
+  auto launch = [&](auto mode_c) {
+    switch (a.k) {
+      case 2: launch_kv(mode_c, std::integral_constant<int, 2>{}); break;
+      case 3: launch_kv(mode_c, std::integral_constant<int, 3>{}); break;
+      case 4: launch_kv(mode_c, std::integral_constant<int, 4>{}); break;
+      case 8: launch_kv(mode_c, std::integral_constant<int, 8>{}); break;
+      default: launch_kv(mode_c, std::integral_constant<int, 0>{}); break;
+    }
+  };
   switch (a.mode) {
-    case TP_SUM: tp_reduce_kernel<TP_SUM><<<TP_GRID, TPR_THREADS, 0, st>>>(a); break;
-    case TP_RESID_NORM: tp_reduce_kernel<TP_RESID_NORM><<<TP_GRID, TPR_THREADS, 0, st>>>(a); break;
-    case TP_RESID: tp_reduce_kernel<TP_RESID><<<TP_GRID, TPR_THREADS, 0, st>>>(a); break;
+    case TP_SUM: launch(std::integral_constant<int, TP_SUM>{}); break;
+    case TP_RESID_NORM: launch(std::integral_constant<int, TP_RESID_NORM>{}); break;
+    case TP_RESID: launch(std::integral_constant<int, TP_RESID>{}); break;
     default: return cudaErrorInvalidValue;
   }
   count_launch();

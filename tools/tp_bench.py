@@ -23,8 +23,11 @@ for k in (2, 4, 8):
         G.sync()
         n = 50
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        # hold every device in a sleep kernel while the host enqueues all launches, so the timed
+        # region is GPU-bound (no host launch gaps, no member waiting for the host to reach it)
         for j in range(k):
             with torch.cuda.device(j):
+                torch.cuda._sleep(int(60e6))  # ~30 ms
                 ev[j][0].record()
         for _ in range(n):
             G.launch(mode, xs, gs)
