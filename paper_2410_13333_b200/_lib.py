@@ -102,7 +102,7 @@ _SIGS = {
     "malleus_k_rmsnorm_bwd": ([i32, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),
     "malleus_k_attention_fwd": ([i32, i32, i32, i32, vp, vp, vp, f32, vp], i32),
     "malleus_k_attention_bwd": ([i32, i32, i32, i32, vp, vp, vp, vp, vp, f32, vp], i32),
-    "malleus_k_tp_reduce": ([i32, i32, i32, i32, i32, f32, C.c_uint64, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+    "malleus_k_tp_reduce": ([i32, i32, i32, i32, i32, i32, f32, C.c_uint64, vp, vp, vp, vp, vp, vp, vp, vp], i32),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -83,14 +83,23 @@ extern "C" malleus_status malleus_k_attention_variant(int32_t variant) {
   return MALLEUS_OK;
 }
 
-extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, int32_t h, int32_t mode, float eps,
-                                              uint64_t epoch, const float* const* part, uint64_t* const* flags,
+static unsigned long long* trace = nullptr;  // MALLEUS_TP_TRACE: stamps of the last call (tools/tp_bench.py)
+
+extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, int32_t h, int32_t mode,
+                                              int32_t part_dtype, float eps, uint64_t epoch, const void* const* part,
+                                              uint64_t* const* flags,
                                               void* const* d0, void* const* d1, float* const* d2, const void* x,
                                               const void* g, void* stream) {
   if (k < 2 || k > MAX_TP || !part || !flags || !d0) return MALLEUS_E_ARG;
   if (mode == TP_RESID_NORM && (!d1 || !d2 || !g)) return MALLEUS_E_ARG;
   if (mode != TP_SUM && !x) return MALLEUS_E_ARG;
   TpArgs a{};
+  if (getenv("MALLEUS_TP_TRACE")) {
+    if (!trace && cudaMallocManaged(&trace, 4 * TP_GRID_MAX * 16 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
+    a.trace = trace ? trace + 4 * TP_GRID_MAX * me : nullptr;
+  }
+  if (part_dtype != MALLEUS_FP32 && part_dtype != MALLEUS_BF16) return MALLEUS_E_ARG;
+  a.part_bf16 = part_dtype == MALLEUS_BF16;
   a.k = k; a.me = me; a.T = T; a.h = h; a.mode = mode; a.eps = eps; a.epoch = epoch;
   a.x = x; a.g = g;
   for (int j = 0; j < k; ++j) {
@@ -102,3 +111,6 @@ extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, 
   }
   return cu(tp_reduce(a, (cudaStream_t)stream));
 }
+
+// debugging aid for tools/tp_bench.py: the globaltimer stamps of the last traced call per member
+extern "C" const unsigned long long* malleus_k_tp_trace_buffer() { return trace; }

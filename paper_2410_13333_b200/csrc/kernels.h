@@ -110,22 +110,25 @@ bool attention_bwd_fuses_rope(int s, int d);
 
 // ---- TP partial-sum reduction over NVLink peer memory, fused with residual / RMSNorm (tp_reduce.cu)
 constexpr int MAX_TP = 16;
-constexpr int TP_GRID = 592;  // fixed on every member (the completion counters count CTAs)
+constexpr int TP_GRID_MAX = 592;  // 4 CTAs of 256 threads per SM; the grid is a function of (T, k) only
 enum { TP_SUM = 0, TP_RESID_NORM = 1, TP_RESID = 2 };
 enum { TPF_READY = 0, TPF_DONE = 16, TPF_TICKET = 32, TPF_WORDS = 64 };  // u64 flag block layout
 struct TpArgs {
   int k, me, T, h, mode;
   float eps;
   unsigned long long epoch;              // 1, 2, ... per reduction under the current plan
-  const float* part[MAX_TP];             // member j's fp32 partial [T, h] for this epoch
+  const void* part[MAX_TP];              // member j's partial [T, h] for this epoch (fp32 or bf16)
+  int part_bf16;                         // partials are bf16 (summed in fp32, member order)
   unsigned long long* flags[MAX_TP];     // member j's flag block (TPF_WORDS u64)
   void* d0[MAX_TP];                      // member j's out: fp32 sum | bf16 x1 | bf16 x'
   void* d1[MAX_TP];                      // member j's normalised bf16 a (TP_RESID_NORM)
   float* d2[MAX_TP];                     // member j's rstd [T] (TP_RESID_NORM)
   const void* x;                         // local bf16 residual input [T, h] (RESID modes)
   const void* g;                         // local bf16 RMSNorm gain [h] (RESID_NORM)
+  unsigned long long* trace;             // optional: per CTA 4 globaltimer stamps (start, ready, rows, end)
 };
 cudaError_t tp_reduce(const TpArgs& a, cudaStream_t st);
+int tp_grid(int T, int k);  // CTAs per member: rows spread evenly over <= TP_GRID_MAX CTAs
 
 // ---- multi-range copy (copy.cu): migration pack / unpack / keep-copies
 struct CopyDesc {

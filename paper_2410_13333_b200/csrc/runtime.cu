@@ -109,6 +109,7 @@ struct Layout {
   float* tpp[2] = {nullptr, nullptr};
   unsigned long long* tpflags = nullptr;
   unsigned long long tp_epoch = 0;
+  bool tp_bf16 = false;  // partials in bf16 (MALLEUS_TP_PARTIAL=bf16): half the NVLink bytes
 };
 
 // bump allocator over an arena whose base may be 0 (sizing pass)
@@ -564,6 +565,10 @@ static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_are
   // TP flag blocks start at zero on every member before any peer can signal (map_peers ends
   // with a world all-reduce, which orders this memset before every later kernel of every rank)
   L.tp_epoch = 0;
+  {
+    const char* e = getenv("MALLEUS_TP_PARTIAL");
+    L.tp_bf16 = e && strcmp(e, "bf16") == 0;
+  }
   if (L.tpflags) CK(cudaMemset(L.tpflags, 0, TPF_WORDS * sizeof(unsigned long long)));
   CK(cudaDeviceSynchronize());
   RET(map_peers(ctx, L, a));
@@ -646,6 +651,8 @@ static malleus_status tp_allreduce(malleus_ctx* ctx, float* buf, size_t n, ncclR
 static bool tp_peer(const Layout& L) { return L.TP > 1 && L.p2p && L.tpflags != nullptr; }
 // where the next row-parallel GEMM writes its fp32 partial
 static float* tp_part(Layout& L) { return tp_peer(L) ? L.tpp[(L.tp_epoch + 1) & 1] : L.part; }
+// the row-parallel GEMM's store mode for that buffer
+static int tp_part_mode(const Layout& L) { return tp_peer(L) && L.tp_bf16 ? GEMM_STORE_BF16 : GEMM_STORE_F32; }
 static Layout& member_layout(Layout& L, int j) {
   const int r = L.plan.pipes[L.pipe].stages[L.stage].ranks[j];
   return L.peer[r] ? *L.peer[r] : L;
@@ -667,6 +674,7 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const float* pa
   a.epoch = ++L.tp_epoch;
   a.x = x;
   a.g = g;
+  a.part_bf16 = L.tp_bf16 ? 1 : 0;
   const int buf = (int)(a.epoch & 1);
   for (int j = 0; j < L.TP; ++j) {
     Layout& M = member_layout(L, j);
@@ -741,7 +749,7 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   CK(attention_fwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
   if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   float* pb = tp_part(L);
-  RET(gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, pb, h, GEMM_STORE_F32, st));
+  RET(gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, pb, h, tp_part_mode(L), st));
   if (tp_peer(L)) {  // x1 = x + sum P, a2 = RMSNorm(x1) in one peer-memory kernel
     RET(tp_reduce_peer(ctx, TP_RESID_NORM, pb, S.x[li], P.g2, [&](Layout& M, TpArgs& a, int j) {
       const SlotLayer& Z = M.slot[si].L[li];
@@ -756,7 +764,7 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   RET(gemm(ctx, T, 2 * F, h, Y.a2, h, false, P.wgu, h, false, Y.gu, 2 * F, GEMM_STORE_BF16, st));
   CK(swiglu_fwd(T, F, Y.gu, Y.u, st));
   pb = tp_part(L);
-  RET(gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, pb, h, GEMM_STORE_F32, st));
+  RET(gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, pb, h, tp_part_mode(L), st));
   if (tp_peer(L)) {  // x[l+1] = x1 + sum P
     RET(tp_reduce_peer(ctx, TP_RESID, pb, Y.x1, nullptr, [&](Layout& M, TpArgs& a, int j) {
       a.d0[j] = M.slot[si].x[li + 1];
@@ -787,7 +795,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
   CK(swiglu_bwd(T, F, Y.gu, L.du, L.dgu, st));
   float* pb = tp_part(L);
-  RET(gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, pb, h, GEMM_STORE_F32, st));
+  RET(gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, pb, h, tp_part_mode(L), st));
   RET(gemm(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
   RET(tp_sum(ctx, pb, st));
   duty_begin(ctx, 4, st);
@@ -800,7 +808,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
     CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
   pb = tp_part(L);
-  RET(gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, pb, h, GEMM_STORE_F32, st));
+  RET(gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, pb, h, tp_part_mode(L), st));
   RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
   RET(tp_sum(ctx, pb, st));
   duty_begin(ctx, 5, st);
@@ -831,7 +839,7 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
   if (L.member == 0)
     CK(reduce_loss(T, L.loss_rows, (float)(1.0 / ((double)L.plan.B * c.seq_len)), L.loss_acc, 1, st));
   float* pb = tp_part(L);
-  RET(gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, pb, h, GEMM_STORE_F32, st));
+  RET(gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, pb, h, tp_part_mode(L), st));
   RET(gemm(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, first ? GEMM_STORE_F32 : GEMM_ACCUM_F32, st));
   RET(tp_sum(ctx, pb, st));
   duty_begin(ctx, 8, st);

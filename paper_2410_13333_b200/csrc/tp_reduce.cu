@@ -26,6 +26,7 @@
 // after this member's ready(e), i.e. after all its earlier stream work (readers of the previous
 // contents) completed.  A wait that exceeds 20 s traps (sticky CUDA error) instead of hanging.
 #include <cuda_bf16.h>
+#include <algorithm>
 #include <type_traits>
 #include "kernels.h"
 
@@ -91,13 +92,15 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 
 // K > 0: member count known at compile time, V = vectors of 8 per thread (h <= 8 * V * TPR_THREADS):
 // the loads of up to KC members are issued before their adds.  K == 0: generic runtime k.
-template <int MODE, int K, int V>
+template <int MODE, int K, int V, bool PB>
 __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_constant__ TpArgs a) {
   constexpr int KC = V >= 4 ? 2 : 3;
   __shared__ float sh[TPR_THREADS / 32];
   __shared__ bool last;
   const int k = K > 0 ? K : a.k;
   const int me = a.me, h = a.h, nv = h / 8;
+  unsigned long long* tr = a.trace ? a.trace + 4 * blockIdx.x : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = now_ns();
   if (threadIdx.x == 0) {
     // ready: only CTA 0 publishes (dispatched first, so it is resident whenever any CTA waits)
     if (blockIdx.x == 0) {
@@ -105,6 +108,7 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
       for (int j = 0; j < k; ++j) st_release_sys(a.flags[j] + TPF_READY + me, a.epoch);
     }
     for (int j = 0; j < k; ++j) wait_geq(a.flags[me] + TPF_READY + j, a.epoch);
+    if (tr) tr[1] = now_ns();
   }
   __syncthreads();
   const int r0 = (int)((long long)me * a.T / k), r1 = (int)((long long)(me + 1) * a.T / k);
@@ -112,13 +116,21 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
     const long long rb = (long long)row * h;
     float4 acc[V][2];
     float4 t[KC][V][2];
-    auto load = [&](float4 (&dst)[V][2], const float* base) {
+    auto load = [&](float4 (&dst)[V][2], const void* base) {
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         const int c = threadIdx.x + i * TPR_THREADS;
         if (c < nv) {
-          dst[i][0] = ldcg4(base + rb + 8 * c);
-          dst[i][1] = ldcg4(base + rb + 8 * c + 4);
+          if (PB) {
+            float f[8];
+            unpack8(__ldcg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + rb) + c), f);
+            dst[i][0] = make_float4(f[0], f[1], f[2], f[3]);
+            dst[i][1] = make_float4(f[4], f[5], f[6], f[7]);
+          } else {
+            const float* b = static_cast<const float*>(base);
+            dst[i][0] = ldcg4(b + rb + 8 * c);
+            dst[i][1] = ldcg4(b + rb + 8 * c + 4);
+          }
         }
       }
     };
@@ -205,6 +217,7 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
   // CTA of this member tells every member "done" and waits for every member's "done"
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (tr) tr[2] = now_ns();
     __threadfence_system();
     const unsigned long long t = atomicAdd(a.flags[me] + TPF_TICKET, 1ull);
     last = t + 1 == a.epoch * (unsigned long long)gridDim.x;
@@ -216,20 +229,32 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
     for (int j = 0; j < k; ++j) wait_geq(a.flags[me] + TPF_DONE + j, a.epoch);
     __threadfence_system();
   }
+  if (tr && threadIdx.x == 0) tr[3] = now_ns();
 }
 
 }  // namespace
+
+int tp_grid(int T, int k) {
+  const int rows = (T + k - 1) / k;
+  const int waves = (rows + TP_GRID_MAX - 1) / TP_GRID_MAX;
+  return std::max(1, (rows + waves - 1) / waves);
+}
 
 cudaError_t tp_reduce(const TpArgs& a, cudaStream_t st) {
   if (a.k < 2 || a.k > MAX_TP || a.me < 0 || a.me >= a.k || a.h % 8 || a.h > 8 * TPR_MAXV * TPR_THREADS ||
       a.T <= 0 || a.epoch == 0)
     return cudaErrorInvalidValue;
   const int vpt = (a.h / 8 + TPR_THREADS - 1) / TPR_THREADS;
+  const int grid = tp_grid(a.T, a.k);
   auto launch_kv = [&](auto mode_c, auto k_c) {
     constexpr int M = decltype(mode_c)::value, K = decltype(k_c)::value;
-    if (vpt <= 1) tp_reduce_kernel<M, K, 1><<<TP_GRID, TPR_THREADS, 0, st>>>(a);
-    else if (vpt == 2) tp_reduce_kernel<M, K, 2><<<TP_GRID, TPR_THREADS, 0, st>>>(a);
-    else tp_reduce_kernel<M, K, TPR_MAXV><<<TP_GRID, TPR_THREADS, 0, st>>>(a);
+    if (a.part_bf16) {
+      if (vpt <= 2) tp_reduce_kernel<M, K, 2, true><<<grid, TPR_THREADS, 0, st>>>(a);
+      else tp_reduce_kernel<M, K, TPR_MAXV, true><<<grid, TPR_THREADS, 0, st>>>(a);
+    } else {
+      if (vpt <= 2) tp_reduce_kernel<M, K, 2, false><<<grid, TPR_THREADS, 0, st>>>(a);
+      else tp_reduce_kernel<M, K, TPR_MAXV, false><<<grid, TPR_THREADS, 0, st>>>(a);
+    }
   };
   auto launch = [&](auto mode_c) {
     switch (a.k) {

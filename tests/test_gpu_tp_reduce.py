@@ -21,12 +21,14 @@ def _ref_sum(parts):
     return s
 
 
-@pytest.mark.parametrize("k,T,h", [(2, 300, 512), (2, 2048, 4096), (4, 257, 1024)])
-def test_tp_reduce_modes(k, T, h):
+@pytest.mark.parametrize("k,T,h,pdt", [(2, 300, 512, "f32"), (2, 2048, 4096, "f32"), (4, 257, 1024, "f32"),
+                                      (2, 300, 512, "bf16"), (4, 2048, 8192, "bf16"), (3, 301, 2048, "bf16")])
+def test_tp_reduce_modes(k, T, h, pdt):
     _need(k)
     from tests.tputil import Group, enable_peer_access
     enable_peer_access(k)
-    G = Group(k, T, h)
+    dt = torch.bfloat16 if pdt == "bf16" else torch.float32
+    G = Group(k, T, h, part_dtype=dt)
     gen = torch.Generator().manual_seed(7)
     x_cpu = (torch.randn(T, h, generator=gen) * 2).to(torch.bfloat16)
     g_cpu = (1 + 0.1 * torch.randn(h, generator=gen)).to(torch.bfloat16)
@@ -34,9 +36,10 @@ def test_tp_reduce_modes(k, T, h):
     gs = [g_cpu.to(f"cuda:{j}") for j in range(k)]
     for rep, mode in enumerate([0, 1, 2, 0, 1]):  # epochs 1..5: both partial buffers, every mode
         buf = (G.epoch + 1) & 1
-        parts = [torch.randn(T, h, generator=gen) for _ in range(k)]
+        parts = [torch.randn(T, h, generator=gen).to(dt) for _ in range(k)]
         for j in range(k):
             G.part[buf][j].copy_(parts[j])
+        parts = [q.float() for q in parts]
         G.sync()
         G.launch(mode, xs, gs)
         G.sync()

@@ -31,10 +31,11 @@ def _ptrs(ts):
 class Group:
     """k members, member j on cuda:j: double-buffered partials, flag blocks, destinations."""
 
-    def __init__(self, k: int, T: int, h: int):
+    def __init__(self, k: int, T: int, h: int, part_dtype=torch.float32):
         self.k, self.T, self.h = k, T, h
+        self.pdt = 0 if part_dtype == torch.bfloat16 else 1  # MALLEUS_BF16 / MALLEUS_FP32
         dev = [torch.device("cuda", j) for j in range(k)]
-        self.part = [[torch.zeros(T, h, device=d) for d in dev] for _ in range(2)]
+        self.part = [[torch.zeros(T, h, device=d, dtype=part_dtype) for d in dev] for _ in range(2)]
         self.flags = [torch.zeros(TPF_WORDS, dtype=torch.int64, device=d) for d in dev]
         self.out32 = [torch.zeros(T, h, device=d) for d in dev]
         self.x1 = [torch.zeros(T, h, dtype=torch.bfloat16, device=d) for d in dev]
@@ -60,7 +61,7 @@ class Group:
         for j in range(self.k):
             with torch.cuda.device(j):
                 st = torch.cuda.current_stream().cuda_stream
-                r = L.lib.malleus_k_tp_reduce(self.k, j, self.T, self.h, mode, eps, self.epoch,
+                r = L.lib.malleus_k_tp_reduce(self.k, j, self.T, self.h, mode, self.pdt, eps, self.epoch,
                                               C.cast(parts, C.c_void_p), C.cast(flags, C.c_void_p),
                                               C.cast(d0, C.c_void_p), C.cast(d1, C.c_void_p) if d1 else None,
                                               C.cast(d2, C.c_void_p) if d2 else None,
