@@ -98,8 +98,8 @@ extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, 
     if (!trace && cudaMallocManaged(&trace, 4 * TP_GRID_MAX * 16 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
     a.trace = trace ? trace + 4 * TP_GRID_MAX * me : nullptr;
   }
-  if (part_dtype != MALLEUS_FP32 && part_dtype != MALLEUS_BF16) return MALLEUS_E_ARG;
-  a.part_bf16 = part_dtype == MALLEUS_BF16;
+  if (part_dtype != 0 && part_dtype != 1) return MALLEUS_E_ARG;
+  a.part_bf16 = part_dtype;
   a.k = k; a.me = me; a.T = T; a.h = h; a.mode = mode; a.eps = eps; a.epoch = epoch;
   a.x = x; a.g = g;
   for (int j = 0; j < k; ++j) {

@@ -33,7 +33,7 @@ class Group:
 
     def __init__(self, k: int, T: int, h: int, part_dtype=torch.float32):
         self.k, self.T, self.h = k, T, h
-        self.pdt = 0 if part_dtype == torch.bfloat16 else 1  # MALLEUS_BF16 / MALLEUS_FP32
+        self.pdt = 1 if part_dtype == torch.bfloat16 else 0  # part_dtype: 0 fp32, 1 bf16
         dev = [torch.device("cuda", j) for j in range(k)]
         self.part = [[torch.zeros(T, h, device=d, dtype=part_dtype) for d in dev] for _ in range(2)]
         self.flags = [torch.zeros(TPF_WORDS, dtype=torch.int64, device=d) for d in dev]
