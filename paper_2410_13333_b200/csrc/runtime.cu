@@ -109,7 +109,7 @@ struct Layout {
   float* tpp[2] = {nullptr, nullptr};
   unsigned long long* tpflags = nullptr;
   unsigned long long tp_epoch = 0;
-  bool tp_bf16 = false;  // partials in bf16 (MALLEUS_TP_PARTIAL=bf16): half the NVLink bytes
+  bool tp_bf16 = true;   // partials in bf16 (default; MALLEUS_TP_PARTIAL=fp32 for fp32)
 };
 
 // bump allocator over an arena whose base may be 0 (sizing pass)
@@ -566,8 +566,10 @@ static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_are
   // with a world all-reduce, which orders this memset before every later kernel of every rank)
   L.tp_epoch = 0;
   {
+    // bf16 partials by default (the row-parallel output dtype of Megatron-style TP, half the
+    // NVLink bytes); MALLEUS_TP_PARTIAL=fp32 keeps them fp32 (bitwise equal to the NCCL path at TP 2)
     const char* e = getenv("MALLEUS_TP_PARTIAL");
-    L.tp_bf16 = e && strcmp(e, "bf16") == 0;
+    L.tp_bf16 = !(e && strcmp(e, "fp32") == 0);
   }
   if (L.tpflags) CK(cudaMemset(L.tpflags, 0, TPF_WORDS * sizeof(unsigned long long)));
   CK(cudaDeviceSynchronize());
