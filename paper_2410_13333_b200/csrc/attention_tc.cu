@@ -15,6 +15,7 @@
 // Output identical in layout to attention.cu: o [T, n*d] bf16, lse [nb, n, s] (natural log).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -52,7 +53,7 @@ __device__ __forceinline__ float ex2(float x) {
 
 __global__ void __launch_bounds__(320, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bfloat16* __restrict__ o,
-                   float* __restrict__ lse, float scale) {
+                   float* __restrict__ lse, float scale, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -78,6 +79,13 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
   const int n_tiles = qb + 1;           // causal: key tiles 0..qb
   const int row0 = b * s + qb * TQ;     // first query row in qkv
   const int nd = n * DH;
+  // debugging aid (MALLEUS_ATTN_TRACE): globaltimer stamps of CTAs (0, 0..1, 0), [event][tile]
+  unsigned long long* tr = (trace && blockIdx.x == 0 && blockIdx.y < 2 && blockIdx.z == 0)
+                               ? trace + blockIdx.y * 8 * 64 : nullptr;
+  auto stamp = [&](int ev, int i) {
+    if (tr && i < 64) { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); tr[ev * 64 + i] = t; }
+  };
+  if (threadIdx.x == 0) stamp(7, 0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
@@ -108,10 +116,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         uint8_t* v = sV + st * K_BYTES;
         const int krow = b * s + i * TK;
         mbar_wait(&k_empty[st], ph ^ 1);
+        stamp(0, i);
         mbar_arrive_expect_tx(&k_full[st], K_BYTES);
         tma_load_2d(k, &tm, &k_full[st], nd + head * DH, krow);
         tma_load_2d(k + PANEL, &tm, &k_full[st], nd + head * DH + 64, krow);
         mbar_wait(&v_empty[st], ph ^ 1);
+        stamp(1, i);
         mbar_arrive_expect_tx(&v_full[st], K_BYTES);
         tma_load_2d(v, &tm, &v_full[st], 2 * nd + head * DH, krow);
         tma_load_2d(v + PANEL, &tm, &v_full[st], 2 * nd + head * DH + 64, krow);
@@ -126,6 +136,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         const int st = j & 1;
         mbar_wait(&v_full[st], (j >> 1) & 1);
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        stamp(3, j);
         tc_fence_after();
         const uint32_t v = smem_u32(sV + st * K_BYTES);
         const uint32_t apj = ap + (j & 1) * P_BYTES;
@@ -143,6 +154,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         const int st = i & 1, sb = i & 1;
         mbar_wait(&k_full[st], (i >> 1) & 1);
         mbar_wait(&s_empty[sb], ((i >> 1) & 1) ^ 1);
+        stamp(2, i);
         tc_fence_after();
         const uint32_t k = smem_u32(sK + st * K_BYTES);
 #pragma unroll
@@ -188,6 +200,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
     for (int i = 0; i < n_tiles; ++i) {
       const int sb = i & 1;
       mbar_wait(&s_full[sb], (i >> 1) & 1);
+      if (warp == 2 && lane == 0) stamp(4, i);
       tc_fence_after();
       float sv[TK / 2];
 #pragma unroll
@@ -210,6 +223,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
 #pragma unroll
       for (int j = 0; j < TK / 2; ++j) mt = fmaxf(mt, sv[j]);
       mt = fmaxf(mt, exchange(mt, i & 1));  // full-row max of this tile
+      if (warp == 2 && lane == 0) stamp(5, i);
       // P buffer i & 1 is free once PV_{i-2} is done
       if (i > 1) {
         mbar_wait(&o_done[i & 1], ((i - 2) >> 1) & 1);
@@ -255,9 +269,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[i & 1]);
+      if (warp == 2 && lane == 0) stamp(6, i);
     }
     // epilogue: O / l (MMAs complete in issue order: the last PV implies all)
     mbar_wait(&o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+    if (warp == 2 && lane == 0) stamp(7, 1);
     tc_fence_after();
     l += exchange(l, n_tiles & 1);  // the slot the last tile did not use
     const float inv = 1.f / l;
@@ -279,6 +295,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       }
     }
     if (half == 0) lse[((long long)b * n + head) * s + q] = (m_used + log2f(l)) / LOG2E;
+    if (warp == 2 && lane == 0) stamp(7, 2);
   }
   tc_fence_before();
   __syncthreads();
@@ -682,6 +699,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 }  // namespace
 
 bool attention_fwd_tc_supported(int s, int d) { return d == DH && s % TQ == 0; }
+unsigned long long* attn_trace_buffer = nullptr;
 
 static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long rows) {
   auto enc = encoder();
@@ -736,8 +754,13 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  static unsigned long long* trace = nullptr;
+  if (getenv("MALLEUS_ATTN_TRACE") && !trace) {
+    if (cudaMallocManaged(&trace, 2 * 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
+    attn_trace_buffer = trace;
+  }
   attn_fwd_tc_kernel<<<dim3(s / TQ, n, nb), 320, SMEM_TC, st>>>(tm, s, n, (__nv_bfloat16*)o, lse,
-                                                                rsqrtf((float)DH)); count_launch();
+                                                                rsqrtf((float)DH), trace); count_launch();
   return cudaGetLastError();
 }
 
