@@ -51,6 +51,21 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x for x <= 0 on the FMA pipe (FA4's trick to offload the MUFU unit, which alone would bound a
+// 128x128 tile at 1024 cycles, as long as the two MMAs): round-to-nearest split x = j + f with the
+// 1.5 * 2^23 magic constant, near-minimax cubic for 2^f on [-0.5, 0.5] (max rel. error 7.5e-5,
+// far below bf16's 2^-9), exponent added in the integer domain; x < -126 (incl. -inf) gives 0.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -127.f);
+  const float t = xc + 12582912.f;
+  const float f = xc - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517147f, f, 0.24261111f), f, 0.693261f), f, 0.99992806f);
+  const float r = __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+  return x < -126.f ? 0.f : r;
+}
+
+// NPOLY of every 8 consecutive P elements take ex2_poly, the rest the MUFU ex2
+template <int NPOLY>
 __global__ void __launch_bounds__(320, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bfloat16* __restrict__ o,
                    float* __restrict__ lse, float scale, unsigned long long* __restrict__ trace) {
@@ -109,22 +124,32 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       mbar_arrive_expect_tx(q_full, Q_BYTES);
       tma_load_2d(sQ, &tm, q_full, head * DH, row0);
       tma_load_2d(sQ + PANEL, &tm, q_full, head * DH + 64, row0);
-      for (int i = 0; i < n_tiles; ++i) {
+      // K runs one tile ahead of V in this thread's program order: K_{i+1} is requested as soon as
+      // its slot frees (S_{i-1} done) instead of queueing behind V_i, whose slot frees only when
+      // O += P_{i-2} V_{i-2} completes (measured: that ordering put the load latency on the
+      // critical path of every tile)
+      auto load_k = [&](int i) {
         const int st = i & 1;
-        const uint32_t ph = (i >> 1) & 1;
         uint8_t* k = sK + st * K_BYTES;
-        uint8_t* v = sV + st * K_BYTES;
-        const int krow = b * s + i * TK;
-        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_wait(&k_empty[st], ((i >> 1) & 1) ^ 1);
         stamp(0, i);
         mbar_arrive_expect_tx(&k_full[st], K_BYTES);
-        tma_load_2d(k, &tm, &k_full[st], nd + head * DH, krow);
-        tma_load_2d(k + PANEL, &tm, &k_full[st], nd + head * DH + 64, krow);
-        mbar_wait(&v_empty[st], ph ^ 1);
+        tma_load_2d(k, &tm, &k_full[st], nd + head * DH, b * s + i * TK);
+        tma_load_2d(k + PANEL, &tm, &k_full[st], nd + head * DH + 64, b * s + i * TK);
+      };
+      auto load_v = [&](int i) {
+        const int st = i & 1;
+        uint8_t* v = sV + st * K_BYTES;
+        mbar_wait(&v_empty[st], ((i >> 1) & 1) ^ 1);
         stamp(1, i);
         mbar_arrive_expect_tx(&v_full[st], K_BYTES);
-        tma_load_2d(v, &tm, &v_full[st], 2 * nd + head * DH, krow);
-        tma_load_2d(v + PANEL, &tm, &v_full[st], 2 * nd + head * DH + 64, krow);
+        tma_load_2d(v, &tm, &v_full[st], 2 * nd + head * DH, b * s + i * TK);
+        tma_load_2d(v + PANEL, &tm, &v_full[st], 2 * nd + head * DH + 64, b * s + i * TK);
+      };
+      load_k(0);
+      for (int i = 0; i < n_tiles; ++i) {
+        if (i + 1 < n_tiles) load_k(i + 1);
+        load_v(i);
       }
     }
   } else if (warp == 1) {
@@ -257,7 +282,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         float p[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          p[j] = ex2(sv[ch * 8 + j] - m_used);
+          const float x = sv[ch * 8 + j] - m_used;
+          p[j] = ((j * NPOLY) % 8 < NPOLY && NPOLY > 0) ? ex2_poly(x) : ex2(x);  // NPOLY spread over the 8
           l += p[j];
         }
         uint4 w;
@@ -750,8 +776,10 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC);
-    if (e != cudaSuccess) return e;
+    for (auto fn : {attn_fwd_tc_kernel<0>, attn_fwd_tc_kernel<2>, attn_fwd_tc_kernel<3>, attn_fwd_tc_kernel<4>}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
   static unsigned long long* trace = nullptr;
@@ -759,8 +787,13 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
     if (cudaMallocManaged(&trace, 2 * 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
     attn_trace_buffer = trace;
   }
-  attn_fwd_tc_kernel<<<dim3(s / TQ, n, nb), 320, SMEM_TC, st>>>(tm, s, n, (__nv_bfloat16*)o, lse,
-                                                                rsqrtf((float)DH), trace); count_launch();
+  static const int npoly = [] {
+    const char* e = getenv("MALLEUS_ATTN_POLY");  // experiments: 0, 2, 3, 4 of every 8 exps in software
+    return e ? atoi(e) : 3;
+  }();
+  auto fn = npoly == 0 ? attn_fwd_tc_kernel<0> : npoly == 2 ? attn_fwd_tc_kernel<2>
+          : npoly == 4 ? attn_fwd_tc_kernel<4> : attn_fwd_tc_kernel<3>;
+  fn<<<dim3(s / TQ, n, nb), 320, SMEM_TC, st>>>(tm, s, n, (__nv_bfloat16*)o, lse, rsqrtf((float)DH), trace); count_launch();
   return cudaGetLastError();
 }
 
