@@ -388,48 +388,57 @@ __device__ __forceinline__ void st_sw128_32(uint8_t* tile, int r, int c0, const 
   }
 }
 
-// dK / dV: CTA = 128 keys of one (sequence, head); loop over query tiles j >= key tile.
-//   TMEM: S^T [0,128), dP^T [128,256), dV [256,384), dK [384,512)
-//   S^T = K Q_j^T, dP^T = V dO_j^T (M = keys); P^T, dS^T -> smem; dV += P^T dO_j; dK += dS^T Q_j
-//   (Q_j / dO_j tiles serve as K-major B for S^T / dP^T and, same bytes, as MN-major B for dK / dV).
-constexpr int BWD1_SMEM = 7 * Q_BYTES + 1024 + 1024 + 1024;
+// ---- backward: 64-wide sub-tiles, P^T / dS^T (and dS) kept in TMEM as the A operand of the second
+// pair of MMAs ("ts" form), S / dP double-buffered in TMEM, 3-stage TMA rings.  Measured on the
+// 128-wide version: shared-memory bandwidth (A and B of every MMA plus P / dS round trips through
+// smem) and exposed TMA latency (single-buffered Q / dO) bounded the loop; here the only smem
+// operands are the TMA-loaded tiles and every load has two sub-tiles of slack.
+constexpr int HPANEL = 64 * 128;          // 64 rows x 128 B (one 64-column half of a 64-row tile)
+constexpr int SUB_STAGE = 4 * HPANEL;     // two 64-row x 128-col bf16 tiles (Q | dO or K | V)
+constexpr int NSUB = 3;                   // ring depth
+
+// dK / dV: CTA = 128 keys of one (sequence, head); loop over 64-query sub-tiles j >= 2 kb.
+//   TMEM: S^T[b] cols [64b, 64b+64), dP^T[b] [128+64b, ..), dV [256,384), dK [384,512); warp half h
+//   overwrites its own 32 S^T / dP^T columns with 16 columns of packed bf16 P^T / dS^T at 32h.
+//   S^T = K Q_j^T and dP^T = V dO_j^T (M = 128 keys, N = 64 queries, A = K / V from smem);
+//   dV += P^T dO_j and dK += dS^T Q_j (A from TMEM, K = 64 queries; Q_j / dO_j MN-major B).
+constexpr int BWD1_SMEM = 2 * 2 * PANEL + NSUB * SUB_STAGE + NSUB * 512 + 256 + 1024;
 
 __global__ void __launch_bounds__(320, 1)
-attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s,
-                       int n, const float* __restrict__ lse, const float* __restrict__ dsum,
-                       __nv_bfloat16* __restrict__ dqkv, float scale, const float2* __restrict__ rope_cs) {
+attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm64,
+                       const __grid_constant__ CUtensorMap tmo64, int s, int n, const float* __restrict__ lse,
+                       const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv, float scale,
+                       const float2* __restrict__ rope_cs) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
-  uint8_t* sV = sK + Q_BYTES;
-  uint8_t* sQ = sV + Q_BYTES;
-  uint8_t* sO = sQ + Q_BYTES;   // dO tile
-  uint8_t* sP = sO + Q_BYTES;   // P^T
-  uint8_t* sS = sP + Q_BYTES;   // dS^T
-  float* sL = reinterpret_cast<float*>(sS + Q_BYTES);  // lse * log2e [128], D [128]
-  float* sD = sL + 128;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sL + 256);
+  uint8_t* sV = sK + 2 * PANEL;
+  uint8_t* ring = sV + 2 * PANEL;                                       // [NSUB][Q | dO]
+  float* sLD = reinterpret_cast<float*>(ring + NSUB * SUB_STAGE);      // [NSUB][lse 64 | D 64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + NSUB * 128);
   uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;
-  uint64_t* qd_empty = bars + 2;
-  uint64_t* sd_full = bars + 3;
-  uint64_t* sd_empty = bars + 4;
-  uint64_t* pd_full = bars + 5;
-  uint64_t* pd_empty = bars + 6;
-  uint64_t* done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* qd_full = bars + 1;   // [NSUB]
+  uint64_t* qd_empty = bars + 4;  // [NSUB]
+  uint64_t* sd_full = bars + 7;   // [2]
+  uint64_t* pd_full = bars + 9;   // [2]
+  uint64_t* done = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x;  // kb = 0 has the most query tiles: scheduled first
+  const int kb = blockIdx.x;  // kb = 0 has the most query sub-tiles: scheduled first
   const int head = blockIdx.y, b = blockIdx.z;
-  const int nq = s / TQ;
   const int nd = n * DH;
+  const int j0 = 2 * kb, n_it = s / 64 - j0;
   const long long lrow = ((long long)b * n + head) * s;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
-    tma_prefetch(&tmo);
-    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], (i == 4 || i == 5) ? 8 : 1);
+    tma_prefetch(&tm64);
+    tma_prefetch(&tmo64);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < NSUB; ++i) { mbar_init(&qd_full[i], 1); mbar_init(&qd_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&sd_full[i], 1); mbar_init(&pd_full[i], 8); }
+    mbar_init(done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -441,102 +450,102 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
   if (warp == 0) {
     if (lane == 0) {
       const int krow = b * s + kb * TK;
-      mbar_arrive_expect_tx(kv_full, 2 * Q_BYTES);
+      mbar_arrive_expect_tx(kv_full, 4 * PANEL);
       tma_load_2d(sK, &tm, kv_full, nd + head * DH, krow);
       tma_load_2d(sK + PANEL, &tm, kv_full, nd + head * DH + 64, krow);
       tma_load_2d(sV, &tm, kv_full, 2 * nd + head * DH, krow);
       tma_load_2d(sV + PANEL, &tm, kv_full, 2 * nd + head * DH + 64, krow);
-      for (int j = kb; j < nq; ++j) {
-        const int it = j - kb;
-        mbar_wait(qd_empty, (it & 1) ^ 1);
-        const int qrow = b * s + j * TQ;
-        mbar_arrive_expect_tx(qd_full, 2 * Q_BYTES + 1024);
-        tma_load_2d(sQ, &tm, qd_full, head * DH, qrow);
-        tma_load_2d(sQ + PANEL, &tm, qd_full, head * DH + 64, qrow);
-        tma_load_2d(sO, &tmo, qd_full, head * DH, qrow);
-        tma_load_2d(sO + PANEL, &tmo, qd_full, head * DH + 64, qrow);
-        bulk_load(sL, lse + lrow + j * TQ, 512, qd_full);
-        bulk_load(sD, dsum + lrow + j * TQ, 512, qd_full);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % NSUB, j = j0 + it;
+        mbar_wait(&qd_empty[st], ((it / NSUB) & 1) ^ 1);
+        uint8_t* q = ring + st * SUB_STAGE;
+        const int qrow = b * s + j * 64;
+        mbar_arrive_expect_tx(&qd_full[st], SUB_STAGE + 512);
+        tma_load_2d(q, &tm64, &qd_full[st], head * DH, qrow);
+        tma_load_2d(q + HPANEL, &tm64, &qd_full[st], head * DH + 64, qrow);
+        tma_load_2d(q + 2 * HPANEL, &tmo64, &qd_full[st], head * DH, qrow);
+        tma_load_2d(q + 3 * HPANEL, &tmo64, &qd_full[st], head * DH + 64, qrow);
+        bulk_load(sLD + st * 128, lse + lrow + j * 64, 256, &qd_full[st]);
+        bulk_load(sLD + st * 128 + 64, dsum + lrow + j * 64, 256, &qd_full[st]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t id_kk = umma_idesc_bf16(128, 128, false, false);
-      constexpr uint32_t id_km = umma_idesc_bf16(128, 128, false, true);
-      const uint32_t ak = smem_u32(sK), av = smem_u32(sV), bq = smem_u32(sQ), bo = smem_u32(sO);
-      const uint32_t ap = smem_u32(sP), as = smem_u32(sS);
-      mbar_wait(kv_full, 0);
-      for (int j = kb; j < nq; ++j) {
-        const int it = j - kb;
-        mbar_wait(qd_full, it & 1);
-        mbar_wait(sd_empty, (it & 1) ^ 1);
+      constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t id_d = umma_idesc_bf16(128, 128, false, true);
+      const uint32_t ak = smem_u32(sK), av = smem_u32(sV);
+      auto issue_dvdk = [&](int i) {
+        const int bb = i & 1, st = i % NSUB;
+        mbar_wait(&pd_full[bb], (i >> 1) & 1);
         tc_fence_after();
+        const uint32_t q = smem_u32(ring + st * SUB_STAGE), o = q + 2 * HPANEL;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t acol = bb * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          umma_f16_ts(tbase + 256, tbase + acol, umma_desc_sw128(o + kk * 2048, HPANEL, 1024), id_d, acc);
+          umma_f16_ts(tbase + 384, tbase + 128 + acol, umma_desc_sw128(q + kk * 2048, HPANEL, 1024), id_d, acc);
+        }
+        umma_commit(&qd_empty[st]);
+      };
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_it; ++it) {
+        const int bb = it & 1, st = it % NSUB;
+        mbar_wait(&qd_full[st], (it / NSUB) & 1);
+        tc_fence_after();
+        const uint32_t q = smem_u32(ring + st * SUB_STAGE), o = q + 2 * HPANEL;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          umma_f16(tbase + 0, umma_desc_sw128(ak + off, 16, 1024), umma_desc_sw128(bq + off, 16, 1024), id_kk,
+          const uint32_t aoff = (kk >> 2) * PANEL + (kk & 3) * 32, boff = (kk >> 2) * HPANEL + (kk & 3) * 32;
+          umma_f16(tbase + bb * 64, umma_desc_sw128(ak + aoff, 16, 1024), umma_desc_sw128(q + boff, 16, 1024), id_s,
                    kk > 0 ? 1u : 0u);
-          umma_f16(tbase + 128, umma_desc_sw128(av + off, 16, 1024), umma_desc_sw128(bo + off, 16, 1024), id_kk,
-                   kk > 0 ? 1u : 0u);
+          umma_f16(tbase + 128 + bb * 64, umma_desc_sw128(av + aoff, 16, 1024), umma_desc_sw128(o + boff, 16, 1024),
+                   id_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(sd_full);
-        mbar_wait(pd_full, it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < TQ / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * PANEL + (kk & 3) * 32;
-          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-          umma_f16(tbase + 256, umma_desc_sw128(ap + aoff, 16, 1024), umma_desc_sw128(bo + kk * 2048, PANEL, 1024),
-                   id_km, acc);
-          umma_f16(tbase + 384, umma_desc_sw128(as + aoff, 16, 1024), umma_desc_sw128(bq + kk * 2048, PANEL, 1024),
-                   id_km, acc);
-        }
-        umma_commit(pd_empty);
-        umma_commit(qd_empty);
+        umma_commit(&sd_full[bb]);
+        if (it > 0) issue_dvdk(it - 1);
       }
+      issue_dvdk(n_it - 1);
       umma_commit(done);
     }
   } else {
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;  // 8 compute warps: two per TMEM lane quarter
+    const int half = (warp - 2) >> 2;   // this warp's 32 query columns of each sub-tile
     const int r = quarter * 32 + lane;  // key row within the tile
     const int key = kb * TK + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = scale * LOG2E;
-    for (int j = kb; j < nq; ++j) {
-      const int it = j - kb;
-      mbar_wait(sd_full, it & 1);
+    for (int it = 0; it < n_it; ++it) {
+      const int bb = it & 1, st = it % NSUB, j = j0 + it;
+      mbar_wait(&sd_full[bb], (it >> 1) & 1);
       tc_fence_after();
-      uint32_t us[2][32], ud[2][32];  // this warp's 64 query columns of S^T and dP^T
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        tmem_ld32(tbase + lane_off + (2 * half + c) * 32, us[c]);
-        tmem_ld32(tbase + lane_off + 128 + (2 * half + c) * 32, ud[c]);
-      }
+      const uint32_t cs = tbase + lane_off + bb * 64 + half * 32;  // S^T columns; dP^T at +128
+      uint32_t us[32], ud[32];
+      tmem_ld32(cs, us);
+      tmem_ld32(cs + 128, ud);
       tmem_wait_ld();
+      const float* L = sLD + st * 128 + half * 32;
+      const float* D = L + 64;
+      const bool diag = j * 64 + half * 32 < key + 32;  // some query column of this warp may precede the key
+      uint32_t pp[16], dd[16];
+#pragma unroll
+      for (int t = 0; t < 32; t += 2) {
+        float p0 = ex2(fmaf(__uint_as_float(us[t]), sl2, -L[t] * LOG2E));
+        float p1 = ex2(fmaf(__uint_as_float(us[t + 1]), sl2, -L[t + 1] * LOG2E));
+        if (diag) {
+          const int qi = j * 64 + half * 32 + t;
+          if (key > qi) p0 = 0.f;
+          if (key > qi + 1) p1 = 0.f;
+        }
+        pp[t / 2] = pack_bf16(p0, p1);
+        dd[t / 2] = pack_bf16(p0 * (__uint_as_float(ud[t]) - D[t]), p1 * (__uint_as_float(ud[t + 1]) - D[t + 1]));
+      }
+      tmem_st16(cs, pp);
+      tmem_st16(cs + 128, dd);
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(sd_empty);
-      if (it > 0) mbar_wait(pd_empty, (it - 1) & 1);  // P^T / dS^T smem free
-      const bool diag = j == kb;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int col = (2 * half + c) * 32;
-        float p[32], ds[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int qi = col + t;
-          float pv = ex2(fmaf(__uint_as_float(us[c][t]), sl2, -sL[qi] * LOG2E));
-          if (diag && key > j * TQ + qi) pv = 0.f;
-          p[t] = pv;
-          ds[t] = pv * (__uint_as_float(ud[c][t]) - sD[qi]);
-        }
-        st_sw128_32(sP, r, col, p);
-        st_sw128_32(sS, r, col, ds);
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(pd_full);
+      if (lane == 0) mbar_arrive(&pd_full[bb]);
     }
     mbar_wait(done, 0);
     tc_fence_after();
@@ -553,43 +562,47 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
   }
 }
 
-// dQ: CTA = 128 queries; loop over key tiles i <= query tile (2-stage K / V ring).
-//   TMEM: S [0,128), dP [128,256), dQ [256,384)
-//   S = Q K_i^T, dP = dO V_i^T (M = queries); dS -> smem; dQ += dS K_i (K_i as MN-major B)
-constexpr int BWD2_SMEM = 3 * Q_BYTES + 2 * 2 * Q_BYTES + 1024 + 1024;
+// dQ: CTA = 128 queries; loop over 64-key sub-tiles i <= 2 qb + 1 (3-stage K | V ring).
+//   TMEM: S[b] cols [64b, ..), dP[b] [128+64b, ..), dQ [256,384); warp half h writes 16 columns of
+//   packed bf16 dS over its own dP columns.  S = Q K_i^T, dP = dO V_i^T (M = 128 queries, N = 64
+//   keys); dQ += dS K_i (A = dS from TMEM, K = 64 keys; K_i MN-major B).
+constexpr int BWD2_SMEM = 2 * 2 * PANEL + NSUB * SUB_STAGE + 256 + 1024;
 
 __global__ void __launch_bounds__(320, 1)
-attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s, int n,
-                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                      float scale, const float2* __restrict__ rope_cs) {
+attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo,
+                      const __grid_constant__ CUtensorMap tm64, int s, int n, const float* __restrict__ lse,
+                      const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv, float scale,
+                      const float2* __restrict__ rope_cs) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sO = sQ + Q_BYTES;
-  uint8_t* sS = sO + Q_BYTES;   // dS
-  uint8_t* sKV = sS + Q_BYTES;  // [2 stages][K | V]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + 4 * Q_BYTES);
+  uint8_t* sO = sQ + 2 * PANEL;
+  uint8_t* ring = sO + 2 * PANEL;  // [NSUB][K | V]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + NSUB * SUB_STAGE);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* sd_full = bars + 5;
-  uint64_t* sd_empty = bars + 6;
-  uint64_t* ds_full = bars + 7;
-  uint64_t* ds_empty = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* kv_full = bars + 1;   // [NSUB]
+  uint64_t* kv_empty = bars + 4;  // [NSUB]
+  uint64_t* sd_full = bars + 7;   // [2]
+  uint64_t* ds_full = bars + 9;   // [2]
+  uint64_t* done = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;
   const int qb = nqb - 1 - blockIdx.x;  // heaviest first
   const int head = blockIdx.y, b = blockIdx.z;
-  const int n_tiles = qb + 1;
+  const int n_it = 2 * qb + 2;          // 64-key sub-tiles up to the diagonal
   const int nd = n * DH;
   const int row0 = b * s + qb * TQ;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
     tma_prefetch(&tmo);
-    for (int i = 0; i < 9; ++i) mbar_init(&bars[i], (i == 6 || i == 7) ? 8 : 1);
+    tma_prefetch(&tm64);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NSUB; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&sd_full[i], 1); mbar_init(&ds_full[i], 8); }
+    mbar_init(done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -600,104 +613,97 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, 2 * Q_BYTES);
+      mbar_arrive_expect_tx(q_full, 4 * PANEL);
       tma_load_2d(sQ, &tm, q_full, head * DH, row0);
       tma_load_2d(sQ + PANEL, &tm, q_full, head * DH + 64, row0);
       tma_load_2d(sO, &tmo, q_full, head * DH, row0);
       tma_load_2d(sO + PANEL, &tmo, q_full, head * DH + 64, row0);
-      for (int i = 0; i < n_tiles; ++i) {
-        const int st = i & 1;
-        mbar_wait(&kv_empty[st], ((i >> 1) & 1) ^ 1);
-        uint8_t* k = sKV + st * 2 * Q_BYTES;
-        uint8_t* v = k + Q_BYTES;
-        const int krow = b * s + i * TK;
-        mbar_arrive_expect_tx(&kv_full[st], 2 * Q_BYTES);
-        tma_load_2d(k, &tm, &kv_full[st], nd + head * DH, krow);
-        tma_load_2d(k + PANEL, &tm, &kv_full[st], nd + head * DH + 64, krow);
-        tma_load_2d(v, &tm, &kv_full[st], 2 * nd + head * DH, krow);
-        tma_load_2d(v + PANEL, &tm, &kv_full[st], 2 * nd + head * DH + 64, krow);
+      for (int i = 0; i < n_it; ++i) {
+        const int st = i % NSUB;
+        mbar_wait(&kv_empty[st], ((i / NSUB) & 1) ^ 1);
+        uint8_t* k = ring + st * SUB_STAGE;
+        const int krow = b * s + i * 64;
+        mbar_arrive_expect_tx(&kv_full[st], SUB_STAGE);
+        tma_load_2d(k, &tm64, &kv_full[st], nd + head * DH, krow);
+        tma_load_2d(k + HPANEL, &tm64, &kv_full[st], nd + head * DH + 64, krow);
+        tma_load_2d(k + 2 * HPANEL, &tm64, &kv_full[st], 2 * nd + head * DH, krow);
+        tma_load_2d(k + 3 * HPANEL, &tm64, &kv_full[st], 2 * nd + head * DH + 64, krow);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t id_kk = umma_idesc_bf16(128, 128, false, false);
-      constexpr uint32_t id_km = umma_idesc_bf16(128, 128, false, true);
-      const uint32_t aq = smem_u32(sQ), ao = smem_u32(sO), as = smem_u32(sS);
+      constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t id_q = umma_idesc_bf16(128, 128, false, true);
+      const uint32_t aq = smem_u32(sQ), ao = smem_u32(sO);
       auto issue_dq = [&](int i) {
-        const int st = i & 1;
-        mbar_wait(ds_full, i & 1);
+        const int bb = i & 1, st = i % NSUB;
+        mbar_wait(&ds_full[bb], (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t k = smem_u32(sKV + st * 2 * Q_BYTES);
+        const uint32_t k = smem_u32(ring + st * SUB_STAGE);
 #pragma unroll
-        for (int kk = 0; kk < TK / 16; ++kk)
-          umma_f16(tbase + 256, umma_desc_sw128(as + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024),
-                   umma_desc_sw128(k + kk * 2048, PANEL, 1024), id_km, (i > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(ds_empty);
+        for (int kk = 0; kk < 4; ++kk)
+          umma_f16_ts(tbase + 256, tbase + 128 + bb * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
+                      umma_desc_sw128(k + kk * 2048, HPANEL, 1024), id_q, (i > 0 || kk > 0) ? 1u : 0u);
         umma_commit(&kv_empty[st]);
       };
       mbar_wait(q_full, 0);
-      for (int i = 0; i < n_tiles; ++i) {
-        const int st = i & 1;
-        mbar_wait(&kv_full[st], (i >> 1) & 1);
-        mbar_wait(sd_empty, (i & 1) ^ 1);
+      for (int i = 0; i < n_it; ++i) {
+        const int bb = i & 1, st = i % NSUB;
+        mbar_wait(&kv_full[st], (i / NSUB) & 1);
         tc_fence_after();
-        const uint32_t k = smem_u32(sKV + st * 2 * Q_BYTES), v = k + Q_BYTES;
+        const uint32_t k = smem_u32(ring + st * SUB_STAGE), v = k + 2 * HPANEL;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          umma_f16(tbase + 0, umma_desc_sw128(aq + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024), id_kk,
+          const uint32_t aoff = (kk >> 2) * PANEL + (kk & 3) * 32, boff = (kk >> 2) * HPANEL + (kk & 3) * 32;
+          umma_f16(tbase + bb * 64, umma_desc_sw128(aq + aoff, 16, 1024), umma_desc_sw128(k + boff, 16, 1024), id_s,
                    kk > 0 ? 1u : 0u);
-          umma_f16(tbase + 128, umma_desc_sw128(ao + off, 16, 1024), umma_desc_sw128(v + off, 16, 1024), id_kk,
-                   kk > 0 ? 1u : 0u);
+          umma_f16(tbase + 128 + bb * 64, umma_desc_sw128(ao + aoff, 16, 1024), umma_desc_sw128(v + boff, 16, 1024),
+                   id_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(sd_full);
+        umma_commit(&sd_full[bb]);
         if (i > 0) issue_dq(i - 1);
       }
-      issue_dq(n_tiles - 1);
+      issue_dq(n_it - 1);
+      umma_commit(done);
     }
   } else {
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - 2) >> 2;  // this warp's 32 key columns of each sub-tile
     const int r = quarter * 32 + lane;
     const int q = qb * TQ + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = scale * LOG2E;
     const long long lrow = ((long long)b * n + head) * s;
     const float L2 = lse[lrow + q] * LOG2E, Dq = dsum[lrow + q];
-    for (int i = 0; i < n_tiles; ++i) {
-      mbar_wait(sd_full, i & 1);
+    for (int i = 0; i < n_it; ++i) {
+      const int bb = i & 1;
+      mbar_wait(&sd_full[bb], (i >> 1) & 1);
       tc_fence_after();
-      // this warp's 64 key columns of S and dP into registers, then hand the TMEM back at once so
-      // the next tile's S / dP MMAs overlap this tile's arithmetic
-      uint32_t us[2][32], ud[2][32];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        tmem_ld32(tbase + lane_off + (2 * half + c) * 32, us[c]);
-        tmem_ld32(tbase + lane_off + 128 + (2 * half + c) * 32, ud[c]);
-      }
+      const uint32_t cs = tbase + lane_off + bb * 64 + half * 32;
+      uint32_t us[32], ud[32];
+      tmem_ld32(cs, us);
+      tmem_ld32(cs + 128, ud);
       tmem_wait_ld();
+      const int k0 = i * 64 + half * 32;
+      const bool diag = k0 + 31 > q;
+      uint32_t dd[16];
+#pragma unroll
+      for (int t = 0; t < 32; t += 2) {
+        float p0 = ex2(fmaf(__uint_as_float(us[t]), sl2, -L2));
+        float p1 = ex2(fmaf(__uint_as_float(us[t + 1]), sl2, -L2));
+        if (diag) {
+          if (k0 + t > q) p0 = 0.f;
+          if (k0 + t + 1 > q) p1 = 0.f;
+        }
+        dd[t / 2] = pack_bf16(p0 * (__uint_as_float(ud[t]) - Dq), p1 * (__uint_as_float(ud[t + 1]) - Dq));
+      }
+      tmem_st16(cs + 128, dd);
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(sd_empty);
-      if (i > 0) mbar_wait(ds_empty, (i - 1) & 1);  // dS smem free: dQ MMA of tile i-1 done
-      const bool diag = i == n_tiles - 1;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int col = (2 * half + c) * 32;
-        float ds[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          float pv = ex2(fmaf(__uint_as_float(us[c][t]), sl2, -L2));
-          if (diag && i * TK + col + t > q) pv = 0.f;
-          ds[t] = pv * (__uint_as_float(ud[c][t]) - Dq);
-        }
-        st_sw128_32(sS, r, col, ds);
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
+      if (lane == 0) mbar_arrive(&ds_full[bb]);
     }
-    mbar_wait(ds_empty, (n_tiles - 1) & 1);  // last dQ MMA done
+    mbar_wait(done, 0);
     tc_fence_after();
     __nv_bfloat16* dq = dqkv + (long long)(b * s + q) * 3 * nd + head * DH;
     store_row_rope(dq, tbase + lane_off + 256, scale, rope_cs ? rope_cs + (long long)q * 64 : nullptr, half, half + 1);
@@ -727,12 +733,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 bool attention_fwd_tc_supported(int s, int d) { return d == DH && s % TQ == 0; }
 unsigned long long* attn_trace_buffer = nullptr;
 
-static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long rows) {
+static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long rows, int box_rows = 128) {
   auto enc = encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -742,9 +748,11 @@ static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long
 // dsum (= rowsum(dO * O)) must already be in `dsum`; writes dq, dk, dv column blocks of dqkv.
 cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float* lse, const void* dout,
                              void* dqkv, const float* dsum, const float2* rope_cs, cudaStream_t st) {
-  CUtensorMap tm, tmo;
+  CUtensorMap tm, tmo, tm64, tmo64;
   const long long T = (long long)nb * s;
-  if (!map_rows(&tm, qkv, 3LL * n * DH, T) || !map_rows(&tmo, dout, (long long)n * DH, T)) return cudaErrorInvalidValue;
+  if (!map_rows(&tm, qkv, 3LL * n * DH, T) || !map_rows(&tmo, dout, (long long)n * DH, T) ||
+      !map_rows(&tm64, qkv, 3LL * n * DH, T, 64) || !map_rows(&tmo64, dout, (long long)n * DH, T, 64))
+    return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD1_SMEM);
@@ -754,9 +762,9 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
     attr = true;
   }
   const float scale = rsqrtf((float)DH);
-  attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 320, BWD1_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
+  attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, lse, dsum,
                                                                       (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
-  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
+  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, tm64, s, n, lse, dsum,
                                                                      (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
   return cudaGetLastError();
 }
@@ -789,7 +797,7 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
   }
   static const int npoly = [] {
     const char* e = getenv("MALLEUS_ATTN_POLY");  // experiments: 0, 2, 3, 4 of every 8 exps in software
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 0;  // measured: with MUFU not the bottleneck the extra FMA work costs ~8%
   }();
   auto fn = npoly == 0 ? attn_fwd_tc_kernel<0> : npoly == 2 ? attn_fwd_tc_kernel<2>
           : npoly == 4 ? attn_fwd_tc_kernel<4> : attn_fwd_tc_kernel<3>;
