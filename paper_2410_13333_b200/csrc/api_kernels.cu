@@ -115,3 +115,4 @@ extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, 
 // debugging aid for tools/tp_bench.py: the globaltimer stamps of the last traced call per member
 extern "C" const unsigned long long* malleus_k_tp_trace_buffer() { return trace; }
 extern "C" const unsigned long long* malleus_k_attn_trace_buffer() { return attn_trace_buffer; }
+extern "C" const unsigned long long* malleus_k_attn_bwd_trace_buffer() { return attn_bwd_trace_buffer; }

@@ -408,9 +408,16 @@ __global__ void __launch_bounds__(320, 1)
 attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm64,
                        const __grid_constant__ CUtensorMap tmo64, int s, int n, const float* __restrict__ lse,
                        const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv, float scale,
-                       const float2* __restrict__ rope_cs) {
+                       const float2* __restrict__ rope_cs, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // debugging aid (MALLEUS_ATTN_TRACE): stamps of CTAs (0, 0..1, 0), [event][iteration]
+  unsigned long long* tr = (trace && blockIdx.x == 0 && blockIdx.y < 2 && blockIdx.z == 0)
+                               ? trace + blockIdx.y * 8 * 64 : nullptr;
+  auto stamp = [&](int ev, int i) {
+    if (tr && i < 64) { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); tr[ev * 64 + i] = t; }
+  };
+  if (threadIdx.x == 0) stamp(7, 0);
   uint8_t* sK = smem;
   uint8_t* sV = sK + 2 * PANEL;
   uint8_t* ring = sV + 2 * PANEL;                                       // [NSUB][Q | dO]
@@ -458,6 +465,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       for (int it = 0; it < n_it; ++it) {
         const int st = it % NSUB, j = j0 + it;
         mbar_wait(&qd_empty[st], ((it / NSUB) & 1) ^ 1);
+        stamp(0, it);
         uint8_t* q = ring + st * SUB_STAGE;
         const int qrow = b * s + j * 64;
         mbar_arrive_expect_tx(&qd_full[st], SUB_STAGE + 512);
@@ -477,6 +485,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       auto issue_dvdk = [&](int i) {
         const int bb = i & 1, st = i % NSUB;
         mbar_wait(&pd_full[bb], (i >> 1) & 1);
+        stamp(3, i);
         tc_fence_after();
         const uint32_t q = smem_u32(ring + st * SUB_STAGE), o = q + 2 * HPANEL;
 #pragma unroll
@@ -492,6 +501,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       for (int it = 0; it < n_it; ++it) {
         const int bb = it & 1, st = it % NSUB;
         mbar_wait(&qd_full[st], (it / NSUB) & 1);
+        stamp(2, it);
         tc_fence_after();
         const uint32_t q = smem_u32(ring + st * SUB_STAGE), o = q + 2 * HPANEL;
 #pragma unroll
@@ -518,6 +528,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
     for (int it = 0; it < n_it; ++it) {
       const int bb = it & 1, st = it % NSUB, j = j0 + it;
       mbar_wait(&sd_full[bb], (it >> 1) & 1);
+      if (warp == 2 && lane == 0) stamp(4, it);
       tc_fence_after();
       const uint32_t cs = tbase + lane_off + bb * 64 + half * 32;  // S^T columns; dP^T at +128
       uint32_t us[32], ud[32];
@@ -540,19 +551,23 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
         pp[t / 2] = pack_bf16(p0, p1);
         dd[t / 2] = pack_bf16(p0 * (__uint_as_float(ud[t]) - D[t]), p1 * (__uint_as_float(ud[t + 1]) - D[t + 1]));
       }
+      if (warp == 2 && lane == 0) stamp(5, it);
       tmem_st16(cs, pp);
       tmem_st16(cs + 128, dd);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&pd_full[bb]);
+      if (warp == 2 && lane == 0) stamp(6, it);
     }
     mbar_wait(done, 0);
+    if (warp == 2 && lane == 0) stamp(7, 1);
     tc_fence_after();
     __nv_bfloat16* dk = dqkv + (long long)(b * s + key) * 3 * nd + nd + head * DH;
     __nv_bfloat16* dv = dk + nd;
     store_row_rope(dk, tbase + lane_off + 384, scale, rope_cs ? rope_cs + (long long)key * 64 : nullptr, half, half + 1);
     store_row_rope(dv, tbase + lane_off + 256, 1.f, nullptr, half, half + 1);
+    if (warp == 2 && lane == 0) stamp(7, 2);
   }
   tc_fence_before();
   __syncthreads();
@@ -732,6 +747,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 
 bool attention_fwd_tc_supported(int s, int d) { return d == DH && s % TQ == 0; }
 unsigned long long* attn_trace_buffer = nullptr;
+unsigned long long* attn_bwd_trace_buffer = nullptr;
 
 static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long rows, int box_rows = 128) {
   auto enc = encoder();
@@ -762,8 +778,13 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
     attr = true;
   }
   const float scale = rsqrtf((float)DH);
+  static unsigned long long* trace = nullptr;
+  if (getenv("MALLEUS_ATTN_TRACE") && !trace) {
+    if (cudaMallocManaged(&trace, 2 * 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
+    attn_bwd_trace_buffer = trace;
+  }
   attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, lse, dsum,
-                                                                      (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
+                                                                      (__nv_bfloat16*)dqkv, scale, rope_cs, trace); count_launch();
   attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, tm64, s, n, lse, dsum,
                                                                      (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
   return cudaGetLastError();

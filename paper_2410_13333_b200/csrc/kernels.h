@@ -107,7 +107,8 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
 // true when attention_bwd with this (s, d) runs the tcgen05 kernels, which apply the RoPE backward
 // rotation to dq / dk in their epilogues when given a (cos, sin) table
 bool attention_bwd_fuses_rope(int s, int d);
-extern unsigned long long* attn_trace_buffer;  // MALLEUS_ATTN_TRACE stamps of the last forward
+extern unsigned long long* attn_trace_buffer;      // MALLEUS_ATTN_TRACE stamps of the last forward
+extern unsigned long long* attn_bwd_trace_buffer;  // ... and of the last dK / dV kernel
 
 // ---- TP partial-sum reduction over NVLink peer memory, fused with residual / RMSNorm (tp_reduce.cu)
 constexpr int MAX_TP = 16;

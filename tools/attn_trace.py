@@ -31,3 +31,22 @@ for cta in range(2):
     print("tile " + " ".join(f"{x:>9s}" for x in names))
     for i in range(s // 128):
         print(f"{i:4d} " + " ".join(f"{(b[e, i]-t0)/1e3:9.2f}" for e in range(7)))
+
+# ---- backward dK / dV kernel: per 64-query sub-tile
+do = torch.randn(T, n * d, device="cuda").to(torch.bfloat16)
+dqkv = torch.empty_like(qkv)
+L.lib.malleus_k_attn_bwd_trace_buffer.restype = C.c_void_p
+for _ in range(3):
+    L.lib.malleus_k_attention_bwd(nb, s, n, d, qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), do.data_ptr(),
+                                  dqkv.data_ptr(), 1e4, st)
+torch.cuda.synchronize()
+addr = L.lib.malleus_k_attn_bwd_trace_buffer()
+buf = np.ctypeslib.as_array((C.c_uint64 * (2 * 8 * 64)).from_address(addr)).reshape(2, 8, 64).astype(np.int64)
+names = ["QdO_issue", "-", "S_issue", "dVdK_iss", "c_start", "c_math", "c_end"]
+for cta in range(2):
+    b = buf[cta]
+    t0 = b[7, 0]
+    print(f"dKV CTA (0,{cta}): epilogue start {(b[7,1]-t0)/1e3:.2f} us, end {(b[7,2]-t0)/1e3:.2f} us")
+    print("iter " + " ".join(f"{x:>9s}" for x in names))
+    for i in range(s // 64):
+        print(f"{i:4d} " + " ".join(f"{(b[e, i]-t0)/1e3:9.2f}" for e in range(7)))
