@@ -395,14 +395,17 @@ __device__ __forceinline__ void st_sw128_32(uint8_t* tile, int r, int c0, const 
 // operands are the TMA-loaded tiles and every load has two sub-tiles of slack.
 constexpr int HPANEL = 64 * 128;          // 64 rows x 128 B (one 64-column half of a 64-row tile)
 constexpr int SUB_STAGE = 4 * HPANEL;     // two 64-row x 128-col bf16 tiles (Q | dO or K | V)
-constexpr int NSUB = 3;                   // ring depth
+constexpr int NSUB1 = 4;                  // Q | dO ring depth (dK / dV kernel)
+constexpr int NSUB = 5;                   // K | V ring depth (dQ kernel)
+// measured (tools/attn_trace.py): a 32 KB TMA sub-tile load takes ~1.4 us under full load, so the ring
+// must cover load latency + MMA + compute: with 3 stages the loop ran at (that chain) / 3 per sub-tile
 
 // dK / dV: CTA = 128 keys of one (sequence, head); loop over 64-query sub-tiles j >= 2 kb.
 //   TMEM: S^T[b] cols [64b, 64b+64), dP^T[b] [128+64b, ..), dV [256,384), dK [384,512); warp half h
 //   overwrites its own 32 S^T / dP^T columns with 16 columns of packed bf16 P^T / dS^T at 32h.
 //   S^T = K Q_j^T and dP^T = V dO_j^T (M = 128 keys, N = 64 queries, A = K / V from smem);
 //   dV += P^T dO_j and dK += dS^T Q_j (A from TMEM, K = 64 queries; Q_j / dO_j MN-major B).
-constexpr int BWD1_SMEM = 2 * 2 * PANEL + NSUB * SUB_STAGE + NSUB * 512 + 256 + 1024;
+constexpr int BWD1_SMEM = 2 * 2 * PANEL + NSUB1 * SUB_STAGE + NSUB1 * 512 + 256 + 1024;
 
 __global__ void __launch_bounds__(320, 1)
 attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm64,
@@ -420,16 +423,16 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
   if (threadIdx.x == 0) stamp(7, 0);
   uint8_t* sK = smem;
   uint8_t* sV = sK + 2 * PANEL;
-  uint8_t* ring = sV + 2 * PANEL;                                       // [NSUB][Q | dO]
-  float* sLD = reinterpret_cast<float*>(ring + NSUB * SUB_STAGE);      // [NSUB][lse 64 | D 64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + NSUB * 128);
+  uint8_t* ring = sV + 2 * PANEL;                                       // [NSUB1][Q | dO]
+  float* sLD = reinterpret_cast<float*>(ring + NSUB1 * SUB_STAGE);      // [NSUB1][lse 64 | D 64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + NSUB1 * 128);
   uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;   // [NSUB]
-  uint64_t* qd_empty = bars + 4;  // [NSUB]
-  uint64_t* sd_full = bars + 7;   // [2]
-  uint64_t* pd_full = bars + 9;   // [2]
-  uint64_t* done = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* qd_full = bars + 1;            // [NSUB1]
+  uint64_t* qd_empty = bars + 1 + NSUB1;   // [NSUB1]
+  uint64_t* sd_full = bars + 1 + 2 * NSUB1;  // [2]
+  uint64_t* pd_full = sd_full + 2;         // [2]
+  uint64_t* done = pd_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x;  // kb = 0 has the most query sub-tiles: scheduled first
@@ -443,7 +446,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
     tma_prefetch(&tm64);
     tma_prefetch(&tmo64);
     mbar_init(kv_full, 1);
-    for (int i = 0; i < NSUB; ++i) { mbar_init(&qd_full[i], 1); mbar_init(&qd_empty[i], 1); }
+    for (int i = 0; i < NSUB1; ++i) { mbar_init(&qd_full[i], 1); mbar_init(&qd_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&sd_full[i], 1); mbar_init(&pd_full[i], 8); }
     mbar_init(done, 1);
     fence_barrier_init();
@@ -463,8 +466,8 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       tma_load_2d(sV, &tm, kv_full, 2 * nd + head * DH, krow);
       tma_load_2d(sV + PANEL, &tm, kv_full, 2 * nd + head * DH + 64, krow);
       for (int it = 0; it < n_it; ++it) {
-        const int st = it % NSUB, j = j0 + it;
-        mbar_wait(&qd_empty[st], ((it / NSUB) & 1) ^ 1);
+        const int st = it % NSUB1, j = j0 + it;
+        mbar_wait(&qd_empty[st], ((it / NSUB1) & 1) ^ 1);
         stamp(0, it);
         uint8_t* q = ring + st * SUB_STAGE;
         const int qrow = b * s + j * 64;
@@ -483,7 +486,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       constexpr uint32_t id_d = umma_idesc_bf16(128, 128, false, true);
       const uint32_t ak = smem_u32(sK), av = smem_u32(sV);
       auto issue_dvdk = [&](int i) {
-        const int bb = i & 1, st = i % NSUB;
+        const int bb = i & 1, st = i % NSUB1;
         mbar_wait(&pd_full[bb], (i >> 1) & 1);
         stamp(3, i);
         tc_fence_after();
@@ -499,8 +502,8 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       };
       mbar_wait(kv_full, 0);
       for (int it = 0; it < n_it; ++it) {
-        const int bb = it & 1, st = it % NSUB;
-        mbar_wait(&qd_full[st], (it / NSUB) & 1);
+        const int bb = it & 1, st = it % NSUB1;
+        mbar_wait(&qd_full[st], (it / NSUB1) & 1);
         stamp(2, it);
         tc_fence_after();
         const uint32_t q = smem_u32(ring + st * SUB_STAGE), o = q + 2 * HPANEL;
@@ -526,7 +529,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = scale * LOG2E;
     for (int it = 0; it < n_it; ++it) {
-      const int bb = it & 1, st = it % NSUB, j = j0 + it;
+      const int bb = it & 1, st = it % NSUB1, j = j0 + it;
       mbar_wait(&sd_full[bb], (it >> 1) & 1);
       if (warp == 2 && lane == 0) stamp(4, it);
       tc_fence_after();
@@ -595,12 +598,12 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
   uint8_t* ring = sO + 2 * PANEL;  // [NSUB][K | V]
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + NSUB * SUB_STAGE);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [NSUB]
-  uint64_t* kv_empty = bars + 4;  // [NSUB]
-  uint64_t* sd_full = bars + 7;   // [2]
-  uint64_t* ds_full = bars + 9;   // [2]
-  uint64_t* done = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* kv_full = bars + 1;            // [NSUB]
+  uint64_t* kv_empty = bars + 1 + NSUB;    // [NSUB]
+  uint64_t* sd_full = bars + 1 + 2 * NSUB;  // [2]
+  uint64_t* ds_full = sd_full + 2;         // [2]
+  uint64_t* done = ds_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;

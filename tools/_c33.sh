@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+S=gpurun_out/c33_status
+timeout 300 python -m pytest tests/test_gpu_kernels.py -x -q -k attention > gpurun_out/c33_kern.log 2>&1; echo kern $? >> $S
+timeout 120 python tools/attn_trace.py > gpurun_out/c33_trace.log 2>&1; echo trace $? >> $S
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"attn_" --csv python tools/attn_one.py > gpurun_out/c33_ncu.csv 2>&1; echo ncu $? >> $S
+cat $S
