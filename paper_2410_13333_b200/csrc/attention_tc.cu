@@ -537,22 +537,32 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       uint32_t us[32], ud[32];
       tmem_ld32(cs, us);
       tmem_ld32(cs + 128, ud);
+      // this warp's 32 (lse, D) pairs: broadcast 128-bit shared loads while the TMEM loads fly
+      float Lv[32], Dv[32];
+      {
+        const float4* L4 = reinterpret_cast<const float4*>(sLD + st * 128 + half * 32);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float4 a = L4[t], d = L4[t + 16];
+          Lv[4 * t] = a.x * LOG2E; Lv[4 * t + 1] = a.y * LOG2E; Lv[4 * t + 2] = a.z * LOG2E; Lv[4 * t + 3] = a.w * LOG2E;
+          Dv[4 * t] = d.x; Dv[4 * t + 1] = d.y; Dv[4 * t + 2] = d.z; Dv[4 * t + 3] = d.w;
+        }
+      }
       tmem_wait_ld();
-      const float* L = sLD + st * 128 + half * 32;
-      const float* D = L + 64;
+      if (warp == 2 && lane == 0) stamp(1, it);
       const bool diag = j * 64 + half * 32 < key + 32;  // some query column of this warp may precede the key
       uint32_t pp[16], dd[16];
 #pragma unroll
       for (int t = 0; t < 32; t += 2) {
-        float p0 = ex2(fmaf(__uint_as_float(us[t]), sl2, -L[t] * LOG2E));
-        float p1 = ex2(fmaf(__uint_as_float(us[t + 1]), sl2, -L[t + 1] * LOG2E));
+        float p0 = ex2(fmaf(__uint_as_float(us[t]), sl2, -Lv[t]));
+        float p1 = ex2(fmaf(__uint_as_float(us[t + 1]), sl2, -Lv[t + 1]));
         if (diag) {
           const int qi = j * 64 + half * 32 + t;
           if (key > qi) p0 = 0.f;
           if (key > qi + 1) p1 = 0.f;
         }
         pp[t / 2] = pack_bf16(p0, p1);
-        dd[t / 2] = pack_bf16(p0 * (__uint_as_float(ud[t]) - D[t]), p1 * (__uint_as_float(ud[t + 1]) - D[t + 1]));
+        dd[t / 2] = pack_bf16(p0 * (__uint_as_float(ud[t]) - Dv[t]), p1 * (__uint_as_float(ud[t + 1]) - Dv[t + 1]));
       }
       if (warp == 2 && lane == 0) stamp(5, it);
       tmem_st16(cs, pp);

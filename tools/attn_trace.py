@@ -42,7 +42,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 addr = L.lib.malleus_k_attn_bwd_trace_buffer()
 buf = np.ctypeslib.as_array((C.c_uint64 * (2 * 8 * 64)).from_address(addr)).reshape(2, 8, 64).astype(np.int64)
-names = ["QdO_issue", "-", "S_issue", "dVdK_iss", "c_start", "c_math", "c_end"]
+names = ["QdO_issue", "c_tmem", "S_issue", "dVdK_iss", "c_start", "c_math", "c_end"]
 for cta in range(2):
     b = buf[cta]
     t0 = b[7, 0]
