@@ -416,7 +416,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // debugging aid (MALLEUS_ATTN_TRACE): stamps of CTAs (0, 0..1, 0), [event][iteration]
   unsigned long long* tr = (trace && blockIdx.x == 0 && blockIdx.y < 2 && blockIdx.z == 0)
-                               ? trace + blockIdx.y * 8 * 64 : nullptr;
+                               ? trace + blockIdx.y * 16 * 64 : nullptr;
   auto stamp = [&](int ev, int i) {
     if (tr && i < 64) { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); tr[ev * 64 + i] = t; }
   };
@@ -572,6 +572,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       __syncwarp();
       if (lane == 0) mbar_arrive(&pd_full[bb]);
       if (warp == 2 && lane == 0) stamp(6, it);
+      if (lane == 0) stamp(8 + warp - 2, it);  // every compute warp's finish
     }
     mbar_wait(done, 0);
     if (warp == 2 && lane == 0) stamp(7, 1);
@@ -793,7 +794,7 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
   const float scale = rsqrtf((float)DH);
   static unsigned long long* trace = nullptr;
   if (getenv("MALLEUS_ATTN_TRACE") && !trace) {
-    if (cudaMallocManaged(&trace, 2 * 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
+    if (cudaMallocManaged(&trace, 2 * 16 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
     attn_bwd_trace_buffer = trace;
   }
   attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, lse, dsum,

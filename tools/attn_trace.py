@@ -41,12 +41,12 @@ for _ in range(3):
                                   dqkv.data_ptr(), 1e4, st)
 torch.cuda.synchronize()
 addr = L.lib.malleus_k_attn_bwd_trace_buffer()
-buf = np.ctypeslib.as_array((C.c_uint64 * (2 * 8 * 64)).from_address(addr)).reshape(2, 8, 64).astype(np.int64)
-names = ["QdO_issue", "c_tmem", "S_issue", "dVdK_iss", "c_start", "c_math", "c_end"]
-for cta in range(2):
+buf = np.ctypeslib.as_array((C.c_uint64 * (2 * 16 * 64)).from_address(addr)).reshape(2, 16, 64).astype(np.int64)
+names = ["QdO_issue", "c_tmem", "S_issue", "dVdK_iss", "c_start", "c_math", "c_end"] + [f"end_w{w}" for w in range(2, 10)]
+for cta in range(1):
     b = buf[cta]
     t0 = b[7, 0]
     print(f"dKV CTA (0,{cta}): epilogue start {(b[7,1]-t0)/1e3:.2f} us, end {(b[7,2]-t0)/1e3:.2f} us")
-    print("iter " + " ".join(f"{x:>9s}" for x in names))
+    print("iter " + " ".join(f"{x:>8s}" for x in names))
     for i in range(s // 64):
-        print(f"{i:4d} " + " ".join(f"{(b[e, i]-t0)/1e3:9.2f}" for e in range(7)))
+        print(f"{i:4d} " + " ".join(f"{(b[e, i]-t0)/1e3:8.2f}" for e in list(range(7)) + list(range(8, 16))))
