@@ -226,21 +226,32 @@ attn_fwd_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat
 template <int D>
 __global__ void attn_dsum_kernel(int s, int n, const __nv_bfloat16* __restrict__ o,
                                  const __nv_bfloat16* __restrict__ dout, float* __restrict__ dsum, long long T) {
-  const long long idx = blockIdx.x * (long long)blockDim.y + threadIdx.y;  // (token, head)
-  if (idx >= T * n) return;
-  const long long t = idx / n;
-  const int head = idx % n;
-  const __nv_bfloat16* a = o + t * n * D + head * D;
-  const __nv_bfloat16* c = dout + t * n * D + head * D;
+  // D / 64 lanes x 128-bit loads per (token, head) row: 8 lanes per row at D = 128, 4 rows per warp
+  constexpr int LPR = D / 16;  // lanes per row, 2 uint4 (16 elements) each
+  const long long idx = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / LPR;  // (token, head)
+  const int sub = threadIdx.x % LPR;
   float acc = 0.f;
-  for (int i = threadIdx.x * 2; i < D; i += 64) {
-    float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + i));
-    float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(c + i));
-    acc += x.x * y.x + x.y * y.y;
+  if (idx < T * n) {
+    const uint4* a = reinterpret_cast<const uint4*>(o + idx * D) + sub * 2;
+    const uint4* c = reinterpret_cast<const uint4*>(dout + idx * D) + sub * 2;
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const uint4 x = a[v], y = c[v];
+      const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&x);
+      const __nv_bfloat162* yp = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 xf = __bfloat1622float2(xp[q]), yf = __bfloat1622float2(yp[q]);
+        acc = fmaf(xf.x, yf.x, acc);
+        acc = fmaf(xf.y, yf.y, acc);
+      }
+    }
   }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (threadIdx.x == 0) {
+  for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (sub == 0 && idx < T * n) {
+    const long long t = idx / n;
+    const int head = (int)(idx % n);
     const long long b = t / s, i = t % s;
     dsum[(b * n + head) * s + i] = acc;
   }
@@ -498,9 +509,11 @@ template <int D>
 cudaError_t bwd_impl(int nb, int s, int n, const void* qkv, const void* o, const float* lse, const void* dout,
                      void* dqkv, float* dsum, cudaStream_t st) {
   const long long T = (long long)nb * s;
-  dim3 pblk(32, 8);
-  attn_dsum_kernel<D><<<(unsigned)((T * n + 7) / 8), pblk, 0, st>>>(s, n, (const __nv_bfloat16*)o,
-                                                                     (const __nv_bfloat16*)dout, dsum, T); count_launch();
+  {
+    const long long threads = T * n * (D / 16);
+    attn_dsum_kernel<D><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(s, n, (const __nv_bfloat16*)o,
+                                                                           (const __nv_bfloat16*)dout, dsum, T); count_launch();
+  }
   const int smem1 = (2 * BKV + 4 * BQB) * Tile<D>::BYTES + 4 * BQB * 4;
   const int smem2 = (2 * 64 + 4 * BKV) * Tile<D>::BYTES;
   auto k1 = attn_bwd_dkv_kernel<D>;
@@ -538,7 +551,7 @@ cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const vo
   if (s % 64) return cudaErrorInvalidValue;
   if (g_attn_variant == 0 && attention_fwd_tc_supported(s, d)) {
     const long long T = (long long)nb * s;
-    attn_dsum_kernel<128><<<(unsigned)((T * n + 7) / 8), dim3(32, 8), 0, st>>>(
+    attn_dsum_kernel<128><<<(unsigned)((T * n * 8 + 255) / 256), 256, 0, st>>>(
         s, n, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dsum, T); count_launch();
     return attention_bwd_tc(nb, s, n, qkv, lse, dout, dqkv, dsum, rope_cs, st);
   }
