@@ -332,7 +332,7 @@ def main():
                 "gpu_launches": int(n_launch),
                 "replan": replan}
     eng.close()
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the oracle on the host cores, N = 1 only
         line["cpu_baseline"] = oracle_sample(cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
