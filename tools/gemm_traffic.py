@@ -43,7 +43,7 @@ def main(path):
             continue
         v = float(r[mv].replace(",", ""))
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3}.get(r[mu], 1)
+                 "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}.get(r[mu], 1)
         launches.setdefault(r[iid], {})[r[mn]] = v * scale
     alg, per_step = c2_algorithmic_bytes()
     last = list(launches.values())[-per_step:]
