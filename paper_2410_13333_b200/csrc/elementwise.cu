@@ -56,6 +56,10 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
     f[2 * i] = t.x; f[2 * i + 1] = t.y;
   }
 }
+__device__ __forceinline__ uint32_t pack2_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
 __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   uint4 u;
   __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&u);
@@ -120,6 +124,7 @@ __device__ __forceinline__ void load_f8(const float4* p, float (&f)[8]) {
   f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 }
 
+template <int V>  // vectors of 8 columns per thread: h <= 8 * V * NORM_THREADS
 __global__ void __launch_bounds__(NORM_THREADS)
 rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x,
                    const uint4* __restrict__ g, const float* __restrict__ rstd,
@@ -127,9 +132,9 @@ rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x
                    uint4* __restrict__ dx_out, float* __restrict__ dg_part) {
   __shared__ float sh[NORM_THREADS / 32];
   const int nv = h / 8;
-  float dg[NORM_MAXV][8];
+  float dg[V][8];
 #pragma unroll
-  for (int i = 0; i < NORM_MAXV; ++i)
+  for (int i = 0; i < V; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) dg[i][j] = 0.f;
   const int r0 = blockIdx.x * rows_per_block;
@@ -138,7 +143,7 @@ rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x
     const float r = rstd[row];
     float dot = 0.f;
 #pragma unroll
-    for (int i = 0; i < NORM_MAXV; ++i) {
+    for (int i = 0; i < V; ++i) {
       const int c = threadIdx.x + i * NORM_THREADS;
       if (c < nv) {
         float xv[8], dv[8], gg[8];
@@ -155,7 +160,7 @@ rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x
     dot = block_sum<NORM_THREADS>(dot, sh);
     const float coef = r * r * r * dot / (float)h;
 #pragma unroll
-    for (int i = 0; i < NORM_MAXV; ++i) {
+    for (int i = 0; i < V; ++i) {
       const int c = threadIdx.x + i * NORM_THREADS;
       if (c < nv) {
         float xv[8], dv[8], gg[8], o[8], rs[8];
@@ -173,7 +178,7 @@ rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x
     }
   }
 #pragma unroll
-  for (int i = 0; i < NORM_MAXV; ++i) {
+  for (int i = 0; i < V; ++i) {
     const int c = threadIdx.x + i * NORM_THREADS;
     if (c < nv) {
       float4* out = reinterpret_cast<float4*>(dg_part + (long long)blockIdx.x * h + c * 8);
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(256) colsum_accum_kernel(int nb, int h, const 
   }
 }
 
-constexpr int BWD_BLOCKS = 296;  // 2 per SM
+constexpr int BWD_BLOCKS = 148 * 6;  // 6 per SM (80 registers at h = 4096): rows in flight to cover the per-row latency chain
 
 // ---------------------------------------------------------------- residual add
 __global__ void residual_add_kernel(long long nv, const uint4* __restrict__ x, const float4* __restrict__ p,
@@ -325,27 +330,50 @@ __global__ void embed_bwd_kernel(int T, int h, const int32_t* __restrict__ tok, 
 // ---------------------------------------------------------------- vocab-parallel cross-entropy
 constexpr int CE_THREADS = 256;
 
-// stats[t] = {local max, sum exp(z - local max), target logit or 0}
+// stats[t] = {local max, sum exp(z - local max), target logit or 0}.  One pass: each thread keeps
+// a running (max, sum) over float4 chunks (rescaled when the max grows), then the block merges the
+// pairs; V % 4 == 0 (vocab splits are multiples of 16).
+__device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+  m = mn;
+}
 __global__ void __launch_bounds__(CE_THREADS)
 ce_stats_kernel(int V, const float* __restrict__ z, const int32_t* __restrict__ tgt, int v0,
                 float* __restrict__ stats) {
-  __shared__ float sh[CE_THREADS / 32];
+  __shared__ float shm[CE_THREADS / 32], shs[CE_THREADS / 32];
   const int t = blockIdx.x;
   const float* zr = z + (long long)t * V;
-  float m = -INFINITY;
-  for (int c = threadIdx.x; c < V; c += CE_THREADS) m = fmaxf(m, zr[c]);
-  m = block_max<CE_THREADS>(m, sh);
-  float s = 0.f;
-  for (int c = threadIdx.x; c < V; c += CE_THREADS) s += __expf(zr[c] - m);
-  s = block_sum<CE_THREADS>(s, sh);
+  const float4* z4 = reinterpret_cast<const float4*>(zr);
+  float m = -INFINITY, s = 0.f;
+  for (int c = threadIdx.x; c < V / 4; c += CE_THREADS) {
+    const float4 v = z4[c];
+    const float cm = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+    if (cm > m) {
+      s = (m == -INFINITY) ? 0.f : s * __expf(m - cm);
+      m = cm;
+    }
+    s += __expf(v.x - m) + __expf(v.y - m) + __expf(v.z - m) + __expf(v.w - m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    ms_merge(m, s, m2, s2);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { shm[w] = m; shs[w] = s; }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    float M = shm[0], S = shs[0];
+    for (int i = 1; i < CE_THREADS / 32; ++i) ms_merge(M, S, shm[i], shs[i]);
     const int y = tgt[t] - v0;
-    stats[3 * t] = m;
-    stats[3 * t + 1] = s;
+    stats[3 * t] = M;
+    stats[3 * t + 1] = S;
     stats[3 * t + 2] = (y >= 0 && y < V) ? zr[y] : 0.f;
   }
 }
 
+// dz = (softmax - onehot) * scale (bf16), float4 in / 4 x bf16 out per thread step
 __global__ void ce_grad_kernel(int V, const float* __restrict__ z, const int32_t* __restrict__ tgt, int v0,
                                const float* __restrict__ gmax, const float* __restrict__ gsum,
                                const float* __restrict__ gtgt, float scale, __nv_bfloat16* __restrict__ dz,
@@ -353,13 +381,17 @@ __global__ void ce_grad_kernel(int V, const float* __restrict__ z, const int32_t
   const int t = blockIdx.x;
   const float lse = gmax[t] + logf(gsum[t]);
   if (threadIdx.x == 0 && loss_rows) loss_rows[t] = lse - gtgt[t];
-  const float* zr = z + (long long)t * V;
-  __nv_bfloat16* dr = dz + (long long)t * V;
+  const float4* z4 = reinterpret_cast<const float4*>(z + (long long)t * V);
+  uint2* d4 = reinterpret_cast<uint2*>(dz + (long long)t * V);
   const int y = tgt[t] - v0;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) {
-    float p = __expf(zr[c] - lse);
-    if (c == y) p -= 1.f;
-    dr[c] = __float2bfloat16_rn(p * scale);
+  for (int c = threadIdx.x; c < V / 4; c += blockDim.x) {
+    const float4 v = z4[c];
+    float p[4] = {__expf(v.x - lse), __expf(v.y - lse), __expf(v.z - lse), __expf(v.w - lse)};
+    if ((y >> 2) == c) p[y & 3] -= 1.f;
+    uint2 o;
+    o.x = pack2_bf16(p[0] * scale, p[1] * scale);
+    o.y = pack2_bf16(p[2] * scale, p[3] * scale);
+    d4[c] = o;
   }
 }
 
@@ -419,8 +451,11 @@ cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float*
   if (h % 8 || h > 8 * NORM_MAXV * NORM_THREADS || T <= 0) return cudaErrorInvalidValue;
   int rpb = (T + BWD_BLOCKS - 1) / BWD_BLOCKS;
   int nb = (T + rpb - 1) / rpb;
-  rmsnorm_bwd_kernel<<<nb, NORM_THREADS, 0, st>>>(T, h, rpb, (const uint4*)x, (const uint4*)g, rstd,
-                                                  (const float4*)dy, (const uint4*)dres, (uint4*)dx_out, scratch); count_launch();
+  const int vpt = (h / 8 + NORM_THREADS - 1) / NORM_THREADS;
+  auto kern = vpt <= 1 ? rmsnorm_bwd_kernel<1> : vpt == 2 ? rmsnorm_bwd_kernel<2>
+            : vpt <= 4 ? rmsnorm_bwd_kernel<4> : rmsnorm_bwd_kernel<NORM_MAXV>;
+  kern<<<nb, NORM_THREADS, 0, st>>>(T, h, rpb, (const uint4*)x, (const uint4*)g, rstd, (const float4*)dy,
+                                    (const uint4*)dres, (uint4*)dx_out, scratch); count_launch();
   colsum_accum_kernel<<<(h + 31) / 32, 256, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
   return cudaGetLastError();
 }
@@ -464,6 +499,7 @@ cudaError_t embed_bwd(int T, int h, const int32_t* tok, const void* dx, float* d
 }
 
 cudaError_t ce_stats(int T, int V, const float* z, const int32_t* tgt, int v0, float* stats, cudaStream_t st) {
+  if (V % 4) return cudaErrorInvalidValue;
   ce_stats_kernel<<<T, CE_THREADS, 0, st>>>(V, z, tgt, v0, stats); count_launch();
   return cudaGetLastError();
 }
@@ -480,6 +516,7 @@ cudaError_t ce_local_sum(int T, const float* stats, const float* gmax, float* su
 
 cudaError_t ce_grad(int T, int V, const float* z, const int32_t* tgt, int v0, const float* gmax, const float* gsum,
                     const float* gtgt, float scale, void* dz, float* loss_rows, cudaStream_t st) {
+  if (V % 4) return cudaErrorInvalidValue;
   ce_grad_kernel<<<T, 256, 0, st>>>(V, z, tgt, v0, gmax, gsum, gtgt, scale, (__nv_bfloat16*)dz, loss_rows); count_launch();
   return cudaGetLastError();
 }
