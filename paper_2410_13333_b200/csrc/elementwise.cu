@@ -188,22 +188,22 @@ rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x
   }
 }
 
-// dg[c] += sum_b part[b][c] in a fixed order (deterministic): block = 32 columns x 8 warps, warp w
-// sums rows w, w+8, ... (lane = column, coalesced), then the 8 warp sums are added in warp order.
-__global__ void __launch_bounds__(256) colsum_accum_kernel(int nb, int h, const float* __restrict__ part,
-                                                           float* __restrict__ dg) {
-  __shared__ float sh[8][33];
+// dg[c] += sum_b part[b][c] in a fixed order (deterministic): block = 32 columns x 32 warps, warp w
+// sums rows w, w+32, ... (lane = column, coalesced), then the 32 warp sums are added in warp order.
+__global__ void __launch_bounds__(1024) colsum_accum_kernel(int nb, int h, const float* __restrict__ part,
+                                                            float* __restrict__ dg) {
+  __shared__ float sh[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
   if (c < h)
-    for (int b = w; b < nb; b += 8) s += part[(long long)b * h + c];
+    for (int b = w; b < nb; b += 32) s += part[(long long)b * h + c];
   sh[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < h) {
     float t = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += sh[i][lane];
+    for (int i = 0; i < 32; ++i) t += sh[i][lane];
     dg[c] += t;
   }
 }
@@ -456,7 +456,7 @@ cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float*
             : vpt <= 4 ? rmsnorm_bwd_kernel<4> : rmsnorm_bwd_kernel<NORM_MAXV>;
   kern<<<nb, NORM_THREADS, 0, st>>>(T, h, rpb, (const uint4*)x, (const uint4*)g, rstd, (const float4*)dy,
                                     (const uint4*)dres, (uint4*)dx_out, scratch); count_launch();
-  colsum_accum_kernel<<<(h + 31) / 32, 256, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
+  colsum_accum_kernel<<<(h + 31) / 32, 1024, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
   return cudaGetLastError();
 }
 
