@@ -153,6 +153,8 @@ def main():
     ap.add_argument("--uniform", action="store_true", help="non-malleable even plan (T_u / T0 runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replan", action="store_true", help="keep the nominal-rate plan (no measured re-plan)")
+    ap.add_argument("--tp4-stage", action="store_true",
+                    help="4 GPUs: one pipeline with the 8-GPU ladder's TP-4 stage (rank 3 at 2x); exercises that path")
     args = ap.parse_args()
     if os.environ.get("MALLEUS_WATCHDOG"):  # debugging aid: dump all stacks if the run hangs
         import faulthandler
@@ -183,6 +185,11 @@ def main():
     B = args.batch
     straggle = STRAGGLER[world] if not args.no_straggler else None
     plan = Pl.ladder_plan(cfg, world, B, b=1, straggle=not args.uniform)
+    if args.tp4_stage:
+        assert world == 4, "--tp4-stage runs on 4 GPUs"
+        straggle = None if args.no_straggler else STRAGGLER[8]
+        p8 = Pl.ladder_plan(cfg, 8, B, b=1, straggle=not args.uniform)
+        plan = Pl.plan([Pl.pipe(p8["pipes"][0]["stages"], B)], 1, B)
     eng = Engine(cfg, rank, world, local)
     eng.apply(plan)
     eng.write_weights(make_weights(cfg, parity=False))

@@ -48,7 +48,8 @@ def world_of(p) -> int:
 
 
 def plan_matrix_c1(cfg, B=8, b=2):
-    """SURVEY §8(d) parity plan matrix P0-P8 on the tiny C1 model (4 heads, F 512, V 256, L 2)."""
+    """SURVEY §8(d) parity plan matrix P0-P8 on the tiny C1 model (4 heads, F 512, V 256, L 2), plus P9
+    (TP 4, uneven FFN / vocab)."""
     L = cfg.n_layers
     m = B // b
     H, F, V = cfg.n_heads, cfg.ffn, cfg.vocab
@@ -66,6 +67,11 @@ def plan_matrix_c1(cfg, B=8, b=2):
     P["P7"] = plan([pipe([ev([0], [0, 1]), s31([1, 2], [1, L])], 1),
                     pipe([ev([3, 4, 5, 6], [0, L])], 3)], b, B, standby=[7])
     P["P8"] = plan([pipe([ev([0], [0, L])], 4), pipe([ev([1], [0, L])], 0)], b, B)
+    # TP 4 with uneven FFN / vocab splits (3:2:2:1) on one pipeline: the stage shape of the 8-GPU
+    # ladder (DP2 x TP4) on 4 GPUs
+    f4 = [3 * F // 8, F // 4, F // 4, F // 8]
+    v4 = [3 * V // 8, V // 4, V // 4, V // 8]
+    P["P9"] = plan([pipe([stage([0, 1, 2, 3], [H // 4] * 4, f4, v4, [0, L])], m)], b, B)
     return P
 
 
