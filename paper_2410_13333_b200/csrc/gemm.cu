@@ -43,6 +43,11 @@ struct GemmParams {
   int tma_epi; // C written by TMA store / reduce-add (CTA-pair kernel)
   const float2* rope_cs;  // fused RoPE (bf16 TMA epilogue only), see GemmDesc
   int rope_cols, rope_s;
+  int n_dst, rows_per_dst;  // row-split destinations (GemmDesc::dst)
+  void* dst[4];
+};
+struct TmapSet {  // per-destination C maps of the row-split TMA epilogue
+  CUtensorMap m[4];
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
@@ -60,6 +65,13 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 // tcgen05.ld) -> registers -> bf16 / fp32 store or fp32 read-add-write (wgrad accumulation).
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t taddr, int row, int col_base) {
   const bool row_ok = row < p.M;
+  void* Cb = p.C;
+  long long crow = row;
+  if (p.n_dst && row_ok) {
+    const int d = row / p.rows_per_dst;
+    Cb = d == 0 ? p.dst[0] : d == 1 ? p.dst[1] : d == 2 ? p.dst[2] : p.dst[3];  // no local-memory indexing
+    crow = row - (long long)d * p.rows_per_dst;
+  }
 #pragma unroll 1
   for (int c = 0; c < 256 / 32; ++c) {
     const int col0 = col_base + c * 32;
@@ -69,7 +81,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
     if (!row_ok || col0 >= p.N) continue;
     const bool full_chunk = p.vec_ok && col0 + 32 <= p.N;
     if (p.mode == GEMM_STORE_BF16) {
-      __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(p.C) + (long long)row * p.ldc + col0;
+      __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(Cb) + crow * p.ldc + col0;
       if (full_chunk) {
         uint4* dst = reinterpret_cast<uint4*>(C);
 #pragma unroll
@@ -85,7 +97,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
         for (int j = 0; j < 32 && col0 + j < p.N; ++j) C[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
       }
     } else {
-      float* C = reinterpret_cast<float*>(p.C) + (long long)row * p.ldc + col0;
+      float* C = reinterpret_cast<float*>(Cb) + crow * p.ldc + col0;
       const bool accum = p.mode == GEMM_ACCUM_F32;
       if (full_chunk) {
         float4* dst = reinterpret_cast<float4*>(C);
@@ -111,10 +123,17 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
 // 128B-swizzled smem box (double buffered) and written with one TMA store, or, for the fp32
 // wgrad accumulation, with one TMA reduce-add (the add happens in L2; the SM never reads C).
 // Out-of-bounds rows / columns are clipped by TMA, so ragged uneven-split shapes need no masks.
-__device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC, uint32_t taddr,
-                                                  int row_box0, int col_base, uint8_t* stg, int& sbuf) {
+__device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC, const TmapSet* tmD,
+                                                  uint32_t taddr, int row_box0, int col_base, uint8_t* stg,
+                                                  int& sbuf) {
   const int lane = threadIdx.x & 31;
   if (row_box0 >= p.M) return;
+  int crow = row_box0;  // store coordinate: in C, or in this box's destination (rows_per_dst % 32 == 0)
+  if (p.n_dst) {
+    const int d = row_box0 / p.rows_per_dst;
+    tmC = &tmD->m[d];
+    crow = row_box0 - d * p.rows_per_dst;
+  }
   if (p.mode == GEMM_STORE_BF16 && p.rope_cs != nullptr && col_base < p.rope_cols) {
     // QKV projection with RoPE fused (half-split pairs (i, i+64) of each 128-column head, reading
     // R3): the two heads of this 256-column tile are rotated in registers before the bf16 store.
@@ -163,7 +182,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(tmC, buf, hc0 + half * 64, row_box0);
+          tma_store_2d(tmC, buf, hc0 + half * 64, crow);
           bulk_commit();
         }
         sbuf ^= 1;
@@ -197,7 +216,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(tmC, buf, col0, row_box0);
+        tma_store_2d(tmC, buf, col0, crow);
         bulk_commit();
       }
       sbuf ^= 1;
@@ -221,8 +240,8 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        if (p.mode == GEMM_ACCUM_F32) tma_reduce_add_2d(tmC, buf, col0, row_box0);
-        else tma_store_2d(tmC, buf, col0, row_box0);
+        if (p.mode == GEMM_ACCUM_F32) tma_reduce_add_2d(tmC, buf, col0, crow);
+        else tma_store_2d(tmC, buf, col0, crow);
         bulk_commit();
       }
       sbuf ^= 1;
@@ -337,6 +356,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+    if (p.n_dst) __threadfence_system();  // row-split stores (possibly peer memory) visible system-wide
   }
   tc_fence_before();
   __syncthreads();
@@ -362,7 +382,8 @@ constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + EPI_STAGE_BYTES + 1024 + 102
 template <bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ CUtensorMap tmC, GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmC, const __grid_constant__ TmapSet tmD,
+                        GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_stage = smem + STAGES2 * STAGE2_BYTES;
@@ -466,13 +487,14 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       tc_fence_after();
       const int row_box0 = tm * 2 * BM2 + rank * BM2 + quarter * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN2;
-      if (p.tma_epi) epilogue_tile_tma(p, &tmC, taddr, row_box0, tn * BN2, stg, sbuf);
+      if (p.tma_epi) epilogue_tile_tma(p, &tmC, &tmD, taddr, row_box0, tn * BN2, stg, sbuf);
       else epilogue_tile(p, taddr, row_box0 + lane, tn * BN2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&tempty[acc]);
     }
     if (lane == 0) bulk_wait_all();
+    if (p.n_dst) __threadfence_system();  // row-split stores (possibly peer memory) visible system-wide
     __syncwarp();
   }
   tc_fence_before();
@@ -603,8 +625,8 @@ void gemm_set_variant(int v) {
 }
 
 template <bool A_MN, bool B_MN>
-static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const GemmParams& p,
-                           cudaStream_t st) {
+static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const TmapSet& td,
+                           const GemmParams& p, cudaStream_t st) {
   static bool attr_set = false;
   auto kern = gemm_tcgen05_2sm_kernel<A_MN, B_MN>;
   if (!attr_set) {
@@ -630,7 +652,7 @@ static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const C
     }
     cudaEventRecord(g_prof.ev[g_prof.used].first, st);
   }
-  kern<<<grid, GEMM_THREADS, GEMM2_SMEM, st>>>(ta, tb, tc, p); count_launch();
+  kern<<<grid, GEMM_THREADS, GEMM2_SMEM, st>>>(ta, tb, tc, td, p); count_launch();
   if (prof) {
     cudaEventRecord(g_prof.ev[g_prof.used].second, st);
     g_prof.flops.push_back(2.0 * p.M * (double)p.N * p.K);
@@ -646,34 +668,51 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
   if ((g.lda % 8) || (g.ldb % 8) || (g.ldc % 4) ||
       (reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15))
     return cudaErrorInvalidValue;
+  if (g.n_dst < 0 || g.n_dst > 4 || (g.n_dst > 0 && (g.rows_per_dst <= 0 || g.n_dst * g.rows_per_dst != g.M ||
+                                                     g.mode == GEMM_ACCUM_F32 || g.rope_cs)))
+    return cudaErrorInvalidValue;
+  const int esz = g.mode == GEMM_STORE_BF16 ? 2 : 4;
+  int vec_ok = (g.ldc * esz) % 16 == 0;
+  if (g.n_dst)
+    for (int d = 0; d < g.n_dst; ++d) vec_ok &= (reinterpret_cast<uintptr_t>(g.dst[d]) & 15) == 0;
+  else
+    vec_ok &= (reinterpret_cast<uintptr_t>(g.C) & 15) == 0;
+  GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, 0, nullptr, 0, 0, g.n_dst, g.rows_per_dst,
+               {g.dst[0], g.dst[1], g.dst[2], g.dst[3]}};
   const bool pair = g_variant == 2 || (g_variant == 0 && g.M >= 256);
   if (pair) {
     CUtensorMap ta, tb;
     bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.lda, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, BM2);
     ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, BN2 / 2));
     if (!ok) return cudaErrorInvalidValue;
-    const int esz = g.mode == GEMM_STORE_BF16 ? 2 : 4;
-    const int vec_ok = ((g.ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0);
     CUtensorMap tc;
-    int tma_epi = vec_ok && g_tma_epi && make_map_c(&tc, g.C, g.N, g.M, g.ldc, g.mode != GEMM_STORE_BF16);
-    if (!tma_epi) memset(&tc, 0, sizeof(tc));
+    TmapSet td;
+    memset(&tc, 0, sizeof(tc));
+    memset(&td, 0, sizeof(td));
+    int tma_epi = vec_ok && g_tma_epi;
+    if (tma_epi && g.n_dst) {  // one C map per destination; 32-row boxes must not straddle two
+      tma_epi = g.rows_per_dst % 32 == 0;
+      for (int d = 0; d < g.n_dst && tma_epi; ++d)
+        tma_epi = make_map_c(&td.m[d], g.dst[d], g.N, g.rows_per_dst, g.ldc, g.mode != GEMM_STORE_BF16);
+    } else if (tma_epi) {
+      tma_epi = make_map_c(&tc, g.C, g.N, g.M, g.ldc, g.mode != GEMM_STORE_BF16);
+    }
     const bool rope = tma_epi && g.rope_cs && g.mode == GEMM_STORE_BF16 && g.rope_cols % 128 == 0;
     if (g.rope_done) *g.rope_done = rope;
-    GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, tma_epi, rope ? g.rope_cs : nullptr, g.rope_cols,
-                 g.rope_s};
-    if (!g.a_mn && !g.b_mn) return launch2<false, false>(ta, tb, tc, p, st);
-    if (!g.a_mn && g.b_mn) return launch2<false, true>(ta, tb, tc, p, st);
-    if (g.a_mn && g.b_mn) return launch2<true, true>(ta, tb, tc, p, st);
-    return launch2<true, false>(ta, tb, tc, p, st);
+    p.tma_epi = tma_epi;
+    p.rope_cs = rope ? g.rope_cs : nullptr;
+    p.rope_cols = g.rope_cols;
+    p.rope_s = g.rope_s;
+    if (!g.a_mn && !g.b_mn) return launch2<false, false>(ta, tb, tc, td, p, st);
+    if (!g.a_mn && g.b_mn) return launch2<false, true>(ta, tb, tc, td, p, st);
+    if (g.a_mn && g.b_mn) return launch2<true, true>(ta, tb, tc, td, p, st);
+    return launch2<true, false>(ta, tb, tc, td, p, st);
   }
   CUtensorMap ta, tb;
   bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.lda, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, BM);
   ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, BN));
   if (!ok) return cudaErrorInvalidValue;
-  const int esz = g.mode == GEMM_STORE_BF16 ? 2 : 4;
-  const int vec_ok = ((g.ldc * esz) % 16 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0);
   if (g.rope_done) *g.rope_done = false;
-  GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, 0, nullptr, 0, 0};
   if (!g.a_mn && !g.b_mn) return launch<false, false>(ta, tb, p, st);
   if (!g.a_mn && g.b_mn) return launch<false, true>(ta, tb, p, st);
   if (g.a_mn && g.b_mn) return launch<true, true>(ta, tb, p, st);

@@ -26,6 +26,11 @@ struct GemmDesc {
   const float2* rope_cs = nullptr;
   int rope_cols = 0, rope_s = 0;
   bool* rope_done = nullptr;
+  // optional row-split destination (reduce-scatter fused into the epilogue, TP partials): row r
+  // goes to dst[r / rows_per_dst] + (r % rows_per_dst) * ldc instead of C (M == n_dst * rows_per_dst;
+  // dst may be peer memory).  The kernel makes its stores visible system-wide before it ends.
+  int n_dst = 0, rows_per_dst = 0;
+  void* dst[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st);
 

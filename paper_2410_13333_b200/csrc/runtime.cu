@@ -655,14 +655,22 @@ static bool tp_peer(const Layout& L) { return L.TP > 1 && L.p2p && L.tpflags != 
 static float* tp_part(Layout& L) { return tp_peer(L) ? L.tpp[(L.tp_epoch + 1) & 1] : L.part; }
 // the row-parallel GEMM's store mode for that buffer
 static int tp_part_mode(const Layout& L) { return tp_peer(L) && L.tp_bf16 ? GEMM_STORE_BF16 : GEMM_STORE_F32; }
+// reduce-scatter fused into the GEMM epilogue: each member's GEMM stores the rows owned by member d
+// straight into d's receive slot (its own index) over NVLink, overlapping the transfer with the
+// GEMM; the reduction kernel then reads only local slots.  Needs bf16 partials, k <= 4 and
+// T / k rows per member in whole 32-row boxes (MALLEUS_TP_NO_SCATTER=1 disables it).
+static bool tp_scatter(const Layout& L) {
+  static const bool off = getenv("MALLEUS_TP_NO_SCATTER") != nullptr;
+  return !off && tp_peer(L) && L.tp_bf16 && L.TP <= 4 && L.T % L.TP == 0 && (L.T / L.TP) % 32 == 0;
+}
 static Layout& member_layout(Layout& L, int j) {
   const int r = L.plan.pipes[L.pipe].stages[L.stage].ranks[j];
   return L.peer[r] ? *L.peer[r] : L;
 }
 // sel(M, a, j) fills member j's destinations a.d0/d1/d2[j] from its layout M
 template <class Sel>
-static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const float* part, const void* x, const void* g,
-                                     Sel sel, cudaStream_t st) {
+static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, const void* g, Sel sel,
+                                     cudaStream_t st) {
   Layout& L = *ctx->L;
   duty_end(ctx, st);
   ev_begin(ctx, st, CAT_TP);
@@ -678,9 +686,15 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const float* pa
   a.g = g;
   a.part_bf16 = L.tp_bf16 ? 1 : 0;
   const int buf = (int)(a.epoch & 1);
+  const bool scatter = tp_scatter(L);
+  const size_t slot = (size_t)(L.T / L.TP) * a.h;  // elements per receive slot (scatter layout)
   for (int j = 0; j < L.TP; ++j) {
     Layout& M = member_layout(L, j);
-    a.part[j] = j == L.member ? part : M.tpp[buf];
+    // the kernel reads part[j] + row * h for its own rows [me*T/k, ...): with the scatter layout
+    // that is local slot j, addressed relative to this member's first row
+    a.part[j] = scatter ? reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(L.tpp[buf]) +
+                                                         ((size_t)j - (size_t)L.member) * slot * 2)
+                        : M.tpp[buf];
     a.flags[j] = M.tpflags;
     sel(M, a, j);
   }
@@ -690,10 +704,28 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const float* pa
 }
 
 // backward input gradients: L.part = sum_j P_j on every member (peer kernel, else NCCL in place)
-static malleus_status tp_sum(malleus_ctx* ctx, float* pb, cudaStream_t st) {
+static malleus_status tp_sum(malleus_ctx* ctx, cudaStream_t st) {
   Layout& L = *ctx->L;
   if (!tp_peer(L)) return tp_allreduce(ctx, L.part, (size_t)L.T * ctx->cfg.hidden, ncclSum, st);
-  return tp_reduce_peer(ctx, TP_SUM, pb, nullptr, nullptr, [&](Layout& M, TpArgs& a, int j) { a.d0[j] = M.part; }, st);
+  return tp_reduce_peer(ctx, TP_SUM, nullptr, nullptr, [&](Layout& M, TpArgs& a, int j) { a.d0[j] = M.part; }, st);
+}
+
+// row-parallel GEMM producing this member's partial sum of a TP reduction (C = A B, [M = T, N = h]):
+// into L.part (no peer path), this member's full partial buffer, or scattered by rows to the members'
+// receive slots (tp_scatter)
+static malleus_status part_gemm(malleus_ctx* ctx, int M, int N, int K, const void* A, long long lda, bool amn,
+                                const void* B, long long ldb, bool bmn, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  if (!tp_scatter(L)) return gemm(ctx, M, N, K, A, lda, amn, B, ldb, bmn, tp_part(L), N, tp_part_mode(L), st);
+  const int buf = (int)((L.tp_epoch + 1) & 1);
+  const int rows = L.T / L.TP;
+  GemmDesc g{M, N, K, A, lda, amn, B, ldb, bmn, nullptr, N, GEMM_STORE_BF16};
+  g.n_dst = L.TP;
+  g.rows_per_dst = rows;
+  for (int d = 0; d < L.TP; ++d)
+    g.dst[d] = reinterpret_cast<uint16_t*>(member_layout(L, d).tpp[buf]) + (size_t)L.member * rows * N;
+  CK(gemm_bf16(g, st));
+  return MALLEUS_OK;
 }
 
 // DUTY straggler emulation: every compute segment (the kernels between two TP collectives) is
@@ -750,10 +782,9 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   }
   CK(attention_fwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
   if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
-  float* pb = tp_part(L);
-  RET(gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, pb, h, tp_part_mode(L), st));
+  RET(part_gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, st));
   if (tp_peer(L)) {  // x1 = x + sum P, a2 = RMSNorm(x1) in one peer-memory kernel
-    RET(tp_reduce_peer(ctx, TP_RESID_NORM, pb, S.x[li], P.g2, [&](Layout& M, TpArgs& a, int j) {
+    RET(tp_reduce_peer(ctx, TP_RESID_NORM, S.x[li], P.g2, [&](Layout& M, TpArgs& a, int j) {
       const SlotLayer& Z = M.slot[si].L[li];
       a.d0[j] = Z.x1; a.d1[j] = Z.a2; a.d2[j] = Z.r2;
     }, st));
@@ -765,10 +796,9 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   }
   RET(gemm(ctx, T, 2 * F, h, Y.a2, h, false, P.wgu, h, false, Y.gu, 2 * F, GEMM_STORE_BF16, st));
   CK(swiglu_fwd(T, F, Y.gu, Y.u, st));
-  pb = tp_part(L);
-  RET(gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, pb, h, tp_part_mode(L), st));
+  RET(part_gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, st));
   if (tp_peer(L)) {  // x[l+1] = x1 + sum P
-    RET(tp_reduce_peer(ctx, TP_RESID, pb, Y.x1, nullptr, [&](Layout& M, TpArgs& a, int j) {
+    RET(tp_reduce_peer(ctx, TP_RESID, Y.x1, nullptr, [&](Layout& M, TpArgs& a, int j) {
       a.d0[j] = M.slot[si].x[li + 1];
     }, st));
   } else {
@@ -796,10 +826,9 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, T, F, h, dy, h, false, P.wd, h, false, L.du, F, GEMM_STORE_BF16, st));
   RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
   CK(swiglu_bwd(T, F, Y.gu, L.du, L.dgu, st));
-  float* pb = tp_part(L);
-  RET(gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, pb, h, tp_part_mode(L), st));
+  RET(part_gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, st));
   RET(gemm(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
-  RET(tp_sum(ctx, pb, st));
+  RET(tp_sum(ctx, st));
   duty_begin(ctx, 4, st);
   CK(rmsnorm_bwd(T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st));
   // attention
@@ -809,10 +838,9 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
     CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
-  pb = tp_part(L);
-  RET(gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, pb, h, tp_part_mode(L), st));
+  RET(part_gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, st));
   RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
-  RET(tp_sum(ctx, pb, st));
+  RET(tp_sum(ctx, st));
   duty_begin(ctx, 5, st);
   CK(rmsnorm_bwd(T, h, S.x[li], P.g1, Y.r1, L.part, dx1, dx, P.dg1, L.scratch, st));
   duty_end(ctx, st);
@@ -840,10 +868,9 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
              L.loss_rows, st));
   if (L.member == 0)
     CK(reduce_loss(T, L.loss_rows, (float)(1.0 / ((double)L.plan.B * c.seq_len)), L.loss_acc, 1, st));
-  float* pb = tp_part(L);
-  RET(gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, pb, h, tp_part_mode(L), st));
+  RET(part_gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, st));
   RET(gemm(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, first ? GEMM_STORE_F32 : GEMM_ACCUM_F32, st));
-  RET(tp_sum(ctx, pb, st));
+  RET(tp_sum(ctx, st));
   duty_begin(ctx, 8, st);
   CK(rmsnorm_bwd(T, h, S.x[L.n_local], L.gf, S.rf, L.part, nullptr, S.dlast, L.dgf, L.scratch, st));
   duty_end(ctx, st);

@@ -101,3 +101,26 @@ def test_tp_peer_reduce_matches_nccl(tmp_path):
         res[tag] = json.load(open(out))
         _assert_ok(res[tag])
     assert res["peer"]["losses"] == res["nccl"]["losses"], (res["peer"]["losses"], res["nccl"]["losses"])
+
+
+@pytest.mark.parametrize("plan", ["P2", "P9"])
+def test_tp_scatter_epilogue_bitwise(plan, tmp_path):
+    """Reduce-scatter fused into the row-parallel GEMM epilogue (rows stored straight into the owning
+    member's receive slot over NVLink) against the unfused peer path (MALLEUS_TP_NO_SCATTER=1): the
+    same bf16 partials summed in the same member order, so a 3-step run's losses agree bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    n = PLAN_WORLD[plan]
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"{plan} needs {n} GPUs")
+    res = {}
+    for tag, extra in (("scatter", {}), ("pull", {"MALLEUS_TP_NO_SCATTER": "1"})):
+        out = tmp_path / f"{tag}.json"
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr=127.0.0.1", "--master-port=29536", os.path.join(ROOT, "tests", "mp_worker.py"), plan,
+               str(out), "3", "c1m"]
+        p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env={**os.environ, **extra})
+        assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+        res[tag] = json.load(open(out))
+        _assert_ok(res[tag])
+    assert res["scatter"]["losses"] == res["pull"]["losses"], (res["scatter"]["losses"], res["pull"]["losses"])
