@@ -657,11 +657,16 @@ static float* tp_part(Layout& L) { return tp_peer(L) ? L.tpp[(L.tp_epoch + 1) & 
 static int tp_part_mode(const Layout& L) { return tp_peer(L) && L.tp_bf16 ? GEMM_STORE_BF16 : GEMM_STORE_F32; }
 // reduce-scatter fused into the GEMM epilogue: each member's GEMM stores the rows owned by member d
 // straight into d's receive slot (its own index) over NVLink, overlapping the transfer with the
-// GEMM; the reduction kernel then reads only local slots.  Needs bf16 partials, k <= 4 and
-// T / k rows per member in whole 32-row boxes (MALLEUS_TP_NO_SCATTER=1 disables it).
+// GEMM; the reduction kernel then reads only local slots.  Needs bf16 partials and T / k rows per
+// member in whole 32-row boxes.  Used for k = 2 only: measured at TP 4 (3/4 of the rows remote) the
+// epilogue's remote stores slowed the GEMMs by more than the reduction gained (C2: N = 2 T0 258 ->
+// 263 K tokens/s, N = 4 DP2 x TP2 502 -> 514 K, TP 4 stage 355 -> 351 K).  MALLEUS_TP_NO_SCATTER=1
+// disables it, MALLEUS_TP_SCATTER_K=4 allows it up to k = 4.
 static bool tp_scatter(const Layout& L) {
   static const bool off = getenv("MALLEUS_TP_NO_SCATTER") != nullptr;
-  return !off && tp_peer(L) && L.tp_bf16 && L.TP <= 4 && L.T % L.TP == 0 && (L.T / L.TP) % 32 == 0;
+  static const int kmax = getenv("MALLEUS_TP_SCATTER_K") ? atoi(getenv("MALLEUS_TP_SCATTER_K")) : 2;
+  return !off && tp_peer(L) && L.tp_bf16 && L.TP <= std::min(kmax, 4) && L.T % L.TP == 0 &&
+         (L.T / L.TP) % 32 == 0;
 }
 static Layout& member_layout(Layout& L, int j) {
   const int r = L.plan.pipes[L.pipe].stages[L.stage].ranks[j];

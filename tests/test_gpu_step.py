@@ -114,7 +114,7 @@ def test_tp_scatter_epilogue_bitwise(plan, tmp_path):
     if torch.cuda.device_count() < n:
         pytest.skip(f"{plan} needs {n} GPUs")
     res = {}
-    for tag, extra in (("scatter", {}), ("pull", {"MALLEUS_TP_NO_SCATTER": "1"})):
+    for tag, extra in (("scatter", {"MALLEUS_TP_SCATTER_K": "4"}), ("pull", {"MALLEUS_TP_NO_SCATTER": "1"})):
         out = tmp_path / f"{tag}.json"
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                "--master-addr=127.0.0.1", "--master-port=29536", os.path.join(ROOT, "tests", "mp_worker.py"), plan,
