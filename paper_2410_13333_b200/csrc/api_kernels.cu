@@ -83,8 +83,6 @@ extern "C" malleus_status malleus_k_attention_variant(int32_t variant) {
   return MALLEUS_OK;
 }
 
-static unsigned long long* trace = nullptr;  // MALLEUS_TP_TRACE: stamps of the last call (tools/tp_bench.py)
-
 extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, int32_t h, int32_t mode,
                                               int32_t part_dtype, float eps, uint64_t epoch, const void* const* part,
                                               uint64_t* const* flags,
@@ -94,10 +92,7 @@ extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, 
   if (mode == TP_RESID_NORM && (!d1 || !d2 || !g)) return MALLEUS_E_ARG;
   if (mode != TP_SUM && !x) return MALLEUS_E_ARG;
   TpArgs a{};
-  if (getenv("MALLEUS_TP_TRACE")) {
-    if (!trace && cudaMallocManaged(&trace, 4 * TP_GRID_MAX * 16 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
-    a.trace = trace ? trace + 4 * TP_GRID_MAX * me : nullptr;
-  }
+  if (getenv("MALLEUS_TP_TRACE")) a.trace = tp_trace_buffer(me);
   if (part_dtype != 0 && part_dtype != 1) return MALLEUS_E_ARG;
   a.part_bf16 = part_dtype;
   a.k = k; a.me = me; a.T = T; a.h = h; a.mode = mode; a.eps = eps; a.epoch = epoch;
@@ -113,6 +108,6 @@ extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, 
 }
 
 // debugging aid for tools/tp_bench.py: the globaltimer stamps of the last traced call per member
-extern "C" const unsigned long long* malleus_k_tp_trace_buffer() { return trace; }
+extern "C" const unsigned long long* malleus_k_tp_trace_buffer() { return tp_trace_buffer(0); }
 extern "C" const unsigned long long* malleus_k_attn_trace_buffer() { return attn_trace_buffer; }
 extern "C" const unsigned long long* malleus_k_attn_bwd_trace_buffer() { return attn_bwd_trace_buffer; }

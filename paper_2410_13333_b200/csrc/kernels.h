@@ -132,8 +132,10 @@ struct TpArgs {
   float* d2[MAX_TP];                     // member j's rstd [T] (TP_RESID_NORM)
   const void* x;                         // local bf16 residual input [T, h] (RESID modes)
   const void* g;                         // local bf16 RMSNorm gain [h] (RESID_NORM)
-  unsigned long long* trace;             // optional: per CTA 4 globaltimer stamps (start, ready, rows, end)
+  unsigned long long* trace;             // optional: per-call globaltimer stamps (MALLEUS_TP_TRACE)
 };
+constexpr int TP_TRACE_CALLS = 4096;
+unsigned long long* tp_trace_buffer(int member);  // managed [TP_TRACE_CALLS][4] per member, lazily allocated
 cudaError_t tp_reduce(const TpArgs& a, cudaStream_t st);
 int tp_grid(int T, int k);  // CTAs per member: rows spread evenly over <= TP_GRID_MAX CTAs
 

@@ -690,6 +690,8 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, 
   a.x = x;
   a.g = g;
   a.part_bf16 = L.tp_bf16 ? 1 : 0;
+  static const bool trace = getenv("MALLEUS_TP_TRACE") != nullptr;  // debugging aid (tools/tp_step_trace.py)
+  if (trace) a.trace = tp_trace_buffer(0);
   const int buf = (int)(a.epoch & 1);
   const bool scatter = tp_scatter(L);
   const size_t slot = (size_t)(L.T / L.TP) * a.h;  // elements per receive slot (scatter layout)

@@ -99,8 +99,10 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
   __shared__ bool last;
   const int k = K > 0 ? K : a.k;
   const int me = a.me, h = a.h, nv = h / 8;
-  unsigned long long* tr = a.trace ? a.trace + 4 * blockIdx.x : nullptr;
-  if (tr && threadIdx.x == 0) tr[0] = now_ns();
+  // optional per-call stamps (debugging aid): [start of CTA 0, CTA 0 saw every ready, last CTA's
+  // rows done, last CTA saw every done] at slot epoch % TP_TRACE_CALLS
+  unsigned long long* tr = a.trace ? a.trace + 4 * (a.epoch % TP_TRACE_CALLS) : nullptr;
+  if (tr && threadIdx.x == 0 && blockIdx.x == 0) tr[0] = now_ns();
   if (threadIdx.x == 0) {
     // ready: only CTA 0 publishes (dispatched first, so it is resident whenever any CTA waits)
     if (blockIdx.x == 0) {
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
       for (int j = 0; j < k; ++j) st_release_sys(a.flags[j] + TPF_READY + me, a.epoch);
     }
     for (int j = 0; j < k; ++j) wait_geq(a.flags[me] + TPF_READY + j, a.epoch);
-    if (tr) tr[1] = now_ns();
+    if (tr && blockIdx.x == 0) tr[1] = now_ns();
   }
   __syncthreads();
   const int r0 = (int)((long long)me * a.T / k), r1 = (int)((long long)(me + 1) * a.T / k);
@@ -217,22 +219,31 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
   // CTA of this member tells every member "done" and waits for every member's "done"
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (tr) tr[2] = now_ns();
     __threadfence_system();
     const unsigned long long t = atomicAdd(a.flags[me] + TPF_TICKET, 1ull);
     last = t + 1 == a.epoch * (unsigned long long)gridDim.x;
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
+    if (tr) tr[2] = now_ns();
     __threadfence_system();
     for (int j = 0; j < k; ++j) st_release_sys(a.flags[j] + TPF_DONE + me, a.epoch);
     for (int j = 0; j < k; ++j) wait_geq(a.flags[me] + TPF_DONE + j, a.epoch);
     __threadfence_system();
+    if (tr) tr[3] = now_ns();
   }
-  if (tr && threadIdx.x == 0) tr[3] = now_ns();
 }
 
 }  // namespace
+
+unsigned long long* tp_trace_buffer(int member) {
+  static unsigned long long* buf = nullptr;
+  if (!buf && cudaMallocManaged(&buf, (size_t)MAX_TP * TP_TRACE_CALLS * 4 * sizeof(unsigned long long)) != cudaSuccess) {
+    cudaGetLastError();
+    buf = nullptr;
+  }
+  return buf ? buf + (size_t)member * TP_TRACE_CALLS * 4 : nullptr;
+}
 
 int tp_grid(int T, int k) {
   const int rows = (T + k - 1) / k;
