@@ -277,10 +277,10 @@ malleus_status malleus_k_attention_bwd(int32_t nb, int32_t s, int32_t n, int32_t
 
 /* One member's part of the TP partial-sum reduction over NVLink peer memory (SURVEY §8(a) S8,
  * K15; PAPER.md:262 row-parallel layers).  k members (2..16); member `me` sums rows
- * [me*T/k, (me+1)*T/k) of the k partials part[0..k-1] ([T, h]; part_dtype 0 = fp32, 1 = bf16;
- * summed in fp32 in member order) and stores
+ * [me*T/k, (me+1)*T/k) of the k partials part[0..k-1] ([T, h]; part_dtype bit 0: partials bf16
+ * (else fp32), bit 1: mode 0 writes a bf16 sum (else fp32); summed in fp32 in member order) and stores
  * the result into every member's destination:
- *   mode 0 (SUM):        d0[j] fp32 [T, h] = sum_j part[j];
+ *   mode 0 (SUM):        d0[j] fp32 or bf16 [T, h] = sum_j part[j];
  *   mode 1 (RESID_NORM): d0[j] bf16 x1 = bf16(x + sum), d1[j] bf16 = x1 * rsqrt(mean(x1^2) + eps) * g,
  *                        d2[j] fp32 [T] = rsqrt(...);  (x: this member's bf16 [T, h]; g: bf16 [h])
  *   mode 2 (RESID):      d0[j] bf16 = bf16(x + sum).

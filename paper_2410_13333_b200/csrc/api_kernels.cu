@@ -93,8 +93,9 @@ extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, 
   if (mode != TP_SUM && !x) return MALLEUS_E_ARG;
   TpArgs a{};
   if (getenv("MALLEUS_TP_TRACE")) a.trace = tp_trace_buffer(me);
-  if (part_dtype != 0 && part_dtype != 1) return MALLEUS_E_ARG;
-  a.part_bf16 = part_dtype;
+  if (part_dtype < 0 || part_dtype > 3) return MALLEUS_E_ARG;
+  a.part_bf16 = part_dtype & 1;
+  a.sum_bf16 = (part_dtype >> 1) & 1;
   a.k = k; a.me = me; a.T = T; a.h = h; a.mode = mode; a.eps = eps; a.epoch = epoch;
   a.x = x; a.g = g;
   for (int j = 0; j < k; ++j) {

@@ -124,12 +124,14 @@ __device__ __forceinline__ void load_f8(const float4* p, float (&f)[8]) {
   f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 }
 
-template <int V>  // vectors of 8 columns per thread: h <= 8 * V * NORM_THREADS
+template <int V, bool DY16>  // vectors of 8 columns per thread: h <= 8 * V * NORM_THREADS; dy bf16?
 __global__ void __launch_bounds__(NORM_THREADS)
 rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x,
                    const uint4* __restrict__ g, const float* __restrict__ rstd,
-                   const float4* __restrict__ dy, const uint4* __restrict__ dres,
+                   const void* __restrict__ dyv, const uint4* __restrict__ dres,
                    uint4* __restrict__ dx_out, float* __restrict__ dg_part) {
+  const float4* dy = static_cast<const float4*>(dyv);
+  const uint4* dy16 = static_cast<const uint4*>(dyv);
   __shared__ float sh[NORM_THREADS / 32];
   const int nv = h / 8;
   float dg[V][8];
@@ -148,7 +150,8 @@ rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x
       if (c < nv) {
         float xv[8], dv[8], gg[8];
         unpack8(x[(long long)row * nv + c], xv);
-        load_f8(dy + ((long long)row * nv + c) * 2, dv);
+        if (DY16) unpack8(dy16[(long long)row * nv + c], dv);
+        else load_f8(dy + ((long long)row * nv + c) * 2, dv);
         unpack8(g[c], gg);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -165,7 +168,8 @@ rmsnorm_bwd_kernel(int T, int h, int rows_per_block, const uint4* __restrict__ x
       if (c < nv) {
         float xv[8], dv[8], gg[8], o[8], rs[8];
         unpack8(x[(long long)row * nv + c], xv);
-        load_f8(dy + ((long long)row * nv + c) * 2, dv);
+        if (DY16) unpack8(dy16[(long long)row * nv + c], dv);
+        else load_f8(dy + ((long long)row * nv + c) * 2, dv);
         unpack8(g[c], gg);
         if (dres) unpack8(dres[(long long)row * nv + c], rs);
 #pragma unroll
@@ -446,15 +450,18 @@ cudaError_t rmsnorm_fwd(int T, int h, const void* x, const float* partial, void*
 
 size_t rmsnorm_bwd_scratch_floats(int T, int h) { return (size_t)BWD_BLOCKS * h; }
 
-cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float* rstd, const float* dy,
-                        const void* dres, void* dx_out, float* dg_accum, float* scratch, cudaStream_t st) {
+cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float* rstd, const void* dy,
+                        const void* dres, void* dx_out, float* dg_accum, float* scratch, cudaStream_t st,
+                        bool dy_bf16) {
   if (h % 8 || h > 8 * NORM_MAXV * NORM_THREADS || T <= 0) return cudaErrorInvalidValue;
   int rpb = (T + BWD_BLOCKS - 1) / BWD_BLOCKS;
   int nb = (T + rpb - 1) / rpb;
   const int vpt = (h / 8 + NORM_THREADS - 1) / NORM_THREADS;
-  auto kern = vpt <= 1 ? rmsnorm_bwd_kernel<1> : vpt == 2 ? rmsnorm_bwd_kernel<2>
-            : vpt <= 4 ? rmsnorm_bwd_kernel<4> : rmsnorm_bwd_kernel<NORM_MAXV>;
-  kern<<<nb, NORM_THREADS, 0, st>>>(T, h, rpb, (const uint4*)x, (const uint4*)g, rstd, (const float4*)dy,
+  auto kern = dy_bf16 ? (vpt <= 1 ? rmsnorm_bwd_kernel<1, true> : vpt == 2 ? rmsnorm_bwd_kernel<2, true>
+                          : vpt <= 4 ? rmsnorm_bwd_kernel<4, true> : rmsnorm_bwd_kernel<NORM_MAXV, true>)
+                     : (vpt <= 1 ? rmsnorm_bwd_kernel<1, false> : vpt == 2 ? rmsnorm_bwd_kernel<2, false>
+                          : vpt <= 4 ? rmsnorm_bwd_kernel<4, false> : rmsnorm_bwd_kernel<NORM_MAXV, false>);
+  kern<<<nb, NORM_THREADS, 0, st>>>(T, h, rpb, (const uint4*)x, (const uint4*)g, rstd, dy,
                                     (const uint4*)dres, (uint4*)dx_out, scratch); count_launch();
   colsum_accum_kernel<<<(h + 31) / 32, 1024, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
   return cudaGetLastError();

@@ -38,8 +38,8 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st);
 cudaError_t rmsnorm_fwd(int T, int h, const void* x, const float* partial, void* x_out,
                         const void* g, float eps, void* y, float* rstd, cudaStream_t st);
 cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float* rstd,
-                        const float* dy, const void* dres, void* dx_out, float* dg_accum,
-                        float* scratch, cudaStream_t st);
+                        const void* dy, const void* dres, void* dx_out, float* dg_accum,
+                        float* scratch, cudaStream_t st, bool dy_bf16 = false);
 size_t rmsnorm_bwd_scratch_floats(int T, int h);
 cudaError_t residual_add(long long n, const void* x, const float* partial, void* out,
                          cudaStream_t st);
@@ -126,6 +126,7 @@ struct TpArgs {
   unsigned long long epoch;              // 1, 2, ... per reduction under the current plan
   const void* part[MAX_TP];              // member j's partial [T, h] for this epoch (fp32 or bf16)
   int part_bf16;                         // partials are bf16 (summed in fp32, member order)
+  int sum_bf16;                          // TP_SUM writes a bf16 sum (else fp32)
   unsigned long long* flags[MAX_TP];     // member j's flag block (TPF_WORDS u64)
   void* d0[MAX_TP];                      // member j's out: fp32 sum | bf16 x1 | bf16 x'
   void* d1[MAX_TP];                      // member j's normalised bf16 a (TP_RESID_NORM)

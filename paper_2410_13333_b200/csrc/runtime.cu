@@ -655,6 +655,8 @@ static bool tp_peer(const Layout& L) { return L.TP > 1 && L.p2p && L.tpflags != 
 static float* tp_part(Layout& L) { return tp_peer(L) ? L.tpp[(L.tp_epoch + 1) & 1] : L.part; }
 // the row-parallel GEMM's store mode for that buffer
 static int tp_part_mode(const Layout& L) { return tp_peer(L) && L.tp_bf16 ? GEMM_STORE_BF16 : GEMM_STORE_F32; }
+// the backward TP sums (input gradients of the norms) are bf16 when the partials are
+static bool tp_sum_bf16(const Layout& L) { return tp_peer(L) && L.tp_bf16; }
 // reduce-scatter fused into the GEMM epilogue: each member's GEMM stores the rows owned by member d
 // straight into d's receive slot (its own index) over NVLink, overlapping the transfer with the
 // GEMM; the reduction kernel then reads only local slots.  Needs bf16 partials and T / k rows per
@@ -690,6 +692,7 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, 
   a.x = x;
   a.g = g;
   a.part_bf16 = L.tp_bf16 ? 1 : 0;
+  a.sum_bf16 = L.tp_bf16 ? 1 : 0;  // bf16 partials => the backward sums go out in bf16 too
   static const bool trace = getenv("MALLEUS_TP_TRACE") != nullptr;  // debugging aid (tools/tp_step_trace.py)
   if (trace) a.trace = tp_trace_buffer(0);
   const int buf = (int)(a.epoch & 1);
@@ -837,7 +840,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
   RET(tp_sum(ctx, st));
   duty_begin(ctx, 4, st);
-  CK(rmsnorm_bwd(T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st));
+  CK(rmsnorm_bwd(T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st, tp_sum_bf16(L)));
   // attention
   RET(gemm(ctx, T, nd, h, dx1, h, false, P.wo, h, false, L.dout, nd, GEMM_STORE_BF16, st));
   RET(gemm(ctx, nd, h, T, Y.o, nd, true, dx1, h, true, P.dwo, h, wm, st));
@@ -849,7 +852,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
   RET(tp_sum(ctx, st));
   duty_begin(ctx, 5, st);
-  CK(rmsnorm_bwd(T, h, S.x[li], P.g1, Y.r1, L.part, dx1, dx, P.dg1, L.scratch, st));
+  CK(rmsnorm_bwd(T, h, S.x[li], P.g1, Y.r1, L.part, dx1, dx, P.dg1, L.scratch, st, tp_sum_bf16(L)));
   duty_end(ctx, st);
   return MALLEUS_OK;
 }
@@ -879,7 +882,7 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
   RET(gemm(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, first ? GEMM_STORE_F32 : GEMM_ACCUM_F32, st));
   RET(tp_sum(ctx, st));
   duty_begin(ctx, 8, st);
-  CK(rmsnorm_bwd(T, h, S.x[L.n_local], L.gf, S.rf, L.part, nullptr, S.dlast, L.dgf, L.scratch, st));
+  CK(rmsnorm_bwd(T, h, S.x[L.n_local], L.gf, S.rf, L.part, nullptr, S.dlast, L.dgf, L.scratch, st, tp_sum_bf16(L)));
   duty_end(ctx, st);
   return MALLEUS_OK;
 }

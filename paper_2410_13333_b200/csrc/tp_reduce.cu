@@ -5,7 +5,7 @@
 // Member m of a TP group of k owns rows [m*T/k, (m+1)*T/k).  For each of its rows it reads the k
 // fp32 partial rows (its own and the k-1 peers', in member order 0..k-1, so every row is summed in
 // one fixed order) and pushes the finished row to every member:
-//   TP_SUM        out = sum_j P_j                          (fp32; backward input gradients)
+//   TP_SUM        out = sum_j P_j                          (fp32 or bf16; backward input gradients)
 //   TP_RESID_NORM x1 = bf16(x + sum_j P_j), a = bf16(x1 * rsqrt(mean(x1^2) + eps) * g), rstd
 //                 (attention output -> residual -> MLP RMSNorm, the same arithmetic as rmsnorm_fwd)
 //   TP_RESID      x' = bf16(x + sum_j P_j)                 (MLP output -> residual)
@@ -166,12 +166,20 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         const int c = threadIdx.x + i * TPR_THREADS;
-        if (c < nv)
-          for (int j = 0; j < k; ++j) {
-            float4* d = reinterpret_cast<float4*>(static_cast<float*>(a.d0[j]) + rb + 8 * c);
-            __stcg(d, acc[i][0]);
-            __stcg(d + 1, acc[i][1]);
+        if (c < nv) {
+          if (a.sum_bf16) {  // bf16 sum (the activation-gradient dtype): half the push bytes
+            const float f[8] = {acc[i][0].x, acc[i][0].y, acc[i][0].z, acc[i][0].w,
+                                acc[i][1].x, acc[i][1].y, acc[i][1].z, acc[i][1].w};
+            const uint4 q = pack8(f);
+            for (int j = 0; j < k; ++j) __stcg(static_cast<uint4*>(a.d0[j]) + (long long)row * nv + c, q);
+          } else {
+            for (int j = 0; j < k; ++j) {
+              float4* d = reinterpret_cast<float4*>(static_cast<float*>(a.d0[j]) + rb + 8 * c);
+              __stcg(d, acc[i][0]);
+              __stcg(d + 1, acc[i][1]);
+            }
           }
+        }
       }
     } else {
       float v[V][8];

@@ -22,13 +22,14 @@ def _ref_sum(parts):
 
 
 @pytest.mark.parametrize("k,T,h,pdt", [(2, 300, 512, "f32"), (2, 2048, 4096, "f32"), (4, 257, 1024, "f32"),
-                                      (2, 300, 512, "bf16"), (4, 2048, 8192, "bf16"), (3, 301, 2048, "bf16")])
+                                      (2, 300, 512, "bf16"), (4, 2048, 8192, "bf16"), (3, 301, 2048, "bf16"),
+                                      (2, 2048, 4096, "bf16sum"), (4, 515, 1024, "bf16sum")])
 def test_tp_reduce_modes(k, T, h, pdt):
     _need(k)
     from tests.tputil import Group, enable_peer_access
     enable_peer_access(k)
-    dt = torch.bfloat16 if pdt == "bf16" else torch.float32
-    G = Group(k, T, h, part_dtype=dt)
+    dt = torch.bfloat16 if pdt.startswith("bf16") else torch.float32
+    G = Group(k, T, h, part_dtype=dt, sum_bf16=pdt == "bf16sum")
     gen = torch.Generator().manual_seed(7)
     x_cpu = (torch.randn(T, h, generator=gen) * 2).to(torch.bfloat16)
     g_cpu = (1 + 0.1 * torch.randn(h, generator=gen)).to(torch.bfloat16)
@@ -45,8 +46,9 @@ def test_tp_reduce_modes(k, T, h, pdt):
         G.sync()
         s = _ref_sum(parts)
         if mode == 0:
+            ref = s.to(torch.bfloat16) if pdt == "bf16sum" else s
             for j in range(k):
-                assert torch.equal(G.out32[j].cpu(), s), (rep, j)
+                assert torch.equal(G.out32[j].cpu(), ref), (rep, j)
             continue
         x1 = (x_cpu.float() + s).to(torch.bfloat16)
         for j in range(k):

@@ -31,13 +31,14 @@ def _ptrs(ts):
 class Group:
     """k members, member j on cuda:j: double-buffered partials, flag blocks, destinations."""
 
-    def __init__(self, k: int, T: int, h: int, part_dtype=torch.float32):
+    def __init__(self, k: int, T: int, h: int, part_dtype=torch.float32, sum_bf16: bool = False):
         self.k, self.T, self.h = k, T, h
-        self.pdt = 1 if part_dtype == torch.bfloat16 else 0  # part_dtype: 0 fp32, 1 bf16
+        # part_dtype bit 0: bf16 partials, bit 1: bf16 SUM output
+        self.pdt = (1 if part_dtype == torch.bfloat16 else 0) | (2 if sum_bf16 else 0)
         dev = [torch.device("cuda", j) for j in range(k)]
         self.part = [[torch.zeros(T, h, device=d, dtype=part_dtype) for d in dev] for _ in range(2)]
         self.flags = [torch.zeros(TPF_WORDS, dtype=torch.int64, device=d) for d in dev]
-        self.out32 = [torch.zeros(T, h, device=d) for d in dev]
+        self.out32 = [torch.zeros(T, h, device=d, dtype=torch.bfloat16 if sum_bf16 else torch.float32) for d in dev]
         self.x1 = [torch.zeros(T, h, dtype=torch.bfloat16, device=d) for d in dev]
         self.a = [torch.zeros(T, h, dtype=torch.bfloat16, device=d) for d in dev]
         self.rstd = [torch.zeros(T, device=d) for d in dev]
