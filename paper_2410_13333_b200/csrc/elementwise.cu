@@ -318,16 +318,42 @@ __global__ void embed_fwd_kernel(int T, int h, const int32_t* __restrict__ tok, 
   for (int c = threadIdx.x; c < nv; c += blockDim.x) x[(long long)t * nv + c] = E[src + c];
 }
 
-__global__ void embed_bwd_kernel(int T, int h, const int32_t* __restrict__ tok, const uint4* __restrict__ dx,
-                                 float* __restrict__ dE) {
-  const int nv = h / 8;
+// dE[v] += sum over positions t with tok[t] == v of dx[t], deterministic: the CTA of the first
+// position of each distinct token sums all of that token's rows in position order and updates the
+// dE row once (no atomics, so repeated tokens give run-to-run identical sums).  Tokens staged in
+// shared memory (T <= EMBED_MAX_T), 8 columns per thread.
+constexpr int EMBED_MAX_T = 8192;
+__global__ void __launch_bounds__(256) embed_bwd_kernel(int T, int h, const int32_t* __restrict__ tok,
+                                                        const uint4* __restrict__ dx, float* __restrict__ dE) {
+  extern __shared__ int32_t stok[];
+  __shared__ int first;
   const int t = blockIdx.x;
-  float* dst = dE + (long long)tok[t] * h;
+  for (int i = threadIdx.x; i < T; i += blockDim.x) stok[i] = tok[i];
+  if (threadIdx.x == 0) first = 1;
+  __syncthreads();
+  const int v = stok[t];
+  for (int i = threadIdx.x; i < t; i += blockDim.x)
+    if (stok[i] == v) first = 0;  // benign race: every writer stores 0
+  __syncthreads();
+  if (!first) return;
+  const int nv = h / 8;
+  float* dst = dE + (long long)v * h;
   for (int c = threadIdx.x; c < nv; c += blockDim.x) {
-    float v[8];
-    unpack8(dx[(long long)t * nv + c], v);
+    float acc[8];
+    unpack8(dx[(long long)t * nv + c], acc);
+    for (int u = t + 1; u < T; ++u)
+      if (stok[u] == v) {
+        float w[8];
+        unpack8(dx[(long long)u * nv + c], w);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) atomicAdd(dst + c * 8 + j, v[j]);
+        for (int j = 0; j < 8; ++j) acc[j] += w[j];
+      }
+    float4* d4 = reinterpret_cast<float4*>(dst + c * 8);
+    float4 o0 = d4[0], o1 = d4[1];
+    o0.x += acc[0]; o0.y += acc[1]; o0.z += acc[2]; o0.w += acc[3];
+    o1.x += acc[4]; o1.y += acc[5]; o1.z += acc[6]; o1.w += acc[7];
+    d4[0] = o0;
+    d4[1] = o1;
   }
 }
 
@@ -501,7 +527,8 @@ cudaError_t embed_fwd(int T, int h, const int32_t* tok, const void* E, void* x, 
 }
 
 cudaError_t embed_bwd(int T, int h, const int32_t* tok, const void* dx, float* dE, cudaStream_t st) {
-  embed_bwd_kernel<<<T, 128, 0, st>>>(T, h, tok, (const uint4*)dx, dE); count_launch();
+  if (T > EMBED_MAX_T || h % 8) return cudaErrorInvalidValue;
+  embed_bwd_kernel<<<T, 256, T * sizeof(int32_t), st>>>(T, h, tok, (const uint4*)dx, dE); count_launch();
   return cudaGetLastError();
 }
 

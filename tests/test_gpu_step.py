@@ -124,3 +124,15 @@ def test_tp_scatter_epilogue_bitwise(plan, tmp_path):
         res[tag] = json.load(open(out))
         _assert_ok(res[tag])
     assert res["scatter"]["losses"] == res["pull"]["losses"], (res["scatter"]["losses"], res["pull"]["losses"])
+
+
+def test_p0_run_to_run_bitwise():
+    """Determinism: every reduction runs in a fixed order (no float atomics; the
+    embedding backward sums repeated tokens in position order), so two runs of the same plan give
+    bit-identical losses over 3 steps (the later losses depend on every gradient through AdamW)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from tests.mp_worker import run
+    a = run("P0", steps=3)
+    b = run("P0", steps=3)
+    assert a["losses"] == b["losses"], (a["losses"], b["losses"])
