@@ -591,46 +591,53 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
   }
 }
 
-// dQ: CTA = 128 queries; loop over 64-key sub-tiles i <= 2 qb + 1 (3-stage K | V ring).
-//   TMEM: S[b] cols [64b, ..), dP[b] [128+64b, ..), dQ [256,384); warp half h writes 16 columns of
-//   packed bf16 dS over its own dP columns.  S = Q K_i^T, dP = dO V_i^T (M = 128 queries, N = 64
-//   keys); dQ += dS K_i (A = dS from TMEM, K = 64 keys; K_i MN-major B).
-constexpr int BWD2_SMEM = 2 * 2 * PANEL + NSUB * SUB_STAGE + 256 + 1024;
+// dQ: CTA = 128 queries; loop over 128-key tiles i <= qb (2-stage K | V ring, 64 KB per stage).
+//   TMEM: S[b] cols [128b, 128b+128) (double-buffered), dP [256,384), dQ [384,512).  Warp half h
+//   overwrites its own 64 dP columns with 32 columns of packed bf16 dS, the A operand of
+//   dQ += dS K_i (K = 128 keys, K_i MN-major B).  MMA order per tile: S_i (overlaps the softmax-
+//   gradient math of tile i-1), then dQ_{i-1} (reads dS_{i-1}), then dP_i (overwrites it; the tensor
+//   pipe runs in order).  All MMAs are N = 128 (full rate; N = 64 runs at 2/3, profiles/r01_mma_probe.log).
+constexpr int KV2_STAGE = 4 * PANEL;  // K (2 panels of 128 rows) | V (2 panels)
+constexpr int BWD2_SMEM = 2 * 2 * PANEL + 2 * KV2_STAGE + 256 + 1024;
 
 __global__ void __launch_bounds__(320, 1)
-attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo,
-                      const __grid_constant__ CUtensorMap tm64, int s, int n, const float* __restrict__ lse,
-                      const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv, float scale,
-                      const float2* __restrict__ rope_cs) {
+attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s, int n,
+                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
+                      float scale, const float2* __restrict__ rope_cs) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sO = sQ + 2 * PANEL;
-  uint8_t* ring = sO + 2 * PANEL;  // [NSUB][K | V]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + NSUB * SUB_STAGE);
+  uint8_t* ring = sO + 2 * PANEL;  // [2][K | V]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * KV2_STAGE);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;            // [NSUB]
-  uint64_t* kv_empty = bars + 1 + NSUB;    // [NSUB]
-  uint64_t* sd_full = bars + 1 + 2 * NSUB;  // [2]
-  uint64_t* ds_full = sd_full + 2;         // [2]
-  uint64_t* done = ds_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_free = bars + 7;    // [2] (8 warp arrivals: S_i read into registers)
+  uint64_t* dp_full = bars + 9;
+  uint64_t* ds_full = bars + 10;  // 8 warp arrivals
+  uint64_t* done = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;
   const int qb = nqb - 1 - blockIdx.x;  // heaviest first
   const int head = blockIdx.y, b = blockIdx.z;
-  const int n_it = 2 * qb + 2;          // 64-key sub-tiles up to the diagonal
+  const int n_it = qb + 1;              // key tiles up to the diagonal
   const int nd = n * DH;
   const int row0 = b * s + qb * TQ;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
     tma_prefetch(&tmo);
-    tma_prefetch(&tm64);
     mbar_init(q_full, 1);
-    for (int i = 0; i < NSUB; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&sd_full[i], 1); mbar_init(&ds_full[i], 8); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1); mbar_init(&s_free[i], 8);
+    }
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 8);
     mbar_init(done, 1);
     fence_barrier_init();
   }
@@ -648,56 +655,61 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
       tma_load_2d(sO, &tmo, q_full, head * DH, row0);
       tma_load_2d(sO + PANEL, &tmo, q_full, head * DH + 64, row0);
       for (int i = 0; i < n_it; ++i) {
-        const int st = i % NSUB;
-        mbar_wait(&kv_empty[st], ((i / NSUB) & 1) ^ 1);
-        uint8_t* k = ring + st * SUB_STAGE;
-        const int krow = b * s + i * 64;
-        mbar_arrive_expect_tx(&kv_full[st], SUB_STAGE);
-        tma_load_2d(k, &tm64, &kv_full[st], nd + head * DH, krow);
-        tma_load_2d(k + HPANEL, &tm64, &kv_full[st], nd + head * DH + 64, krow);
-        tma_load_2d(k + 2 * HPANEL, &tm64, &kv_full[st], 2 * nd + head * DH, krow);
-        tma_load_2d(k + 3 * HPANEL, &tm64, &kv_full[st], 2 * nd + head * DH + 64, krow);
+        const int st = i & 1;
+        mbar_wait(&kv_empty[st], ((i >> 1) & 1) ^ 1);
+        uint8_t* k = ring + st * KV2_STAGE;
+        const int krow = b * s + i * TK;
+        mbar_arrive_expect_tx(&kv_full[st], KV2_STAGE);
+        tma_load_2d(k, &tm, &kv_full[st], nd + head * DH, krow);
+        tma_load_2d(k + PANEL, &tm, &kv_full[st], nd + head * DH + 64, krow);
+        tma_load_2d(k + 2 * PANEL, &tm, &kv_full[st], 2 * nd + head * DH, krow);
+        tma_load_2d(k + 3 * PANEL, &tm, &kv_full[st], 2 * nd + head * DH + 64, krow);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t id_s = umma_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_q = umma_idesc_bf16(128, 128, false, true);
       const uint32_t aq = smem_u32(sQ), ao = smem_u32(sO);
-      auto issue_dq = [&](int i) {
-        const int bb = i & 1, st = i % NSUB;
-        mbar_wait(&ds_full[bb], (i >> 1) & 1);
+      auto issue_dq = [&](int i) {  // dQ += dS_i K_i
+        mbar_wait(ds_full, i & 1);
         tc_fence_after();
-        const uint32_t k = smem_u32(ring + st * SUB_STAGE);
+        const uint32_t k = smem_u32(ring + (i & 1) * KV2_STAGE);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_f16_ts(tbase + 256, tbase + 128 + bb * 64 + (kk >> 1) * 32 + (kk & 1) * 8,
-                      umma_desc_sw128(k + kk * 2048, HPANEL, 1024), id_q, (i > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&kv_empty[st]);
+        for (int kk = 0; kk < TK / 16; ++kk)
+          umma_f16_ts(tbase + 384, tbase + 256 + (kk >> 2) * 64 + (kk & 3) * 8,
+                      umma_desc_sw128(k + kk * 2048, PANEL, 1024), id_q, (i > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&kv_empty[i & 1]);
       };
       mbar_wait(q_full, 0);
       for (int i = 0; i < n_it; ++i) {
-        const int bb = i & 1, st = i % NSUB;
-        mbar_wait(&kv_full[st], (i / NSUB) & 1);
+        const int sb = i & 1;
+        mbar_wait(&kv_full[sb], (i >> 1) & 1);
+        mbar_wait(&s_free[sb], ((i >> 1) & 1) ^ 1);  // S_{i-2} read by the math warps
         tc_fence_after();
-        const uint32_t k = smem_u32(ring + st * SUB_STAGE), v = k + 2 * HPANEL;
+        const uint32_t k = smem_u32(ring + sb * KV2_STAGE), v = k + 2 * PANEL;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * PANEL + (kk & 3) * 32, boff = (kk >> 2) * HPANEL + (kk & 3) * 32;
-          umma_f16(tbase + bb * 64, umma_desc_sw128(aq + aoff, 16, 1024), umma_desc_sw128(k + boff, 16, 1024), id_s,
+          const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
+          umma_f16(tbase + sb * 128, umma_desc_sw128(aq + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024), id_s,
                    kk > 0 ? 1u : 0u);
-          umma_f16(tbase + 128 + bb * 64, umma_desc_sw128(ao + aoff, 16, 1024), umma_desc_sw128(v + boff, 16, 1024),
-                   id_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&sd_full[bb]);
+        umma_commit(&s_full[sb]);
         if (i > 0) issue_dq(i - 1);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
+          umma_f16(tbase + 256, umma_desc_sw128(ao + off, 16, 1024), umma_desc_sw128(v + off, 16, 1024), id_s,
+                   kk > 0 ? 1u : 0u);
+        }
+        umma_commit(dp_full);
       }
       issue_dq(n_it - 1);
       umma_commit(done);
     }
   } else {
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;  // this warp's 32 key columns of each sub-tile
+    const int half = (warp - 2) >> 2;  // this warp's 64 key columns of each tile
     const int r = quarter * 32 + lane;
     const int q = qb * TQ + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
@@ -705,37 +717,48 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
     const long long lrow = ((long long)b * n + head) * s;
     const float L2 = lse[lrow + q] * LOG2E, Dq = dsum[lrow + q];
     for (int i = 0; i < n_it; ++i) {
-      const int bb = i & 1;
-      mbar_wait(&sd_full[bb], (i >> 1) & 1);
+      const int sb = i & 1;
+      mbar_wait(&s_full[sb], (i >> 1) & 1);
+      mbar_wait(dp_full, i & 1);
       tc_fence_after();
-      const uint32_t cs = tbase + lane_off + bb * 64 + half * 32;
-      uint32_t us[32], ud[32];
-      tmem_ld32(cs, us);
-      tmem_ld32(cs + 128, ud);
-      tmem_wait_ld();
-      const int k0 = i * 64 + half * 32;
-      const bool diag = k0 + 31 > q;
-      uint32_t dd[16];
+      const uint32_t cs = tbase + lane_off + sb * 128 + half * 64, cd = tbase + lane_off + 256 + half * 64;
+      const bool diag = i == n_it - 1;
+      uint32_t dd[2][16];
 #pragma unroll
-      for (int t = 0; t < 32; t += 2) {
-        float p0 = ex2(fmaf(__uint_as_float(us[t]), sl2, -L2));
-        float p1 = ex2(fmaf(__uint_as_float(us[t + 1]), sl2, -L2));
-        if (diag) {
-          if (k0 + t > q) p0 = 0.f;
-          if (k0 + t + 1 > q) p1 = 0.f;
+      for (int c = 0; c < 2; ++c) {
+        uint32_t us[32], ud[32];
+        tmem_ld32(cs + c * 32, us);
+        tmem_ld32(cd + c * 32, ud);
+        tmem_wait_ld();
+        if (c == 1) {  // S_i fully in registers: its TMEM buffer may take S_{i+2}
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_free[sb]);
         }
-        dd[t / 2] = pack_bf16(p0 * (__uint_as_float(ud[t]) - Dq), p1 * (__uint_as_float(ud[t + 1]) - Dq));
+        const int k0 = i * TK + half * 64 + c * 32;
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          float p0 = ex2(fmaf(__uint_as_float(us[t]), sl2, -L2));
+          float p1 = ex2(fmaf(__uint_as_float(us[t + 1]), sl2, -L2));
+          if (diag) {
+            if (k0 + t > q) p0 = 0.f;
+            if (k0 + t + 1 > q) p1 = 0.f;
+          }
+          dd[c][t / 2] = pack_bf16(p0 * (__uint_as_float(ud[t]) - Dq), p1 * (__uint_as_float(ud[t + 1]) - Dq));
+        }
       }
-      tmem_st16(cs + 128, dd);
+      // dS over this warp's own dP columns (both 32-column chunks already read)
+      tmem_st16(cd, dd[0]);
+      tmem_st16(cd + 16, dd[1]);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_full[bb]);
+      if (lane == 0) mbar_arrive(ds_full);
     }
     mbar_wait(done, 0);
     tc_fence_after();
     __nv_bfloat16* dq = dqkv + (long long)(b * s + q) * 3 * nd + head * DH;
-    store_row_rope(dq, tbase + lane_off + 256, scale, rope_cs ? rope_cs + (long long)q * 64 : nullptr, half, half + 1);
+    store_row_rope(dq, tbase + lane_off + 384, scale, rope_cs ? rope_cs + (long long)q * 64 : nullptr, half, half + 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -799,7 +822,7 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
   }
   attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, lse, dsum,
                                                                       (__nv_bfloat16*)dqkv, scale, rope_cs, trace); count_launch();
-  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, tm64, s, n, lse, dsum,
+  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
                                                                      (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
   return cudaGetLastError();
 }
