@@ -112,3 +112,4 @@ extern "C" malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, 
 extern "C" const unsigned long long* malleus_k_tp_trace_buffer() { return tp_trace_buffer(0); }
 extern "C" const unsigned long long* malleus_k_attn_trace_buffer() { return attn_trace_buffer; }
 extern "C" const unsigned long long* malleus_k_attn_bwd_trace_buffer() { return attn_bwd_trace_buffer; }
+extern "C" const unsigned long long* malleus_k_attn_dq_trace_buffer() { return attn_dq_trace_buffer; }

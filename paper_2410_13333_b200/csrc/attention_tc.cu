@@ -603,8 +603,13 @@ constexpr int BWD2_SMEM = 2 * 2 * PANEL + 2 * KV2_STAGE + 256 + 1024;
 __global__ void __launch_bounds__(320, 1)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s, int n,
                       const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                      float scale, const float2* __restrict__ rope_cs) {
+                      float scale, const float2* __restrict__ rope_cs, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  unsigned long long* tr = (trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? trace : nullptr;
+  auto stamp = [&](int ev, int i) {
+    if (tr && i < 64) { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); tr[ev * 64 + i] = t; }
+  };
+  if (threadIdx.x == 0) stamp(7, 0);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sO = sQ + 2 * PANEL;
@@ -657,6 +662,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
       for (int i = 0; i < n_it; ++i) {
         const int st = i & 1;
         mbar_wait(&kv_empty[st], ((i >> 1) & 1) ^ 1);
+        stamp(0, i);
         uint8_t* k = ring + st * KV2_STAGE;
         const int krow = b * s + i * TK;
         mbar_arrive_expect_tx(&kv_full[st], KV2_STAGE);
@@ -673,6 +679,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
       const uint32_t aq = smem_u32(sQ), ao = smem_u32(sO);
       auto issue_dq = [&](int i) {  // dQ += dS_i K_i
         mbar_wait(ds_full, i & 1);
+        stamp(3, i);
         tc_fence_after();
         const uint32_t k = smem_u32(ring + (i & 1) * KV2_STAGE);
 #pragma unroll
@@ -686,6 +693,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
         const int sb = i & 1;
         mbar_wait(&kv_full[sb], (i >> 1) & 1);
         mbar_wait(&s_free[sb], ((i >> 1) & 1) ^ 1);  // S_{i-2} read by the math warps
+        stamp(2, i);
         tc_fence_after();
         const uint32_t k = smem_u32(ring + sb * KV2_STAGE), v = k + 2 * PANEL;
 #pragma unroll
@@ -719,7 +727,9 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
     for (int i = 0; i < n_it; ++i) {
       const int sb = i & 1;
       mbar_wait(&s_full[sb], (i >> 1) & 1);
+      if (warp == 2 && lane == 0) stamp(1, i);
       mbar_wait(dp_full, i & 1);
+      if (warp == 2 && lane == 0) stamp(4, i);
       tc_fence_after();
       const uint32_t cs = tbase + lane_off + sb * 128 + half * 64, cd = tbase + lane_off + 256 + half * 64;
       const bool diag = i == n_it - 1;
@@ -748,12 +758,14 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
         }
       }
       // dS over this warp's own dP columns (both 32-column chunks already read)
+      if (warp == 2 && lane == 0) stamp(5, i);
       tmem_st16(cd, dd[0]);
       tmem_st16(cd + 16, dd[1]);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+      if (warp == 2 && lane == 0) stamp(6, i);
     }
     mbar_wait(done, 0);
     tc_fence_after();
@@ -785,6 +797,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 bool attention_fwd_tc_supported(int s, int d) { return d == DH && s % TQ == 0; }
 unsigned long long* attn_trace_buffer = nullptr;
 unsigned long long* attn_bwd_trace_buffer = nullptr;
+unsigned long long* attn_dq_trace_buffer = nullptr;
 
 static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long rows, int box_rows = 128) {
   auto enc = encoder();
@@ -822,8 +835,13 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
   }
   attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, lse, dsum,
                                                                       (__nv_bfloat16*)dqkv, scale, rope_cs, trace); count_launch();
+  static unsigned long long* trace2 = nullptr;
+  if (getenv("MALLEUS_ATTN_TRACE") && !trace2) {
+    if (cudaMallocManaged(&trace2, 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace2 = nullptr;
+    attn_dq_trace_buffer = trace2;
+  }
   attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
-                                                                     (__nv_bfloat16*)dqkv, scale, rope_cs); count_launch();
+                                                                     (__nv_bfloat16*)dqkv, scale, rope_cs, trace2); count_launch();
   return cudaGetLastError();
 }
 

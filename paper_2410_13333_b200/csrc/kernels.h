@@ -114,6 +114,7 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
 bool attention_bwd_fuses_rope(int s, int d);
 extern unsigned long long* attn_trace_buffer;      // MALLEUS_ATTN_TRACE stamps of the last forward
 extern unsigned long long* attn_bwd_trace_buffer;  // ... and of the last dK / dV kernel
+extern unsigned long long* attn_dq_trace_buffer;   // ... and of the last dQ kernel
 
 // ---- TP partial-sum reduction over NVLink peer memory, fused with residual / RMSNorm (tp_reduce.cu)
 constexpr int MAX_TP = 16;

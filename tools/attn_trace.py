@@ -50,3 +50,14 @@ for cta in range(1):
     print("iter " + " ".join(f"{x:>8s}" for x in names))
     for i in range(s // 64):
         print(f"{i:4d} " + " ".join(f"{(b[e, i]-t0)/1e3:8.2f}" for e in list(range(7)) + list(range(8, 16))))
+
+# ---- backward dQ kernel: per 128-key tile of CTA (0, 0, 0)
+L.lib.malleus_k_attn_dq_trace_buffer.restype = C.c_void_p
+addr = L.lib.malleus_k_attn_dq_trace_buffer()
+b = np.ctypeslib.as_array((C.c_uint64 * (8 * 64)).from_address(addr)).reshape(8, 64).astype(np.int64)
+t0 = b[7, 0]
+names = ["KV_issue", "c_s_ok", "S_issue", "dQ_issue", "c_dp_ok", "c_math", "c_end"]
+print("dQ CTA (0,0,0)")
+print("tile " + " ".join(f"{x:>8s}" for x in names))
+for i in range(s // 128):
+    print(f"{i:4d} " + " ".join(f"{(b[e, i]-t0)/1e3:8.2f}" for e in range(7)))
