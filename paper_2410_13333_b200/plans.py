@@ -203,3 +203,37 @@ def _ffn_split(F, rates, tile=128):
 
 def _vocab_split(V, rates, tile=128):
     return _ffn_split(V, rates, tile)
+
+
+def plan_from_rates(cfg, plan, rates: dict, deadband: float = 0.05):
+    """Re-plan from probed straggling rates x_g (PAPER.md:370-374 profiler -> §4 planner), keeping
+    the grouping, stage order and layers: each TP group's heads / FFN tiles / vocab tiles by the
+    min-max apportionment over its members' rates (reading R7), and the micro-batches over the
+    pipelines by min-max on the pipelines' per-micro-batch cost y_i = max over members of
+    (share x rate).  Rates within `deadband` of 1 count as 1 (the 5% trigger,
+    PAPER.md:374), so a recovered cluster returns to the even plan exactly."""
+    import copy
+    x = {r: (1.0 if v < 1.0 + deadband else float(v)) for r, v in rates.items()}
+    p = copy.deepcopy(plan)
+    p["plan_id"] = plan.get("plan_id", 0) + 1
+    H, F, V = cfg.n_heads, cfg.ffn, cfg.vocab
+    y = []
+    for pp in p["pipes"]:
+        y_pipe = 0.0
+        for st in pp["stages"]:
+            xr = [x[r] for r in st["ranks"]]
+            if len(xr) > 1:
+                st["heads"] = _heads_split(H, xr)
+                tile = 128 if F // 128 >= 4 * len(xr) else 16
+                st["ffn"] = _ffn_split(F, xr, tile)
+                tile_v = 128 if V // 128 >= 4 * len(xr) else 16
+                st["vocab"] = _vocab_split(V, xr, tile_v)
+            # stage cost per micro-batch relative to an even, unslowed group (layers x slowest share)
+            share = max(st["heads"][k] / H * xr[k] * len(xr) for k in range(len(xr)))
+            y_pipe += (st["layers"][1] - st["layers"][0]) * share
+        y.append(y_pipe)
+    total_m = sum(pp["n_micro"] for pp in p["pipes"])
+    if len(p["pipes"]) > 1:
+        for pp, m in zip(p["pipes"], _minmax(total_m, y)):
+            pp["n_micro"] = m
+    return p

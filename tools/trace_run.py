@@ -1,8 +1,8 @@
 """Dynamic straggler trace, end to end on 4 B200 (the PAPER.md:822-825
 S1-S6 experiment at 4-GPU scale): a sequence of straggler situations is injected (DUTY mode) while
 training continues; at every transition the Malleus loop runs — probe the per-rank speed
-(malleus_probe_speed), re-plan from the measured compute times (plans.rebalance:
-splits and micro-batches), migrate the model states (malleus_migrate,
+(malleus_probe_speed), re-plan from the probed rates (plans.plan_from_rates:
+min-max splits and micro-batches, 5% dead band), migrate the model states (malleus_migrate,
 PAPER.md:731-733) — and the step time before (stale plan) and after (re-planned) is measured.
 
   python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 tools/trace_run.py
@@ -72,9 +72,7 @@ def main():
         probe = eng.probe(10)
         ref = sorted(probe)[0]
         x_probe = [p / ref for p in probe]
-        comp = [None] * world
-        dist.all_gather_object(comp, eng.timing()["compute"])
-        obj = [Pl.rebalance(cfg, plan, {r: comp[r] for r in range(world)}) if rank == 0 else None]
+        obj = [Pl.plan_from_rates(cfg, plan, {r: x_probe[r] for r in range(world)}) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         new_plan = obj[0]
         mig = eng.migrate(new_plan)
