@@ -225,13 +225,27 @@ def adamw(theta, m, v, g, step: int, lr, beta1, beta2, eps, weight_decay):
     return theta, m, v
 
 
+def clip_grad_norm(g: dict, max_norm: float):
+    """Global-norm gradient clipping, torch.nn.utils.clip_grad_norm_ semantics:
+    total = sqrt(sum over all tensors of sum g^2); coef = max_norm / (total + 1e-6); every gradient
+    is scaled by coef when coef < 1.  float64.  Returns (clipped grads, total)."""
+    total = float(np.sqrt(sum(float(np.sum(np.asarray(v, np.float64) ** 2)) for v in g.values())))
+    coef = max_norm / (total + 1e-6)
+    if coef < 1.0:
+        return {k: np.asarray(v, np.float64) * coef for k, v in g.items()}, total
+    return {k: np.asarray(v, np.float64) for k, v in g.items()}, total
+
+
 def train_step(cfg: ModelCfg, P: dict, M: dict, Vs: dict, tokens, targets, step: int, hp=None):
     """Full step: fwd, bwd, AdamW on all tensors.  Returns (loss, grads, newP, newM, newV)."""
     hp = dict(ADAM_DEFAULT if hp is None else hp)
     loss, g = forward_backward(cfg, P, tokens, targets)
+    gu = g
+    if hp.get("max_grad_norm", 0.0) > 0.0:  # optional global-norm clipping before AdamW
+        gu, _ = clip_grad_norm(g, hp["max_grad_norm"])
     nP, nM, nV = {}, {}, {}
     for k in P:
         wd = hp["weight_decay"] if decays(k) else 0.0
-        nP[k], nM[k], nV[k] = adamw(P[k], M[k], Vs[k], g[k], step, hp["lr"], hp["beta1"],
+        nP[k], nM[k], nV[k] = adamw(P[k], M[k], Vs[k], gu[k], step, hp["lr"], hp["beta1"],
                                     hp["beta2"], hp["eps"], wd)
     return loss, g, nP, nM, nV

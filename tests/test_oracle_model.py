@@ -173,3 +173,25 @@ def test_adamw_vs_torch():
         th, m, v = M.adamw(th, m, v, g, step, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"],
                            hp["weight_decay"])
     assert np.abs(th - p.detach().numpy()).max() <= 1e-15 * 10
+
+
+@pytest.mark.parametrize("max_norm", [0.05, 1.0, 1e6])
+def test_clip_grad_norm_vs_torch(max_norm):
+    """Pin of oracle.model.clip_grad_norm: torch.nn.utils.clip_grad_norm_ (an independent
+    implementation) in float64 on random multi-tensor gradients, active (0.05, 1.0) and inactive
+    (1e6) clipping; the clipped global norm equals max_norm when clipping is active."""
+    rng = np.random.default_rng(3)
+    g = {f"t{i}": rng.normal(size=shp) * s for i, (shp, s) in enumerate([((7, 5), 0.3), ((11,), 2.0), ((3, 4, 2), 0.05)])}
+    ts = [torch.tensor(v, dtype=torch.float64, requires_grad=True) for v in g.values()]
+    for t, v in zip(ts, g.values()):
+        t.grad = torch.tensor(v, dtype=torch.float64)
+    tot_ref = float(torch.nn.utils.clip_grad_norm_(ts, max_norm))
+    out, tot = M.clip_grad_norm(g, max_norm)
+    assert abs(tot - tot_ref) <= 1e-12 * tot_ref
+    for t, k in zip(ts, g):
+        np.testing.assert_allclose(out[k], t.grad.numpy(), rtol=1e-13, atol=0)
+    new_norm = math.sqrt(sum(float(np.sum(v ** 2)) for v in out.values()))
+    if max_norm < tot_ref:
+        assert abs(new_norm - max_norm) <= 1e-5 * max_norm
+    else:
+        assert abs(new_norm - tot_ref) <= 1e-12 * tot_ref
