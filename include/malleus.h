@@ -104,10 +104,15 @@ typedef struct { size_t state, grads, work; } malleus_requirements;
 /* AdamW (torch.optim.AdamW semantics, reading R5).  step = global step count t >= 1.
  * apply_update = 0 -> grad_sync only reduces gradients into RGRAD (no optimizer update);
  * 1 -> reduce (kept in RGRAD) + AdamW + push; 2 -> reduce + AdamW + push without storing RGRAD
- * (saves 4 B/element of HBM traffic; the production setting). */
+ * (saves 4 B/element of HBM traffic; the production setting).
+ * max_grad_norm > 0 (with apply_update != 0): global-norm clipping before AdamW,
+ * torch.nn.utils.clip_grad_norm_ semantics: total = ||reduced gradient||_2
+ * over every element of the model (each counted once, on its owner), coef = min(1, max_grad_norm /
+ * (total + 1e-6)); costs a second pass over the owned pieces and one world all-reduce. */
 typedef struct {
   float lr, beta1, beta2, eps, weight_decay;
   int32_t step, apply_update;
+  float max_grad_norm;
 } malleus_adam_cfg;
 
 typedef struct {
@@ -221,6 +226,9 @@ malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode);
 /* compute / comm breakdown of the last train_step on this rank (ms, from CUDA events):
  * out[0] compute, out[1] tp_comm, out[2] pp_comm, out[3] grad_sync, out[4] total. */
 malleus_status malleus_last_step_timing(malleus_ctx* ctx, float out[5]);
+/* global gradient norm and clipping coefficient of the last clipped grad_sync / train_step
+ * (max_grad_norm > 0); synchronises the device.  coef may be NULL. */
+malleus_status malleus_last_grad_norm(malleus_ctx* ctx, float* norm, float* coef);
 
 /* ---------------------------------------------------------------- instrumentation
  * kernel_launches (local): number of kernels this library has launched since it was loaded

@@ -64,7 +64,7 @@ class Requirements(C.Structure):
 
 class AdamCfg(C.Structure):
     _fields_ = [("lr", f32), ("beta1", f32), ("beta2", f32), ("eps", f32), ("weight_decay", f32),
-                ("step", i32), ("apply_update", i32)]
+                ("step", i32), ("apply_update", i32), ("max_grad_norm", f32)]
 
 
 class MigrateStats(C.Structure):
@@ -93,6 +93,7 @@ _SIGS = {
     "malleus_probe_speed": ([vp, i32, P_f32], i32),
     "malleus_set_slowdown": ([vp, f32, i32], i32),
     "malleus_last_step_timing": ([vp, P_f32], i32),
+    "malleus_last_grad_norm": ([vp, P_f32, P_f32], i32),
     "malleus_kernel_launches": ([], i64),
     "malleus_gemm_profile": ([i32, P_i64, C.POINTER(C.c_double), C.POINTER(C.c_double)], i32),
     "malleus_k_gemm": ([i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, i32, vp], i32),

@@ -91,10 +91,17 @@ struct ChunkDesc {
 struct AdamHyper {
   float lr, b1, b2, eps, wd;
   float bc1, bc2;  // 1 - b1^t, 1 - b2^t
-  int apply;       // 0 reduce only, 1 reduce + AdamW (+ rgrad), 2 AdamW without storing rgrad
+  int apply;       // 0 reduce only, 1 reduce + AdamW (+ rgrad), 2 AdamW without storing rgrad,
+                   // 3 AdamW on rgrad * (*coef) (second pass of a clipped step; no reduction)
+  float* sq = nullptr;          // optional: per-chunk sum of G^2 (deterministic, one float per chunk)
+  const float* coef = nullptr;  // apply 3: clipping coefficient (device)
 };
 cudaError_t reduce_adam(int n_chunks, const ChunkDesc* d_chunks, const PieceDesc* d_pieces,
                         const AdamHyper& hp, cudaStream_t st);
+// global-norm clipping helpers: local = sum of the n per-chunk squares (fixed order, fp64) ->
+// (world all-reduce by the caller) -> coef = min(1, max_norm / (sqrt(total) + 1e-6)), norm = sqrt(total)
+cudaError_t sq_total(int n, const float* sq, double* local, cudaStream_t st);
+cudaError_t clip_coef(const double* total, float max_norm, float* coef, float* norm, cudaStream_t st);
 
 // ---- attention (attention.cu): qkv [T, 3*n*d] bf16 (rope already applied to q,k)
 cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o, float* lse,

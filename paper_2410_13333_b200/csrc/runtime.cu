@@ -97,6 +97,9 @@ struct Layout {
   std::vector<ChunkDesc> chunks;
   PieceDesc* d_pieces = nullptr;
   ChunkDesc* d_chunks = nullptr;
+  float* d_sq = nullptr;      // clipping: per-chunk sum of G^2
+  double* d_norm = nullptr;   // clipping: local, then world, sum of G^2
+  float* d_coef = nullptr;    // clipping: [coef, global norm]
   size_t state_bytes = 0, grads_bytes = 0, work_bytes = 0;
   ncclComm_t tp_comm = nullptr;
   std::vector<int> prev_ranks, next_ranks;  // adjacent stages' members
@@ -446,6 +449,12 @@ static malleus_status free_layout(malleus_ctx* ctx, Layout* L) {
   L->p2p = false;
   if (L->d_pieces) cudaFree(L->d_pieces);
   if (L->d_chunks) cudaFree(L->d_chunks);
+  if (L->d_sq) cudaFree(L->d_sq);
+  if (L->d_norm) cudaFree(L->d_norm);
+  if (L->d_coef) cudaFree(L->d_coef);
+  L->d_sq = nullptr;
+  L->d_norm = nullptr;
+  L->d_coef = nullptr;
   if (L->tp_comm) ncclCommDestroy(L->tp_comm);
   L->d_pieces = nullptr;
   L->d_chunks = nullptr;
@@ -594,6 +603,10 @@ static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_are
     key = L.member;
   }
   NK(ncclCommSplit(ctx->world_comm, color, key, &L.tp_comm, nullptr));
+  CK(cudaMalloc(&L.d_norm, sizeof(double)));
+  CK(cudaMalloc(&L.d_coef, 2 * sizeof(float)));
+  CK(cudaMemset(L.d_coef, 0, 2 * sizeof(float)));
+  if (!L.chunks.empty()) CK(cudaMalloc(&L.d_sq, L.chunks.size() * sizeof(float)));
   if (!L.pieces.empty()) {
     CK(cudaMalloc(&L.d_pieces, L.pieces.size() * sizeof(PieceDesc)));
     CK(cudaMemcpy(L.d_pieces, L.pieces.data(), L.pieces.size() * sizeof(PieceDesc), cudaMemcpyHostToDevice));
@@ -911,6 +924,32 @@ static malleus_status pp_exchange(malleus_ctx* ctx, const uint16_t* send_fwd, ui
   return MALLEUS_OK;
 }
 
+// reduce + AdamW over the owned pieces: one fused pass, or with global-norm clipping two passes
+// around a world all-reduce of the squared norm (collective either way when clipping)
+static malleus_status reduce_and_update(malleus_ctx* ctx, const malleus_adam_cfg* a, cudaStream_t st) {
+  Layout& L = *ctx->L;
+  AdamHyper hp{a->lr, a->beta1, a->beta2, a->eps, a->weight_decay,
+               (float)(1.0 - std::pow((double)a->beta1, a->step)), (float)(1.0 - std::pow((double)a->beta2, a->step)),
+               a->apply_update};
+  const int nc = (int)L.chunks.size();
+  if (!(a->apply_update && a->max_grad_norm > 0.f)) {
+    CK(reduce_adam(nc, L.d_chunks, L.d_pieces, hp, st));
+    return MALLEUS_OK;
+  }
+  AdamHyper h1 = hp;  // pass 1: reduce into rgrad + per-chunk sum of G^2
+  h1.apply = 0;
+  h1.sq = L.d_sq;
+  CK(reduce_adam(nc, L.d_chunks, L.d_pieces, h1, st));
+  CK(sq_total(nc, L.d_sq, L.d_norm, st));  // nc == 0 -> 0
+  NK(ncclAllReduce(L.d_norm, L.d_norm, 1, ncclDouble, ncclSum, ctx->world_comm, st));
+  CK(clip_coef(L.d_norm, a->max_grad_norm, L.d_coef, L.d_coef + 1, st));
+  AdamHyper h2 = hp;  // pass 2: AdamW on rgrad * coef, bf16 cast and push
+  h2.apply = 3;
+  h2.coef = L.d_coef;
+  CK(reduce_adam(nc, L.d_chunks, L.d_pieces, h2, st));
+  return MALLEUS_OK;
+}
+
 static malleus_status grad_sync_impl(malleus_ctx* ctx, const malleus_adam_cfg* a, cudaStream_t st) {
   Layout& L = *ctx->L;
   ev_begin(ctx, st, CAT_SYNC);
@@ -920,10 +959,7 @@ static malleus_status grad_sync_impl(malleus_ctx* ctx, const malleus_adam_cfg* a
     // NVLink, barrier (all pushes landed; nobody still reads a gradient that the next step overwrites)
     float* bar = L.loss_acc + 2;
     NK(ncclAllReduce(bar, bar, 1, ncclFloat, ncclSum, ctx->world_comm, st));
-    AdamHyper hp{a->lr, a->beta1, a->beta2, a->eps, a->weight_decay,
-                 (float)(1.0 - std::pow((double)a->beta1, a->step)),
-                 (float)(1.0 - std::pow((double)a->beta2, a->step)), a->apply_update};
-    CK(reduce_adam((int)L.chunks.size(), L.d_chunks, L.d_pieces, hp, st));
+    RET(reduce_and_update(ctx, a, st));
     NK(ncclAllReduce(bar, bar, 1, ncclFloat, ncclSum, ctx->world_comm, st));
     ev_end(ctx, st);
     return MALLEUS_OK;
@@ -936,10 +972,7 @@ static malleus_status grad_sync_impl(malleus_ctx* ctx, const malleus_adam_cfg* a
     }
     NK(ncclGroupEnd());
   }
-  AdamHyper hp{a->lr, a->beta1, a->beta2, a->eps, a->weight_decay,
-               (float)(1.0 - std::pow((double)a->beta1, a->step)), (float)(1.0 - std::pow((double)a->beta2, a->step)),
-               a->apply_update};
-  CK(reduce_adam((int)L.chunks.size(), L.d_chunks, L.d_pieces, hp, st));
+  RET(reduce_and_update(ctx, a, st));
   if (a->apply_update && !L.pops.empty()) {
     NK(ncclGroupStart());
     for (auto& o : L.pops) {
@@ -1270,6 +1303,17 @@ malleus_status malleus_last_step_timing(malleus_ctx* ctx, float out[5]) {
   }
   out[4] = tot;
   out[0] = tot - out[1] - out[2] - out[3];
+  return MALLEUS_OK;
+}
+
+malleus_status malleus_last_grad_norm(malleus_ctx* ctx, float* norm, float* coef) {
+  GUARD();
+  NEED_PLAN();
+  if (!norm) return MALLEUS_E_ARG;
+  float h[2] = {0.f, 1.f};
+  if (ctx->L->d_coef) CK(cudaMemcpy(h, ctx->L->d_coef, sizeof(h), cudaMemcpyDeviceToHost));
+  *norm = h[1];
+  if (coef) *coef = h[0];
   return MALLEUS_OK;
 }
 

@@ -113,7 +113,14 @@ class Engine:
     # ------------------------------------------------------------------ step
     def adam(self, step: int, apply_update: bool = True, **kw):
         hp = dict(_ADAM_DEFAULT, **kw)
-        return L.AdamCfg(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"], step, int(apply_update))
+        return L.AdamCfg(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"], step, int(apply_update),
+                         float(hp.get("max_grad_norm", 0.0)))
+
+    def grad_norm(self):
+        """(global gradient norm, clipping coefficient) of the last clipped step."""
+        n, c = C.c_float(0), C.c_float(1)
+        check(L.lib.malleus_last_grad_norm(self.ctx, C.byref(n), C.byref(c)), self.ctx, "grad_norm")
+        return n.value, c.value
 
     def train_step(self, tokens: torch.Tensor, targets: torch.Tensor, step: int, apply_update: bool = True,
                    loss_out: torch.Tensor | None = None, stream=None, **adam_kw) -> torch.Tensor:

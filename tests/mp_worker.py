@@ -48,10 +48,13 @@ def run(plan_name: str, rank: int = 0, world: int = 1, local_rank: int = 0, grou
     names = list(tensor_shapes(cfg))
     results = {"losses": []}
     reads_step1 = None
+    clip = float(os.environ.get("MALLEUS_TEST_CLIP", "0"))  # global-norm clipping (max_grad_norm)
     for step in range(1, steps + 1):
-        loss = eng.train_step(dtok, dtgt, step=step, apply_update=True)
+        loss = eng.train_step(dtok, dtgt, step=step, apply_update=True, max_grad_norm=clip)
         torch.cuda.synchronize()
         results["losses"].append(float(loss.item()))
+        if clip > 0:
+            results.setdefault("grad_norms", []).append(eng.grad_norm()[0])
         if step == 1:
             reads_step1 = {n: (eng.read(n, L.KIND_RGRAD), eng.read(n, L.KIND_MASTER), eng.read(n, L.KIND_PARAM))
                            for n in names}
@@ -74,7 +77,17 @@ def check(cfg, W, tok, tgt, names, allr, results, plan):
     out = {"loss": results["losses"][0], "loss_ref": loss_ref,
            "loss_rel": abs(results["losses"][0] - loss_ref) / abs(loss_ref), "grad_rel": {}, "adam_rel": {},
            "push_ok": True, "owned_once": True}
-    hp = M.ADAM_DEFAULT
+    hp = dict(M.ADAM_DEFAULT)
+    clip = float(os.environ.get("MALLEUS_TEST_CLIP", "0"))
+    coef = 1.0
+    if clip > 0:  # the GPU clips its own reduced gradient: reproduce that from the gathered rgrads
+        gs = {n: gather_logical([r[n][0] for r in allr], tensor_shapes(cfg)[n])[0].astype(np.float64) for n in names}
+        _, gpu_norm = M.clip_grad_norm(gs, clip)
+        coef = min(1.0, clip / (gpu_norm + 1e-6))
+        out["grad_norm"] = results["grad_norms"][0]
+        out["grad_norm_rgrad"] = gpu_norm
+        out["clip_coef"] = coef
+        hp["max_grad_norm"] = clip
     for n in names:
         shp = tensor_shapes(cfg)[n]
         g, seen = gather_logical([r[n][0] for r in allr], shp)
@@ -86,7 +99,7 @@ def check(cfg, W, tok, tgt, names, allr, results, plan):
         out["grad_rel"][n] = float(np.abs(g - g_ref[n]).max() / max(np.abs(g_ref[n]).max(), 1e-30))
         master, _ = gather_logical([r[n][1] for r in allr], shp)
         wd = hp["weight_decay"] if M.decays(n) else 0.0
-        th, _, _ = M.adamw(P[n], np.zeros(shp), np.zeros(shp), g.astype(np.float64), 1, hp["lr"], hp["beta1"],
+        th, _, _ = M.adamw(P[n], np.zeros(shp), np.zeros(shp), g.astype(np.float64) * coef, 1, hp["lr"], hp["beta1"],
                            hp["beta2"], hp["eps"], wd)
         out["adam_rel"][n] = float(np.abs(master - th).max() / max(np.abs(th).max(), 1e-30))
         # param push: each holder's bf16 == RNE(master)
@@ -109,6 +122,8 @@ def check(cfg, W, tok, tgt, names, allr, results, plan):
             Pb = {k: bf16_to_f64(bf16_rne(v.astype(np.float32))) for k, v in Pm.items()}
             l, g = M.forward_backward(cfg, Pb, tok, tgt)
             ref_losses.append(l)
+            if clip > 0:
+                g, _ = M.clip_grad_norm(g, clip)
             for k in Pm:
                 wd = hp["weight_decay"] if M.decays(k) else 0.0
                 Pm[k], Mm[k], Vm[k] = M.adamw(Pm[k], Mm[k], Vm[k], g[k], step, hp["lr"], hp["beta1"], hp["beta2"],

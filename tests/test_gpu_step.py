@@ -136,3 +136,32 @@ def test_p0_run_to_run_bitwise():
     a = run("P0", steps=3)
     b = run("P0", steps=3)
     assert a["losses"] == b["losses"], (a["losses"], b["losses"])
+
+
+@pytest.mark.parametrize("plan", ["P0", "P4"])
+def test_grad_clipping(plan, tmp_path, monkeypatch):
+    """Global-norm gradient clipping (malleus_adam_cfg.max_grad_norm, torch clip_grad_norm_
+    semantics): the norm the library computes from the owners' reduced gradients equals the norm
+    of the gathered reduced gradients, the update equals the oracle's AdamW on the clipped gradient,
+    and a 3-step loss curve follows the oracle trained with clipping.  max_grad_norm is set below
+    the step-1 norm so clipping is active."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    n = PLAN_WORLD[plan]
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"{plan} needs {n} GPUs")
+    monkeypatch.setenv("MALLEUS_TEST_CLIP", "0.05")
+    if n == 1:
+        from tests.mp_worker import run
+        r = run(plan, steps=3)
+    else:
+        out = tmp_path / "r.json"
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr=127.0.0.1", "--master-port=29537", os.path.join(ROOT, "tests", "mp_worker.py"), plan,
+               str(out), "3"]
+        p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=dict(os.environ))
+        assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+        r = json.load(open(out))
+    _assert_ok(r)
+    assert r["clip_coef"] < 1.0, r["clip_coef"]  # clipping was active
+    assert abs(r["grad_norm"] - r["grad_norm_rgrad"]) <= 1e-4 * r["grad_norm_rgrad"], (r["grad_norm"], r["grad_norm_rgrad"])
