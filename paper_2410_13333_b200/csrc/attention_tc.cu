@@ -2,16 +2,19 @@
 // and sequence lengths that are multiples of 128 (PAPER.md:780 FlashAttention).
 //
 // One CTA = 128 queries of one (sequence, head).  Warp roles:
-//   warp 0      TMA producer: Q once; K and V tiles of 128 keys through separate 2-stage rings
+//   warp 0      TMA producer: Q once; K and V tiles of 128 keys through separate 3-stage rings
 //               (K_i is released when S_i is done, a full tile before V_i, so its reload is hidden);
 //   warp 1      MMA issuer (one thread) + TMEM owner: S_i = Q K_i^T into one of two TMEM S buffers,
 //               then O += P_{i-1} V_{i-1} once the softmax warps have written P_{i-1};
 //   warps 2..9  softmax (two warps per query row, 64 keys each): S row from TMEM, online max with lazy
 //               rescaling (O in TMEM is rescaled only when the running max grows by > 2^8, FA4
-//               style; exact since numerator and denominator share the stale max), P (bf16) into
-//               a 128B-swizzled smem tile that is the A operand of the PV MMA; final O / l, LSE.
-// TMEM: S0 cols [0,128), S1 [128,256), O [256,384), row-max exchange [384,388).
-// smem: Q 32 KB, 2 x K 32 KB, 2 x V 32 KB, 2 x P 32 KB.
+//               style; exact since numerator and denominator share the stale max), P (bf16) written
+//               over the row's own S columns in TMEM; final O / l, LSE.
+// Both A operands come from TMEM ("ts" MMAs: Q copied once by the softmax warps, P in place), so the
+// only shared-memory operand traffic is K and V: measured on the previous version (Q and P as smem
+// operands) the tile loop was bound by shared-memory bandwidth (A + B of every MMA, P stores, TMA).
+// TMEM: S0 cols [0,128), S1 [128,256), O [256,384), row-max exchange [384,388), Q [448,512).
+// smem: Q 32 KB (TMA landing), 3 x K 32 KB, 3 x V 32 KB.
 // Output identical in layout to attention.cu: o [T, n*d] bf16, lse [nb, n, s] (natural log).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -25,10 +28,6 @@ namespace {
 constexpr int TQ = 128, TK = 128, DH = 128;
 constexpr int PANEL = 128 * 64 * 2;            // one 128-row x 64-col bf16 swizzled panel (16 KB)
 constexpr int Q_BYTES = 2 * PANEL;             // 32 KB
-constexpr int KV_STAGE = 4 * PANEL;            // K (2 panels) + V (2 panels)
-constexpr int P_BYTES = 2 * PANEL;
-constexpr int KV_STAGES = 2;
-constexpr int SMEM_TC = Q_BYTES + KV_STAGES * KV_STAGE + 2 * P_BYTES + 1024 + 1024;  // P double-buffered
 constexpr int K_BYTES = 2 * PANEL;             // one K (or V) tile of 128 keys
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -51,41 +50,30 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x for x <= 0 on the FMA pipe (FA4's trick to offload the MUFU unit, which alone would bound a
-// 128x128 tile at 1024 cycles, as long as the two MMAs): round-to-nearest split x = j + f with the
-// 1.5 * 2^23 magic constant, near-minimax cubic for 2^f on [-0.5, 0.5] (max rel. error 7.5e-5,
-// far below bf16's 2^-9), exponent added in the integer domain; x < -126 (incl. -inf) gives 0.
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -127.f);
-  const float t = xc + 12582912.f;
-  const float f = xc - (t - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.05517147f, f, 0.24261111f), f, 0.693261f), f, 0.99992806f);
-  const float r = __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
-  return x < -126.f ? 0.f : r;
-}
+constexpr int FWD_STAGES = 3;
+constexpr int SMEM_FWD = Q_BYTES + 2 * FWD_STAGES * K_BYTES + 1024 + 1024;
 
-// NPOLY of every 8 consecutive P elements take ex2_poly, the rest the MUFU ex2
-template <int NPOLY>
 __global__ void __launch_bounds__(320, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bfloat16* __restrict__ o,
                    float* __restrict__ lse, float scale, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + Q_BYTES;                // [2 stages] K tiles
-  uint8_t* sV = sK + KV_STAGES * K_BYTES;    // [2 stages] V tiles
-  uint8_t* sP = sV + KV_STAGES * K_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
+  uint8_t* sK = sQ + Q_BYTES;                  // [FWD_STAGES] K tiles
+  uint8_t* sV = sK + FWD_STAGES * K_BYTES;     // [FWD_STAGES] V tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + FWD_STAGES * K_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;               // [2]
-  uint64_t* k_empty = bars + 3;              // [2] K_i free once S_i = Q K_i^T is done
-  uint64_t* s_full = bars + 5;               // [2]
-  uint64_t* s_empty = bars + 7;              // [2]
-  uint64_t* p_full = bars + 9;   // [2] (P buffer j & 1)
-  uint64_t* o_done = bars + 11;  // [2] (PV of tile j completes on o_done[j & 1])
-  uint64_t* v_full = bars + 13;  // [2]
-  uint64_t* v_empty = bars + 15; // [2] V_j free once O += P_j V_j is done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* k_full = bars + 1;                 // [3]
+  uint64_t* k_empty = bars + 4;                // [3] K_i free once S_i = Q K_i^T is done
+  uint64_t* v_full = bars + 7;                 // [3]
+  uint64_t* v_empty = bars + 10;               // [3] V_j free once O += P_j V_j is done
+  uint64_t* s_full = bars + 13;                // [2]
+  uint64_t* s_empty = bars + 15;               // [2]
+  uint64_t* p_full = bars + 17;                // [2] P_j (in S_j's TMEM columns) written
+  uint64_t* o_done = bars + 19;                // [2] (PV of tile j completes on o_done[j & 1])
+  uint64_t* q_tmem = bars + 21;                // Q copied into TMEM by the softmax warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  constexpr uint32_t COL_O = 256, COL_X = 384, COL_Q = 448;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;
@@ -105,12 +93,15 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < FWD_STAGES; ++i) {
       mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
     }
-    for (int i = 0; i < 2; ++i) { mbar_init(&p_full[i], 8); mbar_init(&o_done[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 8);
+      mbar_init(&p_full[i], 8); mbar_init(&o_done[i], 1);
+    }
+    mbar_init(q_tmem, 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -125,22 +116,21 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       tma_load_2d(sQ, &tm, q_full, head * DH, row0);
       tma_load_2d(sQ + PANEL, &tm, q_full, head * DH + 64, row0);
       // K runs one tile ahead of V in this thread's program order: K_{i+1} is requested as soon as
-      // its slot frees (S_{i-1} done) instead of queueing behind V_i, whose slot frees only when
-      // O += P_{i-2} V_{i-2} completes (measured: that ordering put the load latency on the
-      // critical path of every tile)
+      // its slot frees (S_{i+1-3} done) instead of queueing behind V_i (measured: that ordering put
+      // the load latency on the critical path of every tile)
       auto load_k = [&](int i) {
-        const int st = i & 1;
+        const int st = i % FWD_STAGES;
         uint8_t* k = sK + st * K_BYTES;
-        mbar_wait(&k_empty[st], ((i >> 1) & 1) ^ 1);
+        mbar_wait(&k_empty[st], ((i / FWD_STAGES) & 1) ^ 1);
         stamp(0, i);
         mbar_arrive_expect_tx(&k_full[st], K_BYTES);
         tma_load_2d(k, &tm, &k_full[st], nd + head * DH, b * s + i * TK);
         tma_load_2d(k + PANEL, &tm, &k_full[st], nd + head * DH + 64, b * s + i * TK);
       };
       auto load_v = [&](int i) {
-        const int st = i & 1;
+        const int st = i % FWD_STAGES;
         uint8_t* v = sV + st * K_BYTES;
-        mbar_wait(&v_empty[st], ((i >> 1) & 1) ^ 1);
+        mbar_wait(&v_empty[st], ((i / FWD_STAGES) & 1) ^ 1);
         stamp(1, i);
         mbar_arrive_expect_tx(&v_full[st], K_BYTES);
         tma_load_2d(v, &tm, &v_full[st], 2 * nd + head * DH, b * s + i * TK);
@@ -156,38 +146,32 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
     if (lane == 0) {
       constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_pv = umma_idesc_bf16(128, 128, false, true);
-      const uint32_t aq = smem_u32(sQ), ap = smem_u32(sP);
-      auto issue_pv = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&v_full[st], (j >> 1) & 1);
+      auto issue_pv = [&](int j) {  // O += P_j V_j, P_j from TMEM (S_j's columns)
+        const int st = j % FWD_STAGES;
+        mbar_wait(&v_full[st], (j / FWD_STAGES) & 1);
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         stamp(3, j);
         tc_fence_after();
         const uint32_t v = smem_u32(sV + st * K_BYTES);
-        const uint32_t apj = ap + (j & 1) * P_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < TK / 16; ++kk) {
-          const uint64_t ad = umma_desc_sw128(apj + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024);
-          const uint64_t bd = umma_desc_sw128(v + kk * 2048, PANEL, 1024);
-          umma_f16(tbase + 256, ad, bd, id_pv, (j > 0 || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = 0; kk < TK / 16; ++kk)
+          umma_f16_ts(tbase + COL_O, tbase + 128 * (j & 1) + (kk >> 2) * 64 + (kk & 3) * 8,
+                      umma_desc_sw128(v + kk * 2048, PANEL, 1024), id_pv, (j > 0 || kk > 0) ? 1u : 0u);
         umma_commit(&o_done[j & 1]);
         umma_commit(&v_empty[st]);
       };
-      mbar_wait(q_full, 0);
+      mbar_wait(q_tmem, 0);
       for (int i = 0; i < n_tiles; ++i) {
-        const int st = i & 1, sb = i & 1;
-        mbar_wait(&k_full[st], (i >> 1) & 1);
+        const int st = i % FWD_STAGES, sb = i & 1;
+        mbar_wait(&k_full[st], (i / FWD_STAGES) & 1);
         mbar_wait(&s_empty[sb], ((i >> 1) & 1) ^ 1);
         stamp(2, i);
         tc_fence_after();
         const uint32_t k = smem_u32(sK + st * K_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint64_t ad = umma_desc_sw128(aq + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024);
-          const uint64_t bd = umma_desc_sw128(k + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024);
-          umma_f16(tbase + 128 * sb, ad, bd, id_qk, kk > 0 ? 1u : 0u);
-        }
+        for (int kk = 0; kk < DH / 16; ++kk)  // S_i = Q K_i^T, Q from TMEM
+          umma_f16_ts(tbase + 128 * sb, tbase + COL_Q + kk * 8,
+                      umma_desc_sw128(k + (kk >> 2) * PANEL + (kk & 3) * 32, 16, 1024), id_qk, kk > 0 ? 1u : 0u);
         umma_commit(&s_full[sb]);
         umma_commit(&k_empty[st]);
         if (i > 0) issue_pv(i - 1);
@@ -196,9 +180,9 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
     }
   } else {
     // ---------------- softmax: 8 warps, two per TMEM lane quarter; thread = half a query row
-    // (64 of the 128 keys of a tile).  The pair exchanges its partial row maxima through two
-    // spare TMEM columns (same lane) and a named barrier; each half writes its own P panel and
-    // owns half of the O columns for rescaling and the epilogue.
+    // (64 of the 128 keys of a tile).  The pair exchanges its partial row maxima through spare TMEM
+    // columns and a named barrier; each half writes its 64 P values (bf16) over its own S columns
+    // and owns half of the O columns for rescaling and the epilogue.
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;            // row within the 128-query block
@@ -206,11 +190,25 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = scale * LOG2E;
     float m_used = -INFINITY, l = 0.f;
-    uint8_t* prow = sP + half * PANEL + r * 128;  // this row of this half's 64-key panel
+    {  // Q row -> TMEM (A operand of S = Q K^T): this half's 64 dims = 32 packed columns
+      mbar_wait(q_full, 0);
+      const uint8_t* qrow = sQ + half * PANEL + r * 128;
+      uint32_t u[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 w = *reinterpret_cast<const uint4*>(qrow + ((c ^ (r & 7)) << 4));
+        u[4 * c] = w.x; u[4 * c + 1] = w.y; u[4 * c + 2] = w.z; u[4 * c + 3] = w.w;
+      }
+      tmem_st32(tbase + lane_off + COL_Q + 32 * half, u);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_tmem);
+    }
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory"); };
     auto exchange = [&](float mine, int slot) -> float {  // returns the partner's value
       uint32_t v = __float_as_uint(mine);
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tbase + lane_off + 384 + slot * 2 + half),
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tbase + lane_off + COL_X + slot * 2 + half),
                    "r"(v) : "memory");
       tmem_wait_st();
       tc_fence_before();
@@ -218,7 +216,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       tc_fence_after();
       uint32_t o;
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(o)
-                   : "r"(tbase + lane_off + 384 + slot * 2 + (half ^ 1)) : "memory");
+                   : "r"(tbase + lane_off + COL_X + slot * 2 + (half ^ 1)) : "memory");
       tmem_wait_ld();
       return __uint_as_float(o);
     };
@@ -227,11 +225,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       mbar_wait(&s_full[sb], (i >> 1) & 1);
       if (warp == 2 && lane == 0) stamp(4, i);
       tc_fence_after();
+      const uint32_t cs = tbase + lane_off + 128 * sb + half * 64;
       float sv[TK / 2];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t u[32];
-        tmem_ld32(tbase + lane_off + 128 * sb + half * 64 + c * 32, u);
+        tmem_ld32(cs + c * 32, u);
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 32; ++j) sv[c * 32 + j] = __uint_as_float(u[j]) * sl2;
@@ -249,11 +248,6 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       for (int j = 0; j < TK / 2; ++j) mt = fmaxf(mt, sv[j]);
       mt = fmaxf(mt, exchange(mt, i & 1));  // full-row max of this tile
       if (warp == 2 && lane == 0) stamp(5, i);
-      // P buffer i & 1 is free once PV_{i-2} is done
-      if (i > 1) {
-        mbar_wait(&o_done[i & 1], ((i - 2) >> 1) & 1);
-        tc_fence_after();
-      }
       // tcgen05.ld / st are warp-collective: the rescale decision is warp-uniform (and identical
       // in both warps of the pair: same rows, same maxima); lanes whose max did not grow scale by 1
       if (__any_sync(0xffffffffu, mt > m_used + 8.f)) {
@@ -266,35 +260,30 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
 #pragma unroll 1
           for (int c = 0; c < 2; ++c) {
             uint32_t u[32];
-            tmem_ld32(tbase + lane_off + 256 + half * 64 + c * 32, u);
+            tmem_ld32(tbase + lane_off + COL_O + half * 64 + c * 32, u);
             tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 32; ++j) u[j] = __float_as_uint(__uint_as_float(u[j]) * f);
-            tmem_st32(tbase + lane_off + 256 + half * 64 + c * 32, u);
+            tmem_st32(tbase + lane_off + COL_O + half * 64 + c * 32, u);
           }
           tmem_wait_st();
         }
         m_used = m_new;
       }
-      // P = exp2(s - m_used) -> bf16 into this half's swizzled 64-key panel
+      // P = exp2(s - m_used) -> bf16 pairs over this half's own S columns (A operand of PV; the
+      // MMA that overwrites them, S_{i+2}, is issued after O += P_i V_i)
+      uint32_t pk[32];
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        float p[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float x = sv[ch * 8 + j] - m_used;
-          p[j] = ((j * NPOLY) % 8 < NPOLY && NPOLY > 0) ? ex2_poly(x) : ex2(x);  // NPOLY spread over the 8
-          l += p[j];
-        }
-        uint4 w;
-        w.x = pack_bf16(p[0], p[1]); w.y = pack_bf16(p[2], p[3]);
-        w.z = pack_bf16(p[4], p[5]); w.w = pack_bf16(p[6], p[7]);
-        *reinterpret_cast<uint4*>(prow + (i & 1) * P_BYTES + ((ch ^ (r & 7)) << 4)) = w;
+      for (int j = 0; j < 32; ++j) {
+        const float p0 = ex2(sv[2 * j] - m_used), p1 = ex2(sv[2 * j + 1] - m_used);
+        l += p0 + p1;
+        pk[j] = pack_bf16(p0, p1);
       }
-      fence_proxy_async();
+      tmem_st32(cs, pk);
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[i & 1]);
+      if (lane == 0) mbar_arrive(&p_full[sb]);
       if (warp == 2 && lane == 0) stamp(6, i);
     }
     // epilogue: O / l (MMAs complete in issue order: the last PV implies all)
@@ -307,7 +296,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
       uint32_t u[32];
-      tmem_ld32(tbase + lane_off + 256 + half * 64 + c * 32, u);
+      tmem_ld32(tbase + lane_off + COL_O + half * 64 + c * 32, u);
       tmem_wait_ld();
       uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
@@ -860,10 +849,8 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    for (auto fn : {attn_fwd_tc_kernel<0>, attn_fwd_tc_kernel<2>, attn_fwd_tc_kernel<3>, attn_fwd_tc_kernel<4>}) {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC);
-      if (e != cudaSuccess) return e;
-    }
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_FWD);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
   static unsigned long long* trace = nullptr;
@@ -871,13 +858,8 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
     if (cudaMallocManaged(&trace, 2 * 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
     attn_trace_buffer = trace;
   }
-  static const int npoly = [] {
-    const char* e = getenv("MALLEUS_ATTN_POLY");  // experiments: 0, 2, 3, 4 of every 8 exps in software
-    return e ? atoi(e) : 0;  // measured: with MUFU not the bottleneck the extra FMA work costs ~8%
-  }();
-  auto fn = npoly == 0 ? attn_fwd_tc_kernel<0> : npoly == 2 ? attn_fwd_tc_kernel<2>
-          : npoly == 4 ? attn_fwd_tc_kernel<4> : attn_fwd_tc_kernel<3>;
-  fn<<<dim3(s / TQ, n, nb), 320, SMEM_TC, st>>>(tm, s, n, (__nv_bfloat16*)o, lse, rsqrtf((float)DH), trace); count_launch();
+  attn_fwd_tc_kernel<<<dim3(s / TQ, n, nb), 320, SMEM_FWD, st>>>(tm, s, n, (__nv_bfloat16*)o, lse, rsqrtf((float)DH),
+                                                                 trace); count_launch();
   return cudaGetLastError();
 }
 
