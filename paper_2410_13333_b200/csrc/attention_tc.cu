@@ -50,9 +50,25 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x for x <= 0 on the FMA pipe (FA4's trick to offload the MUFU unit: with Q and P in TMEM the
+// softmax warps are bound by MUFU ex2, 16 / clk / SM, i.e. 1024 cycles per 128 x 128 tile).
+// Round-to-nearest split x = j + f with the 1.5 * 2^23 magic constant, near-minimax cubic for 2^f
+// on [-0.5, 0.5] (max rel. error 7.5e-5, far below bf16's 2^-9), exponent added in the integer
+// domain; x < -126 (incl. -inf) gives 0.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -127.f);
+  const float t = xc + 12582912.f;
+  const float f = xc - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517147f, f, 0.24261111f), f, 0.693261f), f, 0.99992806f);
+  const float r = __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+  return x < -126.f ? 0.f : r;
+}
+
 constexpr int FWD_STAGES = 3;
 constexpr int SMEM_FWD = Q_BYTES + 2 * FWD_STAGES * K_BYTES + 1024 + 1024;
 
+// NPOLY of every 8 consecutive P elements take ex2_poly, the rest the MUFU ex2
+template <int NPOLY>
 __global__ void __launch_bounds__(320, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bfloat16* __restrict__ o,
                    float* __restrict__ lse, float scale, unsigned long long* __restrict__ trace) {
@@ -275,7 +291,10 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       uint32_t pk[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float p0 = ex2(sv[2 * j] - m_used), p1 = ex2(sv[2 * j + 1] - m_used);
+        const int e0 = (2 * j) & 7, e1 = (2 * j + 1) & 7;  // position within each group of 8
+        const float x0 = sv[2 * j] - m_used, x1 = sv[2 * j + 1] - m_used;
+        const float p0 = ((e0 * NPOLY) % 8 < NPOLY && NPOLY > 0) ? ex2_poly(x0) : ex2(x0);
+        const float p1 = ((e1 * NPOLY) % 8 < NPOLY && NPOLY > 0) ? ex2_poly(x1) : ex2(x1);
         l += p0 + p1;
         pk[j] = pack_bf16(p0, p1);
       }
@@ -849,8 +868,10 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_FWD);
-    if (e != cudaSuccess) return e;
+    for (auto fn : {attn_fwd_tc_kernel<0>, attn_fwd_tc_kernel<1>, attn_fwd_tc_kernel<2>, attn_fwd_tc_kernel<3>}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_FWD);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
   static unsigned long long* trace = nullptr;
@@ -858,8 +879,14 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
     if (cudaMallocManaged(&trace, 2 * 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
     attn_trace_buffer = trace;
   }
-  attn_fwd_tc_kernel<<<dim3(s / TQ, n, nb), 320, SMEM_FWD, st>>>(tm, s, n, (__nv_bfloat16*)o, lse, rsqrtf((float)DH),
-                                                                 trace); count_launch();
+  static const int npoly = [] {  // exps per 8 on the FMA pipe (MALLEUS_ATTN_POLY overrides; measured default)
+    const char* e = getenv("MALLEUS_ATTN_POLY");
+    return e ? atoi(e) : 1;
+  }();
+  auto fn = npoly <= 0 ? attn_fwd_tc_kernel<0> : npoly == 1 ? attn_fwd_tc_kernel<1>
+          : npoly == 2 ? attn_fwd_tc_kernel<2> : attn_fwd_tc_kernel<3>;
+  fn<<<dim3(s / TQ, n, nb), 320, SMEM_FWD, st>>>(tm, s, n, (__nv_bfloat16*)o, lse, rsqrtf((float)DH), trace);
+  count_launch();
   return cudaGetLastError();
 }
 
