@@ -50,8 +50,8 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x for x <= 0 on the FMA pipe (FA4's trick to offload the MUFU unit: with Q and P in TMEM the
-// softmax warps are bound by MUFU ex2, 16 / clk / SM, i.e. 1024 cycles per 128 x 128 tile).
+// 2^x for x <= 0 on the FMA pipe (FA4's trick to offload the MUFU unit, 16 ex2 / clk / SM, i.e.
+// 1024 cycles per 128 x 128 tile; off by default: measured slower here, see the launcher).
 // Round-to-nearest split x = j + f with the 1.5 * 2^23 magic constant, near-minimax cubic for 2^f
 // on [-0.5, 0.5] (max rel. error 7.5e-5, far below bf16's 2^-9), exponent added in the integer
 // domain; x < -126 (incl. -inf) gives 0.
@@ -879,9 +879,9 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
     if (cudaMallocManaged(&trace, 2 * 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
     attn_trace_buffer = trace;
   }
-  static const int npoly = [] {  // exps per 8 on the FMA pipe (MALLEUS_ATTN_POLY overrides; measured default)
-    const char* e = getenv("MALLEUS_ATTN_POLY");
-    return e ? atoi(e) : 1;
+  static const int npoly = [] {  // exps per 8 on the FMA pipe (MALLEUS_ATTN_POLY); measured C2 forward:
+    const char* e = getenv("MALLEUS_ATTN_POLY");  // 0: 67.8 us, 1: 70.7, 2: 73.3, 3: 76.7 -> off
+    return e ? atoi(e) : 0;
   }();
   auto fn = npoly <= 0 ? attn_fwd_tc_kernel<0> : npoly == 1 ? attn_fwd_tc_kernel<1>
           : npoly == 2 ? attn_fwd_tc_kernel<2> : attn_fwd_tc_kernel<3>;
