@@ -377,19 +377,21 @@ constexpr int A2_BYTES = BM2 * BK * 2;            // 16 KB
 constexpr int B2_BYTES = (BN2 / 2) * BK * 2;      // 16 KB (this CTA's half of N)
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
 constexpr int EPI_STAGE_BYTES = 4 * 2 * 4096;  // 4 epilogue warps x 2 swizzled 4 KB boxes
-constexpr int GEMM2_SMEM = STAGES2 * STAGE2_BYTES + EPI_STAGE_BYTES + 1024 + 1024;
+constexpr int gemm2_smem(int stages) { return stages * STAGE2_BYTES + EPI_STAGE_BYTES + 1024 + 1024; }
 
-template <bool A_MN, bool B_MN>
+// ST: smem ring depth (6 by default; 5 leaves room on each SM for a concurrently running
+// communication kernel, see GemmDesc::co_resident)
+template <bool A_MN, bool B_MN, int ST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const __grid_constant__ TmapSet tmD,
                         GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* epi_stage = smem + STAGES2 * STAGE2_BYTES;
+  uint8_t* epi_stage = smem + ST * STAGE2_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + EPI_STAGE_BYTES);
-  uint64_t* empty = full + STAGES2;
-  uint64_t* tfull = empty + STAGES2;  // [2]
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;  // [2]
   uint64_t* tempty = tfull + 2;       // [2] (leader's copy is the one used)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -406,7 +408,7 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    for (int s = 0; s < STAGES2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
     fence_barrier_init();
   }
@@ -440,7 +442,7 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
             tma_load_2d_2sm(sb, &tmB, &full[stage], n0, k0);
             tma_load_2d_2sm(sb + 8192, &tmB, &full[stage], n0 + 64, k0);
           }
-          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+          if (++stage == ST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -469,7 +471,7 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
             umma_f16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
           umma_commit_2sm_mc(&empty[stage]);
-          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+          if (++stage == ST) { stage = 0; phase ^= 1; }
         }
         umma_commit_2sm_mc(&tfull[acc]);
       }
@@ -624,13 +626,14 @@ void gemm_set_variant(int v) {
   g_tma_epi = v == 3 ? 0 : 1;
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int ST>
 static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const TmapSet& td,
                            const GemmParams& p, cudaStream_t st) {
   static bool attr_set = false;
-  auto kern = gemm_tcgen05_2sm_kernel<A_MN, B_MN>;
+  auto kern = gemm_tcgen05_2sm_kernel<A_MN, B_MN, ST>;
+  constexpr int SMEM2 = gemm2_smem(ST);
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM2_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -652,7 +655,7 @@ static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const C
     }
     cudaEventRecord(g_prof.ev[g_prof.used].first, st);
   }
-  kern<<<grid, GEMM_THREADS, GEMM2_SMEM, st>>>(ta, tb, tc, td, p); count_launch();
+  kern<<<grid, GEMM_THREADS, SMEM2, st>>>(ta, tb, tc, td, p); count_launch();
   if (prof) {
     cudaEventRecord(g_prof.ev[g_prof.used].second, st);
     g_prof.flops.push_back(2.0 * p.M * (double)p.N * p.K);
@@ -703,10 +706,16 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
     p.rope_cs = rope ? g.rope_cs : nullptr;
     p.rope_cols = g.rope_cols;
     p.rope_s = g.rope_s;
-    if (!g.a_mn && !g.b_mn) return launch2<false, false>(ta, tb, tc, td, p, st);
-    if (!g.a_mn && g.b_mn) return launch2<false, true>(ta, tb, tc, td, p, st);
-    if (g.a_mn && g.b_mn) return launch2<true, true>(ta, tb, tc, td, p, st);
-    return launch2<true, false>(ta, tb, tc, td, p, st);
+    if (g.co_resident) {  // 5-stage ring: ~32 KB of smem per SM left for a concurrent kernel
+      if (!g.a_mn && !g.b_mn) return launch2<false, false, 5>(ta, tb, tc, td, p, st);
+      if (!g.a_mn && g.b_mn) return launch2<false, true, 5>(ta, tb, tc, td, p, st);
+      if (g.a_mn && g.b_mn) return launch2<true, true, 5>(ta, tb, tc, td, p, st);
+      return launch2<true, false, 5>(ta, tb, tc, td, p, st);
+    }
+    if (!g.a_mn && !g.b_mn) return launch2<false, false, STAGES2>(ta, tb, tc, td, p, st);
+    if (!g.a_mn && g.b_mn) return launch2<false, true, STAGES2>(ta, tb, tc, td, p, st);
+    if (g.a_mn && g.b_mn) return launch2<true, true, STAGES2>(ta, tb, tc, td, p, st);
+    return launch2<true, false, STAGES2>(ta, tb, tc, td, p, st);
   }
   CUtensorMap ta, tb;
   bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.lda, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, BM);

@@ -31,6 +31,9 @@ struct GemmDesc {
   // dst may be peer memory).  The kernel makes its stores visible system-wide before it ends.
   int n_dst = 0, rows_per_dst = 0;
   void* dst[4] = {nullptr, nullptr, nullptr, nullptr};
+  // leave shared memory on every SM for a kernel running concurrently on another stream (the
+  // backward TP reduction overlapping the weight-gradient GEMM): 5-stage instead of 6-stage ring
+  bool co_resident = false;
 };
 cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st);
 

@@ -147,6 +147,8 @@ struct malleus_ctx {
   std::string err;
   bool sticky = false;
   cudaStream_t side = nullptr;  // hog stream
+  cudaStream_t tp_side = nullptr;             // backward TP reductions overlapping the wgrad GEMM
+  cudaEvent_t tp_ev_a = nullptr, tp_ev_b = nullptr;
   int* hog_flag = nullptr;      // host-mapped
   float slowdown = 1.f;
   int slow_mode = 0;
@@ -649,6 +651,15 @@ static malleus_status gemm(malleus_ctx* ctx, int M, int N, int K, const void* A,
   return MALLEUS_OK;
 }
 
+static malleus_status gemm_co(malleus_ctx* ctx, int M, int N, int K, const void* A, long long lda, bool amn,
+                              const void* B, long long ldb, bool bmn, void* C, long long ldc, int mode,
+                              cudaStream_t st) {  // GEMM leaving room for a concurrent kernel (GemmDesc::co_resident)
+  GemmDesc g{M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, mode};
+  g.co_resident = true;
+  CK(gemm_bf16(g, st));
+  return MALLEUS_OK;
+}
+
 static void duty_begin(malleus_ctx* ctx, int seg, cudaStream_t st);
 static void duty_end(malleus_ctx* ctx, cudaStream_t st);
 
@@ -690,10 +701,12 @@ static Layout& member_layout(Layout& L, int j) {
 // sel(M, a, j) fills member j's destinations a.d0/d1/d2[j] from its layout M
 template <class Sel>
 static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, const void* g, Sel sel,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, bool async = false) {
   Layout& L = *ctx->L;
-  duty_end(ctx, st);
-  ev_begin(ctx, st, CAT_TP);
+  if (!async) {  // async: the caller handles DUTY and times only the exposed wait
+    duty_end(ctx, st);
+    ev_begin(ctx, st, CAT_TP);
+  }
   TpArgs a{};
   a.k = L.TP;
   a.me = L.member;
@@ -722,7 +735,7 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, 
     sel(M, a, j);
   }
   CK(tp_reduce(a, st));
-  ev_end(ctx, st);
+  if (!async) ev_end(ctx, st);
   return MALLEUS_OK;
 }
 
@@ -731,6 +744,36 @@ static malleus_status tp_sum(malleus_ctx* ctx, cudaStream_t st) {
   Layout& L = *ctx->L;
   if (!tp_peer(L)) return tp_allreduce(ctx, L.part, (size_t)L.T * ctx->cfg.hidden, ncclSum, st);
   return tp_reduce_peer(ctx, TP_SUM, nullptr, nullptr, [&](Layout& M, TpArgs& a, int j) { a.d0[j] = M.part; }, st);
+}
+
+// Backward TP sums overlap the weight-gradient GEMM that follows the row-parallel dgrad GEMM: the
+// reduction runs on a side stream (it only reads the partial slots and writes the members' sum
+// buffers; the wgrad GEMM touches neither) while the GEMM, given a 5-stage ring so the reduction's
+// CTAs fit beside it on every SM, runs on the main stream; the main stream joins before the norm's
+// backward reads the sum.  MALLEUS_TP_NO_OVERLAP=1 serialises them.
+static bool tp_overlap(const Layout& L) {
+  static const bool off = getenv("MALLEUS_TP_NO_OVERLAP") != nullptr;
+  return !off && tp_peer(L);
+}
+static malleus_status tp_sum_begin(malleus_ctx* ctx, cudaStream_t st) {
+  if (!ctx->tp_side) {
+    CK(cudaStreamCreateWithFlags(&ctx->tp_side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->tp_ev_a, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->tp_ev_b, cudaEventDisableTiming));
+  }
+  duty_end(ctx, st);
+  CK(cudaEventRecord(ctx->tp_ev_a, st));
+  CK(cudaStreamWaitEvent(ctx->tp_side, ctx->tp_ev_a, 0));
+  RET(tp_reduce_peer(ctx, TP_SUM, nullptr, nullptr, [&](Layout& M, TpArgs& a, int j) { a.d0[j] = M.part; },
+                     ctx->tp_side, true));
+  CK(cudaEventRecord(ctx->tp_ev_b, ctx->tp_side));
+  return MALLEUS_OK;
+}
+static malleus_status tp_sum_end(malleus_ctx* ctx, cudaStream_t st) {
+  ev_begin(ctx, st, CAT_TP);  // the exposed part of the reduction
+  CK(cudaStreamWaitEvent(st, ctx->tp_ev_b, 0));
+  ev_end(ctx, st);
+  return MALLEUS_OK;
 }
 
 // row-parallel GEMM producing this member's partial sum of a TP reduction (C = A B, [M = T, N = h]):
@@ -850,8 +893,14 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
   CK(swiglu_bwd(T, F, Y.gu, L.du, L.dgu, st));
   RET(part_gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, st));
-  RET(gemm(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
-  RET(tp_sum(ctx, st));
+  if (tp_overlap(L)) {
+    RET(tp_sum_begin(ctx, st));
+    RET(gemm_co(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
+    RET(tp_sum_end(ctx, st));
+  } else {
+    RET(gemm(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
+    RET(tp_sum(ctx, st));
+  }
   duty_begin(ctx, 4, st);
   CK(rmsnorm_bwd(T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st, tp_sum_bf16(L)));
   // attention
@@ -862,8 +911,14 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
     CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
   RET(part_gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, st));
-  RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
-  RET(tp_sum(ctx, st));
+  if (tp_overlap(L)) {
+    RET(tp_sum_begin(ctx, st));
+    RET(gemm_co(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
+    RET(tp_sum_end(ctx, st));
+  } else {
+    RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
+    RET(tp_sum(ctx, st));
+  }
   duty_begin(ctx, 5, st);
   CK(rmsnorm_bwd(T, h, S.x[li], P.g1, Y.r1, L.part, dx1, dx, P.dg1, L.scratch, st, tp_sum_bf16(L)));
   duty_end(ctx, st);
@@ -892,8 +947,15 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
   if (L.member == 0)
     CK(reduce_loss(T, L.loss_rows, (float)(1.0 / ((double)L.plan.B * c.seq_len)), L.loss_acc, 1, st));
   RET(part_gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, st));
-  RET(gemm(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, first ? GEMM_STORE_F32 : GEMM_ACCUM_F32, st));
-  RET(tp_sum(ctx, st));
+  const int wm_lm = first ? GEMM_STORE_F32 : GEMM_ACCUM_F32;
+  if (tp_overlap(L)) {
+    RET(tp_sum_begin(ctx, st));
+    RET(gemm_co(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, wm_lm, st));
+    RET(tp_sum_end(ctx, st));
+  } else {
+    RET(gemm(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, wm_lm, st));
+    RET(tp_sum(ctx, st));
+  }
   duty_begin(ctx, 8, st);
   CK(rmsnorm_bwd(T, h, S.x[L.n_local], L.gf, S.rf, L.part, nullptr, S.dlast, L.dgf, L.scratch, st, tp_sum_bf16(L)));
   duty_end(ctx, st);
@@ -1135,6 +1197,12 @@ malleus_status malleus_destroy(malleus_ctx* ctx) {
   for (auto& e : ctx->ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   if (ctx->step_beg) { cudaEventDestroy(ctx->step_beg); cudaEventDestroy(ctx->step_end); }
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->tp_side) {
+    cudaStreamSynchronize(ctx->tp_side);
+    cudaStreamDestroy(ctx->tp_side);
+    cudaEventDestroy(ctx->tp_ev_a);
+    cudaEventDestroy(ctx->tp_ev_b);
+  }
   delete ctx;
   return MALLEUS_OK;
 }
