@@ -262,16 +262,15 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
       s.rgrad = G.take<float>(s.owned_elems);
     }
   }
-  // grad-sync receive staging: one fp32 slot per (owned piece, remote contributing pipeline)
+  // grad-sync receive staging: one fp32 slot per (owned piece, remote contributing pipeline);
+  // standby ranks own nothing, so this sizes to zero for them
   int64_t stage_elems = 0;
-  if (!L.standby || true) {
-    for (TState& s : L.ts)
-      for (const Piece& pc : s.owned)
-        for (size_t i = 0; i < L.plan.pipes.size(); ++i) {
-          if (L.plan.pipes[i].n_micro <= 0) continue;
-          if (sync_holder(cfg, L.plan.pipes[i], s.t, pc.row0) != rank) stage_elems += (pc.e1 - pc.e0 + 3) / 4 * 4;
-        }
-  }
+  for (TState& s : L.ts)
+    for (const Piece& pc : s.owned)
+      for (size_t i = 0; i < L.plan.pipes.size(); ++i) {
+        if (L.plan.pipes[i].n_micro <= 0) continue;
+        if (sync_holder(cfg, L.plan.pipes[i], s.t, pc.row0) != rank) stage_elems += (pc.e1 - pc.e0 + 3) / 4 * 4;
+      }
   L.staging_elems = stage_elems;
   L.staging = G.take<float>(std::max<int64_t>(stage_elems, 1));
 
