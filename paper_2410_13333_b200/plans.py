@@ -72,6 +72,10 @@ def plan_matrix_c1(cfg, B=8, b=2):
     f4 = [3 * F // 8, F // 4, F // 4, F // 8]
     v4 = [3 * V // 8, V // 4, V // 4, V // 8]
     P["P9"] = plan([pipe([stage([0, 1, 2, 3], [H // 4] * 4, f4, v4, [0, L])], m)], b, B)
+    # standby ranks (a removed GPU) on 2 and 4 GPUs: P7's standby and PP-with-TP-change
+    # features without its 8-GPU footprint
+    P["P10"] = plan([pipe([ev([0], [0, L])], m)], b, B, standby=[1])
+    P["P11"] = plan([pipe([ev([0], [0, 1]), s31([1, 2], [1, L])], m)], b, B, standby=[3])
     return P
 
 

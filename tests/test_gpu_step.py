@@ -12,7 +12,8 @@ import torch
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-PLAN_WORLD = {"P0": 1, "P1": 2, "P2": 2, "P3": 2, "P4": 4, "P5": 3, "P6": 3, "P7": 8, "P8": 2, "P9": 4}
+PLAN_WORLD = {"P0": 1, "P1": 2, "P2": 2, "P3": 2, "P4": 4, "P5": 3, "P6": 3, "P7": 8, "P8": 2, "P9": 4,
+              "P10": 2, "P11": 4}
 
 
 def _assert_ok(r):
@@ -63,7 +64,7 @@ def test_multi_gpu_plans_d128(plan, tmp_path):
     _assert_ok(json.load(open(out)))
 
 
-@pytest.mark.parametrize("plan", ["P1", "P2", "P3", "P8", "P5", "P6", "P4", "P9", "P7"])
+@pytest.mark.parametrize("plan", ["P1", "P2", "P3", "P8", "P10", "P5", "P6", "P4", "P9", "P11", "P7"])
 def test_multi_gpu_plans(plan, tmp_path):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")

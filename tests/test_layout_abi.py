@@ -72,7 +72,7 @@ def _check_plan(L, cfg, plan, world, names=None, max_samples=300, seed=0):
                 assert got_own <= set(range(n)) and got_hold <= set(range(n))
 
 
-@pytest.mark.parametrize("pname", ["P0", "P1", "P2", "P3", "P4", "P5", "P6", "P7", "P8", "P9"])
+@pytest.mark.parametrize("pname", ["P0", "P1", "P2", "P3", "P4", "P5", "P6", "P7", "P8", "P9", "P10", "P11"])
 def test_layout_plan_matrix(L, pname):
     cfg = C1_TINY
     p = Pl.plan_matrix_c1(cfg)[pname]

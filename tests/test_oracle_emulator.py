@@ -30,7 +30,7 @@ def _compare(cfg, plan, B, seed=0, steps=1):
         assert _rel(enV[k], nV[k]) <= 1e-12
 
 
-@pytest.mark.parametrize("name", ["P0", "P1", "P2", "P3", "P4", "P5", "P6", "P7", "P8", "P9"])
+@pytest.mark.parametrize("name", ["P0", "P1", "P2", "P3", "P4", "P5", "P6", "P7", "P8", "P9", "P10", "P11"])
 def test_plan_matrix_c1(name):
     cfg = C1_TINY
     _compare(cfg, Pl.plan_matrix_c1(cfg)[name], B=8)
