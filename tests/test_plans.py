@@ -67,3 +67,28 @@ def test_plan_from_rates_valid_and_recovers():
         p = q
     assert [pp["stages"] for pp in p["pipes"]] == [pp["stages"] for pp in even["pipes"]]
     assert [pp["n_micro"] for pp in p["pipes"]] == [8, 8]
+
+
+def test_flops_per_token_matches_survey():
+    """bench.py's algorithmic FLOPs per token (the tokens/s -> TF/s conversion) against SURVEY
+    §8(d)'s per-config values (App. A.3: causal attention at (s+1)/2 keys, LM head included)."""
+    import bench
+    from synth.gen import C3_32B_SLICE, C4_70B_SLICE
+    for cfg, ref in ((C2_7B_SLICE, 5.845e9), (C3_32B_SLICE, 5.526e10), (C4_70B_SLICE, 2.573e10)):
+        assert abs(bench.flops_per_token(cfg) - ref) <= 5e-4 * ref, (cfg, bench.flops_per_token(cfg), ref)
+
+
+@pytest.mark.parametrize("n,rates,want", [
+    (32, [1.0, 1.5], [19, 13]),                  # C2 pipe 0 (SURVEY App. A.5)
+    (32, [1.0, 2.0], [22, 10]),                  # 2-GPU ladder rung
+    (52, [1.0, 1.0, 1.0, 2.0], [15, 15, 15, 7]),  # C3 stage 0
+    (64, [1.0, 1.3, 1.0, 1.0], [17, 13, 17, 17]),  # C4 pipe A
+    (64, [1.0, 1.0, 3.0, 1.0], [20, 20, 4, 20]),   # C4 pipe B under reading R7's tie rule (DESIGN §3)
+])
+def test_minmax_splits_match_survey(n, rates, want):
+    got = Pl._minmax(n, rates)
+    assert got == want
+    # min-max optimality: no split has a smaller max cost (brute force over compositions for 2 members)
+    if len(rates) == 2:
+        best = min(max(a * rates[0], (n - a) * rates[1]) for a in range(1, n))
+        assert max(c * x for c, x in zip(got, rates)) == best
