@@ -760,7 +760,8 @@ static malleus_status tp_sum_begin(malleus_ctx* ctx, cudaStream_t st) {
     CK(cudaEventCreateWithFlags(&ctx->tp_ev_a, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->tp_ev_b, cudaEventDisableTiming));
   }
-  duty_end(ctx, st);
+  // the DUTY segment stays open: the wgrad GEMM that overlaps the reduction is compute of this
+  // segment and is stretched with it (tp_sum_end closes the segment before joining)
   CK(cudaEventRecord(ctx->tp_ev_a, st));
   CK(cudaStreamWaitEvent(ctx->tp_side, ctx->tp_ev_a, 0));
   RET(tp_reduce_peer(ctx, TP_SUM, nullptr, nullptr, [&](Layout& M, TpArgs& a, int j) { a.d0[j] = M.part; },
@@ -769,6 +770,7 @@ static malleus_status tp_sum_begin(malleus_ctx* ctx, cudaStream_t st) {
   return MALLEUS_OK;
 }
 static malleus_status tp_sum_end(malleus_ctx* ctx, cudaStream_t st) {
+  duty_end(ctx, st);
   ev_begin(ctx, st, CAT_TP);  // the exposed part of the reduction
   CK(cudaStreamWaitEvent(st, ctx->tp_ev_b, 0));
   ev_end(ctx, st);
