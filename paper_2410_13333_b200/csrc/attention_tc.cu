@@ -249,7 +249,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         tmem_ld32(cs + c * 32, u);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) sv[c * 32 + j] = __uint_as_float(u[j]) * sl2;
+        for (int j = 0; j < 32; ++j) sv[c * 32 + j] = __uint_as_float(u[j]);  // raw S; scaled in the exp FFMA
       }
       tc_fence_before();
       __syncwarp();
@@ -262,7 +262,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       }
 #pragma unroll
       for (int j = 0; j < TK / 2; ++j) mt = fmaxf(mt, sv[j]);
-      mt = fmaxf(mt, exchange(mt, i & 1));  // full-row max of this tile
+      mt = fmaxf(mt, exchange(mt, i & 1)) * sl2;  // full-row max of this tile, log2 units (sl2 > 0)
       if (warp == 2 && lane == 0) stamp(5, i);
       // tcgen05.ld / st are warp-collective: the rescale decision is warp-uniform (and identical
       // in both warps of the pair: same rows, same maxima); lanes whose max did not grow scale by 1
@@ -292,7 +292,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int e0 = (2 * j) & 7, e1 = (2 * j + 1) & 7;  // position within each group of 8
-        const float x0 = sv[2 * j] - m_used, x1 = sv[2 * j + 1] - m_used;
+        const float x0 = fmaf(sv[2 * j], sl2, -m_used), x1 = fmaf(sv[2 * j + 1], sl2, -m_used);
         const float p0 = ((e0 * NPOLY) % 8 < NPOLY && NPOLY > 0) ? ex2_poly(x0) : ex2(x0);
         const float p1 = ((e1 * NPOLY) % 8 < NPOLY && NPOLY > 0) ? ex2_poly(x1) : ex2(x1);
         l += p0 + p1;
