@@ -89,10 +89,13 @@ typedef struct {
   const int32_t* standby; /* host, [n_standby] */
 } malleus_plan;
 
-/* Device arenas provided by the caller after malleus_plan_requirements.  16-byte aligned.
+/* Device arenas provided by the caller after malleus_plan_requirements.  256-byte aligned
+ * (E_ARG otherwise), each inside a cudaMalloc-backed allocation: plan_apply exports all three to
+ * the other ranks with CUDA IPC (the peers read gradients from grads, store parameters into
+ * state, and the TP reductions read / write partial sums and activations in work over NVLink).
  *   state : bf16 params held + fp32 master/m/v of owned pieces (persistent across steps)
  *   grads : fp32 gradient shards of held tensors (persistent within a step)
- *   work  : activations, saved tensors, staging (scratch)                                 */
+ *   work  : activations, saved tensors, staging, TP reduction buffers and flags (scratch)  */
 typedef struct {
   void* state; size_t state_bytes;
   void* grads; size_t grads_bytes;
