@@ -92,3 +92,37 @@ def test_minmax_splits_match_survey(n, rates, want):
     if len(rates) == 2:
         best = min(max(a * rates[0], (n - a) * rates[1]) for a in range(1, n))
         assert max(c * x for c, x in zip(got, rates)) == best
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_plan_from_rates_random_rates_always_valid(n):
+    """Property: for random probed rates (including extreme stragglers up to 20x), the re-plan keeps
+    every plan invariant (oracle.layout.validate): whole heads >= 1 per member, FFN / vocab splits in
+    multiples of 16 and >= 16, sums exact, sum of micro-batches = B / b."""
+    import numpy as np
+    rng = np.random.default_rng(11 + n)
+    for cfg in (C2_7B_SLICE, C1_TINY):
+        base = Pl.ladder_plan(cfg, n, 16, 1, straggle=False) if cfg is C2_7B_SLICE else None
+        if base is None:
+            if n == 8:
+                continue
+            base = Pl.plan_matrix_c1(cfg, B=8, b=2)["P9" if n == 4 else "P1"]
+        p = base
+        for _ in range(25):
+            rates = {r: float(1.0 + (rng.pareto(1.5) if rng.random() < 0.5 else 0.0)) for r in range(n)}
+            rates = {r: min(x, 20.0) for r, x in rates.items()}
+            p = Pl.plan_from_rates(cfg, p, rates)
+            validate(cfg, p, n)
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_rebalance_random_times_always_valid(n):
+    """Property: plans.rebalance (re-plan from measured per-rank compute times) keeps every plan
+    invariant for random, heavily skewed timings."""
+    import numpy as np
+    rng = np.random.default_rng(23 + n)
+    p = Pl.ladder_plan(C2_7B_SLICE, n, 16, 1, straggle=True)
+    for _ in range(25):
+        t = {r: float(rng.uniform(10.0, 200.0)) for r in range(n)}
+        p = Pl.rebalance(C2_7B_SLICE, p, t)
+        validate(C2_7B_SLICE, p, n)
