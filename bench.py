@@ -33,6 +33,7 @@ import numpy as np  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 STRAGGLER = {1: None, 2: (1, 2.0), 4: (1, 1.5), 8: (3, 2.0)}  # rank, x
+WORKLOAD = "C2: LLaMA-7B-shaped 4-layer slice (h 4096, 32 heads, ffn 11008, V 32000)"
 
 
 def peaks():
@@ -133,10 +134,14 @@ def run_reference(args, cfg):
     v = statistics.median(x["value"] for x in vals)
     cpu = dict(vals[0])
     cpu["value"] = v
+    tokens_per_step = args.batch * cfg.seq_len
     line = {"impl": "reference", "metric": "tokens/s", "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 LLaMA-7B-shaped 4-layer slice, seq 2048, B=16 (oracle sample)"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tokens_per_step / v * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic tokens, random-init weights (seeds 1234/5678)",
+            "config": {"workload": WORKLOAD, "global_batch": args.batch, "seq_len": cfg.seq_len, "micro_batch": 1,
+                       "note": "the CPU fp64 oracle on the host cores, each step a bounded sample of the workload "
+                               "(see cpu_baseline.sample), scaled to whole-step tokens/s"},
             "cpu_baseline": cpu,
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -340,7 +345,7 @@ def main():
         line = {"metric": "tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights (seeds 1234/5678)",
-                "config": {"workload": "C2: LLaMA-7B-shaped 4-layer slice (h 4096, 32 heads, ffn 11008, V 32000)",
+                "config": {"workload": WORKLOAD,
                            "global_batch": B, "seq_len": cfg.seq_len, "micro_batch": 1,
                            "plan": plan_summary(plan), "straggler": (
                                {"rank": straggle[0], "x": straggle[1], "mode": "DUTY"} if straggle else None),
