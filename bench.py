@@ -7,7 +7,7 @@ Workload (config.workload): the LLaMA-7B-shaped 4-layer slice (BASELINE.json con
 32 heads, ffn 11008, vocab 32000, seq 2048, global batch 16 sequences, b = 1), synthetic tokens
 and random-init weights (synth/gen.py, seeds 1234 / 5678).  Plans: SURVEY §8(d) ladder —
 N=1: TP1 (a straggler is degenerate on one GPU, none injected);
-N=2: TP2 with rank 1 slowed 2x (HOG), heads 22/10;
+N=2: TP2 with rank 1 slowed 2x (DUTY: a spin of (x-1) times each compute segment), heads 22/10;
 N=4: the C2 plan, DP2 x TP2, rank 1 slowed 1.5x, heads 19/13, m = (7, 9);
 N=8: DP2 x TP4, rank 3 slowed 2x, m = (7, 9).
 One step = the whole malleable step: embedding, 4 layers fwd+bwd for every micro-batch, LM head +

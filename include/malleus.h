@@ -121,7 +121,7 @@ typedef struct {
 typedef struct {
   uint64_t bytes_sent, bytes_recv; /* this rank, payload bytes of the shard deltas */
   double seconds;                  /* wall, this rank: data movement (keep-copies, pack, NCCL, unpack) */
-  int32_t n_packs;                 /* 4-layer packs */
+  int32_t n_packs;                 /* 4-layer NCCL packs exchanged; 0 on the peer path */
   double total_seconds;            /* wall, this rank, including host planning and comm split */
 } malleus_migrate_stats;
 
@@ -211,9 +211,17 @@ malleus_status malleus_train_step(malleus_ctx* ctx, const int32_t* tokens,
 malleus_status malleus_grad_sync(malleus_ctx* ctx, const malleus_adam_cfg* adam, void* stream);
 
 /* migrate (collective, blocking): move params (to new holders) and fp32 master/m/v (to new
- * owners) from the current plan to new_plan, in packs of 4 consecutive layers, each pack one
- * grouped NCCL send/recv; then new_plan becomes current and new_arenas are
- * used.  The old arenas may be freed by the caller afterwards.  Bit-exact copies. */
+ * owners) from the current plan to new_plan (readings R10/R11); then new_plan
+ * becomes current and new_arenas are used.  The old arenas may be freed by the caller afterwards.
+ * Bit-exact copies.  Two transports, same result:
+ *  - peer path (default when every rank mapped every peer's arenas with CUDA IPC at plan_apply):
+ *    each rank pulls its deltas straight from the sources' old arenas over NVLink in one copy
+ *    kernel together with its keep-copies, between two world barriers (no packing; stats->n_packs
+ *    = 0);
+ *  - NCCL path (MALLEUS_NO_P2P=1 or no peer mapping): per pack of 4 consecutive layers
+ *     the outgoing ranges are packed per peer, exchanged with one grouped NCCL
+ *    send/recv, and unpacked (stats->n_packs = number of packs).
+ * stats may be NULL.  The caller must not run other work on this context concurrently. */
 malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan,
                                const malleus_arenas* new_arenas, malleus_migrate_stats* stats);
 

@@ -546,8 +546,6 @@ static bool make_map_c(CUtensorMap* m, void* ptr, long long N, long long M, long
 }
 
 static int g_num_sms = 0;
-static int g_avail_sms = 0;  // 0 = all SMs; HOG straggler emulation caps the persistent grid
-void set_avail_sms(int n) { g_avail_sms = n; }
 
 static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches += n; }
@@ -598,7 +596,7 @@ static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-  const int sms = (g_avail_sms > 0 && g_avail_sms < g_num_sms) ? g_avail_sms : g_num_sms;
+  const int sms = g_num_sms;
   int grid = tiles < sms ? tiles : sms;
   if (g_prof.on) {
     if (g_prof.used == g_prof.ev.size()) {
@@ -642,7 +640,7 @@ static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const C
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int tiles = ((p.M + 2 * BM2 - 1) / (2 * BM2)) * ((p.N + BN2 - 1) / BN2);
-  const int sms = (g_avail_sms > 0 && g_avail_sms < g_num_sms) ? g_avail_sms : g_num_sms;
+  const int sms = g_num_sms;
   const int clusters = tiles < sms / 2 ? tiles : sms / 2;
   const int grid = 2 * (clusters > 0 ? clusters : 1);
   const bool prof = g_prof.on;

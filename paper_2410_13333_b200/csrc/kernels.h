@@ -161,8 +161,6 @@ cudaError_t copy_ranges(int n, const CopyDesc* d_desc, cudaStream_t st);
 
 // ---- probe / straggler emulation (probe.cu)
 cudaError_t spin_ns(long long ns, cudaStream_t st);
-cudaError_t hog_start(int n_sms, volatile int* stop_flag, cudaStream_t st);
-void set_avail_sms(int n);  // persistent-GEMM grid cap (HOG emulation)
 cudaError_t probe_copy(long long n, const float* src, float* dst, cudaStream_t st);
 
 }  // namespace mls

@@ -39,6 +39,7 @@ std::string validate_plan(const malleus_model_cfg& cfg, const PlanInfo& p, int w
   if (cfg.hidden != cfg.n_heads * cfg.head_dim) return "hidden must equal n_heads * head_dim";
   if (p.b < 1 || p.B < 1 || p.pipes.empty()) return "b >= 1, B >= 1, DP >= 1";
   if (p.pipes.size() > 8) return "DP <= 8";
+  if (world < 1 || world > 16) return "world <= 16 (peer tables hold at most 15 other holders)";
   long long tot = 0;
   for (auto& pp : p.pipes) {
     if (pp.n_micro < 0) return "m_i >= 0";
@@ -56,6 +57,7 @@ std::string validate_plan(const malleus_model_cfg& cfg, const PlanInfo& p, int w
       nxt = st.le;
       const size_t k = st.ranks.size();
       if (k < 1) return "empty stage";
+      if (k > 16) return "TP degree <= 16 (MAX_TP)";
       if (st.heads.size() != k || st.ffn.size() != k || st.vocab.size() != k)
         return "split vectors need one entry per member";
       long long sh = 0, sf = 0, sv = 0;
@@ -86,6 +88,19 @@ std::string validate_plan(const malleus_model_cfg& cfg, const PlanInfo& p, int w
     seen.insert(r);
   }
   if ((int)seen.size() != world) return "every rank of [0, world) must be in exactly one stage or standby";
+  return "";
+}
+
+std::string check_kernel_limits(const malleus_model_cfg& cfg, const PlanInfo& p) {
+  // checked before any rank starts a plan the step cannot run (a kernel would fail mid-step on some
+  // ranks while their peers block in a collective): embedding backward keeps the micro-batch's
+  // token ids in shared memory (T = b*s <= 8192), RMSNorm and the TP reduction keep a row in
+  // registers (h <= 8192, h % 128 for the GEMM tiles), attention has kernels for head_dim 32, 64
+  // and 128 and sequence lengths in multiples of 64
+  if ((long long)p.b * cfg.seq_len > 8192) return "b * seq_len must be <= 8192 (embedding backward)";
+  if (cfg.hidden > 8192 || cfg.hidden % 128) return "hidden must be a multiple of 128 and <= 8192";
+  if (cfg.head_dim != 32 && cfg.head_dim != 64 && cfg.head_dim != 128) return "head_dim must be 32, 64 or 128";
+  if (cfg.seq_len % 64 || cfg.seq_len < 64) return "seq_len must be a multiple of 64";
   return "";
 }
 

@@ -62,6 +62,9 @@ struct Contribution {
 
 PlanInfo plan_from_c(const malleus_plan* p);
 std::string validate_plan(const malleus_model_cfg& cfg, const PlanInfo& p, int world);
+// limits of the sm_100a kernels (checked by plan_requirements / plan_apply / migrate, not by the
+// host-only layout queries)
+std::string check_kernel_limits(const malleus_model_cfg& cfg, const PlanInfo& p);
 
 std::vector<TensorInfo> all_tensors(const malleus_model_cfg& cfg);
 bool tensor_info(const malleus_model_cfg& cfg, int32_t id, TensorInfo* out);

@@ -146,10 +146,8 @@ struct malleus_ctx {
   std::unique_ptr<Layout> L;
   std::string err;
   bool sticky = false;
-  cudaStream_t side = nullptr;  // hog stream
   cudaStream_t tp_side = nullptr;             // backward TP reductions overlapping the wgrad GEMM
   cudaEvent_t tp_ev_a = nullptr, tp_ev_b = nullptr;
-  int* hog_flag = nullptr;      // host-mapped
   float slowdown = 1.f;
   int slow_mode = 0;
   DutyTimer duty[kDutySegs];
@@ -350,7 +348,7 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
 }
 
 // grad-sync op lists and the reduce/Adam piece table (needs bound pointers)
-static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
+static bool build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
   L.gops.clear();
   L.pops.clear();
   L.pieces.clear();
@@ -411,7 +409,10 @@ static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
       for (int hr : holders) {
         if (hr == pc.owner) continue;
         if (L.p2p) {
-          if (rank == pc.owner) pd.push[pd.n_push++] = peer_param(hr, pc.e0);  // NVLink store in the Adam kernel
+          if (rank == pc.owner) {  // NVLink store in the Adam kernel
+            if (pd.n_push >= (int)(sizeof(pd.push) / sizeof(pd.push[0]))) return false;
+            pd.push[pd.n_push++] = peer_param(hr, pc.e0);
+          }
         } else if (rank == pc.owner) {
           L.pops.push_back({s.param + (pc.e0 - s.rows.b * c), (size_t)len, ncclBfloat16, hr, true});
         } else if (rank == hr) {
@@ -440,6 +441,7 @@ static void build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
       }
     }
   }
+  return true;
 }
 
 static malleus_status free_layout(malleus_ctx* ctx, Layout* L) {
@@ -560,6 +562,7 @@ static malleus_status check_plan(malleus_ctx* ctx, const malleus_plan* plan, Pla
   if (!plan) return fail(ctx, MALLEUS_E_ARG, "plan is NULL");
   *out = plan_from_c(plan);
   std::string e = validate_plan(ctx->cfg, *out, ctx->world);
+  if (e.empty()) e = check_kernel_limits(ctx->cfg, *out);
   if (!e.empty()) return fail(ctx, MALLEUS_E_PLAN, e);
   return MALLEUS_OK;
 }
@@ -594,7 +597,8 @@ static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_are
       }
     CK(cudaMemcpy(L.rope_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice));
   }
-  build_sync(ctx->cfg, ctx->rank, L);
+  if (!build_sync(ctx->cfg, ctx->rank, L))
+    return fail(ctx, MALLEUS_E_PLAN, "more than 15 other holders of one piece (world <= 16)");
   // TP communicator: color = global stage index
   int color = NCCL_SPLIT_NOCOLOR, key = 0;
   if (!L.standby) {
@@ -636,13 +640,17 @@ static void ev_end(malleus_ctx* ctx, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ compute pieces
+// debugging aid (MALLEUS_DEBUG_SYNC=1): serialise and trace every GEMM / attention call; read once
+static bool debug_sync() {
+  static const bool on = getenv("MALLEUS_DEBUG_SYNC") != nullptr;
+  return on;
+}
 static malleus_status gemm(malleus_ctx* ctx, int M, int N, int K, const void* A, long long lda, bool amn,
                            const void* B, long long ldb, bool bmn, void* C, long long ldc, int mode,
                            cudaStream_t st) {
   GemmDesc g{M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, mode};
   CK(gemm_bf16(g, st));
-  static const bool dbg = getenv("MALLEUS_DEBUG_SYNC") != nullptr;  // debugging aid: serialize + trace
-  if (dbg) {
+  if (debug_sync()) {
     fprintf(stderr, "[malleus] gemm M=%d N=%d K=%d amn=%d bmn=%d mode=%d ...", M, N, K, amn, bmn, mode);
     CK(cudaStreamSynchronize(st));
     fprintf(stderr, " ok\n");
@@ -713,7 +721,7 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, 
   a.h = ctx->cfg.hidden;
   a.mode = mode;
   a.eps = ctx->cfg.rms_eps;
-  a.epoch = ++L.tp_epoch;
+  a.epoch = L.tp_epoch + 1;  // committed below once the launch was accepted
   a.x = x;
   a.g = g;
   a.part_bf16 = L.tp_bf16 ? 1 : 0;
@@ -734,6 +742,7 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, 
     sel(M, a, j);
   }
   CK(tp_reduce(a, st));
+  L.tp_epoch = a.epoch;
   if (!async) ev_end(ctx, st);
   return MALLEUS_OK;
 }
@@ -848,7 +857,7 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
     if (!rope_done) CK(rope_inplace(T, c.seq_len, L.n_loc, d, Y.qkv, 3LL * nd, 0, c.rope_theta, false, st));
   }
   CK(attention_fwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
-  if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
+  if (debug_sync()) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   RET(part_gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, st));
   if (tp_peer(L)) {  // x1 = x + sum P, a2 = RMSNorm(x1) in one peer-memory kernel
     RET(tp_reduce_peer(ctx, TP_RESID_NORM, S.x[li], P.g2, [&](Layout& M, TpArgs& a, int j) {
@@ -908,7 +917,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, T, nd, h, dx1, h, false, P.wo, h, false, L.dout, nd, GEMM_STORE_BF16, st));
   RET(gemm(ctx, nd, h, T, Y.o, nd, true, dx1, h, true, P.dwo, h, wm, st));
   CK(attention_bwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, L.dqkv, L.dsum, st, L.rope_cs));
-  if (getenv("MALLEUS_DEBUG_SYNC")) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
+  if (debug_sync()) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
     CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
   RET(part_gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, st));
@@ -1181,7 +1190,6 @@ malleus_status malleus_create(const malleus_model_cfg* cfg, int32_t rank, int32_
   ncclUniqueId id;
   memcpy(&id, nccl_uid, 128);
   if (ncclCommInitRank(&ctx->world_comm, world, id, rank) != ncclSuccess) { delete ctx; return MALLEUS_E_NCCL; }
-  cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
   *out = ctx;
   return MALLEUS_OK;
 }
@@ -1191,13 +1199,11 @@ malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode);
 malleus_status malleus_destroy(malleus_ctx* ctx) {
   if (!ctx) return MALLEUS_E_ARG;
   cudaSetDevice(ctx->device);
-  if (ctx->hog_flag) malleus_set_slowdown(ctx, 1.f, 0);
   cudaDeviceSynchronize();
   if (ctx->L) free_layout(ctx, ctx->L.get());
   if (ctx->world_comm) ncclCommDestroy(ctx->world_comm);
   for (auto& e : ctx->ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   if (ctx->step_beg) { cudaEventDestroy(ctx->step_beg); cudaEventDestroy(ctx->step_end); }
-  if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->tp_side) {
     cudaStreamSynchronize(ctx->tp_side);
     cudaStreamDestroy(ctx->tp_side);
@@ -1493,7 +1499,7 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
       stats->bytes_sent = sent;
       stats->bytes_recv = recvd;
       stats->seconds = xfer;
-      stats->n_packs = std::max(1, (ctx->cfg.n_layers + 3) / 4);
+      stats->n_packs = 0;  // peer pull: nothing is packed
       stats->total_seconds = secs;
     }
     return MALLEUS_OK;
@@ -1658,32 +1664,13 @@ malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode) {
   if (!ctx) return MALLEUS_E_ARG;
   cudaSetDevice(ctx->device);
   if (x < 1.f || mode < 0 || mode > 2) return fail(ctx, MALLEUS_E_ARG, "x >= 1, mode in {0,1,2}");
-  // stop a running hog
-  if (ctx->hog_flag) {
-    *(volatile int*)ctx->hog_flag = 1;
-    cudaStreamSynchronize(ctx->side);
-    cudaFreeHost(ctx->hog_flag);
-    ctx->hog_flag = nullptr;
-    set_avail_sms(0);
-  }
   if (mode == 1)
     return fail(ctx, MALLEUS_E_ARG,
-                "HOG mode is disabled: a resident SM-occupying kernel deadlocks any device-wide "
+                "HOG mode is not available: a resident SM-occupying kernel deadlocks any device-wide "
                 "synchronisation (cudaDeviceSynchronize / cudaFree) of the process; use DUTY (2)");
   ctx->slowdown = x;
   ctx->slow_mode = mode;
   for (auto& d : ctx->duty) { d.ms = -1.0; }
-  if (mode == 1 && x > 1.f) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    const int n_hog = std::min(sms - 1, (int)std::lround(sms * (1.0 - 1.0 / x)));
-    CK(cudaHostAlloc((void**)&ctx->hog_flag, sizeof(int), cudaHostAllocMapped));
-    *ctx->hog_flag = 0;
-    int* dflag = nullptr;
-    CK(cudaHostGetDevicePointer((void**)&dflag, ctx->hog_flag, 0));
-    set_avail_sms(sms - n_hog);
-    CK(hog_start(n_hog, dflag, ctx->side));
-  }
   return MALLEUS_OK;
 }
 

@@ -16,7 +16,8 @@
 // reductions of the current plan, identical on every member because they run the same schedule):
 //   ready[j]  = epoch: member j's partial for this epoch is complete (written by CTA 0 of j's
 //               kernel; the partial came from an earlier kernel on j's stream)
-//   ticket    local CTA counter (each CTA fences its stores system-wide, then takes a ticket)
+//   ticket    local CTA counter (each CTA fences its stores system-wide, then takes a ticket; the
+//             last CTA resets it to 0 for the next call)
 //   done[j]   = epoch: every CTA of member j finished pushing its rows (written by j's last CTA);
 //             this member's last CTA waits for done[j] == epoch for all j, so the kernel completes
 //             only when every row of this member's output has landed.
@@ -229,10 +230,13 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
   if (threadIdx.x == 0) {
     __threadfence_system();
     const unsigned long long t = atomicAdd(a.flags[me] + TPF_TICKET, 1ull);
-    last = t + 1 == a.epoch * (unsigned long long)gridDim.x;
+    last = t + 1 == (unsigned long long)gridDim.x;
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
+    // every CTA of this call has taken its ticket: reset the counter for the next call (ordered
+    // before it by the stream), so a call that was rejected or replayed cannot desynchronise it
+    a.flags[me][TPF_TICKET] = 0ull;
     if (tr) tr[2] = now_ns();
     __threadfence_system();
     for (int j = 0; j < k; ++j) st_release_sys(a.flags[j] + TPF_DONE + me, a.epoch);

@@ -209,6 +209,22 @@ def _vocab_split(V, rates, tile=128):
     return _ffn_split(V, rates, tile)
 
 
+def stage_cost(cfg, st, xr, last: bool) -> float:
+    """Per-micro-batch time of a stage in units of algorithmic FLOPs per token at rate 1:
+    max over members of x_k * (layers * (8 h n_k d + 2 s n_k d + 6 h F_k) + [last] 2 h V_k), i.e. the
+    member's QKV/O GEMMs, causal attention, gate/up/down GEMMs and LM-head share (forward; the
+    backward is the same multiple for every term)."""
+    h, d, s = cfg.hidden, cfg.head_dim, cfg.seq_len
+    nl = st["layers"][1] - st["layers"][0]
+    cost = 0.0
+    for k, x in enumerate(xr):
+        w = nl * (8 * h * st["heads"][k] * d + 2 * s * st["heads"][k] * d + 6 * h * st["ffn"][k])
+        if last:
+            w += 2 * h * st["vocab"][k]
+        cost = max(cost, x * w)
+    return cost
+
+
 def plan_from_rates(cfg, plan, rates: dict, deadband: float = 0.05):
     """Re-plan from probed straggling rates x_g (PAPER.md:370-374 profiler -> §4 planner), keeping
     the grouping, stage order and layers: each TP group's heads / FFN tiles / vocab tiles by the
@@ -224,7 +240,7 @@ def plan_from_rates(cfg, plan, rates: dict, deadband: float = 0.05):
     y = []
     for pp in p["pipes"]:
         y_pipe = 0.0
-        for st in pp["stages"]:
+        for j, st in enumerate(pp["stages"]):
             xr = [x[r] for r in st["ranks"]]
             if len(xr) > 1:
                 st["heads"] = _heads_split(H, xr)
@@ -232,9 +248,11 @@ def plan_from_rates(cfg, plan, rates: dict, deadband: float = 0.05):
                 st["ffn"] = _ffn_split(F, xr, tile)
                 tile_v = 128 if V // 128 >= 4 * len(xr) else 16
                 st["vocab"] = _vocab_split(V, xr, tile_v)
-            # stage cost per micro-batch relative to an even, unslowed group (layers x slowest share)
-            share = max(st["heads"][k] / H * xr[k] * len(xr) for k in range(len(xr)))
-            y_pipe += (st["layers"][1] - st["layers"][0]) * share
+            # the pipeline's per-micro-batch cost is its slowest stage, o_i = max_j y_ij * l_ij
+            # (lower problem 547-552); a stage's time is its slowest member's
+            # rate x FLOPs of its shard (head / FFN columns per layer, vocab rows on the last stage)
+            last = j == len(pp["stages"]) - 1
+            y_pipe = max(y_pipe, stage_cost(cfg, st, xr, last))
         y.append(y_pipe)
     total_m = sum(pp["n_micro"] for pp in p["pipes"])
     if len(p["pipes"]) > 1:

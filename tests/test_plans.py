@@ -126,3 +126,22 @@ def test_rebalance_random_times_always_valid(n):
         t = {r: float(rng.uniform(10.0, 200.0)) for r in range(n)}
         p = Pl.rebalance(C2_7B_SLICE, p, t)
         validate(C2_7B_SLICE, p, n)
+
+
+def test_plan_from_rates_mixed_pp_uses_slowest_stage():
+    """a pipeline's per-micro-batch cost is its slowest stage (o_i = max_j y_ij l_ij,
+    PAPER.md:503-506), not the sum of its stages.  A 2-stage 8 + 8-layer pipeline next to a
+    16-layer single-stage pipeline runs a micro-batch in half the time, so at equal rates it must
+    get twice the micro-batches (min-max, Eq.(3))."""
+    from synth.gen import ModelCfg
+    cfg = ModelCfg(n_layers=16, hidden=512, n_heads=4, head_dim=128, ffn=1536, vocab=2048, seq_len=256)
+    ev = lambda ranks, layers: Pl.even_stage(cfg, ranks, layers)
+    # the LM head sits on a last stage in both pipelines; embedding cost is not modelled
+    p = Pl.plan([Pl.pipe([ev([0], [0, 8]), ev([1], [8, 16])], 6), Pl.pipe([ev([2], [0, 16])], 6)], 1, 12)
+    q = Pl.plan_from_rates(cfg, p, {0: 1.0, 1: 1.0, 2: 1.0})
+    validate(cfg, q, 3)
+    assert [pp["n_micro"] for pp in q["pipes"]] == [8, 4]
+    # the stage cost is FLOP-weighted: a 2x straggler that kept an even FFN share costs 2x
+    st = ev([0, 1], [0, 16])
+    c_even = Pl.stage_cost(cfg, st, [1.0, 1.0], False)
+    assert Pl.stage_cost(cfg, st, [1.0, 2.0], False) == pytest.approx(2 * c_even)
