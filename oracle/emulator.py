@@ -179,8 +179,28 @@ def emulate_step(cfg: ModelCfg, P: dict, Mo: dict, Vo: dict, plan: dict, tokens,
             gi = None
         local.append(gi)
         start += n
-    shapes = tensor_shapes(cfg)
     G, nP, nM, nV = {}, {}, {}, {}
+    for name, (full, newp, newm, newv) in _reduce_and_adam(cfg, plan, local, P, Mo, Vo, step, hp).items():
+        G[name] = full
+        nP[name], nM[name], nV[name] = newp, newm, newv
+    return loss, G, nP, nM, nV, local
+
+
+def weighted_reduce(cfg: ModelCfg, plan: dict, local: list) -> dict:
+    """The grad-sync reduction alone (reading R4 / R9): local[i] maps (holder rank,
+    name) -> pipeline i's member-local gradient rows (None for m_i = 0).  Returns the full logical
+    G[name] = sum_i w_i g_i assembled from owned pieces (each element owned exactly once)."""
+    return {n: v[0] for n, v in _reduce_and_adam(cfg, plan, local, None, None, None, 1, None).items()}
+
+
+def _reduce_and_adam(cfg, plan, local, P, Mo, Vo, step, hp):
+    hp = dict(M.ADAM_DEFAULT if hp is None else hp)
+    b, B = plan["micro_batch"], plan["global_batch"]
+    pipes = plan["pipes"]
+    DP = len(pipes)
+    w = [p["n_micro"] * b / B for p in pipes]
+    shapes = tensor_shapes(cfg)
+    out = {}
     for name, shp in shapes.items():
         c = row_width(cfg, name)
         full = np.zeros(int(np.prod(shp)))
@@ -205,6 +225,8 @@ def emulate_step(cfg: ModelCfg, P: dict, Mo: dict, Vo: dict, plan: dict, tokens,
                     acc = acc + w[i] * loc[lo - r0 * c:hi - r0 * c]
                 full[lo:hi] = acc
                 covered[lo:hi] += 1
+                if P is None:
+                    continue
                 wd = hp["weight_decay"] if M.decays(name) else 0.0
                 th = P[name].reshape(-1)[lo:hi]
                 mm = Mo[name].reshape(-1)[lo:hi]
@@ -212,6 +234,5 @@ def emulate_step(cfg: ModelCfg, P: dict, Mo: dict, Vo: dict, plan: dict, tokens,
                 newp[lo:hi], newm[lo:hi], newv[lo:hi] = M.adamw(
                     th, mm, vv, acc, step, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], wd)
         assert np.all(covered == 1), f"{name}: every element must be owned exactly once"
-        G[name] = full.reshape(shp)
-        nP[name], nM[name], nV[name] = (t.reshape(shp) for t in (newp, newm, newv))
-    return loss, G, nP, nM, nV, local
+        out[name] = tuple(t.reshape(shp) for t in (full, newp, newm, newv))
+    return out

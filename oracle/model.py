@@ -122,6 +122,66 @@ def cross_entropy(z, y):
     return lse - zt, p - onehot
 
 
+# ----------------------------------------------------------------------------- one layer
+def _heads(t, n, d):  # [Bn, s, n*d] -> [Bn, n, s, d]
+    Bn, s = t.shape[0], t.shape[1]
+    return t.reshape(Bn, s, n, d).transpose(0, 2, 1, 3)
+
+
+def _unheads(t):  # [Bn, n, s, d] -> [Bn, s, n*d]
+    Bn, n, s, d = t.shape
+    return t.transpose(0, 2, 1, 3).reshape(Bn, s, n * d)
+
+
+def layer_fwd(cfg: ModelCfg, p, x0, phi):
+    """One decoder layer (SURVEY §8(c) algorithm): p(name) -> that layer's tensor; x0 [Bn, s, h].
+    Returns (x_out, saved activations for layer_bwd)."""
+    n, d, eps = cfg.n_heads, cfg.head_dim, cfg.rms_eps
+    a, r1 = rmsnorm_fwd(x0, p("g1"), eps)
+    q = rope_fwd(_heads(a @ p("wq").T, n, d), phi)
+    k = rope_fwd(_heads(a @ p("wk").T, n, d), phi)
+    v = _heads(a @ p("wv").T, n, d)
+    o4, Pm = attention_fwd(q, k, v)
+    o = _unheads(o4)
+    x1 = x0 + o @ p("wo")
+    a2, r2 = rmsnorm_fwd(x1, p("g2"), eps)
+    G = a2 @ p("wg").T
+    U = a2 @ p("wu").T
+    u = swiglu_fwd(G, U)
+    return x1 + u @ p("wd"), (x0, a, r1, q, k, v, o4, Pm, o, x1, a2, r2, G, U, u)
+
+
+def layer_bwd(cfg: ModelCfg, p, saved, dx, phi):
+    """Backward of layer_fwd: dx = gradient of the layer output.  Returns (gradient of the layer
+    input, {tensor: weight gradient}) with the SURVEY §8(c) backward equations."""
+    n, d, h = cfg.n_heads, cfg.head_dim, cfg.hidden
+    x0, a, r1, q, k, v, o4, Pm, o, x1, a2, r2, G, U, u = saved
+    g = {}
+    # MLP
+    du = dx @ p("wd").T
+    g["wd"] = u.reshape(-1, cfg.ffn).T @ dx.reshape(-1, h)
+    dG, dU = swiglu_bwd(G, U, du)
+    g["wg"] = dG.reshape(-1, cfg.ffn).T @ a2.reshape(-1, h)
+    g["wu"] = dU.reshape(-1, cfg.ffn).T @ a2.reshape(-1, h)
+    da2 = dG @ p("wg") + dU @ p("wu")
+    dxn, g["g2"] = rmsnorm_bwd(x1, p("g2"), r2, da2)
+    dx1 = dx + dxn
+    # attention
+    do = dx1 @ p("wo").T
+    g["wo"] = o.reshape(-1, n * d).T @ dx1.reshape(-1, h)
+    dq4, dk4, dv4 = attention_bwd(q, k, v, o4, Pm, _heads(do, n, d))
+    dq = _unheads(rope_bwd(dq4, phi))
+    dk = _unheads(rope_bwd(dk4, phi))
+    dv = _unheads(dv4)
+    a_f = a.reshape(-1, h)
+    g["wq"] = dq.reshape(-1, n * d).T @ a_f
+    g["wk"] = dk.reshape(-1, n * d).T @ a_f
+    g["wv"] = dv.reshape(-1, n * d).T @ a_f
+    da = dq @ p("wq") + dk @ p("wk") + dv @ p("wv")
+    dxn, g["g1"] = rmsnorm_bwd(x0, p("g1"), r1, da)
+    return dx1 + dxn, g
+
+
 # ----------------------------------------------------------------------------- step
 def forward_backward(cfg: ModelCfg, P: dict, tokens: np.ndarray, targets: np.ndarray,
                      n_norm: int | None = None):
@@ -134,30 +194,11 @@ def forward_backward(cfg: ModelCfg, P: dict, tokens: np.ndarray, targets: np.nda
     N = Bn * s if n_norm is None else n_norm
     phi = rope_angles(cfg, s)
 
-    def heads(t):  # [Bn, s, n*d] -> [Bn, n, s, d]
-        return t.reshape(Bn, s, n, d).transpose(0, 2, 1, 3)
-
-    def unheads(t):
-        return t.transpose(0, 2, 1, 3).reshape(Bn, s, n * d)
-
     x = P["E"][tokens]                                      # [Bn, s, h]
     saved = []
     for l in range(cfg.n_layers):
-        p = lambda t: P[f"{l}.{t}"]
-        x0 = x
-        a, r1 = rmsnorm_fwd(x0, p("g1"), eps)
-        q = rope_fwd(heads(a @ p("wq").T), phi)
-        k = rope_fwd(heads(a @ p("wk").T), phi)
-        v = heads(a @ p("wv").T)
-        o4, Pm = attention_fwd(q, k, v)
-        o = unheads(o4)
-        x1 = x0 + o @ p("wo")
-        a2, r2 = rmsnorm_fwd(x1, p("g2"), eps)
-        G = a2 @ p("wg").T
-        U = a2 @ p("wu").T
-        u = swiglu_fwd(G, U)
-        x = x1 + u @ p("wd")
-        saved.append((x0, a, r1, q, k, v, o4, Pm, o, x1, a2, r2, G, U, u))
+        x, sv = layer_fwd(cfg, lambda t, l=l: P[f"{l}.{t}"], x, phi)
+        saved.append(sv)
 
     xf, rf = rmsnorm_fwd(x, P["gf"], eps)
     z = xf @ P["Wlm"].T                                      # [Bn, s, V]
@@ -170,31 +211,8 @@ def forward_backward(cfg: ModelCfg, P: dict, tokens: np.ndarray, targets: np.nda
     dxf = dz @ P["Wlm"]
     dx, g["gf"] = rmsnorm_bwd(x, P["gf"], rf, dxf)
     for l in reversed(range(cfg.n_layers)):
-        p = lambda t: P[f"{l}.{t}"]
-        x0, a, r1, q, k, v, o4, Pm, o, x1, a2, r2, G, U, u = saved[l]
-        # MLP
-        du = dx @ p("wd").T
-        g[f"{l}.wd"] = u.reshape(-1, cfg.ffn).T @ dx.reshape(-1, h)
-        dG, dU = swiglu_bwd(G, U, du)
-        g[f"{l}.wg"] = dG.reshape(-1, cfg.ffn).T @ a2.reshape(-1, h)
-        g[f"{l}.wu"] = dU.reshape(-1, cfg.ffn).T @ a2.reshape(-1, h)
-        da2 = dG @ p("wg") + dU @ p("wu")
-        dxn, g[f"{l}.g2"] = rmsnorm_bwd(x1, p("g2"), r2, da2)
-        dx1 = dx + dxn
-        # attention
-        do = dx1 @ p("wo").T
-        g[f"{l}.wo"] = o.reshape(-1, n * d).T @ dx1.reshape(-1, h)
-        dq4, dk4, dv4 = attention_bwd(q, k, v, o4, Pm, heads(do))
-        dq = unheads(rope_bwd(dq4, phi))
-        dk = unheads(rope_bwd(dk4, phi))
-        dv = unheads(dv4)
-        a_f = a.reshape(-1, h)
-        g[f"{l}.wq"] = dq.reshape(-1, n * d).T @ a_f
-        g[f"{l}.wk"] = dk.reshape(-1, n * d).T @ a_f
-        g[f"{l}.wv"] = dv.reshape(-1, n * d).T @ a_f
-        da = dq @ p("wq") + dk @ p("wk") + dv @ p("wv")
-        dxn, g[f"{l}.g1"] = rmsnorm_bwd(x0, p("g1"), r1, da)
-        dx = dx1 + dxn
+        dx, gl = layer_bwd(cfg, lambda t, l=l: P[f"{l}.{t}"], saved[l], dx, phi)
+        g.update({f"{l}.{t}": v for t, v in gl.items()})
     gE = np.zeros_like(P["E"])
     np.add.at(gE, tokens.reshape(-1), dx.reshape(-1, h))
     g["E"] = gE
