@@ -203,12 +203,19 @@ malleus_status malleus_migration_query(const malleus_model_cfg* cfg, const malle
  * AdamW on owned pieces (if apply_update), bf16 push of the updated pieces to every holder. */
 malleus_status malleus_layer_fwd(malleus_ctx* ctx, int32_t layer, int32_t slot,
                                  const void* x_in, void* x_out, void* stream);
+/* layer_bwd: dy = gradient of the layer output, dx receives the gradient of its input (device bf16
+ * [b*s, h]; dx may alias dy), using the activations layer_fwd saved for (layer, slot).  The layer's
+ * weight gradients are ACCUMULATED (+=) into its fp32 GRAD rows: call malleus_zero_grads first to
+ * start a new accumulation (plan_apply and migrate leave GRAD zeroed; train_step overwrites GRAD
+ * with its first micro-batch).  grad_sync then reduces GRAD as the pipeline's gradient. */
 malleus_status malleus_layer_bwd(malleus_ctx* ctx, int32_t layer, int32_t slot,
                                  const void* dy, void* dx, void* stream);
 malleus_status malleus_train_step(malleus_ctx* ctx, const int32_t* tokens,
                                   const int32_t* targets, float* loss_dev,
                                   const malleus_adam_cfg* adam, void* stream);
 malleus_status malleus_grad_sync(malleus_ctx* ctx, const malleus_adam_cfg* adam, void* stream);
+/* zero_grads (local): GRAD = 0 for every tensor this rank holds (enqueued on stream). */
+malleus_status malleus_zero_grads(malleus_ctx* ctx, void* stream);
 
 /* migrate (collective, blocking): move params (to new holders) and fp32 master/m/v (to new
  * owners) from the current plan to new_plan (readings R10/R11); then new_plan
@@ -314,7 +321,65 @@ malleus_status malleus_k_tp_reduce(int32_t k, int32_t me, int32_t T, int32_t h, 
                                    int32_t part_dtype, float eps, uint64_t epoch, const void* const* part,
                                    uint64_t* const* flags,
                                    void* const* d0, void* const* d1, float* const* d2, const void* x,
-                                   const void* g, void* stream);
+                                   const void* g, const int32_t* row_split, void* stream);
+/* row_split (host, [k + 1] or NULL): member j reduces rows [row_split[j], row_split[j+1]) instead of
+ * the even [j*T/k, (j+1)*T/k); 0 = row_split[0] <= ... <= row_split[k] = T.  The runtime sizes the
+ * shares like the members' column shares (speed-proportional replicated work, SURVEY §7 hard part
+ * (e)).  All members must pass the same split.  Members may live on one device (each on its own
+ * stream, grids small enough to be co-resident: the parity tests do this). */
+
+/* ---------------------------------------------------------------- single-device drivers of the
+ * multi-GPU rows.  They run the same kernels the runtime runs for
+ * these rows, with every "rank's" buffer on one device, so their arithmetic can be checked against
+ * the oracle on a one-GPU box. */
+
+/* One owned ZeRO-1 piece for malleus_k_reduce_adam (the runtime's per-piece descriptor; reading
+ * R9).  All pointers are device pointers; src[i] are the contributing pipelines'
+ * fp32 gradient rows of the piece in pipeline order with weights w[i] = m_i b / B (reading R4,
+ * PAPER.md:523); master/m/v/rgrad the owner's fp32 state of the piece, param the owner's bf16 copy,
+ * push[q] the other holders' bf16 copies (the fused param push, S17).  master, m, v, rgrad, src 16-byte
+ * aligned and len % 4 == 0 select the vector path; anything else runs the scalar path. */
+typedef struct {
+  int64_t len;
+  int32_t n_src;  /* 1..8 */
+  int32_t decay;  /* AdamW weight decay on this tensor (2-D tensors, reading R5) */
+  const float* src[8];
+  float w[8];
+  float *master, *m, *v, *rgrad;
+  uint16_t* param;
+  int32_t n_push; /* 0..15 */
+  uint16_t* push[15];
+} malleus_piece;
+
+/* Fused batch-weighted reduce + AdamW + bf16 cast + push over n pieces (K14 + K9 + S17,
+ * SURVEY §8(a) S15-S17): rgrad = sum_i w_i src_i (fp32, fixed pipeline order), then, if
+ * adam->apply_update, AdamW on (master, m, v) with that gradient and param = push[q] = RNE(master).
+ * adam->max_grad_norm > 0 clips by the norm of these pieces only (the runtime sums it over the
+ * world): norm_coef (device float[2] or NULL) receives (coef, norm).  pieces is a host array, copied
+ * during the call; enqueues on stream. */
+malleus_status malleus_k_reduce_adam(int32_t n, const malleus_piece* pieces, const malleus_adam_cfg* adam,
+                                     float* norm_coef, void* stream);
+
+/* Multi-range byte copy (the migration keep / pull / pack / unpack kernel, K11):
+ * copies[i].bytes bytes from src to dst for every i (device pointers, ranges must not overlap;
+ * bytes % 2 == 0).  copies is a host array, copied during the call. */
+typedef struct {
+  const void* src;
+  void* dst;
+  int64_t bytes;
+} malleus_copy;
+malleus_status malleus_k_copy_ranges(int32_t n, const malleus_copy* copies, void* stream);
+
+/* Vocab-parallel cross entropy of one micro-batch over k LM-head members on one device (SURVEY
+ * §8(a) S11): member j holds logits z[j] (device fp32 [T, V[j]], vocab rows [v0_j, v0_j + V[j]),
+ * v0_j = sum_{i<j} V[i]).  The runtime's kernels run per member: local (max, sum exp, target logit),
+ * the TP combine of max and of (sum, target) — done here by a k-way device kernel in member order
+ * instead of the NCCL all-reduce — then dz[j] = bf16((softmax - onehot) * scale) for the member's
+ * columns (device bf16 [T, V[j]]) and, from member 0, loss_rows (device fp32 [T]) = lse - z_target.
+ * tgt: device int32 [T].  V[j] % 4 == 0. */
+malleus_status malleus_k_vocab_ce(int32_t k, int32_t T, const int32_t* V, const float* const* z,
+                                  const int32_t* tgt, float scale, void* const* dz, float* loss_rows,
+                                  void* stream);
 
 #ifdef __cplusplus
 }

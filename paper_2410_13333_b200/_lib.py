@@ -67,6 +67,16 @@ class AdamCfg(C.Structure):
                 ("step", i32), ("apply_update", i32), ("max_grad_norm", f32)]
 
 
+class Piece(C.Structure):
+    _fields_ = [("len", i64), ("n_src", i32), ("decay", i32), ("src", vp * 8), ("w", f32 * 8),
+                ("master", vp), ("m", vp), ("v", vp), ("rgrad", vp), ("param", vp), ("n_push", i32),
+                ("push", vp * 15)]
+
+
+class Copy(C.Structure):
+    _fields_ = [("src", vp), ("dst", vp), ("bytes", i64)]
+
+
 class MigrateStats(C.Structure):
     _fields_ = [("bytes_sent", C.c_uint64), ("bytes_recv", C.c_uint64), ("seconds", C.c_double),
                 ("n_packs", i32), ("total_seconds", C.c_double)]
@@ -103,7 +113,12 @@ _SIGS = {
     "malleus_k_rmsnorm_bwd": ([i32, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),
     "malleus_k_attention_fwd": ([i32, i32, i32, i32, vp, vp, vp, f32, vp], i32),
     "malleus_k_attention_bwd": ([i32, i32, i32, i32, vp, vp, vp, vp, vp, f32, vp], i32),
-    "malleus_k_tp_reduce": ([i32, i32, i32, i32, i32, i32, f32, C.c_uint64, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+    "malleus_k_tp_reduce": ([i32, i32, i32, i32, i32, i32, f32, C.c_uint64, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+                            i32),
+    "malleus_k_reduce_adam": ([i32, vp, C.POINTER(AdamCfg), vp, vp], i32),
+    "malleus_k_copy_ranges": ([i32, vp, vp], i32),
+    "malleus_k_vocab_ce": ([i32, i32, vp, vp, vp, f32, vp, vp, vp], i32),
+    "malleus_zero_grads": ([vp, vp], i32),
 }
 
 EXPORTED = tuple(_SIGS)

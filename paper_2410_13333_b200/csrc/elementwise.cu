@@ -458,6 +458,17 @@ __global__ void fill_kernel(long long n, float* __restrict__ p, float v) {
     p[i] = v;
 }
 
+struct CombinePtrs {
+  float* p[MAX_TP];
+};
+__global__ void tp_combine_kernel(int k, int n, CombinePtrs b, int op) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float v = b.p[0][i];
+    for (int j = 1; j < k; ++j) v = op == 0 ? fmaxf(v, b.p[j][i]) : v + b.p[j][i];
+    for (int j = 0; j < k; ++j) b.p[j][i] = v;
+  }
+}
+
 inline int grid_for(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   return (int)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
@@ -562,6 +573,14 @@ cudaError_t reduce_loss(int T, const float* rows, float scale, float* out, int a
 
 cudaError_t cast_f32_bf16(long long n, const float* in, void* out, cudaStream_t st) {
   cast_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, in, (__nv_bfloat16*)out); count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t tp_combine_local(int k, int n, float* const* bufs, int op, cudaStream_t st) {
+  if (k < 1 || k > MAX_TP || n < 0) return cudaErrorInvalidValue;
+  CombinePtrs b{};
+  for (int j = 0; j < k; ++j) b.p[j] = bufs[j];
+  tp_combine_kernel<<<grid_for(n, 256), 256, 0, st>>>(k, n, b, op); count_launch();
   return cudaGetLastError();
 }
 

@@ -65,6 +65,9 @@ cudaError_t ce_local_sum(int T, const float* stats, const float* gmax, float* su
 cudaError_t reduce_loss(int T, const float* loss_rows, float scale, float* out, int accumulate,
                         cudaStream_t st);
 cudaError_t cast_f32_bf16(long long n, const float* in, void* out, cudaStream_t st);
+// k-way elementwise combine of k device buffers of n floats (op 0 max, 1 sum in buffer order), the
+// result written back to every buffer: the single-device stand-in of a TP all-reduce (tests)
+cudaError_t tp_combine_local(int k, int n, float* const* bufs, int op, cudaStream_t st);
 cudaError_t fill_f32(long long n, float* p, float v, cudaStream_t st);
 
 // ---- optimizer: fused batch-weighted reduce + AdamW on owned pieces (adam.cu)
@@ -144,12 +147,16 @@ struct TpArgs {
   float* d2[MAX_TP];                     // member j's rstd [T] (TP_RESID_NORM)
   const void* x;                         // local bf16 residual input [T, h] (RESID modes)
   const void* g;                         // local bf16 RMSNorm gain [h] (RESID_NORM)
+  int uneven;                            // rows of member j are [row0[j], row0[j+1]) (else even)
+  int row0[MAX_TP + 1];
   unsigned long long* trace;             // optional: per-call globaltimer stamps (MALLEUS_TP_TRACE)
 };
 constexpr int TP_TRACE_CALLS = 4096;
 unsigned long long* tp_trace_buffer(int member);  // managed [TP_TRACE_CALLS][4] per member, lazily allocated
 cudaError_t tp_reduce(const TpArgs& a, cudaStream_t st);
-int tp_grid(int T, int k);  // CTAs per member: rows spread evenly over <= TP_GRID_MAX CTAs
+int tp_grid(int rows);  // CTAs for one member's rows: spread evenly over <= TP_GRID_MAX CTAs
+// rows [*r0, *r1) reduced by member me (even split, or a.row0 when a.uneven)
+void tp_rows(const TpArgs& a, int me, int* r0, int* r1);
 
 // ---- multi-range copy (copy.cu): migration pack / unpack / keep-copies
 struct CopyDesc {
@@ -157,6 +164,7 @@ struct CopyDesc {
   char* dst;
   long long bytes;  // <= 64 KB per descriptor (host splits longer ranges)
 };
+constexpr long long COPY_CHUNK = 64 * 1024;  // bytes per descriptor (one CTA)
 cudaError_t copy_ranges(int n, const CopyDesc* d_desc, cudaStream_t st);
 
 // ---- probe / straggler emulation (probe.cu)

@@ -113,6 +113,8 @@ struct Layout {
   unsigned long long* tpflags = nullptr;
   unsigned long long tp_epoch = 0;
   bool tp_bf16 = true;   // partials in bf16 (default; MALLEUS_TP_PARTIAL=fp32 for fp32)
+  bool tp_uneven = false; // K15 rows follow the members' column shares (MALLEUS_TP_ROWS=speed)
+  int tp_row0[MAX_TP + 1] = {};
 };
 
 // bump allocator over an arena whose base may be 0 (sizing pass)
@@ -567,6 +569,47 @@ static malleus_status check_plan(malleus_ctx* ctx, const malleus_plan* plan, Pla
   return MALLEUS_OK;
 }
 
+// K15 row shares.  Even by default.  MALLEUS_TP_ROWS=speed sizes member j's rows like its share of
+// the stage's work, w_j = l * (8 h n_j d + 2 s n_j d + 6 h F_j) (+ 2 h V_j on the last stage): a plan
+// made for rates x_j gives w_j ~ 1/x_j, so the replicated per-token work of the reduction, residual
+// and norm follows the member's speed like its columns do (SURVEY §7 hard part (e)).  Rows in units
+// of 32 (largest remainder).  Under DUTY emulation the reduction is communication, not stretched
+// compute, so even rows are the faster choice there.
+static void tp_row_split(const malleus_model_cfg& c, Layout& L) {
+  L.tp_uneven = false;
+  if (L.standby || L.TP <= 1) return;
+  static const bool speed = [] {
+    const char* e = getenv("MALLEUS_TP_ROWS");
+    return e && strcmp(e, "speed") == 0;
+  }();
+  if (!speed) return;
+  const StageInfo& st = L.plan.pipes[L.pipe].stages[L.stage];
+  const int k = L.TP, T = L.T, unit = T % 32 == 0 && T / 32 >= k ? 32 : 1, units = T / unit;
+  std::vector<double> w(k);
+  double tot = 0;
+  for (int j = 0; j < k; ++j) {
+    const double n = st.heads[j], f = st.ffn[j];
+    w[j] = L.n_local * (8.0 * c.hidden * n * c.head_dim + 2.0 * c.seq_len * n * c.head_dim + 6.0 * c.hidden * f) +
+           (L.last ? 2.0 * c.hidden * st.vocab[j] : 0.0);
+    tot += w[j];
+  }
+  std::vector<int> cnt(k);
+  std::vector<std::pair<double, int>> rem;
+  int used = 0;
+  for (int j = 0; j < k; ++j) {
+    const double q = units * w[j] / tot;
+    cnt[j] = (int)q;
+    used += cnt[j];
+    rem.push_back({-(q - cnt[j]), j});
+  }
+  std::sort(rem.begin(), rem.end());
+  for (int i = 0; used < units; ++i, ++used) cnt[rem[i % k].second]++;
+  L.tp_row0[0] = 0;
+  for (int j = 0; j < k; ++j) L.tp_row0[j + 1] = L.tp_row0[j] + cnt[j] * unit;
+  L.tp_row0[k] = T;  // the ragged tail (T % unit) goes to the last member
+  L.tp_uneven = true;
+}
+
 // bind arenas, split communicators, upload the piece table (collective: ncclCommSplit)
 static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_arenas* a) {
   if (!a) return fail(ctx, MALLEUS_E_ARG, "arenas is NULL");
@@ -584,6 +627,7 @@ static malleus_status bind_layout(malleus_ctx* ctx, Layout& L, const malleus_are
     const char* e = getenv("MALLEUS_TP_PARTIAL");
     L.tp_bf16 = !(e && strcmp(e, "fp32") == 0);
   }
+  tp_row_split(ctx->cfg, L);
   if (L.tpflags) CK(cudaMemset(L.tpflags, 0, TPF_WORDS * sizeof(unsigned long long)));
   CK(cudaDeviceSynchronize());
   RET(map_peers(ctx, L, a));
@@ -698,7 +742,7 @@ static bool tp_sum_bf16(const Layout& L) { return tp_peer(L) && L.tp_bf16; }
 static bool tp_scatter(const Layout& L) {
   static const bool off = getenv("MALLEUS_TP_NO_SCATTER") != nullptr;
   static const int kmax = getenv("MALLEUS_TP_SCATTER_K") ? atoi(getenv("MALLEUS_TP_SCATTER_K")) : 2;
-  return !off && tp_peer(L) && L.tp_bf16 && L.TP <= std::min(kmax, 4) && L.T % L.TP == 0 &&
+  return !off && tp_peer(L) && L.tp_bf16 && !L.tp_uneven && L.TP <= std::min(kmax, 4) && L.T % L.TP == 0 &&
          (L.T / L.TP) % 32 == 0;
 }
 static Layout& member_layout(Layout& L, int j) {
@@ -726,6 +770,8 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, 
   a.g = g;
   a.part_bf16 = L.tp_bf16 ? 1 : 0;
   a.sum_bf16 = L.tp_bf16 ? 1 : 0;  // bf16 partials => the backward sums go out in bf16 too
+  a.uneven = L.tp_uneven ? 1 : 0;
+  for (int j = 0; j <= L.TP; ++j) a.row0[j] = L.tp_row0[j];
   static const bool trace = getenv("MALLEUS_TP_TRACE") != nullptr;  // debugging aid (tools/tp_step_trace.py)
   if (trace) a.trace = tp_trace_buffer(0);
   const int buf = (int)(a.epoch & 1);
@@ -1363,6 +1409,14 @@ malleus_status malleus_grad_sync(malleus_ctx* ctx, const malleus_adam_cfg* adam,
   return grad_sync_impl(ctx, adam, (cudaStream_t)stream);
 }
 
+malleus_status malleus_zero_grads(malleus_ctx* ctx, void* stream) {
+  GUARD();
+  NEED_PLAN();
+  for (TState& s : ctx->L->ts)
+    if (s.held) CK(cudaMemsetAsync(s.grad, 0, (s.rows.e - s.rows.b) * s.t.cols * 4, (cudaStream_t)stream));
+  return MALLEUS_OK;
+}
+
 malleus_status malleus_last_step_timing(malleus_ctx* ctx, float out[5]) {
   GUARD();
   if (!out) return MALLEUS_E_ARG;
@@ -1426,7 +1480,7 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
   };
   cudaStream_t st = 0;
   uint64_t sent = 0, recvd = 0;
-  constexpr long long CHUNK = 64 * 1024;
+  constexpr long long CHUNK = COPY_CHUNK;
   auto add_copy = [&](std::vector<CopyDesc>& v, const char* s, char* d, long long bytes) {
     for (long long o = 0; o < bytes; o += CHUNK) v.push_back({s + o, d + o, std::min(CHUNK, bytes - o)});
   };

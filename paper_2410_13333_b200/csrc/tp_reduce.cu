@@ -2,7 +2,8 @@
 // "TP reduce + residual + norm"; PAPER.md:262 row-parallel layers).  One kernel per reduction, no
 // NCCL: reduce-scatter + all-gather through peer loads / stores.
 //
-// Member m of a TP group of k owns rows [m*T/k, (m+1)*T/k).  For each of its rows it reads the k
+// Member m of a TP group of k owns rows [m*T/k, (m+1)*T/k), or an uneven range sized like its
+// column share (TpArgs::row0) so that the replicated per-token work follows the member's speed.  For each of its rows it reads the k
 // fp32 partial rows (its own and the k-1 peers', in member order 0..k-1, so every row is summed in
 // one fixed order) and pushes the finished row to every member:
 //   TP_SUM        out = sum_j P_j                          (fp32 or bf16; backward input gradients)
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
     if (tr && blockIdx.x == 0) tr[1] = now_ns();
   }
   __syncthreads();
-  const int r0 = (int)((long long)me * a.T / k), r1 = (int)((long long)(me + 1) * a.T / k);
+  const int r0 = a.uneven ? a.row0[me] : (int)((long long)me * a.T / k);
+  const int r1 = a.uneven ? a.row0[me + 1] : (int)((long long)(me + 1) * a.T / k);
   for (int row = r0 + blockIdx.x; row < r1; row += gridDim.x) {
     const long long rb = (long long)row * h;
     float4 acc[V][2];
@@ -257,18 +259,29 @@ unsigned long long* tp_trace_buffer(int member) {
   return buf ? buf + (size_t)member * TP_TRACE_CALLS * 4 : nullptr;
 }
 
-int tp_grid(int T, int k) {
-  const int rows = (T + k - 1) / k;
+int tp_grid(int rows) {
   const int waves = (rows + TP_GRID_MAX - 1) / TP_GRID_MAX;
-  return std::max(1, (rows + waves - 1) / waves);
+  return std::max(1, waves > 0 ? (rows + waves - 1) / waves : 1);
+}
+
+void tp_rows(const TpArgs& a, int me, int* r0, int* r1) {
+  *r0 = a.uneven ? a.row0[me] : (int)((long long)me * a.T / a.k);
+  *r1 = a.uneven ? a.row0[me + 1] : (int)((long long)(me + 1) * a.T / a.k);
 }
 
 cudaError_t tp_reduce(const TpArgs& a, cudaStream_t st) {
   if (a.k < 2 || a.k > MAX_TP || a.me < 0 || a.me >= a.k || a.h % 8 || a.h > 8 * TPR_MAXV * TPR_THREADS ||
       a.T <= 0 || a.epoch == 0)
     return cudaErrorInvalidValue;
+  if (a.uneven) {
+    if (a.row0[0] != 0 || a.row0[a.k] != a.T) return cudaErrorInvalidValue;
+    for (int j = 0; j < a.k; ++j)
+      if (a.row0[j + 1] < a.row0[j]) return cudaErrorInvalidValue;
+  }
   const int vpt = (a.h / 8 + TPR_THREADS - 1) / TPR_THREADS;
-  const int grid = tp_grid(a.T, a.k);
+  int r0, r1;
+  tp_rows(a, a.me, &r0, &r1);
+  const int grid = tp_grid(r1 - r0);
   auto launch_kv = [&](auto mode_c, auto k_c) {
     constexpr int M = decltype(mode_c)::value, K = decltype(k_c)::value;
     if (a.part_bf16) {

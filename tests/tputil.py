@@ -29,26 +29,33 @@ def _ptrs(ts):
 
 
 class Group:
-    """k members, member j on cuda:j: double-buffered partials, flag blocks, destinations."""
+    """k members: double-buffered partials, flag blocks, destinations.  devices[j] is member j's GPU
+    (default cuda:j, one member per GPU, peer access enabled); members sharing one GPU each run on
+    their own stream (their grids must be small enough to be co-resident).  rows: optional uneven
+    row split [k + 1] (row_split of malleus_k_tp_reduce)."""
 
-    def __init__(self, k: int, T: int, h: int, part_dtype=torch.float32, sum_bf16: bool = False):
+    def __init__(self, k: int, T: int, h: int, part_dtype=torch.float32, sum_bf16: bool = False,
+                 devices=None, rows=None):
         self.k, self.T, self.h = k, T, h
         # part_dtype bit 0: bf16 partials, bit 1: bf16 SUM output
         self.pdt = (1 if part_dtype == torch.bfloat16 else 0) | (2 if sum_bf16 else 0)
-        dev = [torch.device("cuda", j) for j in range(k)]
+        self.devices = list(range(k)) if devices is None else list(devices)
+        dev = [torch.device("cuda", j) for j in self.devices]
         self.part = [[torch.zeros(T, h, device=d, dtype=part_dtype) for d in dev] for _ in range(2)]
         self.flags = [torch.zeros(TPF_WORDS, dtype=torch.int64, device=d) for d in dev]
         self.out32 = [torch.zeros(T, h, device=d, dtype=torch.bfloat16 if sum_bf16 else torch.float32) for d in dev]
         self.x1 = [torch.zeros(T, h, dtype=torch.bfloat16, device=d) for d in dev]
         self.a = [torch.zeros(T, h, dtype=torch.bfloat16, device=d) for d in dev]
         self.rstd = [torch.zeros(T, device=d) for d in dev]
+        self.streams = [torch.cuda.Stream(device=d) for d in dev]
+        self.rows = (C.c_int32 * (k + 1))(*rows) if rows is not None else None
         self.epoch = 0
-        for d in dev:
+        for d in set(self.devices):
             torch.cuda.synchronize(d)
 
     def launch(self, mode: int, x=None, g=None, eps: float = 1e-5) -> None:
         """One reduction of the partials in buffer (epoch + 1) & 1; all members launched
-        asynchronously on their devices' current streams."""
+        asynchronously, each on its own stream (after the device's current stream)."""
         self.epoch += 1
         buf = self.epoch & 1
         parts = _ptrs(self.part[buf])
@@ -60,16 +67,19 @@ class Group:
         else:
             d0, d1, d2 = _ptrs(self.x1), None, None
         for j in range(self.k):
-            with torch.cuda.device(j):
-                st = torch.cuda.current_stream().cuda_stream
+            dj = self.devices[j]
+            with torch.cuda.device(dj):
+                self.streams[j].wait_stream(torch.cuda.current_stream(dj))
+                st = self.streams[j].cuda_stream
                 r = L.lib.malleus_k_tp_reduce(self.k, j, self.T, self.h, mode, self.pdt, eps, self.epoch,
                                               C.cast(parts, C.c_void_p), C.cast(flags, C.c_void_p),
                                               C.cast(d0, C.c_void_p), C.cast(d1, C.c_void_p) if d1 else None,
                                               C.cast(d2, C.c_void_p) if d2 else None,
                                               x[j].data_ptr() if x is not None else None,
-                                              g[j].data_ptr() if g is not None else None, st)
+                                              g[j].data_ptr() if g is not None else None,
+                                              C.cast(self.rows, C.c_void_p) if self.rows is not None else None, st)
                 assert r == 0, r
 
     def sync(self) -> None:
-        for j in range(self.k):
-            torch.cuda.synchronize(j)
+        for d in set(self.devices):
+            torch.cuda.synchronize(d)
