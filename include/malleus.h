@@ -48,10 +48,18 @@ typedef enum {
  * RMSNorm eps, RoPE half-split with theta (readings R2/R3), SwiGLU FFN, untied embedding and
  * LM head.  Logical tensors are stored split-axis-outermost with hidden innermost (reading R9):
  * Wq, Wk, Wv, WoT [n*d, h]; Wg, Wu, WdT [ffn, h]; E, Wlm [vocab, h]; norm gains [h]. */
+/* Arithmetic of the step (reading R6).  BF16: bf16 params and activations, fp32 accumulation,
+ * statistics, gradients and optimizer state; tcgen05 tensor-core GEMMs and attention.  FP32: the
+ * parity mode of the north star ("<= 1e-4 in fp32 mode"): fp32 params and activations everywhere,
+ * SIMT fp32 GEMMs and attention with plain FFMA (no TF32, no tensor cores), the TP reductions over
+ * NCCL; for correctness checks, not for speed.  In FP32 mode the PARAM kind is fp32 (== MASTER). */
+typedef enum { MALLEUS_BF16 = 0, MALLEUS_FP32 = 1 } malleus_dtype;
+
 typedef struct {
   int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab, seq_len;
   float rms_eps;    /* 1e-5 */
   float rope_theta; /* 1e4 */
+  int32_t dtype;    /* malleus_dtype */
 } malleus_model_cfg;
 
 /* One pipeline stage = one TP group.  Per-member split vectors are the
@@ -134,7 +142,7 @@ typedef struct malleus_ctx malleus_ctx;
 #define MALLEUS_T_LM_HEAD 0x7FFF0002
 enum { MALLEUS_KIND_PARAM = 0, MALLEUS_KIND_GRAD = 1, MALLEUS_KIND_MASTER = 2,
        MALLEUS_KIND_ADAM_M = 3, MALLEUS_KIND_ADAM_V = 4, MALLEUS_KIND_RGRAD = 5 };
-/* PARAM: bf16 held rows; GRAD: fp32 local (pipeline-mean) gradient of held rows;
+/* PARAM: bf16 held rows (fp32 in FP32 mode); GRAD: fp32 local (pipeline-mean) gradient of held rows;
  * MASTER/ADAM_M/ADAM_V: fp32 owned pieces; RGRAD: fp32 reduced gradient of owned pieces
  * (sum_i w_i g_i, written by malleus_grad_sync). */
 
@@ -160,7 +168,7 @@ malleus_status malleus_plan_apply(malleus_ctx* ctx, const malleus_plan* plan,
                                   const malleus_arenas* arenas);
 
 /* write_tensor (local, blocking): host_full is the whole logical tensor (PARAM: bf16 bits
- * uint16[numel]; MASTER/ADAM_M/ADAM_V: float[numel]); the rank stores its held rows / owned
+ * uint16[numel], float[numel] in FP32 mode; MASTER/ADAM_M/ADAM_V: float[numel]); the rank stores its held rows / owned
  * pieces.  Writing PARAM also initialises MASTER = param and zeroes m, v of owned pieces.
  * read_local (local, blocking): copies this rank's elements of (tensor, kind) to host_dst as a
  * concatenation of flat element ranges [ranges[2i], ranges[2i+1]) of the logical tensor.

@@ -35,7 +35,7 @@ STATUS = {0: "OK", 1: "E_ARG", 2: "E_PLAN", 3: "E_CUDA", 4: "E_NCCL", 5: "E_NOME
 class ModelCfg(C.Structure):
     _fields_ = [("n_layers", i32), ("hidden", i32), ("n_heads", i32), ("n_kv_heads", i32),
                 ("head_dim", i32), ("ffn", i32), ("vocab", i32), ("seq_len", i32),
-                ("rms_eps", f32), ("rope_theta", f32)]
+                ("rms_eps", f32), ("rope_theta", f32), ("dtype", i32)]
 
 
 class Stage(C.Structure):
@@ -139,9 +139,12 @@ def check(status: int, ctx=None, what: str = ""):
         raise MalleusError(f"{what}: {STATUS.get(status, status)}: {msg}")
 
 
-def make_cfg(cfg) -> ModelCfg:
+DTYPES = {"bf16": 0, "fp32": 1}
+
+
+def make_cfg(cfg, dtype: str = "bf16") -> ModelCfg:
     return ModelCfg(cfg.n_layers, cfg.hidden, cfg.n_heads, cfg.n_heads, cfg.head_dim, cfg.ffn,
-                    cfg.vocab, cfg.seq_len, cfg.rms_eps, cfg.rope_theta)
+                    cfg.vocab, cfg.seq_len, cfg.rms_eps, cfg.rope_theta, DTYPES[dtype])
 
 
 class PlanStruct:

@@ -62,6 +62,11 @@ __global__ void __launch_bounds__(256) reduce_adam_kernel(const ChunkDesc* __res
         *reinterpret_cast<float4*>(pd.master + i) = th;
         *reinterpret_cast<float4*>(pd.m + i) = m;
         *reinterpret_cast<float4*>(pd.v + i) = v;
+        if (pd.param_f32) {  // FP32 parity mode: the param copies are the fp32 master itself
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(pd.param) + i) = th;
+          for (int q = 0; q < pd.n_push; ++q) *reinterpret_cast<float4*>(reinterpret_cast<float*>(pd.push[q]) + i) = th;
+          continue;
+        }
         __nv_bfloat162 lo = __floats2bfloat162_rn(th.x, th.y), hi = __floats2bfloat162_rn(th.z, th.w);
         uint2 pk;
         pk.x = *reinterpret_cast<uint32_t*>(&lo);
@@ -84,6 +89,11 @@ __global__ void __launch_bounds__(256) reduce_adam_kernel(const ChunkDesc* __res
       pd.m[i] = m;
       pd.v[i] = v;
       pd.master[i] = th;
+      if (pd.param_f32) {
+        reinterpret_cast<float*>(pd.param)[i] = th;
+        for (int q = 0; q < pd.n_push; ++q) reinterpret_cast<float*>(pd.push[q])[i] = th;
+        continue;
+      }
       __nv_bfloat16 b = __float2bfloat16_rn(th);
       pd.param[i] = *reinterpret_cast<uint16_t*>(&b);
       for (int q = 0; q < pd.n_push; ++q) pd.push[q][i] = *reinterpret_cast<uint16_t*>(&b);

@@ -403,25 +403,35 @@ ce_stats_kernel(int V, const float* __restrict__ z, const int32_t* __restrict__ 
   }
 }
 
-// dz = (softmax - onehot) * scale (bf16), float4 in / 4 x bf16 out per thread step
+// dz = (softmax - onehot) * scale (bf16, or fp32 in the FP32 parity mode), float4 in per thread step
+template <bool F32>
 __global__ void ce_grad_kernel(int V, const float* __restrict__ z, const int32_t* __restrict__ tgt, int v0,
                                const float* __restrict__ gmax, const float* __restrict__ gsum,
-                               const float* __restrict__ gtgt, float scale, __nv_bfloat16* __restrict__ dz,
+                               const float* __restrict__ gtgt, float scale, void* __restrict__ dzv,
                                float* __restrict__ loss_rows) {
   const int t = blockIdx.x;
   const float lse = gmax[t] + logf(gsum[t]);
   if (threadIdx.x == 0 && loss_rows) loss_rows[t] = lse - gtgt[t];
   const float4* z4 = reinterpret_cast<const float4*>(z + (long long)t * V);
-  uint2* d4 = reinterpret_cast<uint2*>(dz + (long long)t * V);
   const int y = tgt[t] - v0;
   for (int c = threadIdx.x; c < V / 4; c += blockDim.x) {
     const float4 v = z4[c];
-    float p[4] = {__expf(v.x - lse), __expf(v.y - lse), __expf(v.z - lse), __expf(v.w - lse)};
+    float p[4];
+    if (F32) {
+      p[0] = expf(v.x - lse); p[1] = expf(v.y - lse); p[2] = expf(v.z - lse); p[3] = expf(v.w - lse);
+    } else {
+      p[0] = __expf(v.x - lse); p[1] = __expf(v.y - lse); p[2] = __expf(v.z - lse); p[3] = __expf(v.w - lse);
+    }
     if ((y >> 2) == c) p[y & 3] -= 1.f;
-    uint2 o;
-    o.x = pack2_bf16(p[0] * scale, p[1] * scale);
-    o.y = pack2_bf16(p[2] * scale, p[3] * scale);
-    d4[c] = o;
+    if (F32) {
+      reinterpret_cast<float4*>(static_cast<float*>(dzv) + (long long)t * V)[c] =
+          make_float4(p[0] * scale, p[1] * scale, p[2] * scale, p[3] * scale);
+    } else {
+      uint2 o;
+      o.x = pack2_bf16(p[0] * scale, p[1] * scale);
+      o.y = pack2_bf16(p[2] * scale, p[3] * scale);
+      reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(dzv) + (long long)t * V)[c] = o;
+    }
   }
 }
 
@@ -560,9 +570,11 @@ cudaError_t ce_local_sum(int T, const float* stats, const float* gmax, float* su
 }
 
 cudaError_t ce_grad(int T, int V, const float* z, const int32_t* tgt, int v0, const float* gmax, const float* gsum,
-                    const float* gtgt, float scale, void* dz, float* loss_rows, cudaStream_t st) {
+                    const float* gtgt, float scale, void* dz, float* loss_rows, cudaStream_t st, bool dz_f32) {
   if (V % 4) return cudaErrorInvalidValue;
-  ce_grad_kernel<<<T, 256, 0, st>>>(V, z, tgt, v0, gmax, gsum, gtgt, scale, (__nv_bfloat16*)dz, loss_rows); count_launch();
+  if (dz_f32) ce_grad_kernel<true><<<T, 256, 0, st>>>(V, z, tgt, v0, gmax, gsum, gtgt, scale, dz, loss_rows);
+  else ce_grad_kernel<false><<<T, 256, 0, st>>>(V, z, tgt, v0, gmax, gsum, gtgt, scale, dz, loss_rows);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -663,6 +663,7 @@ static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const C
 }
 
 cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
+  if (g.f32) return gemm_f32(g, st);
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
   cudaError_t e = get_encoder();
   if (e != cudaSuccess) return e;

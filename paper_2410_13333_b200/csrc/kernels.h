@@ -34,8 +34,27 @@ struct GemmDesc {
   // leave shared memory on every SM for a kernel running concurrently on another stream (the
   // backward TP reduction overlapping the weight-gradient GEMM): 5-stage instead of 6-stage ring
   bool co_resident = false;
+  // FP32 parity mode: A, B, C fp32 (GEMM_STORE_BF16 then stores the fp32 activation), SIMT kernel
+  bool f32 = false;
 };
-cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st);
+cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st);  // dispatches to gemm_f32 when g.f32
+
+// ---- FP32 parity mode (fp32.cu): IEEE fp32 activations, plain FFMA (no TF32), deterministic
+cudaError_t gemm_f32(const GemmDesc& g, cudaStream_t st);
+cudaError_t rmsnorm_fwd_f32(int T, int h, const float* x, const float* partial, float* x_out, const float* g,
+                            float eps, float* y, float* rstd, cudaStream_t st);
+cudaError_t rmsnorm_bwd_f32(int T, int h, const float* x, const float* g, const float* rstd, const float* dy,
+                            const float* dres, float* dx_out, float* dg_accum, cudaStream_t st);
+cudaError_t residual_add_f32(long long n, const float* x, const float* p, float* out, cudaStream_t st);
+cudaError_t rope_f32(int T, int s, int n, int d, float* buf, long long ld, int col0, float theta, bool inverse,
+                     cudaStream_t st);
+cudaError_t swiglu_fwd_f32(int T, int F, const float* gu, float* u, cudaStream_t st);
+cudaError_t swiglu_bwd_f32(int T, int F, const float* gu, const float* du, float* dgu, cudaStream_t st);
+cudaError_t embed_fwd_f32(int T, int h, const int32_t* tok, const float* E, float* x, cudaStream_t st);
+cudaError_t embed_bwd_f32(int T, int h, const int32_t* tok, const float* dx, float* dE, cudaStream_t st);
+cudaError_t attention_fwd_f32(int nb, int s, int n, int d, const float* qkv, float* o, float* lse, cudaStream_t st);
+cudaError_t attention_bwd_f32(int nb, int s, int n, int d, const float* qkv, const float* o, const float* lse,
+                              const float* dout, float* dqkv, float* dsum, cudaStream_t st);
 
 // ---- elementwise / normalisation (elementwise.cu)
 cudaError_t rmsnorm_fwd(int T, int h, const void* x, const float* partial, void* x_out,
@@ -58,7 +77,7 @@ cudaError_t ce_stats(int T, int V, const float* z, const int32_t* tgt, int v0, f
 // step 2 (after TP reduction of stats): loss rows and dz = (softmax - onehot) * scale (bf16)
 cudaError_t ce_grad(int T, int V, const float* z, const int32_t* tgt, int v0, const float* gmax,
                     const float* gsum, const float* gtgt, float scale, void* dz, float* loss_rows,
-                    cudaStream_t st);
+                    cudaStream_t st, bool dz_f32 = false);
 cudaError_t ce_combine_max(int T, const float* stats, float* gmax, cudaStream_t st);
 cudaError_t ce_local_sum(int T, const float* stats, const float* gmax, float* sum_tgt,
                          cudaStream_t st);
@@ -79,7 +98,7 @@ struct PieceDesc {
   int n_src;
   int decay;                 // apply weight decay (2-D tensors)
   int vec;                   // all pointers 16-byte aligned (param 8-byte), len % 4 == 0
-  int pad_;
+  int param_f32;             // FP32 parity mode: param / push copies are fp32 (= master)
   float* master;
   float* m;
   float* v;

@@ -114,6 +114,10 @@ struct Layout {
   unsigned long long tp_epoch = 0;
   bool tp_bf16 = true;   // partials in bf16 (default; MALLEUS_TP_PARTIAL=fp32 for fp32)
   bool tp_uneven = false; // K15 rows follow the members' column shares (MALLEUS_TP_ROWS=speed)
+  // FP32 parity mode (malleus_model_cfg.dtype == MALLEUS_FP32): params and activations fp32,
+  // SIMT fp32 kernels (fp32.cu); aes = bytes per param / activation element (2 bf16, 4 fp32)
+  bool f32 = false;
+  int aes = 2;
   int tp_row0[MAX_TP + 1] = {};
 };
 
@@ -196,6 +200,8 @@ static malleus_status fail(malleus_ctx* ctx, malleus_status s, const std::string
 // ------------------------------------------------------------------ layout construction
 static void build_shape(const malleus_model_cfg& cfg, const PlanInfo& p, int rank, Layout& L) {
   L.plan = p;
+  L.f32 = cfg.dtype == MALLEUS_FP32;
+  L.aes = L.f32 ? 4 : 2;
   locate(p, rank, &L.pipe, &L.stage, &L.member);
   L.standby = L.pipe < 0;
   L.T = p.b * cfg.seq_len;
@@ -241,7 +247,8 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
     const bool group_start = s.t.layer < 0 || s.t.idx == LT_G1;
     const int64_t n = (s.rows.e - s.rows.b) * s.t.cols;
     const size_t al = group_start ? 256 : 16;
-    s.param = S.take<uint16_t>((size_t)((n + 7) / 8 * 8), al);
+    s.param = L.f32 ? reinterpret_cast<uint16_t*>(S.take<float>((size_t)((n + 3) / 4 * 4), al))
+                    : S.take<uint16_t>((size_t)((n + 7) / 8 * 8), al);
     s.grad = G.take<float>((size_t)((n + 3) / 4 * 4), al);
   }
   // owned pieces: master, m, v in state; rgrad in grads
@@ -294,26 +301,28 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
     }
     // activations
     const int64_t T = L.T, nd = (int64_t)L.n_loc * d, F = L.F_loc;
+    // activation buffers: bf16, or fp32 in the parity mode
+    auto act = [&](int64_t n) { return L.f32 ? reinterpret_cast<uint16_t*>(W.take<float>(n)) : W.take<uint16_t>(n); };
     L.slot.assign(L.slots, Slot{});
     for (Slot& sl : L.slot) {
       sl.x.resize(L.n_local + 1);
-      for (auto& x : sl.x) x = W.take<uint16_t>(T * h);
+      for (auto& x : sl.x) x = act(T * h);
       sl.L.resize(L.n_local);
       for (SlotLayer& y : sl.L) {
-        y.a1 = W.take<uint16_t>(T * h);
-        y.qkv = W.take<uint16_t>(T * 3 * nd);
-        y.o = W.take<uint16_t>(T * nd);
-        y.x1 = W.take<uint16_t>(T * h);
-        y.a2 = W.take<uint16_t>(T * h);
-        y.gu = W.take<uint16_t>(T * 2 * F);
-        y.u = W.take<uint16_t>(T * F);
+        y.a1 = act(T * h);
+        y.qkv = act(T * 3 * nd);
+        y.o = act(T * nd);
+        y.x1 = act(T * h);
+        y.a2 = act(T * h);
+        y.gu = act(T * 2 * F);
+        y.u = act(T * F);
         y.r1 = W.take<float>(T);
         y.r2 = W.take<float>(T);
         y.lse = W.take<float>(T * L.n_loc);
       }
       if (L.last) {
-        sl.xf = W.take<uint16_t>(T * h);
-        sl.dlast = W.take<uint16_t>(T * h);
+        sl.xf = act(T * h);
+        sl.dlast = act(T * h);
         sl.rf = W.take<float>(T);
       }
     }
@@ -325,18 +334,18 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
     }
     L.scratch = W.take<float>(rmsnorm_bwd_scratch_floats((int)T, (int)h));
     L.dsum = W.take<float>(T * L.n_loc);
-    if (cfg.head_dim == 128) L.rope_cs = W.take<float2>((size_t)cfg.seq_len * 64);
-    L.dxa = W.take<uint16_t>(T * h);
-    L.dxb = W.take<uint16_t>(T * h);
-    L.dxc = W.take<uint16_t>(T * h);
-    L.dyrecv = W.take<uint16_t>(T * h);
-    L.dqkv = W.take<uint16_t>(T * 3 * nd);
-    L.dout = W.take<uint16_t>(T * nd);
-    L.dgu = W.take<uint16_t>(T * 2 * F);
-    L.du = W.take<uint16_t>(T * F);
+    if (cfg.head_dim == 128 && !L.f32) L.rope_cs = W.take<float2>((size_t)cfg.seq_len * 64);
+    L.dxa = act(T * h);
+    L.dxb = act(T * h);
+    L.dxc = act(T * h);
+    L.dyrecv = act(T * h);
+    L.dqkv = act(T * 3 * nd);
+    L.dout = act(T * nd);
+    L.dgu = act(T * 2 * F);
+    L.du = act(T * F);
     if (L.last) {
       L.logits = W.take<float>(T * L.V_loc);
-      L.dlogits = W.take<uint16_t>(T * L.V_loc);
+      L.dlogits = act(T * L.V_loc);
       L.stats = W.take<float>(3 * T);
       L.gmax = W.take<float>(T);
       L.sumtgt = W.take<float>(2 * T);
@@ -347,6 +356,11 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
   L.state_bytes = S.off + 256;
   L.grads_bytes = G.off + 256;
   L.work_bytes = W.off + 256;
+}
+
+// address of flat element e of tensor s's held parameter rows (bf16 or fp32 storage)
+static uint16_t* param_at(const Layout& L, const TState& s, int64_t e) {
+  return reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(s.param) + (e - s.rows.b * s.t.cols) * L.aes);
 }
 
 // grad-sync op lists and the reduce/Adam piece table (needs bound pointers)
@@ -368,7 +382,7 @@ static bool build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
     };
     auto peer_param = [&](int r, int64_t e) {
       TState& q = r == rank ? s : L.peer[r]->ts[ti];
-      return q.param + (e - q.rows.b * c);
+      return param_at(L, q, e);
     };
     for (const Piece& pc : pieces(cfg, p, s.t)) {
       const int64_t len = pc.e1 - pc.e0;
@@ -416,9 +430,9 @@ static bool build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
             pd.push[pd.n_push++] = peer_param(hr, pc.e0);
           }
         } else if (rank == pc.owner) {
-          L.pops.push_back({s.param + (pc.e0 - s.rows.b * c), (size_t)len, ncclBfloat16, hr, true});
+          L.pops.push_back({param_at(L, s, pc.e0), (size_t)len, L.f32 ? ncclFloat : ncclBfloat16, hr, true});
         } else if (rank == hr) {
-          L.pops.push_back({s.param + (pc.e0 - s.rows.b * c), (size_t)len, ncclBfloat16, pc.owner, false});
+          L.pops.push_back({param_at(L, s, pc.e0), (size_t)len, L.f32 ? ncclFloat : ncclBfloat16, pc.owner, false});
         }
       }
       if (pc.owner == rank) {
@@ -430,11 +444,13 @@ static bool build_sync(const malleus_model_cfg& cfg, int rank, Layout& L) {
         pd.m = s.m + off;
         pd.v = s.v + off;
         pd.rgrad = s.rgrad + off;
-        pd.param = s.param + (pc.e0 - s.rows.b * c);
-        bool vec = (len % 4 == 0) && ((uintptr_t)pd.param % 8 == 0);
+        pd.param = param_at(L, s, pc.e0);
+        pd.param_f32 = L.f32 ? 1 : 0;
+        const uintptr_t pal = L.f32 ? 16 : 8;  // param / push copies: float4 or 4 x bf16 stores
+        bool vec = (len % 4 == 0) && ((uintptr_t)pd.param % pal == 0);
         for (uintptr_t q : {(uintptr_t)pd.master, (uintptr_t)pd.m, (uintptr_t)pd.v, (uintptr_t)pd.rgrad}) vec &= q % 16 == 0;
         for (int k = 0; k < pd.n_src; ++k) vec &= (uintptr_t)pd.src[k] % 16 == 0;
-        for (int k = 0; k < pd.n_push; ++k) vec &= (uintptr_t)pd.push[k] % 8 == 0;
+        for (int k = 0; k < pd.n_push; ++k) vec &= (uintptr_t)pd.push[k] % pal == 0;
         pd.vec = vec ? 1 : 0;
         const int pid = (int)L.pieces.size();
         L.pieces.push_back(pd);
@@ -693,6 +709,7 @@ static malleus_status gemm(malleus_ctx* ctx, int M, int N, int K, const void* A,
                            const void* B, long long ldb, bool bmn, void* C, long long ldc, int mode,
                            cudaStream_t st) {
   GemmDesc g{M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, mode};
+  g.f32 = ctx->L && ctx->L->f32;
   CK(gemm_bf16(g, st));
   if (debug_sync()) {
     fprintf(stderr, "[malleus] gemm M=%d N=%d K=%d amn=%d bmn=%d mode=%d ...", M, N, K, amn, bmn, mode);
@@ -707,6 +724,7 @@ static malleus_status gemm_co(malleus_ctx* ctx, int M, int N, int K, const void*
                               cudaStream_t st) {  // GEMM leaving room for a concurrent kernel (GemmDesc::co_resident)
   GemmDesc g{M, N, K, A, lda, amn, B, ldb, bmn, C, ldc, mode};
   g.co_resident = true;
+  g.f32 = ctx->L && ctx->L->f32;
   CK(gemm_bf16(g, st));
   return MALLEUS_OK;
 }
@@ -725,7 +743,7 @@ static malleus_status tp_allreduce(malleus_ctx* ctx, float* buf, size_t n, ncclR
 }
 
 // ---- TP reduction over NVLink peer memory (tp_reduce.cu), fused with residual / RMSNorm
-static bool tp_peer(const Layout& L) { return L.TP > 1 && L.p2p && L.tpflags != nullptr; }
+static bool tp_peer(const Layout& L) { return L.TP > 1 && L.p2p && L.tpflags != nullptr && !L.f32; }
 // where the next row-parallel GEMM writes its fp32 partial
 static float* tp_part(Layout& L) { return tp_peer(L) ? L.tpp[(L.tp_epoch + 1) & 1] : L.part; }
 // the row-parallel GEMM's store mode for that buffer
@@ -883,6 +901,61 @@ static void duty_end(malleus_ctx* ctx, cudaStream_t st) {
   ctx->cur_seg = -1;
 }
 
+// activation kernels: bf16 path, or the fp32 parity kernels (fp32.cu) when L.f32
+#define F(p) reinterpret_cast<float*>(const_cast<void*>(static_cast<const void*>(p)))
+static cudaError_t k_norm_fwd(const Layout& L, int T, int h, const void* x, const float* part, void* x_out,
+                              const void* g, float eps, void* y, float* rstd, cudaStream_t st) {
+  if (L.f32) return rmsnorm_fwd_f32(T, h, F(x), part, F(x_out), F(g), eps, F(y), rstd, st);
+  return rmsnorm_fwd(T, h, x, part, x_out, g, eps, y, rstd, st);
+}
+static cudaError_t k_norm_bwd(const Layout& L, int T, int h, const void* x, const void* g, const float* rstd,
+                              const void* dy, const void* dres, void* dx, float* dg, float* scratch, cudaStream_t st,
+                              bool dy_bf16) {
+  if (L.f32) return rmsnorm_bwd_f32(T, h, F(x), F(g), rstd, F(dy), dres ? F(dres) : nullptr, F(dx), dg, st);
+  return rmsnorm_bwd(T, h, x, g, rstd, dy, dres, dx, dg, scratch, st, dy_bf16);
+}
+static cudaError_t k_rope(const Layout& L, int T, int s, int n, int d, void* buf, long long ld, float theta,
+                          bool inverse, cudaStream_t st) {
+  if (L.f32) return rope_f32(T, s, n, d, F(buf), ld, 0, theta, inverse, st);
+  return rope_inplace(T, s, n, d, buf, ld, 0, theta, inverse, st);
+}
+static cudaError_t k_attn_fwd(const Layout& L, int nb, int s, int n, int d, const void* qkv, void* o, float* lse,
+                              cudaStream_t st) {
+  if (L.f32) return attention_fwd_f32(nb, s, n, d, F(qkv), F(o), lse, st);
+  return attention_fwd(nb, s, n, d, qkv, o, lse, st);
+}
+static cudaError_t k_attn_bwd(const Layout& L, int nb, int s, int n, int d, const void* qkv, const void* o,
+                              const float* lse, const void* dout, void* dqkv, float* dsum, cudaStream_t st,
+                              const float2* rope_cs) {
+  if (L.f32) return attention_bwd_f32(nb, s, n, d, F(qkv), F(o), lse, F(dout), F(dqkv), dsum, st);
+  return attention_bwd(nb, s, n, d, qkv, o, lse, dout, dqkv, dsum, st, rope_cs);
+}
+static cudaError_t k_swiglu_fwd(const Layout& L, int T, int Fc, const void* gu, void* u, cudaStream_t st) {
+  if (L.f32) return swiglu_fwd_f32(T, Fc, F(gu), F(u), st);
+  return swiglu_fwd(T, Fc, gu, u, st);
+}
+static cudaError_t k_swiglu_bwd(const Layout& L, int T, int Fc, const void* gu, const void* du, void* dgu,
+                                cudaStream_t st) {
+  if (L.f32) return swiglu_bwd_f32(T, Fc, F(gu), F(du), F(dgu), st);
+  return swiglu_bwd(T, Fc, gu, du, dgu, st);
+}
+static cudaError_t k_residual(const Layout& L, long long n, const void* x, const float* part, void* out,
+                              cudaStream_t st) {
+  if (L.f32) return residual_add_f32(n, F(x), part, F(out), st);
+  return residual_add(n, x, part, out, st);
+}
+static cudaError_t k_embed_fwd(const Layout& L, int T, int h, const int32_t* tok, const void* E, void* x,
+                               cudaStream_t st) {
+  if (L.f32) return embed_fwd_f32(T, h, tok, F(E), F(x), st);
+  return embed_fwd(T, h, tok, E, x, st);
+}
+static cudaError_t k_embed_bwd(const Layout& L, int T, int h, const int32_t* tok, const void* dx, float* dE,
+                               cudaStream_t st) {
+  if (L.f32) return embed_bwd_f32(T, h, tok, F(dx), dE, st);
+  return embed_bwd(T, h, tok, dx, dE, st);
+}
+#undef F
+
 static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStream_t st) {
   Layout& L = *ctx->L;
   const malleus_model_cfg& c = ctx->cfg;
@@ -891,18 +964,19 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   SlotLayer& Y = S.L[li];
   LayerPtrs& P = L.lp[li];
   duty_begin(ctx, 0, st);
-  CK(rmsnorm_fwd(T, h, S.x[li], nullptr, nullptr, P.g1, c.rms_eps, Y.a1, Y.r1, st));
+  CK(k_norm_fwd(L, T, h, S.x[li], nullptr, nullptr, P.g1, c.rms_eps, Y.a1, Y.r1, st));
   {  // QKV projection; RoPE fused into the epilogue when the kernel supports it
     bool rope_done = false;
     GemmDesc g{T, 3 * nd, h, Y.a1, h, false, P.wqkv, h, false, Y.qkv, 3 * nd, GEMM_STORE_BF16};
+    g.f32 = L.f32;
     g.rope_cs = L.rope_cs;
     g.rope_cols = 2 * nd;
     g.rope_s = c.seq_len;
     g.rope_done = &rope_done;
     CK(gemm_bf16(g, st));
-    if (!rope_done) CK(rope_inplace(T, c.seq_len, L.n_loc, d, Y.qkv, 3LL * nd, 0, c.rope_theta, false, st));
+    if (!rope_done) CK(k_rope(L, T, c.seq_len, L.n_loc, d, Y.qkv, 3LL * nd, c.rope_theta, false, st));
   }
-  CK(attention_fwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
+  CK(k_attn_fwd(L, L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
   if (debug_sync()) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   RET(part_gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, st));
   if (tp_peer(L)) {  // x1 = x + sum P, a2 = RMSNorm(x1) in one peer-memory kernel
@@ -914,10 +988,10 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   } else {
     RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
     duty_begin(ctx, 1, st);
-    CK(rmsnorm_fwd(T, h, S.x[li], L.part, Y.x1, P.g2, c.rms_eps, Y.a2, Y.r2, st));
+    CK(k_norm_fwd(L, T, h, S.x[li], L.part, Y.x1, P.g2, c.rms_eps, Y.a2, Y.r2, st));
   }
   RET(gemm(ctx, T, 2 * F, h, Y.a2, h, false, P.wgu, h, false, Y.gu, 2 * F, GEMM_STORE_BF16, st));
-  CK(swiglu_fwd(T, F, Y.gu, Y.u, st));
+  CK(k_swiglu_fwd(L, T, F, Y.gu, Y.u, st));
   RET(part_gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, st));
   if (tp_peer(L)) {  // x[l+1] = x1 + sum P
     RET(tp_reduce_peer(ctx, TP_RESID, Y.x1, nullptr, [&](Layout& M, TpArgs& a, int j) {
@@ -926,7 +1000,7 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   } else {
     RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
     duty_begin(ctx, 2, st);
-    CK(residual_add((long long)T * h, Y.x1, L.part, S.x[li + 1], st));
+    CK(k_residual(L, (long long)T * h, Y.x1, L.part, S.x[li + 1], st));
     duty_end(ctx, st);
   }
   return MALLEUS_OK;
@@ -947,7 +1021,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   duty_begin(ctx, 3, st);
   RET(gemm(ctx, T, F, h, dy, h, false, P.wd, h, false, L.du, F, GEMM_STORE_BF16, st));
   RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
-  CK(swiglu_bwd(T, F, Y.gu, L.du, L.dgu, st));
+  CK(k_swiglu_bwd(L, T, F, Y.gu, L.du, L.dgu, st));
   RET(part_gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, st));
   if (tp_overlap(L)) {
     RET(tp_sum_begin(ctx, st));
@@ -958,14 +1032,14 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 4, st);
-  CK(rmsnorm_bwd(T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st, tp_sum_bf16(L)));
+  CK(k_norm_bwd(L, T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st, tp_sum_bf16(L)));
   // attention
   RET(gemm(ctx, T, nd, h, dx1, h, false, P.wo, h, false, L.dout, nd, GEMM_STORE_BF16, st));
   RET(gemm(ctx, nd, h, T, Y.o, nd, true, dx1, h, true, P.dwo, h, wm, st));
-  CK(attention_bwd(L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, L.dqkv, L.dsum, st, L.rope_cs));
+  CK(k_attn_bwd(L, L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, L.dqkv, L.dsum, st, L.rope_cs));
   if (debug_sync()) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
-    CK(rope_inplace(T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, 0, c.rope_theta, true, st));
+    CK(k_rope(L, T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, c.rope_theta, true, st));
   RET(part_gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, st));
   if (tp_overlap(L)) {
     RET(tp_sum_begin(ctx, st));
@@ -976,7 +1050,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 5, st);
-  CK(rmsnorm_bwd(T, h, S.x[li], P.g1, Y.r1, L.part, dx1, dx, P.dg1, L.scratch, st, tp_sum_bf16(L)));
+  CK(k_norm_bwd(L, T, h, S.x[li], P.g1, Y.r1, L.part, dx1, dx, P.dg1, L.scratch, st, tp_sum_bf16(L)));
   duty_end(ctx, st);
   return MALLEUS_OK;
 }
@@ -989,7 +1063,7 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
   Slot& S = L.slot[si];
   const PipeInfo& pp = L.plan.pipes[L.pipe];
   duty_begin(ctx, 6, st);
-  CK(rmsnorm_fwd(T, h, S.x[L.n_local], nullptr, nullptr, L.gf, c.rms_eps, S.xf, S.rf, st));
+  CK(k_norm_fwd(L, T, h, S.x[L.n_local], nullptr, nullptr, L.gf, c.rms_eps, S.xf, S.rf, st));
   RET(gemm(ctx, T, V, h, S.xf, h, false, L.Wlm, h, false, L.logits, V, GEMM_STORE_F32, st));
   CK(ce_stats(T, V, L.logits, tgt, L.v0, L.stats, st));
   CK(ce_combine_max(T, L.stats, L.gmax, st));
@@ -999,7 +1073,7 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
   duty_begin(ctx, 7, st);
   const double n_tok = (double)pp.n_micro * L.plan.b * c.seq_len;
   CK(ce_grad(T, V, L.logits, tgt, L.v0, L.gmax, L.sumtgt, L.sumtgt + T, (float)(1.0 / n_tok), L.dlogits,
-             L.loss_rows, st));
+             L.loss_rows, st, L.f32));
   if (L.member == 0)
     CK(reduce_loss(T, L.loss_rows, (float)(1.0 / ((double)L.plan.B * c.seq_len)), L.loss_acc, 1, st));
   RET(part_gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, st));
@@ -1013,7 +1087,7 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 8, st);
-  CK(rmsnorm_bwd(T, h, S.x[L.n_local], L.gf, S.rf, L.part, nullptr, S.dlast, L.dgf, L.scratch, st, tp_sum_bf16(L)));
+  CK(k_norm_bwd(L, T, h, S.x[L.n_local], L.gf, S.rf, L.part, nullptr, S.dlast, L.dgf, L.scratch, st, tp_sum_bf16(L)));
   duty_end(ctx, st);
   return MALLEUS_OK;
 }
@@ -1024,19 +1098,20 @@ static malleus_status pp_exchange(malleus_ctx* ctx, const uint16_t* send_fwd, ui
                                   const uint16_t* send_bwd, uint16_t* recv_bwd, cudaStream_t st) {
   Layout& L = *ctx->L;
   const size_t n = (size_t)L.T * ctx->cfg.hidden;
+  const ncclDataType_t adt = L.f32 ? ncclFloat : ncclBfloat16;
   if (!send_fwd && !recv_fwd && !send_bwd && !recv_bwd) return MALLEUS_OK;
   ev_begin(ctx, st, CAT_PP);
   NK(ncclGroupStart());
   if (send_fwd)
     for (size_t r = 0; r < L.next_ranks.size(); ++r)
-      if ((int)(r % L.TP) == L.member) NK(ncclSend(send_fwd, n, ncclBfloat16, L.next_ranks[r], ctx->world_comm, st));
+      if ((int)(r % L.TP) == L.member) NK(ncclSend(send_fwd, n, adt, L.next_ranks[r], ctx->world_comm, st));
   if (recv_fwd)
-    NK(ncclRecv(recv_fwd, n, ncclBfloat16, L.prev_ranks[L.member % L.prev_ranks.size()], ctx->world_comm, st));
+    NK(ncclRecv(recv_fwd, n, adt, L.prev_ranks[L.member % L.prev_ranks.size()], ctx->world_comm, st));
   if (send_bwd)
     for (size_t q = 0; q < L.prev_ranks.size(); ++q)
-      if ((int)(q % L.TP) == L.member) NK(ncclSend(send_bwd, n, ncclBfloat16, L.prev_ranks[q], ctx->world_comm, st));
+      if ((int)(q % L.TP) == L.member) NK(ncclSend(send_bwd, n, adt, L.prev_ranks[q], ctx->world_comm, st));
   if (recv_bwd)
-    NK(ncclRecv(recv_bwd, n, ncclBfloat16, L.next_ranks[L.member % L.next_ranks.size()], ctx->world_comm, st));
+    NK(ncclRecv(recv_bwd, n, adt, L.next_ranks[L.member % L.next_ranks.size()], ctx->world_comm, st));
   NK(ncclGroupEnd());
   ev_end(ctx, st);
   return MALLEUS_OK;
@@ -1134,7 +1209,7 @@ static malleus_status train_step_impl(malleus_ctx* ctx, const int32_t* tokens, c
     auto fwd = [&](int j) -> malleus_status {
       const int si = j % L.slots;
       Slot& S = L.slot[si];
-      if (L.first) CK(embed_fwd(L.T, c.hidden, tok_mb(j), L.E, S.x[0], st));
+      if (L.first) CK(k_embed_fwd(L, L.T, c.hidden, tok_mb(j), L.E, S.x[0], st));
       for (int li = 0; li < L.n_local; ++li) RET(layer_fwd_impl(ctx, li, si, st));
       if (L.last) RET(head_fwd_bwd(ctx, si, tgt_mb(j), j == 0, st));
       return MALLEUS_OK;
@@ -1151,7 +1226,7 @@ static malleus_status train_step_impl(malleus_ctx* ctx, const int32_t* tokens, c
         RET(layer_bwd_impl(ctx, li, si, cur, out, j == 0, st));
         cur = out;
       }
-      if (L.first) CK(embed_bwd(L.T, c.hidden, tok_mb(j), cur, L.dE, st));
+      if (L.first) CK(k_embed_bwd(L, L.T, c.hidden, tok_mb(j), cur, L.dE, st));
       *dx_out = const_cast<uint16_t*>(cur);
       return MALLEUS_OK;
     };
@@ -1228,7 +1303,8 @@ malleus_status malleus_create(const malleus_model_cfg* cfg, int32_t rank, int32_
   ctx->rank = rank;
   ctx->world = world;
   ctx->device = device;
-  if (cfg->hidden % 128 || cfg->head_dim % 32 || cfg->seq_len % 64) {
+  if (cfg->hidden % 128 || cfg->head_dim % 32 || cfg->seq_len % 64 ||
+      (cfg->dtype != MALLEUS_BF16 && cfg->dtype != MALLEUS_FP32)) {
     delete ctx;
     return MALLEUS_E_ARG;
   }
@@ -1304,14 +1380,16 @@ malleus_status malleus_write_tensor(malleus_ctx* ctx, int32_t tensor_id, int32_t
   if (it == L.tix.end()) return fail(ctx, MALLEUS_E_ARG, "unknown tensor id");
   TState& s = L.ts[it->second];
   const int64_t c = s.t.cols;
-  if (kind == MALLEUS_KIND_PARAM) {
-    const uint16_t* h = static_cast<const uint16_t*>(host);
+  if (kind == MALLEUS_KIND_PARAM) {  // bf16 bit patterns, or fp32 values in the parity mode
+    const char* hb = static_cast<const char*>(host);
     if (s.held)
-      CK(cudaMemcpy(s.param, h + s.rows.b * c, (s.rows.e - s.rows.b) * c * 2, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(s.param, hb + s.rows.b * c * L.aes, (s.rows.e - s.rows.b) * c * L.aes, cudaMemcpyHostToDevice));
     if (s.owned_elems) {
       std::vector<float> tmp(s.owned_elems);
       for (size_t i = 0; i < s.owned.size(); ++i)
-        for (int64_t e = s.owned[i].e0; e < s.owned[i].e1; ++e) tmp[s.owned_off[i] + e - s.owned[i].e0] = bf16_to_f32(h[e]);
+        for (int64_t e = s.owned[i].e0; e < s.owned[i].e1; ++e)
+          tmp[s.owned_off[i] + e - s.owned[i].e0] =
+              L.f32 ? reinterpret_cast<const float*>(hb)[e] : bf16_to_f32(reinterpret_cast<const uint16_t*>(hb)[e]);
       CK(cudaMemcpy(s.master, tmp.data(), s.owned_elems * 4, cudaMemcpyHostToDevice));
       CK(cudaMemset(s.m, 0, s.owned_elems * 4));
       CK(cudaMemset(s.v, 0, s.owned_elems * 4));
@@ -1344,7 +1422,7 @@ malleus_status malleus_read_local(malleus_ctx* ctx, int32_t tensor_id, int32_t k
   if (kind == MALLEUS_KIND_PARAM || kind == MALLEUS_KIND_GRAD) {
     if (s.held) rs.push_back({s.rows.b * c, s.rows.e * c});
     src = kind == MALLEUS_KIND_PARAM ? (const void*)s.param : (const void*)s.grad;
-    esz = kind == MALLEUS_KIND_PARAM ? 2 : 4;
+    esz = kind == MALLEUS_KIND_PARAM ? (size_t)L.aes : 4;
   } else {
     for (auto& pc : s.owned) rs.push_back({pc.e0, pc.e1});
     src = kind == MALLEUS_KIND_MASTER ? s.master : kind == MALLEUS_KIND_ADAM_M ? s.m
@@ -1373,7 +1451,7 @@ malleus_status malleus_layer_fwd(malleus_ctx* ctx, int32_t layer, int32_t slot, 
     return fail(ctx, MALLEUS_E_ARG, "layer not held by this rank or bad slot / pointers");
   cudaStream_t st = (cudaStream_t)stream;
   const int li = layer - L.lb;
-  const size_t bytes = (size_t)L.T * ctx->cfg.hidden * 2;
+  const size_t bytes = (size_t)L.T * ctx->cfg.hidden * L.aes;
   CK(cudaMemcpyAsync(L.slot[slot].x[li], x_in, bytes, cudaMemcpyDeviceToDevice, st));
   RET(layer_fwd_impl(ctx, li, slot, st));
   CK(cudaMemcpyAsync(x_out, L.slot[slot].x[li + 1], bytes, cudaMemcpyDeviceToDevice, st));
@@ -1389,7 +1467,7 @@ malleus_status malleus_layer_bwd(malleus_ctx* ctx, int32_t layer, int32_t slot, 
     return fail(ctx, MALLEUS_E_ARG, "layer not held by this rank or bad slot / pointers");
   cudaStream_t st = (cudaStream_t)stream;
   RET(layer_bwd_impl(ctx, layer - L.lb, slot, (const uint16_t*)dy, L.dxb == dx ? L.dxa : L.dxb, false, st));
-  CK(cudaMemcpyAsync(dx, L.dxb == dx ? L.dxa : L.dxb, (size_t)L.T * ctx->cfg.hidden * 2, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(dx, L.dxb == dx ? L.dxa : L.dxb, (size_t)L.T * ctx->cfg.hidden * L.aes, cudaMemcpyDeviceToDevice, st));
   return MALLEUS_OK;
 }
 
@@ -1466,9 +1544,9 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
   auto locate_ptr = [](Layout& Lx, int32_t tid, int kind, int64_t e, size_t* esz) -> char* {
     TState& s = Lx.ts[Lx.tix[tid]];
     if (kind == MALLEUS_KIND_PARAM) {
-      *esz = 2;
+      *esz = (size_t)Lx.aes;
       if (!s.held) return nullptr;
-      return reinterpret_cast<char*>(s.param + (e - s.rows.b * s.t.cols));
+      return reinterpret_cast<char*>(param_at(Lx, s, e));
     }
     *esz = 4;
     for (size_t i = 0; i < s.owned.size(); ++i)
@@ -1497,7 +1575,7 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
           size_t es;
           char* src = locate_ptr(O, ns.t.id, MALLEUS_KIND_PARAM, lo * c, &es);
           char* dst = locate_ptr(*NL, ns.t.id, MALLEUS_KIND_PARAM, lo * c, &es);
-          add_copy(keep, src, dst, (hi - lo) * c * 2);
+          add_copy(keep, src, dst, (hi - lo) * c * NL->aes);
         }
       }
     }
@@ -1522,7 +1600,7 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
     std::vector<CopyDesc> descs = keep;
     for (auto& t : trp) {
       if (t.dst != me) {
-        if (t.src == me) sent += (t.e1 - t.e0) * (t.kind == MALLEUS_KIND_PARAM ? 2 : 4);
+        if (t.src == me) sent += (t.e1 - t.e0) * (t.kind == MALLEUS_KIND_PARAM ? O.aes : 4);
         continue;
       }
       size_t es;
@@ -1582,7 +1660,7 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
   std::vector<CopyDesc> descs = keep;
   // sizes per peer first (canonical order), then descriptors
   for (auto& t : tr) {
-    size_t es = t.kind == MALLEUS_KIND_PARAM ? 2 : 4;
+    size_t es = t.kind == MALLEUS_KIND_PARAM ? (size_t)O.aes : 4;
     const long long b = (t.e1 - t.e0) * (long long)es;
     Pack& P = packs[pack_of(t.tensor)];
     if (t.src == me) P.send[t.dst].bytes += pad16(b);

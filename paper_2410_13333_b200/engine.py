@@ -38,8 +38,10 @@ def tensor_names(cfg):
 class Engine:
     """One malleus context (one process == one GPU)."""
 
-    def __init__(self, cfg, rank: int = 0, world: int = 1, device: int | None = None, group=None):
+    def __init__(self, cfg, rank: int = 0, world: int = 1, device: int | None = None, group=None,
+                 dtype: str = "bf16"):
         self.cfg = cfg
+        self.dtype = dtype  # "bf16", or "fp32" (parity mode: fp32 params / activations, SIMT kernels)
         self.rank, self.world = rank, world
         self.device = torch.cuda.current_device() if device is None else device
         torch.cuda.set_device(self.device)
@@ -51,7 +53,7 @@ class Engine:
             obj = [bytes(uid.raw) if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0, group=group)
             uid = C.create_string_buffer(obj[0], 128)
-        self._ccfg = L.make_cfg(cfg)
+        self._ccfg = L.make_cfg(cfg, dtype)
         ctx = C.c_void_p()
         check(L.lib.malleus_create(C.byref(self._ccfg), rank, world, self.device, uid, C.byref(ctx)), None, "create")
         self.ctx = ctx
@@ -89,8 +91,11 @@ class Engine:
 
     # ------------------------------------------------------------------ state I/O
     def write_weights(self, weights_bf16: dict):
+        """bf16 bit patterns per tensor (synth.gen); in fp32 mode their exact fp32 values are written."""
         for name, arr in weights_bf16.items():
             a = np.ascontiguousarray(arr, dtype=np.uint16)
+            if self.dtype == "fp32":
+                a = np.ascontiguousarray((a.astype(np.uint32) << 16).view(np.float32))
             check(L.lib.malleus_write_tensor(self.ctx, name_to_id(name), L.KIND_PARAM, a.ctypes.data), self.ctx,
                   f"write_tensor {name}")
 
@@ -104,7 +109,7 @@ class Engine:
         tid = name_to_id(name)
         check(L.lib.malleus_read_local(self.ctx, tid, kind, None, None, C.byref(nr), C.byref(ne)), self.ctx, "read")
         ranges = (C.c_int64 * max(1, 2 * nr.value))()
-        dtype = np.uint16 if kind == L.KIND_PARAM else np.float32
+        dtype = np.uint16 if kind == L.KIND_PARAM and self.dtype == "bf16" else np.float32
         out = np.empty(max(ne.value, 1), dtype=dtype)
         check(L.lib.malleus_read_local(self.ctx, tid, kind, out.ctypes.data, ranges, C.byref(nr), C.byref(ne)),
               self.ctx, "read")

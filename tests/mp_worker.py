@@ -32,13 +32,13 @@ CONFIGS = {"c1": C1_TINY, "c1m": C1_MED}
 
 
 def run(plan_name: str, rank: int = 0, world: int = 1, local_rank: int = 0, group=None, steps: int = 1,
-        cfg_name: str = "c1"):
+        cfg_name: str = "c1", dtype: str = "bf16"):
     cfg = CONFIGS[cfg_name]
     B, b = 8, 2
     plan = Pl.plan_matrix_c1(cfg, B=B, b=b)[plan_name]
     assert Pl.world_of(plan) == world, (plan_name, world)
     torch.cuda.set_device(local_rank)
-    eng = Engine(cfg, rank, world, local_rank, group=group)
+    eng = Engine(cfg, rank, world, local_rank, group=group, dtype=dtype)
     eng.apply(plan)
     W = make_weights(cfg)
     eng.write_weights(W)
@@ -67,10 +67,10 @@ def run(plan_name: str, rank: int = 0, world: int = 1, local_rank: int = 0, grou
         allr = [reads_step1]
     if rank != 0:
         return None
-    return check(cfg, W, tok, tgt, names, allr, results, plan)
+    return check(cfg, W, tok, tgt, names, allr, results, plan, dtype)
 
 
-def check(cfg, W, tok, tgt, names, allr, results, plan):
+def check(cfg, W, tok, tgt, names, allr, results, plan, dtype="bf16"):
     from oracle import model as M
     P = M.params_f64(W)
     loss_ref, g_ref = M.forward_backward(cfg, P, tok, tgt)
@@ -102,8 +102,9 @@ def check(cfg, W, tok, tgt, names, allr, results, plan):
         th, _, _ = M.adamw(P[n], np.zeros(shp), np.zeros(shp), g.astype(np.float64) * coef, 1, hp["lr"], hp["beta1"],
                            hp["beta2"], hp["eps"], wd)
         out["adam_rel"][n] = float(np.abs(master - th).max() / max(np.abs(th).max(), 1e-30))
-        # param push: each holder's bf16 == RNE(master)
-        want = bf16_rne(master.reshape(-1).astype(np.float32))
+        # param push: each holder's bf16 == RNE(master) (fp32 mode: == master)
+        want = bf16_rne(master.reshape(-1).astype(np.float32)) if dtype == "bf16" else \
+            master.reshape(-1).astype(np.float32)
         for r in allr:
             (ranges, vals) = r[n][2]
             off = 0
@@ -119,7 +120,8 @@ def check(cfg, W, tok, tgt, names, allr, results, plan):
         ref_losses = []
         from synth.gen import bf16_to_f64
         for step in range(1, len(results["losses"]) + 1):
-            Pb = {k: bf16_to_f64(bf16_rne(v.astype(np.float32))) for k, v in Pm.items()}
+            Pb = {k: bf16_to_f64(bf16_rne(v.astype(np.float32))) if dtype == "bf16" else
+                  v.astype(np.float32).astype(np.float64) for k, v in Pm.items()}
             l, g = M.forward_backward(cfg, Pb, tok, tgt)
             ref_losses.append(l)
             if clip > 0:
@@ -139,8 +141,9 @@ if __name__ == "__main__":
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     dist.init_process_group("gloo")
     cfg_name = sys.argv[4] if len(sys.argv) > 4 else "c1"
+    dtype = sys.argv[5] if len(sys.argv) > 5 else "bf16"
     r = run(plan_name, dist.get_rank(), dist.get_world_size(), int(os.environ.get("LOCAL_RANK", 0)), steps=steps,
-            cfg_name=cfg_name)
+            cfg_name=cfg_name, dtype=dtype)
     if dist.get_rank() == 0:
         json.dump(r, open(out_path, "w"), indent=1)
     dist.barrier()
