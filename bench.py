@@ -147,15 +147,46 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def setup_workload(args, cfg_c2, world):
+    """(cfg, malleable plan, {rank: nominal x}, uniform plan, workload name) for --workload."""
+    from paper_2410_13333_b200 import plans as Pl
+    from synth import gen
+    if args.workload == "c2":
+        cfg, B = cfg_c2, args.batch
+        plan = Pl.ladder_plan(cfg, world, B, b=1, straggle=True)
+        uni = Pl.ladder_plan(cfg, world, B, b=1, straggle=False)
+        st = STRAGGLER[world]
+        strag = {st[0]: st[1]} if st else {}
+        if args.tp4_stage:
+            assert world == 4, "--tp4-stage runs on 4 GPUs"
+            p8 = Pl.ladder_plan(cfg, 8, B, b=1, straggle=True)
+            plan = Pl.plan([Pl.pipe(p8["pipes"][0]["stages"], B)], 1, B)
+            uni = Pl.plan([Pl.pipe([Pl.even_stage(cfg, [0, 1, 2, 3], [0, cfg.n_layers])], B)], 1, B)
+            strag = {STRAGGLER[8][0]: STRAGGLER[8][1]}
+        return cfg, plan, strag, uni, WORKLOAD
+    assert world == 8, f"--workload {args.workload} is an 8-GPU configuration"
+    if args.workload == "c3":
+        cfg = gen.C3_32B_SLICE
+        plan, strag, uni = Pl.c3_plan(cfg)
+        return cfg, plan, strag, uni, "C3: LLaMA-32B-shaped 16-layer slice (h 6656, 52 heads, ffn 17920), TP4 x PP2"
+    cfg = gen.C4_70B_SLICE
+    plan, strag, uni = Pl.c4_plan(cfg)
+    return cfg, plan, strag, uni, "C4: LLaMA-70B-shaped 4-layer slice (h 8192, 64 heads, ffn 28672), DP2 x TP4"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="malleus", choices=["malleus", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
+                    help="c2: the BASELINE metric config (1/2/4/8 ladder); c3 / c4: the 8-GPU configs")
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--no-straggler", action="store_true")
     ap.add_argument("--uniform", action="store_true", help="non-malleable even plan (T_u / T0 runs)")
+    ap.add_argument("--no-baselines", action="store_true",
+                    help="N > 1: skip the T0 (uniform, no straggler) and T_u (uniform, straggler) phases")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replan", action="store_true", help="keep the nominal-rate plan (no measured re-plan)")
     ap.add_argument("--tp4-stage", action="store_true",
@@ -166,9 +197,8 @@ def main():
         faulthandler.dump_traceback_later(int(os.environ["MALLEUS_WATCHDOG"]), exit=True)
 
     from synth.gen import C2_7B_SLICE
-    cfg = C2_7B_SLICE
     if args.impl == "reference":
-        run_reference(args, cfg)
+        run_reference(args, C2_7B_SLICE)
         return
 
     import torch
@@ -184,26 +214,20 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
     torch.cuda.set_device(local)
-    group = None
     if world > 1:
         dist.init_process_group("gloo")
-    B = args.batch
-    straggle = STRAGGLER[world] if not args.no_straggler else None
-    plan = Pl.ladder_plan(cfg, world, B, b=1, straggle=not args.uniform)
-    if args.tp4_stage:
-        assert world == 4, "--tp4-stage runs on 4 GPUs"
-        straggle = None if args.no_straggler else STRAGGLER[8]
-        p8 = Pl.ladder_plan(cfg, 8, B, b=1, straggle=not args.uniform)
-        plan = Pl.plan([Pl.pipe(p8["pipes"][0]["stages"], B)], 1, B)
+    cfg, plan, strag, uni, workload = setup_workload(args, C2_7B_SLICE, world)
+    B = plan["global_batch"]
+    if args.no_straggler:
+        strag = {}
+    if args.uniform:
+        plan = uni
     eng = Engine(cfg, rank, world, local)
-    eng.apply(plan)
-    eng.write_weights(make_weights(cfg, parity=False))
     tok, tgt = make_tokens(cfg, B)
     dtok = torch.tensor(tok, device="cuda")
     dtgt = torch.tensor(tgt, device="cuda")
-    if straggle and straggle[0] == rank:
-        eng.set_slowdown(straggle[1], 2)  # DUTY: compute segments stretched x-fold on this rank
     stream = torch.cuda.current_stream()
+    tokens_per_step = B * cfg.seq_len
 
     def barrier():
         torch.cuda.synchronize()
@@ -211,28 +235,59 @@ def main():
             dist.barrier()
 
     step = 1
-    for _ in range(max(args.warmup, 3)):
-        eng.train_step(dtok, dtgt, step=step, apply_update=2)
-        step += 1
+
+    def run_steps(n):
+        nonlocal step
+        for _ in range(n):
+            eng.train_step(dtok, dtgt, step=step, apply_update=2)
+            step += 1
+
+    def timed(n):
+        """device ms per step over n steps, max over ranks"""
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a.record(stream)
+        run_steps(n)
+        b.record(stream)
+        barrier()
+        t = torch.tensor([a.elapsed_time(b) / n], dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def inject(on: bool):
+        if rank in strag:
+            if on:
+                eng.set_slowdown(strag[rank], 2)  # DUTY: compute segments stretched x-fold on this rank
+            else:
+                eng.set_slowdown(1.0, 0)
+
+    baselines = None
+    if world > 1 and strag and not args.no_baselines and not args.uniform:
+        # SURVEY §8(d) protocol: T0 = uniform plan without injection, T_u = the same plan with the
+        # straggler(s) injected (non-malleable reference), then the malleable plan (T_s = value)
+        eng.apply(uni)
+        eng.write_weights(make_weights(cfg, parity=False))
+        run_steps(max(args.warmup, 3))
+        t0_ms = timed(args.steps)
+        inject(True)
+        run_steps(2)
+        tu_ms = timed(args.steps)
+        eng.migrate(plan)
+        baselines = {"t0_tokens_s": tokens_per_step / (t0_ms / 1e3), "t0_ms_per_step": t0_ms,
+                     "tu_tokens_s": tokens_per_step / (tu_ms / 1e3), "tu_ms_per_step": tu_ms,
+                     "uniform_plan": plan_summary(uni)}
+    else:
+        eng.apply(plan)
+        eng.write_weights(make_weights(cfg, parity=False))
+        inject(True)
+    run_steps(max(args.warmup, 3))
     barrier()
     replan = None
-    if world > 1 and straggle and not args.no_replan:
+    if world > 1 and strag and not args.no_replan and not args.uniform:
         # The Malleus loop (PAPER.md:378-384): profile -> re-plan -> migrate.  Time the initial
         # (nominal-rate) plan, re-apportion the splits and micro-batches from each rank's measured
         # compute time (reading R12), migrate the model states to the new plan, then measure.
-        def timed(n):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            nonlocal step
-            barrier()
-            a.record(stream)
-            for _ in range(n):
-                eng.train_step(dtok, dtgt, step=step, apply_update=2)
-                step += 1
-            b.record(stream)
-            barrier()
-            t = torch.tensor([a.elapsed_time(b) / n], dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            return float(t.item())
         ms_before = timed(3)
         comp = [None] * world
         dist.all_gather_object(comp, eng.timing()["compute"])
@@ -242,21 +297,17 @@ def main():
         mig = eng.migrate(new_plan)
         allm = [None] * world
         dist.all_gather_object(allm, mig)
-        for _ in range(2):
-            eng.train_step(dtok, dtgt, step=step, apply_update=2)
-            step += 1
+        run_steps(2)
         ms_after = timed(3)
         kept = ms_after <= ms_before
         if kept:
             plan = new_plan
         else:  # the measured re-plan did not pay off: migrate back (a planner keeps the faster plan)
             eng.migrate(plan)
-            for _ in range(2):
-                eng.train_step(dtok, dtgt, step=step, apply_update=2)
-                step += 1
+            run_steps(2)
         barrier()
-        replan = {"tokens_s_before": B * cfg.seq_len / (ms_before / 1e3), "ms_per_step_before": ms_before,
-                  "tokens_s_replanned": B * cfg.seq_len / (ms_after / 1e3), "replanned_plan_kept": kept,
+        replan = {"tokens_s_before": tokens_per_step / (ms_before / 1e3), "ms_per_step_before": ms_before,
+                  "tokens_s_replanned": tokens_per_step / (ms_after / 1e3), "replanned_plan_kept": kept,
                   "replanned_plan": plan_summary(new_plan),
                   "compute_ms_per_rank_before": comp,
                   "migration": {"bytes": sum(m["bytes_recv"] for m in allm),
@@ -271,9 +322,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record(stream)
-    for _ in range(args.steps):
-        eng.train_step(dtok, dtgt, step=step, apply_update=2)
-        step += 1
+    run_steps(args.steps)
     e1.record(stream)
     barrier()
     n_launch = (L.lib.malleus_kernel_launches() - n0) // args.steps
@@ -287,23 +336,40 @@ def main():
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms_max = float(t_ms.item())
-    tokens_per_step = B * cfg.seq_len
     value = tokens_per_step / (ms_max / 1e3)
 
     # the same K steps again without the per-GEMM roofline events (they cost ~2-3% of the step):
     # reported beside `value`, which keeps the instrumented timed region the roofline comes from
-    barrier()
-    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e4.record(stream)
-    for _ in range(args.steps):
-        eng.train_step(dtok, dtgt, step=step, apply_update=2)
-        step += 1
-    e5.record(stream)
-    barrier()
-    t_un = torch.tensor([e4.elapsed_time(e5) / args.steps], dtype=torch.float64)
+    value_uninstr = tokens_per_step / (timed(args.steps) / 1e3)
+
+    # measured straggling rates (readings R12 / R13): the fixed probe (malleus_probe_speed, injection
+    # active) x_g = t_g / median_g t, and the in-run work-normalised estimate x_g = (t_g^comp / W_g) /
+    # median(t^comp / W) from this rank's compute time of the last step and its assigned FLOPs
+    measured = None
     if world > 1:
-        dist.all_reduce(t_un, op=dist.ReduceOp.MAX)
-    value_uninstr = tokens_per_step / (float(t_un.item()) / 1e3)
+        comp = [None] * world
+        dist.all_gather_object(comp, eng.timing()["compute"])
+        probe = eng.probe(30)
+        active = [r for r in range(world) if Pl.member_flops(cfg, plan, r) > 0]
+        med = statistics.median(probe[r] for r in active)
+        x_probe = {r: probe[r] / med for r in active}
+        rate = {r: comp[r] / Pl.member_flops(cfg, plan, r) for r in active}
+        med_r = statistics.median(rate.values())
+        x_work = {r: rate[r] / med_r for r in active}
+        n_act = len(active)
+        measured = {"x_nominal": {str(r): strag.get(r, 1.0) for r in active},
+                    "x_probe": {str(r): round(v, 4) for r, v in x_probe.items()},
+                    "x_work_normalised": {str(r): round(v, 4) for r, v in x_work.items()},
+                    "surviving_fraction_probe": sum(1.0 / max(1.0, v) for v in x_probe.values()) / n_act,
+                    "surviving_fraction_nominal": sum(1.0 / strag.get(r, 1.0) for r in active) / n_act}
+        if baselines:
+            t0 = baselines["t0_tokens_s"]
+            for key in ("probe", "nominal"):
+                target = 0.85 * t0 * measured[f"surviving_fraction_{key}"]
+                measured[f"target_tokens_s_{key}"] = target  # BJ pass bar T_s >= 0.85 T0 sum(1/x)/N
+                measured[f"pass_{key}"] = value >= target
+            measured["malleable_speedup_vs_uniform"] = value / baselines["tu_tokens_s"]
+            measured["ts_over_t0_times_surviving_probe"] = value / (t0 * measured["surviving_fraction_probe"])
 
     # e2e: the public API call with the step's inputs copied from pinned host memory and the loss read back
     htok = torch.tensor(tok).pin_memory()
@@ -338,17 +404,22 @@ def main():
             "gemm_share_of_step": gemm_share}
     prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(prof):
-        roof["traffic"] = json.load(open(prof)).get("bytes_per_launch")
+        tr = json.load(open(prof))
+        roof["traffic"] = tr.get("bytes_per_launch")
+        if tr.get("source"):
+            roof["traffic_source"] = tr["source"]
     step_tf = flops_per_token(cfg) * value / 1e12
     line = None
     if rank == 0:
         line = {"metric": "tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights (seeds 1234/5678)",
-                "config": {"workload": WORKLOAD,
+                "config": {"workload": workload,
                            "global_batch": B, "seq_len": cfg.seq_len, "micro_batch": 1,
-                           "plan": plan_summary(plan), "straggler": (
-                               {"rank": straggle[0], "x": straggle[1], "mode": "DUTY"} if straggle else None),
+                           "plan": plan_summary(plan),
+                           "straggler": ({"ranks": {str(r): x for r, x in strag.items()}, "mode": "DUTY",
+                                          "emulation": "spin of (x-1) x each compute segment's measured time"}
+                                         if strag else None),
                            "l2": "working set >> 126 MB L2 (no flush needed)"},
                 "step_tflops": step_tf,
                 "roofline": roof,
@@ -360,6 +431,8 @@ def main():
                 "gpu_launches": int(n_launch),
                 "instrumentation": {"per_gemm_cuda_events_in_timed_region": True,
                                     "tokens_s_same_steps_without_events": value_uninstr},
+                "baselines": baselines,
+                "straggling_measured": measured,
                 "replan": replan}
     eng.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the oracle on the host cores, N = 1 only

@@ -241,7 +241,8 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan,
                                const malleus_arenas* new_arenas, malleus_migrate_stats* stats);
 
 /* probe_speed (collective, blocking): fixed micro-benchmark (bf16 GEMM + HBM copy) timed with
- * CUDA events (§5.2), all-gathered: ms_per_rank[world] (host).
+ * CUDA events (§5.2), all-gathered: ms_per_rank[world] (host) = the median over 5
+ * rounds of the mean time of one iteration in a round of `iters`.
  * set_slowdown (local): straggler emulation for tests and benchmarks (PAPER.md:818-825 uses
  * competing processes).  mode 0 = off, 1 = HOG (persistent kernel occupying a fraction of SMs
  * on a side stream), 2 = DUTY (spin kernel of (x-1) * t after every compute op on the rank's

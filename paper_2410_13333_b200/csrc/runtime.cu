@@ -1767,18 +1767,25 @@ malleus_status malleus_probe_speed(malleus_ctx* ctx, int32_t iters, float* ms_pe
     if (i == 2) CK(cudaStreamSynchronize(st));
   }
   CK(cudaStreamSynchronize(st));
-  cudaEventRecord(e0, st);
-  for (int i = 0; i < iters; ++i) {
-    duty_begin(ctx, 9, st);
-    CK(gemm_bf16(g, st));
-    CK(probe_copy((long long)n * n / 2, (const float*)a, (float*)cbuf, st));
-    duty_end(ctx, st);
+  // median of 5 rounds of `iters` iterations: robust against a clock excursion in one round (a
+  // uniform cluster must read x = 1 +- 2%, SURVEY §8(c) probe pin)
+  std::vector<float> rounds;
+  for (int rd = 0; rd < 5; ++rd) {
+    cudaEventRecord(e0, st);
+    for (int i = 0; i < iters; ++i) {
+      duty_begin(ctx, 9, st);
+      CK(gemm_bf16(g, st));
+      CK(probe_copy((long long)n * n / 2, (const float*)a, (float*)cbuf, st));
+      duty_end(ctx, st);
+    }
+    cudaEventRecord(e1, st);
+    CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    rounds.push_back(t / iters);
   }
-  cudaEventRecord(e1, st);
-  CK(cudaEventSynchronize(e1));
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  ms /= iters;
+  std::sort(rounds.begin(), rounds.end());
+  float ms = rounds[rounds.size() / 2];
   CK(cudaMemcpy(dev + ctx->rank, &ms, 4, cudaMemcpyHostToDevice));
   NK(ncclAllGather(dev + ctx->rank, dev, 1, ncclFloat, ctx->world_comm, st));
   CK(cudaStreamSynchronize(st));

@@ -259,3 +259,59 @@ def plan_from_rates(cfg, plan, rates: dict, deadband: float = 0.05):
         for pp, m in zip(p["pipes"], _minmax(total_m, y)):
             pp["n_micro"] = m
     return p
+
+
+# ----------------------------------------------------------------------------- named workloads
+# BASELINE.json configs C3 / C4 as concrete plans (SURVEY §8(d) "Concrete synthetic inputs"), so an
+# 8-GPU run exercises non-uniform layers with PP and two-straggler cross-layout sync.  Each returns
+# (plan, stragglers {rank: nominal x}, uniform plan for the T0 / T_u runs).
+
+def c3_plan(cfg, B: int = 16):
+    """C3 (32B-shaped 16-layer slice, 8 GPUs): TP4 x PP2, DP1.  Stage 0 = GPUs 0-3 with GPU 3 at 2x:
+    heads 15/15/15/7 (min-max over rates (1, 1, 1, 2)), FFN 128-column tiles 40/40/40/20; stage 1 =
+    GPUs 4-7 even (13 heads, 35 tiles).  Layers (7, 9): the slow stage takes fewer layers (PAPER.md:
+    331-333 non-uniform layer assignment; even TP would need (5, 11)).  m = B (b = 1)."""
+    rates = [1.0, 1.0, 1.0, 2.0]
+    st0 = stage([0, 1, 2, 3], _heads_split(cfg.n_heads, rates), _ffn_split(cfg.ffn, rates),
+                even(cfg.vocab, 4, 16), [0, 7])
+    st1 = even_stage(cfg, [4, 5, 6, 7], [7, cfg.n_layers])
+    uni = plan([pipe([even_stage(cfg, [0, 1, 2, 3], [0, cfg.n_layers // 2]),
+                      even_stage(cfg, [4, 5, 6, 7], [cfg.n_layers // 2, cfg.n_layers])], B)], 1, B)
+    return plan([pipe([st0, st1], B)], 1, B), {3: 2.0}, uni
+
+
+def c4_plan(cfg, B: int = 32):
+    """C4 (70B-shaped 4-layer slice, 8 GPUs): DP2 x TP4.  Pipeline A = GPUs 0-3 with GPU 1 at 1.3x,
+    pipeline B = GPUs 4-7 with GPU 6 at 3x; heads / FFN tiles / vocab tiles by the min-max split of
+    each group's rates (reading R7); micro-batches by min-max over the pipelines' per-micro-batch
+    cost: the layouts of the two pipelines differ, so the gradient sync takes the
+    cross-layout path."""
+    ra, rb = [1.0, 1.3, 1.0, 1.0], [1.0, 1.0, 3.0, 1.0]
+    L = cfg.n_layers
+    sa = stage([0, 1, 2, 3], _heads_split(cfg.n_heads, ra), _ffn_split(cfg.ffn, ra), _vocab_split(cfg.vocab, ra),
+               [0, L])
+    sb = stage([4, 5, 6, 7], _heads_split(cfg.n_heads, rb), _ffn_split(cfg.ffn, rb), _vocab_split(cfg.vocab, rb),
+               [0, L])
+    y = [stage_cost(cfg, sa, ra, True), stage_cost(cfg, sb, rb, True)]
+    ma, mb = _minmax(B, y)
+    uni = plan([pipe([even_stage(cfg, [0, 1, 2, 3], [0, L])], B // 2),
+                pipe([even_stage(cfg, [4, 5, 6, 7], [0, L])], B - B // 2)], 1, B)
+    return plan([pipe([sa], ma), pipe([sb], mb)], 1, B), {1: 1.3, 6: 3.0}, uni
+
+
+def member_flops(cfg, plan: dict, rank: int) -> float:
+    """Algorithmic FLOPs of `rank` per step (reading R12's W_g): 3 x (forward per token of its shard:
+    QKV/O 8 h n_k d, causal attention 2 (s + 1) n_k d ((s+1)/2 keys on average), gate/up/down 6 h F_k per
+    layer, LM head 2 h V_k on the
+    last stage) x the pipeline's m_i b s tokens.  0 for standby ranks."""
+    for pp in plan["pipes"]:
+        for j, st in enumerate(pp["stages"]):
+            if rank in st["ranks"]:
+                k = st["ranks"].index(rank)
+                h, d, s = cfg.hidden, cfg.head_dim, cfg.seq_len
+                nl = st["layers"][1] - st["layers"][0]
+                w = nl * (8 * h * st["heads"][k] * d + 2 * (s + 1) * st["heads"][k] * d + 6 * h * st["ffn"][k])
+                if j == len(pp["stages"]) - 1:
+                    w += 2 * h * st["vocab"][k]
+                return 3.0 * w * pp["n_micro"] * plan["micro_batch"] * s
+    return 0.0

@@ -145,3 +145,36 @@ def test_plan_from_rates_mixed_pp_uses_slowest_stage():
     st = ev([0, 1], [0, 16])
     c_even = Pl.stage_cost(cfg, st, [1.0, 1.0], False)
     assert Pl.stage_cost(cfg, st, [1.0, 2.0], False) == pytest.approx(2 * c_even)
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_named_8gpu_workloads_validate(name):
+    """BASELINE configs C3 / C4 as runnable plans: they validate under the
+    oracle's Eq.(1) rules and the library's layout arithmetic, respect the
+    kernel limits (b*s <= 8192, h <= 8192, h % 128), and carry SURVEY §8(d)'s shapes."""
+    from synth.gen import C3_32B_SLICE, C4_70B_SLICE
+    from tests.test_layout_abi import _query  # noqa: F401  (loads the library: host-only queries)
+    cfg = C3_32B_SLICE if name == "c3" else C4_70B_SLICE
+    plan, strag, uni = (Pl.c3_plan if name == "c3" else Pl.c4_plan)(cfg)
+    validate(cfg, plan, 8)
+    validate(cfg, uni, 8)
+    assert plan["micro_batch"] * cfg.seq_len <= 8192 and cfg.hidden <= 8192 and cfg.hidden % 128 == 0
+    if name == "c3":
+        st0, st1 = plan["pipes"][0]["stages"]
+        assert st0["heads"] == [15, 15, 15, 7] and [f // 128 for f in st0["ffn"]] == [40, 40, 40, 20]
+        assert st0["layers"] == [0, 7] and st1["layers"] == [7, 16] and strag == {3: 2.0}
+    else:
+        assert [pp["n_micro"] for pp in plan["pipes"]] == [17, 15]  # SURVEY §8(d): m = (17, 15)
+        assert plan["pipes"][0]["stages"][0]["heads"] != plan["pipes"][1]["stages"][0]["heads"]  # cross-layout
+        assert strag == {1: 1.3, 6: 3.0}
+
+
+def test_member_flops_sum_to_the_step():
+    """reading R12's W_g: summed over the ranks of an even single-pipeline plan, the per-rank FLOPs
+    equal the step's algorithmic FLOPs (bench.flops_per_token x tokens), embedding excluded."""
+    import bench
+    cfg = C2_7B_SLICE
+    for n in (1, 2):
+        p = Pl.ladder_plan(cfg, n, 16, straggle=False)
+        tot = sum(Pl.member_flops(cfg, p, r) for r in range(n))
+        assert tot == pytest.approx(bench.flops_per_token(cfg) * 16 * cfg.seq_len, rel=1e-12)
