@@ -153,6 +153,19 @@ enum { MALLEUS_KIND_PARAM = 0, MALLEUS_KIND_GRAD = 1, MALLEUS_KIND_MASTER = 2,
 malleus_status malleus_nccl_unique_id(uint8_t out[128]);
 malleus_status malleus_create(const malleus_model_cfg* cfg, int32_t rank, int32_t world,
                               int32_t device, const uint8_t nccl_uid[128], malleus_ctx** out);
+/* wait (local): block until the work enqueued on `stream` has completed, or until timeout_ms elapses
+ * (timeout_ms <= 0: no limit).  This is the failure detector of PAPER.md:745 ("we add a threshold
+ * for communication calls during training in order to detect failures"): a step whose TP
+ * reductions, pipeline transfers or gradient exchange wait for an unresponsive GPU does not finish.
+ * On timeout — or when a device-side communication wait of the peer-memory TP reduction gave up
+ * after MALLEUS_COMM_TIMEOUT_MS (default 20000) — the context enters the failed state: the device
+ * spin-waits are released (process-wide abort word), every NCCL communicator of the context is
+ * aborted (ncclCommAbort), the stream is drained, and MALLEUS_E_TIMEOUT is returned; every later call
+ * except malleus_last_error / malleus_destroy returns MALLEUS_E_STATE.  Recovery is
+ * the caller's: destroy the context, create one on the surviving GPUs, apply a plan computed with
+ * the unresponsive GPUs' straggling rates set to infinity, and load the latest checkpoint
+ * (write_tensor of every kind).  Caller-owned arenas stay valid (they are not freed here). */
+malleus_status malleus_wait(malleus_ctx* ctx, void* stream, int32_t timeout_ms);
 malleus_status malleus_destroy(malleus_ctx* ctx);
 const char* malleus_last_error(const malleus_ctx* ctx); /* never NULL; static if ctx == NULL */
 const char* malleus_version(void);
@@ -244,9 +257,9 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan,
  * CUDA events (§5.2), all-gathered: ms_per_rank[world] (host) = the median over 5
  * rounds of the mean time of one iteration in a round of `iters`.
  * set_slowdown (local): straggler emulation for tests and benchmarks (PAPER.md:818-825 uses
- * competing processes).  mode 0 = off, 1 = HOG (persistent kernel occupying a fraction of SMs
- * on a side stream), 2 = DUTY (spin kernel of (x-1) * t after every compute op on the rank's
- * stream).  x >= 1. */
+ * competing processes).  mode 0 = off, 2 = DUTY (spin kernel of (x-1) * t after every compute
+ * segment on the rank's stream).  Mode 1 (HOG, an SM-occupying resident kernel) is rejected with
+ * E_ARG: a resident kernel deadlocks every device-wide synchronisation of the process.  x >= 1. */
 malleus_status malleus_probe_speed(malleus_ctx* ctx, int32_t iters, float* ms_per_rank);
 malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode);
 
@@ -280,6 +293,25 @@ malleus_status malleus_k_gemm(int32_t M, int32_t N, int32_t K, const void* A, in
                               int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, void* C,
                               int64_t ldc, int32_t mode, void* stream);
 
+/* The GEMM with a fused epilogue (the TP-1 residual of S7 / S10 and the SwiGLU of S9 / S12,
+ * SURVEY §8(a); "LLaMA-2 architecture"), C = A B (K-major A and B, bf16 out):
+ *   res != NULL (glu = 0): C = bf16(A B + res), res bf16 [M, N] row stride ldr (16-byte aligned,
+ *     N % 8 == 0);
+ *   glu = 1 (SwiGLU forward): N = 2F, B = [W_g; W_u] [2F, K]; C = gu [M, 2F] (bf16 G | U, ldc = 2F)
+ *     and aux = u [M, F] = bf16(silu(G) * U) on the bf16-rounded G, U;
+ *   glu = 2 (SwiGLU backward): N = F, A B = du (rounded to bf16), aux_in = gu [M, 2F]; aux = dgu
+ *     [M, 2F] = [dG | dU] with dU = du * G * s, dG = du * U * s * (1 + G (1 - s)), s = sigmoid(G);
+ *     C receives du instead when the kernel cannot fuse.
+ * *fused (may be NULL) = 1 when the kernel applied the SwiGLU (CTA-pair TMA epilogue: M >= 256),
+ * else 0 (then C holds the plain product and aux is untouched).  E_ARG on a violated layout. */
+malleus_status malleus_k_gemm_fused(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, const void* B,
+                                    int64_t ldb, void* C, int64_t ldc, const void* res, int64_t ldr,
+                                    int32_t glu, void* aux, const void* aux_in, int32_t* fused, void* stream);
+/* Failure-detection controls of the kernel-level entry points (tests): set (1) / clear (0) the
+ * process-wide abort word that releases every device-side communication wait; read the status word
+ * (nonzero: a wait gave up, after the timeout or on abort), clearing it when clear != 0. */
+malleus_status malleus_k_comm_abort(int32_t value);
+int32_t malleus_k_comm_status(int32_t clear);
 /* GEMM kernel selection for all subsequent GEMMs (tests / benchmarks): 0 = automatic (CTA pair,
  * tcgen05.mma.cta_group::2 with 256x256 tiles, when M >= 256; single CTA 128x256 otherwise),
  * 1 = always single CTA, 2 = always CTA pair (TMA-store / TMA-reduce-add epilogue), 3 = always CTA

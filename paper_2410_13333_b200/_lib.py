@@ -108,6 +108,10 @@ _SIGS = {
     "malleus_gemm_profile": ([i32, P_i64, C.POINTER(C.c_double), C.POINTER(C.c_double)], i32),
     "malleus_k_gemm": ([i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, i32, vp], i32),
     "malleus_k_gemm_variant": ([i32], i32),
+    "malleus_k_comm_abort": ([i32], i32),
+    "malleus_k_comm_status": ([i32], i32),
+    "malleus_wait": ([vp, vp, i32], i32),
+    "malleus_k_gemm_fused": ([i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, i32, vp, vp, vp, vp], i32),
     "malleus_k_attention_variant": ([i32], i32),
     "malleus_k_rmsnorm_fwd": ([i32, i32, vp, vp, vp, vp, f32, vp, vp, vp], i32),
     "malleus_k_rmsnorm_bwd": ([i32, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),
@@ -133,10 +137,15 @@ class MalleusError(RuntimeError):
     pass
 
 
+class CommTimeout(MalleusError):
+    """MALLEUS_E_TIMEOUT: a communication call exceeded the failure threshold."""
+
+
 def check(status: int, ctx=None, what: str = ""):
     if status != 0:
         msg = lib.malleus_last_error(ctx).decode() if ctx is not None else ""
-        raise MalleusError(f"{what}: {STATUS.get(status, status)}: {msg}")
+        cls = CommTimeout if status == 7 else MalleusError
+        raise cls(f"{what}: {STATUS.get(status, status)}: {msg}")
 
 
 DTYPES = {"bf16": 0, "fp32": 1}

@@ -18,6 +18,31 @@ extern "C" malleus_status malleus_k_gemm(int32_t M, int32_t N, int32_t K, const 
   return cu(gemm_bf16(g, (cudaStream_t)stream));
 }
 
+extern "C" malleus_status malleus_k_gemm_fused(int32_t M, int32_t N, int32_t K, const void* A, int64_t lda,
+                                               const void* B, int64_t ldb, void* C, int64_t ldc, const void* res,
+                                               int64_t ldr, int32_t glu, void* aux, const void* aux_in,
+                                               int32_t* fused, void* stream) {
+  if (!A || !B || !C || glu < 0 || glu > 2 || (glu && res) || (glu && !aux) || (glu == 2 && !aux_in))
+    return MALLEUS_E_ARG;
+  GemmDesc g{M, N, K, A, lda, false, B, ldb, false, C, ldc, GEMM_STORE_BF16};
+  g.res = res;
+  g.ldr = ldr;
+  g.glu = glu;
+  g.aux = aux;
+  g.aux_in = aux_in;
+  bool done = false;
+  g.glu_done = &done;
+  malleus_status s = cu(gemm_bf16(g, (cudaStream_t)stream));
+  if (fused) *fused = done ? 1 : 0;
+  return s;
+}
+
+extern "C" malleus_status malleus_k_comm_abort(int32_t value) {
+  comm_abort(value ? 1u : 0u);
+  return MALLEUS_OK;
+}
+extern "C" int32_t malleus_k_comm_status(int32_t clear) { return (int32_t)comm_status(clear != 0); }
+
 extern "C" malleus_status malleus_k_rmsnorm_fwd(int32_t T, int32_t h, const void* x, const float* partial,
                                                 void* x_out, const void* g, float eps, void* y, float* rstd,
                                                 void* stream) {

@@ -7,8 +7,8 @@
 //
 // Layout: qkv [T, 3*n*d] bf16, T = nb * s; q | k | v column blocks, head j at columns j*d.
 // RoPE has already been applied to q and k (elementwise.cu).  o [T, n*d]; lse [nb, n, s] fp32.
-// Attention is 2-5% of step FLOPs; a tcgen05 version is future work
-// (DESIGN.md §Kernels).
+// This mma.sync path serves the shapes the tcgen05 kernels (attention_tc.cu: d = 128, s % 128 == 0)
+// do not cover, e.g. the tiny parity model C1 (d = 32).
 #include <cuda_bf16.h>
 #include "kernels.h"
 

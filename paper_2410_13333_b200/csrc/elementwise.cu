@@ -320,34 +320,59 @@ __global__ void embed_fwd_kernel(int T, int h, const int32_t* __restrict__ tok, 
 
 // dE[v] += sum over positions t with tok[t] == v of dx[t], deterministic: the CTA of the first
 // position of each distinct token sums all of that token's rows in position order and updates the
-// dE row once (no atomics, so repeated tokens give run-to-run identical sums).  Tokens staged in
-// shared memory (T <= EMBED_MAX_T), 8 columns per thread.
+// dE row once (no atomics, so repeated tokens give run-to-run identical sums).  The CTA first
+// compacts the later positions holding the same token into a shared list in position order
+// (warp ballots, chunks of 256 positions), so the gather loop only visits the duplicates (few
+// under uniform tokens).  Tokens staged in shared memory (T <= EMBED_MAX_T), 8 columns per thread.
 constexpr int EMBED_MAX_T = 8192;
-__global__ void __launch_bounds__(256) embed_bwd_kernel(int T, int h, const int32_t* __restrict__ tok,
-                                                        const uint4* __restrict__ dx, float* __restrict__ dE) {
-  extern __shared__ int32_t stok[];
-  __shared__ int first;
+constexpr int EMBED_THREADS = 256;
+__global__ void __launch_bounds__(EMBED_THREADS) embed_bwd_kernel(int T, int h, const int32_t* __restrict__ tok,
+                                                                  const uint4* __restrict__ dx, float* __restrict__ dE) {
+  extern __shared__ int32_t stok[];           // [T] tokens, then [T] duplicate positions
+  int32_t* dup = stok + T;
+  __shared__ int first, n_dup;
+  __shared__ int wcnt[EMBED_THREADS / 32];
   const int t = blockIdx.x;
-  for (int i = threadIdx.x; i < T; i += blockDim.x) stok[i] = tok[i];
-  if (threadIdx.x == 0) first = 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < T; i += EMBED_THREADS) stok[i] = tok[i];
+  if (threadIdx.x == 0) { first = 1; n_dup = 0; }
   __syncthreads();
   const int v = stok[t];
-  for (int i = threadIdx.x; i < t; i += blockDim.x)
+  for (int i = threadIdx.x; i < t; i += EMBED_THREADS)
     if (stok[i] == v) first = 0;  // benign race: every writer stores 0
   __syncthreads();
   if (!first) return;
+  for (int base = t + 1; base < T; base += EMBED_THREADS) {  // ordered compaction of positions > t
+    const int u = base + threadIdx.x;
+    const bool hit = u < T && stok[u] == v;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) wcnt[w] = __popc(m);
+    __syncthreads();
+    if (hit) {
+      int off = n_dup + __popc(m & ((1u << lane) - 1u));
+      for (int j = 0; j < w; ++j) off += wcnt[j];
+      dup[off] = u;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int j = 0; j < EMBED_THREADS / 32; ++j) s += wcnt[j];
+      n_dup += s;
+    }
+    __syncthreads();
+  }
+  const int nd = n_dup;
   const int nv = h / 8;
   float* dst = dE + (long long)v * h;
-  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+  for (int c = threadIdx.x; c < nv; c += EMBED_THREADS) {
     float acc[8];
     unpack8(dx[(long long)t * nv + c], acc);
-    for (int u = t + 1; u < T; ++u)
-      if (stok[u] == v) {
-        float w[8];
-        unpack8(dx[(long long)u * nv + c], w);
+    for (int k = 0; k < nd; ++k) {
+      float x8[8];
+      unpack8(dx[(long long)dup[k] * nv + c], x8);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += w[j];
-      }
+      for (int j = 0; j < 8; ++j) acc[j] += x8[j];
+    }
     float4* d4 = reinterpret_cast<float4*>(dst + c * 8);
     float4 o0 = d4[0], o1 = d4[1];
     o0.x += acc[0]; o0.y += acc[1]; o0.z += acc[2]; o0.w += acc[3];
@@ -549,7 +574,14 @@ cudaError_t embed_fwd(int T, int h, const int32_t* tok, const void* E, void* x, 
 
 cudaError_t embed_bwd(int T, int h, const int32_t* tok, const void* dx, float* dE, cudaStream_t st) {
   if (T > EMBED_MAX_T || h % 8) return cudaErrorInvalidValue;
-  embed_bwd_kernel<<<T, 256, T * sizeof(int32_t), st>>>(T, h, tok, (const uint4*)dx, dE); count_launch();
+  static bool attr = false;  // 2 * T int32 of dynamic smem: up to 64 KB
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(embed_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         2 * EMBED_MAX_T * (int)sizeof(int32_t));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  embed_bwd_kernel<<<T, EMBED_THREADS, 2 * T * sizeof(int32_t), st>>>(T, h, tok, (const uint4*)dx, dE); count_launch();
   return cudaGetLastError();
 }
 

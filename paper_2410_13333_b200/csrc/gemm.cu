@@ -22,6 +22,7 @@
 #include <utility>
 #include <vector>
 #include <cstring>
+#include <cstdlib>
 #include "ptx.cuh"
 #include "kernels.h"
 
@@ -45,6 +46,13 @@ struct GemmParams {
   int rope_cols, rope_s;
   int n_dst, rows_per_dst;  // row-split destinations (GemmDesc::dst)
   void* dst[4];
+  const void* res;          // fused residual (bf16, row stride ldr), GemmDesc::res
+  long long ldr;
+  int glu;                  // fused SwiGLU epilogue (GemmDesc::glu), CTA-pair TMA epilogue only
+  const void* aux_in;       // glu 2: saved gu [M][2F] (row stride ld_aux_in)
+  long long ld_aux_in;
+  int dbg;                  // experiment switches of the glu 2 epilogue (MALLEUS_GLU2_DBG): 1 no smem
+                            // reads of G/U, 2 no math, 4 no stores, 8 no G/U TMA loads (results are then wrong)
 };
 struct TmapSet {  // per-destination C maps of the row-split TMA epilogue
   CUtensorMap m[4];
@@ -59,6 +67,246 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   int r = t % per_group;
   tm = first_m + r % gsz;
   tn = r / gsz;
+}
+
+// r[0..8) (fp32 bits) += the 8 bf16 values of q
+__device__ __forceinline__ void add_bf16x8(uint32_t* r, uint4 q) {
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(b[i]);
+    r[2 * i] = __float_as_uint(__uint_as_float(r[2 * i]) + f.x);
+    r[2 * i + 1] = __float_as_uint(__uint_as_float(r[2 * i + 1]) + f.y);
+  }
+}
+__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + __expf(-x)); }
+
+// one 32-row x 64-column bf16 box of the TMA epilogue: lane = row, ra / rb = columns [0, 32) and
+// [32, 64) as fp32 bits, packed to bf16 (RNE) into a 128B-swizzled 4 KB staging buffer and
+// written by one TMA store (double-buffered: waits until the store issued two boxes ago has read
+// its buffer)
+__device__ __forceinline__ void stage_store_bf16(const CUtensorMap* tm, uint8_t* stg, int& sbuf,
+                                                 const uint32_t (&ra)[32], const uint32_t (&rb)[32], int c0, int c1) {
+  const int lane = threadIdx.x & 31;
+  uint8_t* buf = stg + sbuf * 4096;
+  if (lane == 0) bulk_wait_read<1>();
+  __syncwarp();
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) {
+    const uint32_t* r = ch < 4 ? ra : rb;
+    const int o = (ch & 3) * 8;
+    uint4 w;
+    w.x = pack_bf16(__uint_as_float(r[o + 0]), __uint_as_float(r[o + 1]));
+    w.y = pack_bf16(__uint_as_float(r[o + 2]), __uint_as_float(r[o + 3]));
+    w.z = pack_bf16(__uint_as_float(r[o + 4]), __uint_as_float(r[o + 5]));
+    w.w = pack_bf16(__uint_as_float(r[o + 6]), __uint_as_float(r[o + 7]));
+    *reinterpret_cast<uint4*>(buf + lane * 128 + ((ch ^ (lane & 7)) << 4)) = w;
+  }
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tm, buf, c0, c1);
+    bulk_commit();
+  }
+  sbuf ^= 1;
+}
+// the same for a box already packed to bf16 (8 x 16 bytes per lane)
+__device__ __forceinline__ void stage_store_packed(const CUtensorMap* tm, uint8_t* stg, int& sbuf,
+                                                   const uint4 (&q)[8], int c0, int c1) {
+  const int lane = threadIdx.x & 31;
+  uint8_t* buf = stg + sbuf * 4096;
+  if (lane == 0) bulk_wait_read<1>();
+  __syncwarp();
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) *reinterpret_cast<uint4*>(buf + lane * 128 + ((ch ^ (lane & 7)) << 4)) = q[ch];
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tm, buf, c0, c1);
+    bulk_commit();
+  }
+  sbuf ^= 1;
+}
+
+// SwiGLU forward epilogue (glu 1): the accumulator holds gate columns [j0, j0 + 128) in TMEM
+// columns [0, 128) and the matching up columns in [128, 256).  G and U are rounded to bf16 (the
+// saved pre-activations, reading R6) and stored into gu's two halves; u = silu(G) * U (fp32 math on
+// the bf16 values, as the standalone kernel) is stored into u.  Maps: tmC = gu[:, :F], tmD->m[0] =
+// gu[:, F:], tmD->m[1] = u (each F columns wide, so ragged F is clipped by TMA).
+__device__ __forceinline__ void epilogue_glu_fwd(const GemmParams& p, const CUtensorMap* tmC, const TmapSet* tmD,
+                                                 uint32_t taddr, int crow, int j0, uint8_t* stg, int& sbuf) {
+  const int F = p.N >> 1;
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    const int col0 = j0 + c * 64;
+    uint32_t g0[32], g1[32], u0[32], u1[32];
+    tmem_ld32(taddr + c * 64, g0);
+    tmem_ld32(taddr + c * 64 + 32, g1);
+    tmem_ld32(taddr + 128 + c * 64, u0);
+    tmem_ld32(taddr + 128 + c * 64 + 32, u1);
+    tmem_wait_ld();
+    if (col0 >= F) continue;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      g0[j] = __float_as_uint(bf16r(__uint_as_float(g0[j])));
+      g1[j] = __float_as_uint(bf16r(__uint_as_float(g1[j])));
+      u0[j] = __float_as_uint(bf16r(__uint_as_float(u0[j])));
+      u1[j] = __float_as_uint(bf16r(__uint_as_float(u1[j])));
+    }
+    stage_store_bf16(tmC, stg, sbuf, g0, g1, col0, crow);
+    stage_store_bf16(&tmD->m[0], stg, sbuf, u0, u1, col0, crow);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float a = __uint_as_float(g0[j]), b = __uint_as_float(g1[j]);
+      u0[j] = __float_as_uint(a * sigmoid_f(a) * __uint_as_float(u0[j]));
+      u1[j] = __float_as_uint(b * sigmoid_f(b) * __uint_as_float(u1[j]));
+    }
+    stage_store_bf16(&tmD->m[1], stg, sbuf, u0, u1, col0, crow);
+  }
+}
+
+// Epilogue operand boxes read from HBM (the saved gu of glu 2, the residual) are staged by TMA into
+// the warp's own two 4 KB staging buffers (the same 128B-swizzled 32-row x 64-column layout the
+// output boxes use; lane = row), completing on the warp's mbarrier: per-lane row loads from global
+// memory (32 rows per instruction) measured ~60 us slower per C2 du GEMM.
+__device__ __forceinline__ void epi_load_boxes(uint8_t* buf, uint64_t* ebar, const CUtensorMap* m0,
+                                               const CUtensorMap* m1, int c0, int c1) {
+  mbar_arrive_expect_tx(ebar, m1 ? 8192 : 4096);
+  tma_load_2d(buf, m0, ebar, c0, c1);
+  if (m1) tma_load_2d(buf + 4096, m1, ebar, c0, c1);
+}
+__device__ __forceinline__ void epi_read_box(const uint8_t* buf, uint4 (&q)[8]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int v = 0; v < 8; ++v) q[v] = *reinterpret_cast<const uint4*>(buf + lane * 128 + ((v ^ (lane & 7)) << 4));
+}
+
+// SwiGLU backward epilogue (glu 2) of the down-projection dgrad du = dy W_d: D = bf16(du) (reading
+// R6), G / U from the saved gu (tmD->m[2] / m[3]), dU = D * G * s, dG = D * U * s * (1 + G (1 - s)),
+// s = sigmoid(G), stored into dgu's halves (tmD->m[0] = dgu[:, :F], tmD->m[1] = dgu[:, F:]); du
+// itself is not stored.  Staging per warp: [0, 8K) G | U load boxes (chunk 0's issued by the caller
+// before the accumulator wait, chunk c + 1's as soon as chunk c is in registers), [8K, 16K) dG | dU.
+__device__ __forceinline__ void epilogue_glu_bwd(const GemmParams& p, const TmapSet* tmD, uint32_t taddr,
+                                                 int row_box0, int crow, int col_base, uint8_t* stg, uint64_t* ebar,
+                                                 uint32_t& ephase) {
+  const int lane = threadIdx.x & 31;
+  const int F = p.N;
+  uint8_t* out = stg + 8192;
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    const int col0 = col_base + c * 64;
+    if (col0 >= F) break;  // warp-uniform: the remaining chunks are past the edge too
+    uint32_t d0[32], d1[32];
+    tmem_ld32(taddr + c * 64, d0);
+    tmem_ld32(taddr + c * 64 + 32, d1);
+    tmem_wait_ld();
+    if (!(p.dbg & 8)) {
+      mbar_wait(ebar, ephase);
+      ephase ^= 1;
+    }
+    uint4 gq[8], uq[8];
+    if (!(p.dbg & 1)) {
+      epi_read_box(stg, gq);
+      epi_read_box(stg + 4096, uq);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) { gq[v] = make_uint4(0x3f803f80u, 0, 0, 0); uq[v] = gq[v]; }
+    }
+    fence_proxy_async();  // these generic reads before the async-proxy (TMA) write of the next chunk
+    __syncwarp();  // every lane has its rows: the load buffers may take the next chunk
+    if (lane == 0 && c + 1 < 4 && col0 + 64 < F && !(p.dbg & 8))
+      epi_load_boxes(stg, ebar, &tmD->m[2], &tmD->m[3], col0 + 64, row_box0);
+#pragma unroll
+    for (int v = 0; v < 8 && !(p.dbg & 2); ++v) {
+      uint32_t* d = v < 4 ? d0 + 8 * v : d1 + 8 * (v - 4);
+      const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&gq[v]);
+      const __nv_bfloat162* ub = reinterpret_cast<const __nv_bfloat162*>(&uq[v]);
+      float dU[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 G = __bfloat1622float2(gb[i]), U = __bfloat1622float2(ub[i]);
+        const float D0 = bf16r(__uint_as_float(d[2 * i])), D1 = bf16r(__uint_as_float(d[2 * i + 1]));
+        const float s0 = sigmoid_f(G.x), s1 = sigmoid_f(G.y);
+        dU[2 * i] = D0 * G.x * s0;
+        dU[2 * i + 1] = D1 * G.y * s1;
+        d[2 * i] = __float_as_uint(D0 * U.x * s0 * (1.f + G.x * (1.f - s0)));
+        d[2 * i + 1] = __float_as_uint(D1 * U.y * s1 * (1.f + G.y * (1.f - s1)));
+      }
+      uq[v].x = pack_bf16(dU[0], dU[1]);
+      uq[v].y = pack_bf16(dU[2], dU[3]);
+      uq[v].z = pack_bf16(dU[4], dU[5]);
+      uq[v].w = pack_bf16(dU[6], dU[7]);
+    }
+    if (lane == 0) bulk_wait_read<0>();  // the previous chunk's stores have read the output buffers
+    __syncwarp();
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+      const uint32_t* r = ch < 4 ? d0 : d1;
+      const int o = (ch & 3) * 8;
+      uint4 w;
+      w.x = pack_bf16(__uint_as_float(r[o + 0]), __uint_as_float(r[o + 1]));
+      w.y = pack_bf16(__uint_as_float(r[o + 2]), __uint_as_float(r[o + 3]));
+      w.z = pack_bf16(__uint_as_float(r[o + 4]), __uint_as_float(r[o + 5]));
+      w.w = pack_bf16(__uint_as_float(r[o + 6]), __uint_as_float(r[o + 7]));
+      *reinterpret_cast<uint4*>(out + lane * 128 + ((ch ^ (lane & 7)) << 4)) = w;
+      *reinterpret_cast<uint4*>(out + 4096 + lane * 128 + ((ch ^ (lane & 7)) << 4)) = uq[ch];
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0 && !(p.dbg & 4)) {
+      tma_store_2d(&tmD->m[0], out, col0, crow);
+      tma_store_2d(&tmD->m[1], out + 4096, col0, crow);
+      bulk_commit();
+    }
+  }
+}
+
+// Residual epilogue (bf16 store of acc + res): staging per warp [0, 4K) the residual box (chunk 0's
+// issued by the caller before the accumulator wait, chunk c + 1's once chunk c is in registers),
+// [4K, 8K) the output box (tmD->m[0] = res).
+__device__ __forceinline__ void epilogue_residual(const GemmParams& p, const CUtensorMap* tmC, const TmapSet* tmD,
+                                                  uint32_t taddr, int row_box0, int col_base, uint8_t* stg,
+                                                  uint64_t* ebar, uint32_t& ephase) {
+  const int lane = threadIdx.x & 31;
+  uint8_t* out = stg + 4096;
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    const int col0 = col_base + c * 64;
+    if (col0 >= p.N) break;
+    uint32_t r0[32], r1[32];
+    tmem_ld32(taddr + c * 64, r0);
+    tmem_ld32(taddr + c * 64 + 32, r1);
+    tmem_wait_ld();
+    mbar_wait(ebar, ephase);
+    ephase ^= 1;
+    uint4 q[8];
+    epi_read_box(stg, q);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0 && c + 1 < 4 && col0 + 64 < p.N) epi_load_boxes(stg, ebar, &tmD->m[0], nullptr, col0 + 64, row_box0);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) add_bf16x8(v < 4 ? r0 + 8 * v : r1 + 8 * (v - 4), q[v]);
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+      const uint32_t* r = ch < 4 ? r0 : r1;
+      const int o = (ch & 3) * 8;
+      uint4 w;
+      w.x = pack_bf16(__uint_as_float(r[o + 0]), __uint_as_float(r[o + 1]));
+      w.y = pack_bf16(__uint_as_float(r[o + 2]), __uint_as_float(r[o + 3]));
+      w.z = pack_bf16(__uint_as_float(r[o + 4]), __uint_as_float(r[o + 5]));
+      w.w = pack_bf16(__uint_as_float(r[o + 6]), __uint_as_float(r[o + 7]));
+      *reinterpret_cast<uint4*>(out + lane * 128 + ((ch ^ (lane & 7)) << 4)) = w;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmC, out, col0, row_box0);
+      bulk_commit();
+    }
+  }
 }
 
 // Epilogue of one 256-column accumulator for one row per thread: TMEM (32 lanes x 32 columns per
@@ -82,6 +330,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
     const bool full_chunk = p.vec_ok && col0 + 32 <= p.N;
     if (p.mode == GEMM_STORE_BF16) {
       __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(Cb) + crow * p.ldc + col0;
+      if (p.res) {  // fused residual: C = bf16(acc + res), res rows 16-byte aligned, N % 8 == 0
+        const uint4* rp = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.res) +
+                                                         (long long)row * p.ldr + col0);
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (col0 + 8 * v < p.N) add_bf16x8(r + 8 * v, __ldg(rp + v));
+      }
       if (full_chunk) {
         uint4* dst = reinterpret_cast<uint4*>(C);
 #pragma unroll
@@ -123,9 +378,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tadd
 // 128B-swizzled smem box (double buffered) and written with one TMA store, or, for the fp32
 // wgrad accumulation, with one TMA reduce-add (the add happens in L2; the SM never reads C).
 // Out-of-bounds rows / columns are clipped by TMA, so ragged uneven-split shapes need no masks.
+template <int GLU>
 __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC, const TmapSet* tmD,
                                                   uint32_t taddr, int row_box0, int col_base, uint8_t* stg,
-                                                  int& sbuf) {
+                                                  int& sbuf, uint64_t* ebar, uint32_t& ephase) {
   const int lane = threadIdx.x & 31;
   if (row_box0 >= p.M) return;
   int crow = row_box0;  // store coordinate: in C, or in this box's destination (rows_per_dst % 32 == 0)
@@ -134,6 +390,9 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
     tmC = &tmD->m[d];
     crow = row_box0 - d * p.rows_per_dst;
   }
+  if constexpr (GLU == 1) { epilogue_glu_fwd(p, tmC, tmD, taddr, crow, col_base, stg, sbuf); return; }
+  if constexpr (GLU == 2) { epilogue_glu_bwd(p, tmD, taddr, row_box0, crow, col_base, stg, ebar, ephase); return; }
+  if constexpr (GLU == 3) { epilogue_residual(p, tmC, tmD, taddr, row_box0, col_base, stg, ebar, ephase); return; }
   if (p.mode == GEMM_STORE_BF16 && p.rope_cs != nullptr && col_base < p.rope_cols) {
     // QKV projection with RoPE fused (half-split pairs (i, i+64) of each 128-column head, reading
     // R3): the two heads of this 256-column tile are rotated in registers before the bf16 store.
@@ -377,23 +636,29 @@ constexpr int A2_BYTES = BM2 * BK * 2;            // 16 KB
 constexpr int B2_BYTES = (BN2 / 2) * BK * 2;      // 16 KB (this CTA's half of N)
 constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
 constexpr int EPI_STAGE_BYTES = 4 * 2 * 4096;  // 4 epilogue warps x 2 swizzled 4 KB boxes
-constexpr int gemm2_smem(int stages) { return stages * STAGE2_BYTES + EPI_STAGE_BYTES + 1024 + 1024; }
+// per-warp staging: 8 KB, or 16 KB for the SwiGLU backward (8 KB of prefetched G | U boxes + 8 KB of
+// dG | dU output boxes; that variant runs a 5-stage operand ring to make room)
+constexpr int epi_warp_bytes(int glu) { return glu == 2 ? 16384 : 8192; }
+constexpr int gemm2_smem(int stages, int glu = 0) {
+  return stages * STAGE2_BYTES + 4 * epi_warp_bytes(glu) + 1024 + 1024;
+}
 
 // ST: smem ring depth (6 by default; 5 leaves room on each SM for a concurrently running
 // communication kernel, see GemmDesc::co_resident)
-template <bool A_MN, bool B_MN, int ST>
+template <bool A_MN, bool B_MN, int ST, int GLU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ CUtensorMap tmC, const __grid_constant__ TmapSet tmD,
-                        GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC,
+                        const __grid_constant__ TmapSet tmD, GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_stage = smem + ST * STAGE2_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + EPI_STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + 4 * epi_warp_bytes(GLU));
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;  // [2]
   uint64_t* tempty = tfull + 2;       // [2] (leader's copy is the one used)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ebar = tempty + 3;        // [4] epilogue warps' operand-box barriers (GLU 2 / 3)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -401,15 +666,20 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   const bool leader = rank == 0;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int tiles_m = (p.M + 2 * BM2 - 1) / (2 * BM2);
-  const int tiles_n = (p.N + BN2 - 1) / BN2;
+  // glu 1: a tile is 128 gate columns (B rows from tmB, staged by the even CTA) next to the same
+  // 128 up columns (tmB2, odd CTA), so the pair's 256-column accumulator holds both halves
+  const int tiles_n = GLU == 1 ? ((p.N >> 1) + BN2 / 2 - 1) / (BN2 / 2) : (p.N + BN2 - 1) / BN2;
   const int n_tiles = tiles_m * tiles_n;
   const int n_kb = (p.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (GLU == 1) tma_prefetch(&tmB2);
     for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    if (GLU >= 2)
+      for (int w = 0; w < 4; ++w) mbar_init(&ebar[w], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc2(tmem_slot, 512);
@@ -423,7 +693,9 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       int stage = 0; uint32_t phase = 0;
       for (int t = cid; t < n_tiles; t += ncl) {
         int tm, tn; tile_coords(t, tiles_m, tiles_n, tm, tn);
-        const int m0 = tm * 2 * BM2 + rank * BM2, n0 = tn * BN2 + rank * (BN2 / 2);
+        const int m0 = tm * 2 * BM2 + rank * BM2;
+        const int n0 = GLU == 1 ? tn * (BN2 / 2) : tn * BN2 + rank * (BN2 / 2);
+        const CUtensorMap* mB = GLU == 1 && rank ? &tmB2 : &tmB;
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE2_BYTES;
@@ -437,10 +709,10 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
             tma_load_2d_2sm(sa + 8192, &tmA, &full[stage], m0 + 64, k0);
           }
           if (!B_MN) {
-            tma_load_2d_2sm(sb, &tmB, &full[stage], k0, n0);
+            tma_load_2d_2sm(sb, mB, &full[stage], k0, n0);
           } else {
-            tma_load_2d_2sm(sb, &tmB, &full[stage], n0, k0);
-            tma_load_2d_2sm(sb + 8192, &tmB, &full[stage], n0 + 64, k0);
+            tma_load_2d_2sm(sb, mB, &full[stage], n0, k0);
+            tma_load_2d_2sm(sb + 8192, mB, &full[stage], n0 + 64, k0);
           }
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
@@ -478,18 +750,26 @@ gemm_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
     }
   } else {
     const int quarter = warp & 3;
-    uint8_t* stg = epi_stage + (warp - 2) * 2 * 4096;
+    uint8_t* stg = epi_stage + (warp - 2) * epi_warp_bytes(GLU);
     int sbuf = 0;
+    uint32_t ephase = 0;
     int it = 0;
     for (int t = cid; t < n_tiles; t += ncl, ++it) {
       int tm, tn; tile_coords(t, tiles_m, tiles_n, tm, tn);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      const int row_box0 = tm * 2 * BM2 + rank * BM2 + quarter * 32;
+      if constexpr (GLU == 2) {  // G | U boxes of the tile's first chunk: independent of the accumulator
+        if (lane == 0 && !(p.dbg & 8)) epi_load_boxes(stg, &ebar[warp - 2], &tmD.m[2], &tmD.m[3], tn * BN2, row_box0);
+      } else if constexpr (GLU == 3) {
+        if (lane == 0) epi_load_boxes(stg, &ebar[warp - 2], &tmD.m[0], nullptr, tn * BN2, row_box0);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row_box0 = tm * 2 * BM2 + rank * BM2 + quarter * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN2;
-      if (p.tma_epi) epilogue_tile_tma(p, &tmC, &tmD, taddr, row_box0, tn * BN2, stg, sbuf);
+      if (GLU || p.tma_epi)
+        epilogue_tile_tma<GLU>(p, &tmC, &tmD, taddr, row_box0, GLU == 1 ? tn * (BN2 / 2) : tn * BN2, stg, sbuf,
+                               &ebar[warp - 2], ephase);
       else epilogue_tile(p, taddr, row_box0 + lane, tn * BN2);
       tc_fence_before();
       __syncwarp();
@@ -624,12 +904,12 @@ void gemm_set_variant(int v) {
   g_tma_epi = v == 3 ? 0 : 1;
 }
 
-template <bool A_MN, bool B_MN, int ST>
-static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const TmapSet& td,
-                           const GemmParams& p, cudaStream_t st) {
+template <bool A_MN, bool B_MN, int ST, int GLU = 0>
+static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb2, const CUtensorMap& tc,
+                           const TmapSet& td, const GemmParams& p, cudaStream_t st) {
   static bool attr_set = false;
-  auto kern = gemm_tcgen05_2sm_kernel<A_MN, B_MN, ST>;
-  constexpr int SMEM2 = gemm2_smem(ST);
+  auto kern = gemm_tcgen05_2sm_kernel<A_MN, B_MN, ST, GLU>;
+  constexpr int SMEM2 = gemm2_smem(ST, GLU);
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
     if (e != cudaSuccess) return e;
@@ -639,7 +919,8 @@ static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const C
     int dev; cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int tiles = ((p.M + 2 * BM2 - 1) / (2 * BM2)) * ((p.N + BN2 - 1) / BN2);
+  const int tiles_n = p.glu == 1 ? ((p.N >> 1) + BN2 / 2 - 1) / (BN2 / 2) : (p.N + BN2 - 1) / BN2;
+  const int tiles = ((p.M + 2 * BM2 - 1) / (2 * BM2)) * tiles_n;
   const int sms = g_num_sms;
   const int clusters = tiles < sms / 2 ? tiles : sms / 2;
   const int grid = 2 * (clusters > 0 ? clusters : 1);
@@ -653,7 +934,7 @@ static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const C
     }
     cudaEventRecord(g_prof.ev[g_prof.used].first, st);
   }
-  kern<<<grid, GEMM_THREADS, SMEM2, st>>>(ta, tb, tc, td, p); count_launch();
+  kern<<<grid, GEMM_THREADS, SMEM2, st>>>(ta, tb, tb2, tc, td, p); count_launch();
   if (prof) {
     cudaEventRecord(g_prof.ev[g_prof.used].second, st);
     g_prof.flops.push_back(2.0 * p.M * (double)p.N * p.K);
@@ -663,7 +944,8 @@ static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const C
 }
 
 cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
-  if (g.f32) return gemm_f32(g, st);
+  if (g.glu_done) *g.glu_done = false;
+  if (g.f32) return (g.res || g.glu) ? cudaErrorInvalidValue : gemm_f32(g, st);
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
   cudaError_t e = get_encoder();
   if (e != cudaSuccess) return e;
@@ -673,6 +955,13 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
   if (g.n_dst < 0 || g.n_dst > 4 || (g.n_dst > 0 && (g.rows_per_dst <= 0 || g.n_dst * g.rows_per_dst != g.M ||
                                                      g.mode == GEMM_ACCUM_F32 || g.rope_cs)))
     return cudaErrorInvalidValue;
+  if (g.res && (g.mode != GEMM_STORE_BF16 || g.n_dst || g.rope_cs || g.glu || (g.ldr % 8) || (g.N % 8) ||
+                (reinterpret_cast<uintptr_t>(g.res) & 15)))
+    return cudaErrorInvalidValue;
+  if (g.glu < 0 || g.glu > 2 || (g.glu && (g.mode != GEMM_STORE_BF16 || g.n_dst || g.rope_cs || g.b_mn || !g.aux)))
+    return cudaErrorInvalidValue;
+  if (g.glu == 1 && (g.N % 32)) return cudaErrorInvalidValue;  // F = N / 2, F % 16 == 0
+  if (g.glu == 2 && ((g.N % 16) || !g.aux_in || (reinterpret_cast<uintptr_t>(g.aux_in) & 15))) return cudaErrorInvalidValue;
   const int esz = g.mode == GEMM_STORE_BF16 ? 2 : 4;
   int vec_ok = (g.ldc * esz) % 16 == 0;
   if (g.n_dst)
@@ -680,10 +969,11 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
   else
     vec_ok &= (reinterpret_cast<uintptr_t>(g.C) & 15) == 0;
   GemmParams p{g.M, g.N, g.K, g.C, g.ldc, g.mode, vec_ok, 0, nullptr, 0, 0, g.n_dst, g.rows_per_dst,
-               {g.dst[0], g.dst[1], g.dst[2], g.dst[3]}};
+               {g.dst[0], g.dst[1], g.dst[2], g.dst[3]}, g.res, g.ldr, 0, nullptr, 0, 0};
   const bool pair = g_variant == 2 || (g_variant == 0 && g.M >= 256);
   if (pair) {
-    CUtensorMap ta, tb;
+    CUtensorMap ta, tb, tb2;
+    memset(&tb2, 0, sizeof(tb2));
     bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.lda, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, BM2);
     ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64) : make_map(&tb, g.B, g.K, g.N, g.ldb, BN2 / 2));
     if (!ok) return cudaErrorInvalidValue;
@@ -699,22 +989,68 @@ cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st) {
     } else if (tma_epi) {
       tma_epi = make_map_c(&tc, g.C, g.N, g.M, g.ldc, g.mode != GEMM_STORE_BF16);
     }
+    // fused SwiGLU (TMA epilogue only): per-half B maps (glu 1) and per-half output maps, each F
+    // columns wide so that TMA clips a ragged F at the half's own edge
+    if (tma_epi && g.glu == 1) {
+      const int F = g.N / 2;
+      const char* B = static_cast<const char*>(g.B);
+      bool gok = make_map(&tb, B, g.K, F, g.ldb, BN2 / 2) &&
+                 make_map(&tb2, B + (size_t)F * g.ldb * 2, g.K, F, g.ldb, BN2 / 2) &&
+                 make_map_c(&tc, g.C, F, g.M, g.ldc, false) &&
+                 make_map_c(&td.m[0], static_cast<char*>(g.C) + (size_t)F * 2, F, g.M, g.ldc, false) &&
+                 make_map_c(&td.m[1], g.aux, F, g.M, F, false) && (reinterpret_cast<uintptr_t>(g.aux) & 15) == 0;
+      if (!gok) {  // plain GEMM (the caller runs the standalone SwiGLU)
+        make_map(&tb, g.B, g.K, g.N, g.ldb, BN2 / 2);
+        make_map_c(&tc, g.C, g.N, g.M, g.ldc, false);
+      } else {
+        p.glu = 1;
+      }
+    } else if (tma_epi && g.glu == 2) {
+      const int F = g.N;
+      char* gin = static_cast<char*>(const_cast<void*>(g.aux_in));
+      bool gok = make_map_c(&td.m[0], g.aux, F, g.M, 2LL * F, false) &&
+                 make_map_c(&td.m[1], static_cast<char*>(g.aux) + (size_t)F * 2, F, g.M, 2LL * F, false) &&
+                 make_map_c(&td.m[2], gin, F, g.M, 2LL * F, false) &&
+                 make_map_c(&td.m[3], gin + (size_t)F * 2, F, g.M, 2LL * F, false) &&
+                 (reinterpret_cast<uintptr_t>(g.aux) & 15) == 0;
+      if (gok) {
+        p.glu = 2;
+        p.aux_in = g.aux_in;
+        p.ld_aux_in = 2LL * F;
+        static const int dbg = getenv("MALLEUS_GLU2_DBG") ? atoi(getenv("MALLEUS_GLU2_DBG")) : 0;
+        p.dbg = dbg;
+      }
+    } else if (tma_epi && g.res) {  // residual staged by TMA (EPI 3); the direct epilogues read it per row
+      if (make_map_c(&td.m[0], const_cast<void*>(g.res), g.N, g.M, g.ldr, false)) p.glu = 3;
+    }
+    if (g.glu_done) *g.glu_done = p.glu == 1 || p.glu == 2;
     const bool rope = tma_epi && g.rope_cs && g.mode == GEMM_STORE_BF16 && g.rope_cols % 128 == 0;
     if (g.rope_done) *g.rope_done = rope;
     p.tma_epi = tma_epi;
     p.rope_cs = rope ? g.rope_cs : nullptr;
     p.rope_cols = g.rope_cols;
     p.rope_s = g.rope_s;
-    if (g.co_resident) {  // 5-stage ring: ~32 KB of smem per SM left for a concurrent kernel
-      if (!g.a_mn && !g.b_mn) return launch2<false, false, 5>(ta, tb, tc, td, p, st);
-      if (!g.a_mn && g.b_mn) return launch2<false, true, 5>(ta, tb, tc, td, p, st);
-      if (g.a_mn && g.b_mn) return launch2<true, true, 5>(ta, tb, tc, td, p, st);
-      return launch2<true, false, 5>(ta, tb, tc, td, p, st);
+    if (p.glu == 1) return launch2<false, false, STAGES2, 1>(ta, tb, tb2, tc, td, p, st);
+    if (p.glu == 2) {
+      if (g.a_mn) return launch2<true, false, 5, 2>(ta, tb, tb2, tc, td, p, st);
+      return launch2<false, false, 5, 2>(ta, tb, tb2, tc, td, p, st);
     }
-    if (!g.a_mn && !g.b_mn) return launch2<false, false, STAGES2>(ta, tb, tc, td, p, st);
-    if (!g.a_mn && g.b_mn) return launch2<false, true, STAGES2>(ta, tb, tc, td, p, st);
-    if (g.a_mn && g.b_mn) return launch2<true, true, STAGES2>(ta, tb, tc, td, p, st);
-    return launch2<true, false, STAGES2>(ta, tb, tc, td, p, st);
+    if (p.glu == 3) {
+      if (!g.a_mn && g.b_mn) return launch2<false, true, STAGES2, 3>(ta, tb, tb2, tc, td, p, st);
+      if (!g.a_mn && !g.b_mn) return launch2<false, false, STAGES2, 3>(ta, tb, tb2, tc, td, p, st);
+      if (g.a_mn && g.b_mn) return launch2<true, true, STAGES2, 3>(ta, tb, tb2, tc, td, p, st);
+      return launch2<true, false, STAGES2, 3>(ta, tb, tb2, tc, td, p, st);
+    }
+    if (g.co_resident) {  // 5-stage ring: ~32 KB of smem per SM left for a concurrent kernel
+      if (!g.a_mn && !g.b_mn) return launch2<false, false, 5>(ta, tb, tb2, tc, td, p, st);
+      if (!g.a_mn && g.b_mn) return launch2<false, true, 5>(ta, tb, tb2, tc, td, p, st);
+      if (g.a_mn && g.b_mn) return launch2<true, true, 5>(ta, tb, tb2, tc, td, p, st);
+      return launch2<true, false, 5>(ta, tb, tb2, tc, td, p, st);
+    }
+    if (!g.a_mn && !g.b_mn) return launch2<false, false, STAGES2>(ta, tb, tb2, tc, td, p, st);
+    if (!g.a_mn && g.b_mn) return launch2<false, true, STAGES2>(ta, tb, tb2, tc, td, p, st);
+    if (g.a_mn && g.b_mn) return launch2<true, true, STAGES2>(ta, tb, tb2, tc, td, p, st);
+    return launch2<true, false, STAGES2>(ta, tb, tb2, tc, td, p, st);
   }
   CUtensorMap ta, tb;
   bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.lda, 64) : make_map(&ta, g.A, g.K, g.M, g.lda, BM);

@@ -36,6 +36,20 @@ struct GemmDesc {
   bool co_resident = false;
   // FP32 parity mode: A, B, C fp32 (GEMM_STORE_BF16 then stores the fp32 activation), SIMT kernel
   bool f32 = false;
+  // optional residual add fused into the bf16 epilogue (TP-1 row-parallel GEMMs, S7 / S10 + the
+  // residual of S8): C = bf16(acc + res[row][col]), res bf16 with row stride ldr.  Every bf16 kernel.
+  const void* res = nullptr;
+  long long ldr = 0;
+  // optional SwiGLU fused into the epilogue; CTA-pair TMA epilogue only,
+  // *glu_done reports whether the kernel applied it (else C holds the plain GEMM result):
+  //   glu = 1 (forward, gate/up GEMM): N = 2F, B rows [0, F) = W_g and [F, 2F) = W_u (K-major);
+  //           C = gu [M][2F] (bf16 pre-activations, ldc = 2F) and aux = u = silu(G) * U [M][F].
+  //   glu = 2 (backward, down dgrad): N = F, the GEMM result is du; aux_in = gu [M][2F] (saved
+  //           pre-activations) and aux = dgu [M][2F] = [dG | dU]; C is not written when fused.
+  int glu = 0;
+  void* aux = nullptr;
+  const void* aux_in = nullptr;
+  bool* glu_done = nullptr;
 };
 cudaError_t gemm_bf16(const GemmDesc& g, cudaStream_t st);  // dispatches to gemm_f32 when g.f32
 
@@ -148,6 +162,20 @@ extern unsigned long long* attn_trace_buffer;      // MALLEUS_ATTN_TRACE stamps 
 extern unsigned long long* attn_bwd_trace_buffer;  // ... and of the last dK / dV kernel
 extern unsigned long long* attn_dq_trace_buffer;   // ... and of the last dQ kernel
 
+// ---- failure detection ("we add a threshold for communication calls during training
+// in order to detect failures"): a process-wide abort word and status word in mapped pinned host
+// memory, polled by every device-side communication wait (the peer-memory TP reduction).  A wait
+// that exceeds the timeout (MALLEUS_COMM_TIMEOUT_MS, default 20000) or sees the abort word gives up:
+// it sets the status word and the kernel returns (no trap: the context stays usable for teardown).
+struct CommGuard {
+  const volatile unsigned* abort;  // device alias of the host abort word
+  unsigned* status;                // device alias of the host status word (1 = a wait gave up)
+  unsigned long long timeout_ns;
+};
+CommGuard comm_guard();        // lazily allocated; zero pointers if mapped memory is unavailable
+void comm_abort(unsigned v);   // host: set / clear the abort word
+unsigned comm_status(bool clear);
+
 // ---- TP partial-sum reduction over NVLink peer memory, fused with residual / RMSNorm (tp_reduce.cu)
 constexpr int MAX_TP = 16;
 constexpr int TP_GRID_MAX = 592;  // 4 CTAs of 256 threads per SM; the grid is a function of (T, k) only
@@ -169,6 +197,7 @@ struct TpArgs {
   int uneven;                            // rows of member j are [row0[j], row0[j+1]) (else even)
   int row0[MAX_TP + 1];
   unsigned long long* trace;             // optional: per-call globaltimer stamps (MALLEUS_TP_TRACE)
+  CommGuard guard;                       // filled by tp_reduce()
 };
 constexpr int TP_TRACE_CALLS = 4096;
 unsigned long long* tp_trace_buffer(int member);  // managed [TP_TRACE_CALLS][4] per member, lazily allocated

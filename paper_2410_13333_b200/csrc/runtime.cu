@@ -9,8 +9,11 @@
 //   * 1F1B pipelining over this pipeline's m_i micro-batches with NCCL P2P
 //     between stages whose TP degrees may differ (receiver r <- sender r mod TP_prev);
 //   * the batch-weighted cross-layout gradient reduction to owners + AdamW + bf16 push
-//     (readings R4, R9), NCCL P2P per refined piece, one group;
-//   * migration to a new plan in 4-layer packs, one grouped NCCL send/recv each;
+//     (readings R4, R9): owners read the other pipelines' gradient rows over
+//     NVLink (CUDA IPC) and push the updated bf16 rows from the optimizer kernel (NCCL P2P per
+//     refined piece is the fallback without peer mapping);
+//   * migration to a new plan: peer pulls of the deltas over NVLink, or 4-layer
+//     packs with one grouped NCCL send/recv each as the fallback;
 //   * probe and straggler emulation.
 #include <cuda.h>
 #include <nccl.h>
@@ -23,6 +26,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.h"
@@ -152,6 +156,7 @@ struct malleus_ctx {
   std::unique_ptr<Layout> L;
   std::string err;
   bool sticky = false;
+  bool failed = false;                        // malleus_wait timed out: communicators aborted
   cudaStream_t tp_side = nullptr;             // backward TP reductions overlapping the wgrad GEMM
   cudaEvent_t tp_ev_a = nullptr, tp_ev_b = nullptr;
   float slowdown = 1.f;
@@ -978,30 +983,62 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   }
   CK(k_attn_fwd(L, L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
   if (debug_sync()) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
-  RET(part_gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, st));
+  // TP 1: the residual add is fused into the row-parallel GEMM's epilogue (x1 = bf16(x + o W_o^T),
+  // no fp32 partial round trip); the norm then reads x1
+  const bool fuse_res = L.TP == 1 && !L.f32;
+  if (fuse_res) {
+    GemmDesc g{T, h, nd, Y.o, nd, false, P.wo, h, true, Y.x1, h, GEMM_STORE_BF16};
+    g.res = S.x[li];
+    g.ldr = h;
+    CK(gemm_bf16(g, st));
+  } else {
+    RET(part_gemm(ctx, T, h, nd, Y.o, nd, false, P.wo, h, true, st));
+  }
   if (tp_peer(L)) {  // x1 = x + sum P, a2 = RMSNorm(x1) in one peer-memory kernel
     RET(tp_reduce_peer(ctx, TP_RESID_NORM, S.x[li], P.g2, [&](Layout& M, TpArgs& a, int j) {
       const SlotLayer& Z = M.slot[si].L[li];
       a.d0[j] = Z.x1; a.d1[j] = Z.a2; a.d2[j] = Z.r2;
     }, st));
     duty_begin(ctx, 1, st);
+  } else if (fuse_res) {
+    duty_end(ctx, st);
+    duty_begin(ctx, 1, st);
+    CK(k_norm_fwd(L, T, h, Y.x1, nullptr, nullptr, P.g2, c.rms_eps, Y.a2, Y.r2, st));
   } else {
     RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
     duty_begin(ctx, 1, st);
     CK(k_norm_fwd(L, T, h, S.x[li], L.part, Y.x1, P.g2, c.rms_eps, Y.a2, Y.r2, st));
   }
-  RET(gemm(ctx, T, 2 * F, h, Y.a2, h, false, P.wgu, h, false, Y.gu, 2 * F, GEMM_STORE_BF16, st));
-  CK(k_swiglu_fwd(L, T, F, Y.gu, Y.u, st));
-  RET(part_gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, st));
-  if (tp_peer(L)) {  // x[l+1] = x1 + sum P
-    RET(tp_reduce_peer(ctx, TP_RESID, Y.x1, nullptr, [&](Layout& M, TpArgs& a, int j) {
-      a.d0[j] = M.slot[si].x[li + 1];
-    }, st));
-  } else {
-    RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
-    duty_begin(ctx, 2, st);
-    CK(k_residual(L, (long long)T * h, Y.x1, L.part, S.x[li + 1], st));
+  {  // gate/up projection; SwiGLU fused into the epilogue when the kernel supports it
+    bool glu_done = false;
+    GemmDesc g{T, 2 * F, h, Y.a2, h, false, P.wgu, h, false, Y.gu, 2 * F, GEMM_STORE_BF16};
+    g.f32 = L.f32;
+    if (!L.f32) {
+      g.glu = 1;
+      g.aux = Y.u;
+      g.glu_done = &glu_done;
+    }
+    CK(gemm_bf16(g, st));
+    if (!glu_done) CK(k_swiglu_fwd(L, T, F, Y.gu, Y.u, st));
+  }
+  if (fuse_res) {  // x[l+1] = bf16(x1 + u W_d^T) in the epilogue
+    GemmDesc g{T, h, F, Y.u, F, false, P.wd, h, true, S.x[li + 1], h, GEMM_STORE_BF16};
+    g.res = Y.x1;
+    g.ldr = h;
+    CK(gemm_bf16(g, st));
     duty_end(ctx, st);
+  } else {
+    RET(part_gemm(ctx, T, h, F, Y.u, F, false, P.wd, h, true, st));
+    if (tp_peer(L)) {  // x[l+1] = x1 + sum P
+      RET(tp_reduce_peer(ctx, TP_RESID, Y.x1, nullptr, [&](Layout& M, TpArgs& a, int j) {
+        a.d0[j] = M.slot[si].x[li + 1];
+      }, st));
+    } else {
+      RET(tp_allreduce(ctx, L.part, (size_t)T * h, ncclSum, st));
+      duty_begin(ctx, 2, st);
+      CK(k_residual(L, (long long)T * h, Y.x1, L.part, S.x[li + 1], st));
+      duty_end(ctx, st);
+    }
   }
   return MALLEUS_OK;
 }
@@ -1019,9 +1056,20 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   uint16_t* dx1 = L.dxc;
   // MLP
   duty_begin(ctx, 3, st);
-  RET(gemm(ctx, T, F, h, dy, h, false, P.wd, h, false, L.du, F, GEMM_STORE_BF16, st));
-  RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
-  CK(k_swiglu_bwd(L, T, F, Y.gu, L.du, L.dgu, st));
+  {  // du = dy W_d with the SwiGLU backward fused into the epilogue (dgu straight from the GEMM)
+    bool glu_done = false;
+    GemmDesc g{T, F, h, dy, h, false, P.wd, h, false, L.du, F, GEMM_STORE_BF16};
+    g.f32 = L.f32;
+    if (!L.f32) {
+      g.glu = 2;
+      g.aux = L.dgu;
+      g.aux_in = Y.gu;
+      g.glu_done = &glu_done;
+    }
+    CK(gemm_bf16(g, st));
+    RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
+    if (!glu_done) CK(k_swiglu_bwd(L, T, F, Y.gu, L.du, L.dgu, st));
+  }
   RET(part_gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, st));
   if (tp_overlap(L)) {
     RET(tp_sum_begin(ctx, st));
@@ -1318,10 +1366,59 @@ malleus_status malleus_create(const malleus_model_cfg* cfg, int32_t rank, int32_
 
 malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode);
 
+// Failure detection and the failed state: see include/malleus.h.
+malleus_status malleus_wait(malleus_ctx* ctx, void* stream, int32_t timeout_ms) {
+  GUARD();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, st));
+  const auto t0 = std::chrono::steady_clock::now();
+  auto elapsed_ms = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
+  bool done = false;
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) { done = true; break; }
+    if (q != cudaErrorNotReady) { cudaEventDestroy(ev); CK(q); }
+    if (comm_status(false)) break;  // a device-side communication wait gave up
+    if (timeout_ms > 0 && elapsed_ms() > timeout_ms) break;
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  if (done && !comm_status(false)) {
+    cudaEventDestroy(ev);
+    return MALLEUS_OK;
+  }
+  // failure path: release our spin-waits, abort every NCCL communicator (their kernels exit), drain
+  const double waited = elapsed_ms();
+  comm_abort(1u);
+  if (ctx->L && ctx->L->tp_comm) { ncclCommAbort(ctx->L->tp_comm); ctx->L->tp_comm = nullptr; }
+  if (ctx->world_comm) { ncclCommAbort(ctx->world_comm); ctx->world_comm = nullptr; }
+  const auto t1 = std::chrono::steady_clock::now();
+  while (cudaEventQuery(ev) == cudaErrorNotReady &&
+         std::chrono::steady_clock::now() - t1 < std::chrono::seconds(30))
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
+  cudaEventDestroy(ev);
+  cudaGetLastError();
+  comm_abort(0u);
+  comm_status(true);
+  ctx->sticky = true;
+  ctx->failed = true;
+  char msg[256];
+  snprintf(msg, sizeof msg,
+           "rank %d: communication did not complete within %.0f ms (PAPER.md:745 failure threshold); the context "
+           "is failed: destroy it and resume the surviving GPUs from the latest checkpoint (PAPER.md:735)",
+           ctx->rank, waited);
+  ctx->err = msg;
+  return MALLEUS_E_TIMEOUT;
+}
+
 malleus_status malleus_destroy(malleus_ctx* ctx) {
   if (!ctx) return MALLEUS_E_ARG;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  cudaGetLastError();
   if (ctx->L) free_layout(ctx, ctx->L.get());
   if (ctx->world_comm) ncclCommDestroy(ctx->world_comm);
   for (auto& e : ctx->ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }

@@ -26,9 +26,12 @@
 // it has seen ready(e + 1) from every member, i.e. after every member finished reading epoch e.
 // A member's output buffers (activations, or the fp32 sum) are written by peers in epoch e only
 // after this member's ready(e), i.e. after all its earlier stream work (readers of the previous
-// contents) completed.  A wait that exceeds 20 s traps (sticky CUDA error) instead of hanging.
+// contents) completed.  A wait that exceeds the communication timeout, or sees the process-wide
+// abort word (malleus_wait's failure path), gives up: it sets the status word and the
+// kernel returns without completing the reduction (kernels.h CommGuard).
 #include <cuda_bf16.h>
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include "kernels.h"
 
@@ -54,13 +57,23 @@ __device__ __forceinline__ unsigned long long now_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ void wait_geq(const unsigned long long* p, unsigned long long target) {
-  if (ld_acquire_sys(p) >= target) return;
+// spin until *p >= target; false if the guard's abort word is set or the timeout passed (the status
+// word records it).  The host words are read over PCIe only every 256 polls.
+__device__ __forceinline__ bool wait_geq(const unsigned long long* p, unsigned long long target, const CommGuard& g) {
+  if (ld_acquire_sys(p) >= target) return true;
   const unsigned long long t0 = now_ns();
+  unsigned it = 0;
   while (ld_acquire_sys(p) < target) {
     __nanosleep(64);
-    if (now_ns() - t0 > 20000000000ull) __trap();  // a member never arrived: fail loudly
+    if ((++it & 255u) == 0u) {
+      const bool ab = g.abort && *g.abort != 0u;
+      if (ab || now_ns() - t0 > g.timeout_ns) {
+        if (g.status) atomicOr(g.status, 1u);
+        return false;
+      }
+    }
   }
+  return true;
 }
 
 __device__ __forceinline__ float4 ldcg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
@@ -98,7 +111,7 @@ template <int MODE, int K, int V, bool PB>
 __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_constant__ TpArgs a) {
   constexpr int KC = V >= 4 ? 2 : 3;
   __shared__ float sh[TPR_THREADS / 32];
-  __shared__ bool last;
+  __shared__ bool last, gave_up;
   const int k = K > 0 ? K : a.k;
   const int me = a.me, h = a.h, nv = h / 8;
   // optional per-call stamps (debugging aid): [start of CTA 0, CTA 0 saw every ready, last CTA's
@@ -106,15 +119,17 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
   unsigned long long* tr = a.trace ? a.trace + 4 * (a.epoch % TP_TRACE_CALLS) : nullptr;
   if (tr && threadIdx.x == 0 && blockIdx.x == 0) tr[0] = now_ns();
   if (threadIdx.x == 0) {
+    gave_up = false;
     // ready: only CTA 0 publishes (dispatched first, so it is resident whenever any CTA waits)
     if (blockIdx.x == 0) {
       __threadfence_system();
       for (int j = 0; j < k; ++j) st_release_sys(a.flags[j] + TPF_READY + me, a.epoch);
     }
-    for (int j = 0; j < k; ++j) wait_geq(a.flags[me] + TPF_READY + j, a.epoch);
+    for (int j = 0; j < k && !gave_up; ++j) gave_up = !wait_geq(a.flags[me] + TPF_READY + j, a.epoch, a.guard);
     if (tr && blockIdx.x == 0) tr[1] = now_ns();
   }
   __syncthreads();
+  if (gave_up) return;  // a member never arrived (failure path): the status word says so
   const int r0 = a.uneven ? a.row0[me] : (int)((long long)me * a.T / k);
   const int r1 = a.uneven ? a.row0[me + 1] : (int)((long long)(me + 1) * a.T / k);
   for (int row = r0 + blockIdx.x; row < r1; row += gridDim.x) {
@@ -242,13 +257,16 @@ __global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_
     if (tr) tr[2] = now_ns();
     __threadfence_system();
     for (int j = 0; j < k; ++j) st_release_sys(a.flags[j] + TPF_DONE + me, a.epoch);
-    for (int j = 0; j < k; ++j) wait_geq(a.flags[me] + TPF_DONE + j, a.epoch);
+    for (int j = 0; j < k; ++j)
+      if (!wait_geq(a.flags[me] + TPF_DONE + j, a.epoch, a.guard)) break;
     __threadfence_system();
     if (tr) tr[3] = now_ns();
   }
 }
 
 }  // namespace
+
+static unsigned* g_guard_host = nullptr;  // [abort, status], mapped pinned host memory
 
 unsigned long long* tp_trace_buffer(int member) {
   static unsigned long long* buf = nullptr;
@@ -269,7 +287,43 @@ void tp_rows(const TpArgs& a, int me, int* r0, int* r1) {
   *r1 = a.uneven ? a.row0[me + 1] : (int)((long long)(me + 1) * a.T / a.k);
 }
 
-cudaError_t tp_reduce(const TpArgs& a, cudaStream_t st) {
+CommGuard comm_guard() {
+  static CommGuard g{nullptr, nullptr, 0};
+  static bool init = false;
+  if (!init) {
+    init = true;
+    const char* e = getenv("MALLEUS_COMM_TIMEOUT_MS");
+    g.timeout_ns = (unsigned long long)(e ? atof(e) : 20000.0) * 1000000ull;
+    unsigned* h = nullptr;
+    if (cudaHostAlloc((void**)&h, 2 * sizeof(unsigned), cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
+      h[0] = h[1] = 0u;
+      unsigned* d = nullptr;
+      if (cudaHostGetDevicePointer((void**)&d, h, 0) == cudaSuccess) {
+        g.abort = d;
+        g.status = d + 1;
+        g_guard_host = h;
+      }
+    }
+    cudaGetLastError();
+  }
+  return g;
+}
+void comm_abort(unsigned v) {
+  comm_guard();
+  if (g_guard_host) reinterpret_cast<volatile unsigned*>(g_guard_host)[0] = v;
+}
+unsigned comm_status(bool clear) {
+  comm_guard();
+  if (!g_guard_host) return 0u;
+  volatile unsigned* h = g_guard_host;
+  const unsigned s = h[1];
+  if (clear) h[1] = 0u;
+  return s;
+}
+
+cudaError_t tp_reduce(const TpArgs& a0, cudaStream_t st) {
+  TpArgs a = a0;
+  a.guard = comm_guard();
   if (a.k < 2 || a.k > MAX_TP || a.me < 0 || a.me >= a.k || a.h % 8 || a.h > 8 * TPR_MAXV * TPR_THREADS ||
       a.T <= 0 || a.epoch == 0)
     return cudaErrorInvalidValue;

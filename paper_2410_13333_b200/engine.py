@@ -6,6 +6,8 @@ the NCCL unique id; every step of the hot path runs inside the library.
 from __future__ import annotations
 
 import ctypes as C
+import glob
+import json
 import os
 
 import numpy as np
@@ -26,6 +28,17 @@ def name_to_id(name: str) -> int:
         return L.T_LM_HEAD
     layer, t = name.split(".")
     return int(layer) * 16 + ("g1", "wq", "wk", "wv", "wo", "g2", "wg", "wu", "wd").index(t)
+
+
+def _numel(cfg, name: str) -> int:
+    h, nd, F, V = cfg.hidden, cfg.n_heads * cfg.head_dim, cfg.ffn, cfg.vocab
+    if name in ("E", "Wlm"):
+        return V * h
+    if name == "gf":
+        return h
+    t = name.split(".")[1]
+    return {"g1": h, "g2": h, "wq": nd * h, "wk": nd * h, "wv": nd * h, "wo": nd * h,
+            "wg": F * h, "wu": F * h, "wd": F * h}[t]
 
 
 def tensor_names(cfg):
@@ -114,6 +127,91 @@ class Engine:
         check(L.lib.malleus_read_local(self.ctx, tid, kind, out.ctypes.data, ranges, C.byref(nr), C.byref(ne)),
               self.ctx, "read")
         return [(ranges[2 * i], ranges[2 * i + 1]) for i in range(nr.value)], out[:ne.value]
+
+    # ------------------------------------------------------------------ checkpoint
+    _KINDS = (("param", L.KIND_PARAM), ("master", L.KIND_MASTER), ("m", L.KIND_ADAM_M), ("v", L.KIND_ADAM_V))
+
+    def save_checkpoint(self, path: str, step: int):
+        """Collective over the caller's ranks (each writes its own file): every rank stores its OWNED
+        pieces (ZeRO-1, reading R9) of fp32 master / m / v and the bf16 (fp32 in parity mode) params
+        of the same element ranges, so the files partition the model state exactly once and can be
+        loaded onto any other plan or world size (the surviving GPUs).
+        Format: <path>/rank<r>.npz with '<tensor>|<kind>|ranges' (int64 [n, 2] flat element ranges)
+        and '<tensor>|<kind>|vals'; <path>/meta.json (step, world, dtype, model shape) from rank 0."""
+        os.makedirs(path, exist_ok=True)
+        torch.cuda.synchronize(self.device)
+        arrs = {}
+        for name in tensor_names(self.cfg):
+            owned, master = self.read(name, L.KIND_MASTER)
+            if not owned:
+                continue
+            held, param = self.read(name, L.KIND_PARAM)
+            pv = []
+            for e0, e1 in owned:  # params of the owned ranges (owned pieces lie inside held rows)
+                off = 0
+                for h0, h1 in held:
+                    if h0 <= e0 and e1 <= h1:
+                        pv.append(param[off + e0 - h0: off + e1 - h0])
+                        break
+                    off += h1 - h0
+                else:
+                    raise RuntimeError(f"owned range {e0, e1} of {name} not held")
+            rg = np.asarray(owned, dtype=np.int64).reshape(-1, 2)
+            arrs[f"{name}|param|vals"] = np.concatenate(pv)
+            arrs[f"{name}|master|vals"] = master
+            for tag, kind in self._KINDS[2:]:
+                _, vals = self.read(name, kind)
+                arrs[f"{name}|{tag}|vals"] = vals
+            arrs[f"{name}|ranges"] = rg
+        np.savez(os.path.join(path, f"rank{self.rank}.npz"), **arrs)
+        if self.rank == 0:
+            c = self.cfg
+            meta = {"step": int(step), "world": self.world, "dtype": self.dtype,
+                    "model": [c.n_layers, c.hidden, c.n_heads, c.head_dim, c.ffn, c.vocab, c.seq_len]}
+            with open(os.path.join(path, "meta.json"), "w") as f:
+                json.dump(meta, f)
+
+    def load_checkpoint(self, path: str) -> int:
+        """Load a checkpoint written by save_checkpoint (on any plan / world) into this rank's current
+        plan: the logical tensors are assembled from every rank file (each element exactly once) and
+        written with write_tensor, PARAM first (it resets master / m / v), then MASTER, ADAM_M, ADAM_V.
+        Returns the step stored in meta.json."""
+        meta = json.load(open(os.path.join(path, "meta.json")))
+        c = self.cfg
+        if meta["model"] != [c.n_layers, c.hidden, c.n_heads, c.head_dim, c.ffn, c.vocab, c.seq_len] or \
+                meta["dtype"] != self.dtype:
+            raise ValueError("checkpoint model shape / dtype does not match this engine")
+        files = [np.load(f) for f in sorted(glob.glob(os.path.join(path, "rank*.npz")))]
+        for name in tensor_names(c):
+            n = _numel(c, name)
+            full = {tag: np.zeros(n, dtype=np.float32) for tag, _ in self._KINDS}
+            pbits = self.dtype == "bf16"
+            full["param"] = np.zeros(n, dtype=np.uint16 if pbits else np.float32)
+            seen = np.zeros(n, dtype=np.int32)
+            for f in files:
+                key = f"{name}|ranges"
+                if key not in f:
+                    continue
+                off = 0
+                vals = {tag: f[f"{name}|{tag}|vals"] for tag, _ in self._KINDS}
+                for e0, e1 in f[key]:
+                    for tag in vals:
+                        full[tag][e0:e1] = vals[tag][off: off + e1 - e0]
+                    seen[e0:e1] += 1
+                    off += e1 - e0
+            if not np.all(seen == 1):
+                raise ValueError(f"checkpoint does not cover {name} exactly once")
+            for tag, kind in self._KINDS:
+                a = np.ascontiguousarray(full[tag])
+                check(L.lib.malleus_write_tensor(self.ctx, name_to_id(name), kind, a.ctypes.data), self.ctx,
+                      f"write_tensor {name} {tag}")
+        return int(meta["step"])
+
+    def wait(self, timeout_ms: int, stream=None):
+        """Failure detector: raises _lib.CommTimeout when the enqueued work does not
+        finish within timeout_ms; the context is then failed (destroy it, resume from a checkpoint)."""
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        check(L.lib.malleus_wait(self.ctx, st, int(timeout_ms)), self.ctx, "wait")
 
     # ------------------------------------------------------------------ step
     def adam(self, step: int, apply_update: bool = True, **kw):

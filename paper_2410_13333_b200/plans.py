@@ -29,6 +29,9 @@ def plan(pipes, b, B, standby=(), plan_id=0):
             "standby": list(standby)}
 
 
+plan_fn = plan  # alias for helpers whose arguments shadow the name
+
+
 def pipe(stages, n_micro):
     return {"stages": stages, "n_micro": n_micro}
 
@@ -259,6 +262,113 @@ def plan_from_rates(cfg, plan, rates: dict, deadband: float = 0.05):
         for pp, m in zip(p["pipes"], _minmax(total_m, y)):
             pp["n_micro"] = m
     return p
+
+
+# TP efficiency per group size (the paper's rho_n: "the coefficient of efficiency
+# degradation when the group consists of n GPUs ... profiled and computed beforehand"), as time per
+# unit of work relative to one GPU: measured on B200 with the C2 shape (round-1 T0 runs):
+# TP1 203.5 ms / step, TP2 120.3 ms (203.5 / (2 x 120.3) = 0.85), the TP-4 stage 92.4 ms (0.55).
+TP_EFF = {1: 1.0, 2: 0.85, 3: 0.7, 4: 0.55}
+
+
+def _group_cost(cfg, st, xr, last, eff):
+    """Per-micro-batch time of a stage after a min-max re-split over its members (reading R8's
+    group rate with the TP efficiency of its size), in FLOP units at rate 1."""
+    k = len(xr)
+    s2 = dict(st)
+    if k > 1:
+        s2["heads"] = _heads_split(cfg.n_heads, xr)
+        s2["ffn"] = _ffn_split(cfg.ffn, xr, 128 if cfg.ffn // 128 >= 4 * k else 16)
+        s2["vocab"] = _vocab_split(cfg.vocab, xr, 128 if cfg.vocab // 128 >= 4 * k else 16)
+    else:
+        s2["heads"], s2["ffn"], s2["vocab"] = [cfg.n_heads], [cfg.ffn], [cfg.vocab]
+    return stage_cost(cfg, s2, xr, last) / eff.get(k, min(eff.values())), s2
+
+
+def replan(cfg, base_plan, rates: dict, deadband: float = 0.05, eff=None, min_gain: float = 0.05):
+    """The planner run by the asynchronous re-planning loop and the standby
+    re-probe: always plans from the BASE grouping (all GPUs), so a GPU removed earlier
+    is re-admitted as soon as its probed rate recovers.  Per TP group it chooses which members to
+    keep — removing a heavy straggler when its group then runs faster by more than `min_gain`
+    (zero layers for groups with high straggling rates; here per member, the group
+    shrinks) — with the removed GPUs listed as standby; the kept members get min-max head / FFN /
+    vocab splits (reading R7), and the micro-batches are apportioned min-max over the pipelines'
+    per-micro-batch costs.  Layers and stage order are those of the base plan."""
+    import copy
+    import itertools
+    eff = TP_EFF if eff is None else eff
+    x = {r: (1.0 if v < 1.0 + deadband else float(v)) for r, v in rates.items()}
+    p = copy.deepcopy(base_plan)
+    p["plan_id"] = base_plan.get("plan_id", 0) + 1
+    standby = set(base_plan.get("standby", []))
+    y = []
+    for pp in p["pipes"]:
+        y_pipe = 0.0
+        for j, st in enumerate(pp["stages"]):
+            last = j == len(pp["stages"]) - 1
+            ranks = list(st["ranks"])
+            full_cost, best = _group_cost(cfg, st, [x[r] for r in ranks], last, eff)
+            best_cost, best_ranks = full_cost, ranks
+            for n_keep in range(len(ranks) - 1, 0, -1):
+                for keep in itertools.combinations(ranks, n_keep):
+                    c, s2 = _group_cost(cfg, st, [x[r] for r in keep], last, eff)
+                    if c < best_cost * (1.0 - min_gain) and c < full_cost * (1.0 - min_gain):
+                        best_cost, best, best_ranks = c, s2, list(keep)
+            standby |= set(ranks) - set(best_ranks)
+            st["ranks"] = best_ranks
+            st["heads"], st["ffn"], st["vocab"] = best["heads"], best["ffn"], best["vocab"]
+            y_pipe = max(y_pipe, best_cost)
+        y.append(y_pipe)
+    p["standby"] = sorted(standby)
+    total_m = sum(pp["n_micro"] for pp in p["pipes"])
+    if len(p["pipes"]) > 1:
+        for pp, m in zip(p["pipes"], _minmax(total_m, y)):
+            pp["n_micro"] = m
+    return p
+
+
+def survivor_plan(cfg, plan, failed, rates=None):
+    """Recovery plan after a failure ("loading the latest model checkpoint onto the
+    remaining GPUs and setting the straggling rates of unresponsive GPUs as infinite"): an infinite
+    rate removes a GPU from its group, so the failed ranks leave their stages; a pipeline that lost a
+    whole stage cannot run and is dropped (its micro-batches go to the others); the survivors are
+    renumbered 0..N'-1 in rank order and re-split min-max by `rates` (default 1).  Returns
+    (plan on the new ranks, {old rank: new rank})."""
+    import copy
+    failed = set(failed)
+    rates = rates or {}
+    pipes = []
+    for pp in plan["pipes"]:
+        stages = []
+        for st in pp["stages"]:
+            keep = [r for r in st["ranks"] if r not in failed]
+            if not keep:
+                break
+            stages.append((keep, list(st["layers"])))
+        else:
+            pipes.append(stages)
+    if not pipes:
+        raise ValueError("no pipeline survives the failure")
+    survivors = sorted({r for stages in pipes for keep, _ in stages for r in keep} |
+                       (set(plan.get("standby", [])) - failed))
+    remap = {r: i for i, r in enumerate(survivors)}
+    out_pipes, y = [], []
+    for stages in pipes:
+        sts, y_pipe = [], 0.0
+        for j, (keep, layers) in enumerate(stages):
+            xr = [float(rates.get(r, 1.0)) for r in keep]
+            last = j == len(stages) - 1
+            c, s2 = _group_cost(cfg, {"layers": layers}, xr, last, TP_EFF)
+            sts.append(stage([remap[r] for r in keep], s2["heads"], s2["ffn"], s2["vocab"], layers))
+            y_pipe = max(y_pipe, c)
+        out_pipes.append(sts)
+        y.append(y_pipe)
+    total_m = sum(pp["n_micro"] for pp in plan["pipes"])
+    ms = _minmax(total_m, y) if len(out_pipes) > 1 else [total_m]
+    new = plan_fn([pipe(sts, m) for sts, m in zip(out_pipes, ms)], plan["micro_batch"], plan["global_batch"],
+                  standby=[remap[r] for r in plan.get("standby", []) if r not in failed],
+                  plan_id=plan.get("plan_id", 0) + 1)
+    return copy.deepcopy(new), remap
 
 
 # ----------------------------------------------------------------------------- named workloads

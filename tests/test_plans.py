@@ -178,3 +178,85 @@ def test_member_flops_sum_to_the_step():
         p = Pl.ladder_plan(cfg, n, 16, straggle=False)
         tot = sum(Pl.member_flops(cfg, p, r) for r in range(n))
         assert tot == pytest.approx(bench.flops_per_token(cfg) * 16 * cfg.seq_len, rel=1e-12)
+
+
+# ---- the asynchronous re-planner (plans.replan): standby removal and re-admission
+def _rates(xs, n=4):
+    return {r: xs.get(r, 1.0) for r in range(n)}
+
+
+def test_replan_uniform_is_base():
+    cfg = C2_7B_SLICE
+    base = Pl.ladder_plan(cfg, 4, 16, straggle=False)
+    p = Pl.replan(cfg, base, _rates({}))
+    validate(cfg, p, 4)
+    assert p["pipes"] == base["pipes"] and p["standby"] == []
+
+
+@pytest.mark.parametrize("xs", [{1: 1.5}, {3: 3.0}, {1: 2.0, 3: 1.5}, {0: 1.3, 2: 2.5}])
+def test_replan_moderate_stragglers_keep_every_gpu(xs):
+    """Uneven splits absorb moderate stragglers: nobody is removed, the min-max splits follow x."""
+    cfg = C2_7B_SLICE
+    base = Pl.ladder_plan(cfg, 4, 16, straggle=False)
+    p = Pl.replan(cfg, base, _rates(xs))
+    validate(cfg, p, 4)
+    assert p["standby"] == []
+    for pp in p["pipes"]:
+        st = pp["stages"][0]
+        xr = [xs.get(r, 1.0) for r in st["ranks"]]
+        slow = max(range(len(xr)), key=lambda k: xr[k])
+        if xr[slow] > 1.05:
+            assert st["heads"][slow] < cfg.n_heads // 2
+    assert sum(pp["n_micro"] for pp in p["pipes"]) == 16
+
+
+def test_replan_removes_heavy_straggler_and_readmits():
+    """x = 12 (the paper's level-3 rate) in a TP-2 group: with the measured TP efficiency the
+    group runs faster without it, so it goes to standby; when its (re-)probed rate recovers the
+    next replan from the base grouping re-admits it."""
+    cfg = C2_7B_SLICE
+    base = Pl.ladder_plan(cfg, 4, 16, straggle=False)
+    p = Pl.replan(cfg, base, _rates({3: 12.0}))
+    validate(cfg, p, 4)
+    assert p["standby"] == [3]
+    assert [st["ranks"] for st in p["pipes"][1]["stages"]] == [[2]]
+    assert p["pipes"][0]["n_micro"] > p["pipes"][1]["n_micro"]  # the shrunk pipeline takes fewer micro-batches
+    q = Pl.replan(cfg, base, _rates({}))
+    validate(cfg, q, 4)
+    assert q["standby"] == [] and q["pipes"] == base["pipes"]
+
+
+def test_replan_removal_only_when_it_pays():
+    """Removal is chosen iff the group's cost (min-max split, TP efficiency of its size) drops by
+    more than min_gain; with TP efficiency 1 (no TP overhead) keeping every GPU is never worse."""
+    cfg = C2_7B_SLICE
+    base = Pl.ladder_plan(cfg, 4, 16, straggle=False)
+    p = Pl.replan(cfg, base, _rates({3: 12.0}), eff={1: 1.0, 2: 1.0})
+    assert p["standby"] == []
+
+
+# ---- recovery after a failure (PAPER.md:735): survivors re-planned with x = infinity for the lost GPUs
+@pytest.mark.parametrize("name,failed", [("P1", [1]), ("P2", [0]), ("P4", [1]), ("P4", [2, 3]), ("P6", [2]),
+                                         ("P5", [2]), ("P9", [3])])
+def test_survivor_plan_valid(name, failed):
+    cfg = C1_TINY
+    p = Pl.plan_matrix_c1(cfg)[name]
+    world = Pl.world_of(p)
+    q, remap = Pl.survivor_plan(cfg, p, failed)
+    validate(cfg, q, len(remap))
+    assert set(remap) == set(range(world)) - set(failed)
+    assert sorted(remap.values()) == list(range(len(remap)))
+    assert sum(pp["n_micro"] for pp in q["pipes"]) * q["micro_batch"] == q["global_batch"]
+    used = {r for pp in q["pipes"] for st in pp["stages"] for r in st["ranks"]}
+    assert used | set(q["standby"]) == set(range(len(remap)))
+
+
+def test_survivor_plan_drops_broken_pipeline():
+    """A pipeline that lost a whole stage cannot run: its micro-batches move to the others."""
+    cfg = C1_TINY
+    p = Pl.plan_matrix_c1(cfg)["P4"]  # pipe0 = TP2 {0, 1}, pipe1 = TP2 {2, 3}
+    q, remap = Pl.survivor_plan(cfg, p, [0, 1])
+    assert len(q["pipes"]) == 1 and q["pipes"][0]["n_micro"] * q["micro_batch"] == q["global_batch"]
+    assert remap == {2: 0, 3: 1}
+    with pytest.raises(ValueError):
+        Pl.survivor_plan(cfg, Pl.plan_matrix_c1(cfg)["P1"], [0, 1])

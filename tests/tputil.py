@@ -53,9 +53,10 @@ class Group:
         for d in set(self.devices):
             torch.cuda.synchronize(d)
 
-    def launch(self, mode: int, x=None, g=None, eps: float = 1e-5) -> None:
+    def launch(self, mode: int, x=None, g=None, eps: float = 1e-5, skip=()) -> None:
         """One reduction of the partials in buffer (epoch + 1) & 1; all members launched
-        asynchronously, each on its own stream (after the device's current stream)."""
+        asynchronously, each on its own stream (after the device's current stream).  Members in
+        `skip` are not launched (an unresponsive member, for the failure-detection tests)."""
         self.epoch += 1
         buf = self.epoch & 1
         parts = _ptrs(self.part[buf])
@@ -67,6 +68,8 @@ class Group:
         else:
             d0, d1, d2 = _ptrs(self.x1), None, None
         for j in range(self.k):
+            if j in skip:
+                continue
             dj = self.devices[j]
             with torch.cuda.device(dj):
                 self.streams[j].wait_stream(torch.cuda.current_stream(dj))

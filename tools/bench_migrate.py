@@ -3,8 +3,8 @@
 C5 (BASELINE.json configs[4]): LLaMA-110B-shaped 4-layer slice (h 8192, 64 heads, ffn 49152,
 V 32000, seq 4096, B 16), DP2 x TP4 on 8 GPUs; plan A has the 2x straggler on GPU 3 (pipeline 0,
 heads 19/19/19/7), plan B on GPU 6 (pipeline 1).  With --gpus 4 the same shapes run DP2 x TP2 and
-the straggler moves GPU 1 -> GPU 3.  Timed: malleus_migrate(A -> B) (4-layer packs, grouped NCCL
-P2P) between barriers; GB/s = bytes moved over all ranks / max seconds over ranks.
+the straggler moves GPU 1 -> GPU 3.  Timed: malleus_migrate(A -> B) (peer pulls over NVLink by
+default; 4-layer packs with grouped NCCL P2P, under MALLEUS_NO_P2P=1) between barriers; GB/s = bytes moved over all ranks / max seconds over ranks.
 Parameter values are not initialised (the copy moves bytes regardless of content); bit-exactness is
 tests/test_gpu_migrate.py's job.
   python -m torch.distributed.run --nproc-per-node N tools/bench_migrate.py --gpus N

@@ -1,17 +1,31 @@
 """Dynamic straggler trace, end to end on 4 B200 (the PAPER.md:822-825
 S1-S6 experiment at 4-GPU scale): a sequence of straggler situations is injected (DUTY mode) while
-training continues; at every transition the Malleus loop runs — probe the per-rank speed
-(malleus_probe_speed), re-plan from the probed rates (plans.plan_from_rates:
-min-max splits and micro-batches, 5% dead band), migrate the model states (malleus_migrate,
-PAPER.md:731-733) — and the step time before (stale plan) and after (re-planned) is measured.
+training continues, and the Malleus loop reacts:
 
-  python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 tools/trace_run.py
+  * profiler: every situation is probed with malleus_probe_speed; the probe is
+    world-collective, so GPUs on standby are re-probed too and are re-admitted when
+    their rate recovers; rates are x_g = t_g / t_ref with t_ref the median probe of a start-up
+    calibration without injection (reading R12); a change beyond 5% triggers re-planning;
+  * planner, asynchronous: rank 0 runs plans.replan (min-max splits per group,
+    removal of a heavy straggler when its group runs faster without it, micro-batches min-max over
+    the pipelines) on a background thread while all ranks keep training on the stale plan; after
+    every step the ranks agree (one broadcast) whether the new plan is ready, and migrate at that
+    step boundary (malleus_migrate);
+  * the step time with the stale plan and with the new plan is measured.
 
-Reports per situation: injected and probed x, the plan, T_stale, T_replanned, migration time, and
+  python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 tools/trace_run.py [--sync]
+
+--sync: the round-1 loop (plan_from_rates between steps, no overlap, no removal).
+Reports per situation: injected and probed x, the plan and standby set, planner wall time and the
+number of steps trained while it ran, T_stale, T_replanned, migration time / bytes, and
 R_actual = T_replanned / T0 against R_opt = N / sum(1/x) (the paper's theoretic optimum)."""
+import argparse
+import concurrent.futures as cf
 import json
 import os
+import statistics
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -27,17 +41,23 @@ SITUATIONS = [  # rank -> x
     ("S2 rank1 2x", {1: 2.0}),
     ("S3 rank1 2x + rank3 1.5x", {1: 2.0, 3: 1.5}),
     ("S4 rank3 3x", {3: 3.0}),
-    ("S5 recovered", {}),
+    ("S5 rank3 12x (removed)", {3: 12.0}),
+    ("S6 recovered (re-admitted)", {}),
 ]
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sync", action="store_true")
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     assert world == 4, "the trace is defined for 4 GPUs (DP2 x TP2)"
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     cfg, B = C2_7B_SLICE, 16
-    plan = Pl.ladder_plan(cfg, world, B, b=1, straggle=False)
+    base = Pl.ladder_plan(cfg, world, B, b=1, straggle=False)
+    plan = base
     eng = Engine(cfg, rank, world, local)
     eng.apply(plan)
     eng.write_weights(make_weights(cfg, parity=False))
@@ -45,6 +65,11 @@ def main():
     dtok, dtgt = torch.tensor(tok, device="cuda"), torch.tensor(tgt, device="cuda")
     stream = torch.cuda.current_stream()
     step = [1]
+    pool = cf.ThreadPoolExecutor(max_workers=1) if rank == 0 else None
+
+    def one_step():
+        eng.train_step(dtok, dtgt, step=step[0], apply_update=2)
+        step[0] += 1
 
     def steps(n):
         torch.cuda.synchronize()
@@ -52,8 +77,7 @@ def main():
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(n):
-            eng.train_step(dtok, dtgt, step=step[0], apply_update=2)
-            step[0] += 1
+            one_step()
         b.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
@@ -63,29 +87,57 @@ def main():
 
     steps(3)  # warm-up
     t0 = steps(5)
+    t_ref = statistics.median(eng.probe(10))  # start-up calibration, no injection (reading R12)
+    x_prev = [1.0] * world
     rows = []
     for name, xs in SITUATIONS:
         x = xs.get(rank, 1.0)
         eng.set_slowdown(x, 2 if x > 1.0 else 0)
         steps(2)  # the DUTY timers learn the segment durations
-        t_stale = steps(4)
-        probe = eng.probe(10)
-        ref = sorted(probe)[0]
-        x_probe = [p / ref for p in probe]
-        obj = [Pl.plan_from_rates(cfg, plan, {r: x_probe[r] for r in range(world)}) if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        new_plan = obj[0]
-        mig = eng.migrate(new_plan)
+        t_stale = steps(3)
+        probe = eng.probe(10)  # every rank, standby included
+        x_probe = [p / t_ref for p in probe]
+        trig = any(abs(a - b) / b > 0.05 + 1e-12 for a, b in zip(x_probe, x_prev))
+        x_prev = x_probe
+        plan_s, stale_steps = 0.0, 0
+        if args.sync:
+            obj = [Pl.plan_from_rates(cfg, plan, {r: x_probe[r] for r in range(world)}) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            new_plan = obj[0]
+        else:
+            fut = None
+            if rank == 0:
+                def planner(rates):
+                    t = time.perf_counter()
+                    p = Pl.replan(cfg, base, rates)
+                    return p, time.perf_counter() - t
+                fut = pool.submit(planner, {r: x_probe[r] for r in range(world)})
+            while True:  # keep training on the stale plan until the planner is done
+                one_step()
+                stale_steps += 1
+                flag = torch.tensor([1 if (rank == 0 and fut.done()) else 0])
+                dist.broadcast(flag, src=0)
+                if flag.item():
+                    break
+            obj = [fut.result() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            new_plan, plan_s = obj[0]
+        changed = json.dumps(new_plan["pipes"]) != json.dumps(plan["pipes"]) or new_plan["standby"] != plan["standby"]
+        mig = {"total_seconds": 0.0, "bytes_recv": 0}
+        if changed:
+            mig = eng.migrate(new_plan)
+            plan = new_plan
         allm = [None] * world
         dist.all_gather_object(allm, mig)
         steps(2)
         t_new = steps(4)
-        plan = new_plan
         xs_all = [xs.get(r, 1.0) for r in range(world)]
         r_opt = world / sum(1.0 / v for v in xs_all)
         rows.append({
-            "situation": name, "x_injected": xs_all, "x_probed": [round(v, 3) for v in x_probe],
-            "plan": [{"m": p["n_micro"], "heads": [s["heads"] for s in p["stages"]]} for p in plan["pipes"]],
+            "situation": name, "x_injected": xs_all, "x_probed": [round(v, 3) for v in x_probe], "triggered": trig,
+            "plan": [{"m": p["n_micro"], "ranks": [s["ranks"] for s in p["stages"]],
+                      "heads": [s["heads"] for s in p["stages"]]} for p in plan["pipes"]],
+            "standby": plan["standby"], "planner_s": round(plan_s, 4), "steps_during_planning": stale_steps,
             "ms_stale_plan": round(t_stale, 2), "ms_replanned": round(t_new, 2),
             "migration_s": round(max(m["total_seconds"] for m in allm), 4),
             "migration_GB": round(sum(m["bytes_recv"] for m in allm) / 1e9, 3),
@@ -96,8 +148,12 @@ def main():
         if rank == 0:
             print(json.dumps(rows[-1]), flush=True)
     if rank == 0:
-        print(json.dumps({"T0_ms": round(t0, 2), "T0_tokens_s": round(B * cfg.seq_len / (t0 / 1e3)),
-                          "situations": len(rows)}), flush=True)
+        summary = {"T0_ms": round(t0, 2), "T0_tokens_s": round(B * cfg.seq_len / (t0 / 1e3)),
+                   "situations": len(rows), "mode": "sync" if args.sync else "async planner + standby re-probe"}
+        print(json.dumps(summary), flush=True)
+        if args.out:
+            json.dump({"summary": summary, "rows": rows}, open(args.out, "w"), indent=1)
+    eng.set_slowdown(1.0, 0)
     eng.close()
     dist.destroy_process_group()
 
