@@ -159,8 +159,9 @@ malleus_status malleus_create(const malleus_model_cfg* cfg, int32_t rank, int32_
  * reductions, pipeline transfers or gradient exchange wait for an unresponsive GPU does not finish.
  * On timeout — or when a device-side communication wait of the peer-memory TP reduction gave up
  * after MALLEUS_COMM_TIMEOUT_MS (default 20000) — the context enters the failed state: the device
- * spin-waits are released (process-wide abort word), every NCCL communicator of the context is
- * aborted (ncclCommAbort), the stream is drained, and MALLEUS_E_TIMEOUT is returned; every later call
+ * spin-waits are released (process-wide abort word, kept set until malleus_destroy has drained the
+ * device), every NCCL communicator of the context is aborted (ncclCommAbort), the stream is drained,
+ * and MALLEUS_E_TIMEOUT is returned; every later call
  * except malleus_last_error / malleus_destroy returns MALLEUS_E_STATE.  Recovery is
  * the caller's: destroy the context, create one on the surviving GPUs, apply a plan computed with
  * the unresponsive GPUs' straggling rates set to infinity, and load the latest checkpoint
@@ -332,6 +333,10 @@ malleus_status malleus_k_rmsnorm_fwd(int32_t T, int32_t h, const void* x, const 
 malleus_status malleus_k_rmsnorm_bwd(int32_t T, int32_t h, const void* x, const void* g,
                                      const float* rstd, const float* dy, const void* dres,
                                      void* dx_out, float* dg_accum, void* stream);
+/* The same with a bf16 input gradient dy [T, h] (the TP sums and TP-1 dgrad outputs of the step). */
+malleus_status malleus_k_rmsnorm_bwd16(int32_t T, int32_t h, const void* x, const void* g, const float* rstd,
+                                       const void* dy, const void* dres, void* dx_out, float* dg_accum,
+                                       void* stream);
 /* Causal attention on qkv [T, 3*n*d] (q | k | v column blocks, T = nb * s tokens, sequences of
  * length s), RoPE applied in place to q and k first (fwd) / to dq, dk last (bwd).
  * o: bf16 [T, n*d]; lse: fp32 [nb, n, s]. */

@@ -32,15 +32,16 @@ def _layer_fwd(cfg, P, l, st, x, phi, Bn, s):
     mem = []
     for k in range(len(st["ranks"])):
         r0, r1_ = member_rows(cfg, st, f"{l}.wq", k)
-        nk = (r1_ - r0) // d
-        hd = lambda t: t.reshape(Bn, s, nk, d).transpose(0, 2, 1, 3)
-        q = M.rope_fwd(hd(a @ g("wq")[r0:r1_].T), phi)
-        kk = M.rope_fwd(hd(a @ g("wk")[r0:r1_].T), phi)
-        v = hd(a @ g("wv")[r0:r1_].T)
+        c0, c1 = member_rows(cfg, st, f"{l}.wk", k)  # the member's KV heads (GQA groups)
+        nk, nkv = (r1_ - r0) // d, (c1 - c0) // d
+        hd = lambda t, n_: t.reshape(Bn, s, n_, d).transpose(0, 2, 1, 3)
+        q = M.rope_fwd(hd(a @ g("wq")[r0:r1_].T, nk), phi)
+        kk = M.rope_fwd(hd(a @ g("wk")[c0:c1].T, nkv), phi)
+        v = hd(a @ g("wv")[c0:c1].T, nkv)
         o4, Pm = M.attention_fwd(q, kk, v)
         o = o4.transpose(0, 2, 1, 3).reshape(Bn, s, nk * d)
         part = part + o @ g("wo")[r0:r1_]
-        mem.append((r0, r1_, nk, q, kk, v, o4, Pm, o))
+        mem.append((r0, r1_, nk, q, kk, v, o4, Pm, o, c0, c1))
     x1 = x + part
     a2, r2 = M.rmsnorm_fwd(x1, g("g2"), cfg.rms_eps)
     part = np.zeros_like(x)
@@ -73,18 +74,18 @@ def _layer_bwd(cfg, P, l, st, saved, dx, phi, Bn, s, acc):
         acc[(k, f"{l}.g2")] += dg2
     dx1 = dx + dxn
     da = np.zeros_like(dx)
-    for k, (r0, r1_, nk, q, kk, v, o4, Pm, o) in enumerate(mem):
+    for k, (r0, r1_, nk, q, kk, v, o4, Pm, o, c0, c1) in enumerate(mem):
         hd = lambda t: t.reshape(Bn, s, nk, d).transpose(0, 2, 1, 3)
-        uh = lambda t: t.transpose(0, 2, 1, 3).reshape(Bn, s, nk * d)
+        uh = lambda t: t.transpose(0, 2, 1, 3).reshape(Bn, s, t.shape[1] * d)
         do = dx1 @ g("wo")[r0:r1_].T
         acc[(k, f"{l}.wo")] += o.reshape(-1, nk * d).T @ dx1.reshape(-1, h)
         dq4, dk4, dv4 = M.attention_bwd(q, kk, v, o4, Pm, hd(do))
         dq, dk, dv = uh(M.rope_bwd(dq4, phi)), uh(M.rope_bwd(dk4, phi)), uh(dv4)
         af = a.reshape(-1, h)
         acc[(k, f"{l}.wq")] += dq.reshape(-1, nk * d).T @ af
-        acc[(k, f"{l}.wk")] += dk.reshape(-1, nk * d).T @ af
-        acc[(k, f"{l}.wv")] += dv.reshape(-1, nk * d).T @ af
-        da = da + dq @ g("wq")[r0:r1_] + dk @ g("wk")[r0:r1_] + dv @ g("wv")[r0:r1_]
+        acc[(k, f"{l}.wk")] += dk.reshape(-1, c1 - c0).T @ af
+        acc[(k, f"{l}.wv")] += dv.reshape(-1, c1 - c0).T @ af
+        da = da + dq @ g("wq")[r0:r1_] + dk @ g("wk")[c0:c1] + dv @ g("wv")[c0:c1]
     dxn, dg1 = M.rmsnorm_bwd(x0, g("g1"), r1, da)
     for k in range(len(st["ranks"])):
         acc[(k, f"{l}.g1")] += dg1

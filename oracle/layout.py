@@ -65,6 +65,9 @@ def member_rows(cfg: ModelCfg, stage: dict, name: str, k: int):
         return 0, n_rows
     unit = {"heads": cfg.head_dim, "ffn": 1, "vocab": 1}[kind]
     vec = {"heads": stage["heads"], "ffn": stage["ffn"], "vocab": stage["vocab"]}[kind]
+    if name.endswith((".wk", ".wv")):  # GQA: a member holds the KV heads of its whole query-head groups
+        g = cfg.n_heads // getattr(cfg, "kv_heads", cfg.n_heads)
+        vec = [c // g for c in vec]
     r0 = unit * sum(vec[:k])
     return r0, r0 + unit * vec[k]
 
@@ -98,6 +101,8 @@ def validate(cfg: ModelCfg, plan: dict, world: int) -> None:
                 vec = st[key]
                 if len(vec) != ks or sum(vec) != total:
                     raise PlanError(f"{key} split must have one entry per member and sum to {total}")
+                if key == "heads":  # whole KV groups per member (GQA; 1 for MHA)
+                    gran = cfg.n_heads // getattr(cfg, "kv_heads", cfg.n_heads)
                 if any(v < gran or v % gran for v in vec):
                     raise PlanError(f"{key} split entries must be >= {gran} and multiples of {gran}")
             for r in st["ranks"]:

@@ -69,8 +69,22 @@ def rope_bwd(dq, phi):
     return rope_fwd(dq, -phi)
 
 
+def _expand_kv(t, n):
+    """GQA: [B, n_kv, s, d] -> [B, n, s, d], query head j reads KV head j // (n / n_kv) (LLaMA-2-70B
+    grouping: each KV head serves a block of consecutive query heads).  n_kv == n: unchanged."""
+    return np.repeat(t, n // t.shape[1], axis=1)
+
+
+def _reduce_kv(t, n_kv):
+    """Backward of _expand_kv: sum the gradients of each KV head's group of query heads."""
+    B, n, s, d = t.shape
+    return t.reshape(B, n_kv, n // n_kv, s, d).sum(axis=2)
+
+
 def attention_fwd(q, k, v):
-    """q,k,v [B, n, s, d].  S = q k^T/sqrt(d) + causal; P = softmax(S); o = P v."""
+    """q [B, n, s, d]; k, v [B, n_kv, s, d] (n_kv = n: MHA).  S = q k^T/sqrt(d) + causal;
+    P = softmax(S); o = P v."""
+    k, v = _expand_kv(k, q.shape[1]), _expand_kv(v, q.shape[1])
     d = q.shape[-1]
     s = q.shape[-2]
     S = (q @ np.swapaxes(k, -1, -2)) / np.sqrt(d)          # [B, n, s, s]
@@ -84,7 +98,10 @@ def attention_fwd(q, k, v):
 
 
 def attention_bwd(q, k, v, o, P, do):
-    """dV = P^T dO; dP = dO V^T; dS = P*(dP - rowsum(dO*O)); dQ = dS K/sqrt(d); dK = dS^T Q/sqrt(d)."""
+    """dV = P^T dO; dP = dO V^T; dS = P*(dP - rowsum(dO*O)); dQ = dS K/sqrt(d); dK = dS^T Q/sqrt(d).
+    GQA: K / V expanded to the query heads as in the forward, dK / dV summed over each group."""
+    n_kv = k.shape[1]
+    k, v = _expand_kv(k, q.shape[1]), _expand_kv(v, q.shape[1])
     d = q.shape[-1]
     dv = np.swapaxes(P, -1, -2) @ do
     dP = do @ np.swapaxes(v, -1, -2)
@@ -92,7 +109,7 @@ def attention_bwd(q, k, v, o, P, do):
     dS = P * (dP - D)
     dq = (dS @ k) / np.sqrt(d)
     dk = (np.swapaxes(dS, -1, -2) @ q) / np.sqrt(d)
-    return dq, dk, dv
+    return dq, _reduce_kv(dk, n_kv), _reduce_kv(dv, n_kv)
 
 
 def sigmoid(x):
@@ -137,10 +154,11 @@ def layer_fwd(cfg: ModelCfg, p, x0, phi):
     """One decoder layer (SURVEY §8(c) algorithm): p(name) -> that layer's tensor; x0 [Bn, s, h].
     Returns (x_out, saved activations for layer_bwd)."""
     n, d, eps = cfg.n_heads, cfg.head_dim, cfg.rms_eps
+    nkv = getattr(cfg, "kv_heads", n)
     a, r1 = rmsnorm_fwd(x0, p("g1"), eps)
     q = rope_fwd(_heads(a @ p("wq").T, n, d), phi)
-    k = rope_fwd(_heads(a @ p("wk").T, n, d), phi)
-    v = _heads(a @ p("wv").T, n, d)
+    k = rope_fwd(_heads(a @ p("wk").T, nkv, d), phi)
+    v = _heads(a @ p("wv").T, nkv, d)
     o4, Pm = attention_fwd(q, k, v)
     o = _unheads(o4)
     x1 = x0 + o @ p("wo")
@@ -174,9 +192,10 @@ def layer_bwd(cfg: ModelCfg, p, saved, dx, phi):
     dk = _unheads(rope_bwd(dk4, phi))
     dv = _unheads(dv4)
     a_f = a.reshape(-1, h)
+    kd = getattr(cfg, "kv_heads", n) * d
     g["wq"] = dq.reshape(-1, n * d).T @ a_f
-    g["wk"] = dk.reshape(-1, n * d).T @ a_f
-    g["wv"] = dv.reshape(-1, n * d).T @ a_f
+    g["wk"] = dk.reshape(-1, kd).T @ a_f
+    g["wv"] = dv.reshape(-1, kd).T @ a_f
     da = dq @ p("wq") + dk @ p("wk") + dv @ p("wv")
     dxn, g["g1"] = rmsnorm_bwd(x0, p("g1"), r1, da)
     return dx1 + dxn, g

@@ -109,6 +109,7 @@ _SIGS = {
     "malleus_k_gemm": ([i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, i32, vp], i32),
     "malleus_k_gemm_variant": ([i32], i32),
     "malleus_k_comm_abort": ([i32], i32),
+    "malleus_k_rmsnorm_bwd16": ([i32, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),
     "malleus_k_comm_status": ([i32], i32),
     "malleus_wait": ([vp, vp, i32], i32),
     "malleus_k_gemm_fused": ([i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, i32, vp, vp, vp, vp], i32),

@@ -37,6 +37,19 @@ extern "C" malleus_status malleus_k_gemm_fused(int32_t M, int32_t N, int32_t K, 
   return s;
 }
 
+extern "C" malleus_status malleus_k_rmsnorm_bwd16(int32_t T, int32_t h, const void* x, const void* g,
+                                                  const float* rstd, const void* dy, const void* dres, void* dx_out,
+                                                  float* dg_accum, void* stream) {
+  if (!x || !g || !rstd || !dy || !dx_out || !dg_accum) return MALLEUS_E_ARG;
+  float* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&scratch, rmsnorm_bwd_scratch_floats(T, h) * sizeof(float),
+                                  (cudaStream_t)stream);
+  if (e != cudaSuccess) return MALLEUS_E_CUDA;
+  e = rmsnorm_bwd(T, h, x, g, rstd, dy, dres, dx_out, dg_accum, scratch, (cudaStream_t)stream, true);
+  cudaFreeAsync(scratch, (cudaStream_t)stream);
+  return cu(e);
+}
+
 extern "C" malleus_status malleus_k_comm_abort(int32_t value) {
   comm_abort(value ? 1u : 0u);
   return MALLEUS_OK;

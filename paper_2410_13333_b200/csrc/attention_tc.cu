@@ -13,7 +13,8 @@
 // Both A operands come from TMEM ("ts" MMAs: Q copied once by the softmax warps, P in place), so the
 // only shared-memory operand traffic is K and V: measured on the previous version (Q and P as smem
 // operands) the tile loop was bound by shared-memory bandwidth (A + B of every MMA, P stores, TMA).
-// TMEM: S0 cols [0,128), S1 [128,256), O [256,384), row-max exchange [384,388), Q [448,512).
+// TMEM: S0 cols [0,128), S1 [128,256), O [256,384), Q [448,512).  The pair of warps sharing a row
+// exchanges row statistics through shared memory (the Q landing buffer, free once Q is in TMEM).
 // smem: Q 32 KB (TMA landing), 3 x K 32 KB, 3 x V 32 KB.
 // Output identical in layout to attention.cu: o [T, n*d] bf16, lse [nb, n, s] (natural log).
 #include <cuda.h>
@@ -89,7 +90,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
   uint64_t* o_done = bars + 19;                // [2] (PV of tile j completes on o_done[j & 1])
   uint64_t* q_tmem = bars + 21;                // Q copied into TMEM by the softmax warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
-  constexpr uint32_t COL_O = 256, COL_X = 384, COL_Q = 448;
+  constexpr uint32_t COL_O = 256, COL_Q = 448;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;
@@ -222,19 +223,14 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
       if (lane == 0) mbar_arrive(q_tmem);
     }
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory"); };
+    // the pair exchanges its partial row statistics through shared memory — the Q landing buffer,
+    // free once Q is in TMEM (every softmax warp copied its part before the first S was issued) —
+    // in two alternating slots: [slot][half][row]
+    float* xch = reinterpret_cast<float*>(sQ);
     auto exchange = [&](float mine, int slot) -> float {  // returns the partner's value
-      uint32_t v = __float_as_uint(mine);
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tbase + lane_off + COL_X + slot * 2 + half),
-                   "r"(v) : "memory");
-      tmem_wait_st();
-      tc_fence_before();
+      xch[(slot * 2 + half) * TQ + r] = mine;
       pair_sync();
-      tc_fence_after();
-      uint32_t o;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(o)
-                   : "r"(tbase + lane_off + COL_X + slot * 2 + (half ^ 1)) : "memory");
-      tmem_wait_ld();
-      return __uint_as_float(o);
+      return xch[(slot * 2 + (half ^ 1)) * TQ + r];
     };
     for (int i = 0; i < n_tiles; ++i) {
       const int sb = i & 1;
@@ -347,52 +343,45 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
-// One 128-wide fp32 TMEM row (this thread's lane) * scale -> bf16 global row, optionally rotated
-// by -phi (RoPE backward, half-split pairs (i, i+64); cs = this position's (cos, sin) row).
-__device__ __forceinline__ void store_row_rope(__nv_bfloat16* dst, uint32_t taddr, float scale, const float2* cs,
-                                               int c0 = 0, int c1 = 2) {
-#pragma unroll 1
-  for (int c = c0; c < c1; ++c) {
-    uint32_t ua[32], ub[32];
-    tmem_ld32(taddr + c * 32, ua);       // cols 32c ..      (i)
-    tmem_ld32(taddr + 64 + c * 32, ub);  // cols 64 + 32c .. (i + 64)
-    tmem_wait_ld();
-    float a[32], bb[32];
+// The (cos, sin) pairs of one 32-column chunk of this thread's row, loaded before the accumulator is
+// final so their latency overlaps the last MMAs (the epilogue then only waits for TMEM).
+__device__ __forceinline__ void load_cs32(const float2* cs_row, int c, float2 (&cs)[32]) {
+  const float4* p = reinterpret_cast<const float4*>(cs_row + c * 32);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      float x = __uint_as_float(ua[j]) * scale, y = __uint_as_float(ub[j]) * scale;
-      if (cs) {
-        const float2 t = cs[c * 32 + j];
-        const float x2 = x * t.x + y * t.y;
-        y = y * t.x - x * t.y;
-        x = x2;
-      }
-      a[j] = x;
-      bb[j] = y;
-    }
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      uint4 wa, wb;
-      wa.x = pack_bf16(a[8 * v], a[8 * v + 1]); wa.y = pack_bf16(a[8 * v + 2], a[8 * v + 3]);
-      wa.z = pack_bf16(a[8 * v + 4], a[8 * v + 5]); wa.w = pack_bf16(a[8 * v + 6], a[8 * v + 7]);
-      wb.x = pack_bf16(bb[8 * v], bb[8 * v + 1]); wb.y = pack_bf16(bb[8 * v + 2], bb[8 * v + 3]);
-      wb.z = pack_bf16(bb[8 * v + 4], bb[8 * v + 5]); wb.w = pack_bf16(bb[8 * v + 6], bb[8 * v + 7]);
-      reinterpret_cast<uint4*>(dst + c * 32)[v] = wa;
-      reinterpret_cast<uint4*>(dst + 64 + c * 32)[v] = wb;
-    }
+  for (int q = 0; q < 16; ++q) {
+    const float4 v = __ldg(p + q);
+    cs[2 * q] = make_float2(v.x, v.y);
+    cs[2 * q + 1] = make_float2(v.z, v.w);
   }
 }
-
-// write 32 consecutive bf16 (cols c0..c0+31 of row r) into a 2-panel K-major 128B-swizzled tile
-__device__ __forceinline__ void st_sw128_32(uint8_t* tile, int r, int c0, const float (&v)[32]) {
+// store_row_rope for the single chunk c with preloaded (cos, sin) (rope = false: no rotation)
+__device__ __forceinline__ void store_row_rope_pre(__nv_bfloat16* dst, uint32_t taddr, float scale, bool rope,
+                                                   const float2 (&cs)[32], int c) {
+  uint32_t ua[32], ub[32];
+  tmem_ld32(taddr + c * 32, ua);
+  tmem_ld32(taddr + 64 + c * 32, ub);
+  tmem_wait_ld();
+  float a[32], bb[32];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int col = c0 + q * 8;
-    const int panel = col >> 6, c16 = (col & 63) >> 3;
-    uint4 w;
-    w.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]); w.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-    w.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]); w.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-    *reinterpret_cast<uint4*>(tile + panel * PANEL + r * 128 + ((c16 ^ (r & 7)) << 4)) = w;
+  for (int j = 0; j < 32; ++j) {
+    float x = __uint_as_float(ua[j]) * scale, y = __uint_as_float(ub[j]) * scale;
+    if (rope) {
+      const float x2 = x * cs[j].x + y * cs[j].y;
+      y = y * cs[j].x - x * cs[j].y;
+      x = x2;
+    }
+    a[j] = x;
+    bb[j] = y;
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    uint4 wa, wb;
+    wa.x = pack_bf16(a[8 * v], a[8 * v + 1]); wa.y = pack_bf16(a[8 * v + 2], a[8 * v + 3]);
+    wa.z = pack_bf16(a[8 * v + 4], a[8 * v + 5]); wa.w = pack_bf16(a[8 * v + 6], a[8 * v + 7]);
+    wb.x = pack_bf16(bb[8 * v], bb[8 * v + 1]); wb.y = pack_bf16(bb[8 * v + 2], bb[8 * v + 3]);
+    wb.z = pack_bf16(bb[8 * v + 4], bb[8 * v + 5]); wb.w = pack_bf16(bb[8 * v + 6], bb[8 * v + 7]);
+    reinterpret_cast<uint4*>(dst + c * 32)[v] = wa;
+    reinterpret_cast<uint4*>(dst + 64 + c * 32)[v] = wb;
   }
 }
 
@@ -404,7 +393,6 @@ __device__ __forceinline__ void st_sw128_32(uint8_t* tile, int r, int c0, const 
 constexpr int HPANEL = 64 * 128;          // 64 rows x 128 B (one 64-column half of a 64-row tile)
 constexpr int SUB_STAGE = 4 * HPANEL;     // two 64-row x 128-col bf16 tiles (Q | dO or K | V)
 constexpr int NSUB1 = 4;                  // Q | dO ring depth (dK / dV kernel)
-constexpr int NSUB = 5;                   // K | V ring depth (dQ kernel)
 // measured (tools/attn_trace.py): a 32 KB TMA sub-tile load takes ~1.4 us under full load, so the ring
 // must cover load latency + MMA + compute: with 3 stages the loop ran at (that chain) / 3 per sub-tile
 
@@ -582,13 +570,15 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
       if (warp == 2 && lane == 0) stamp(6, it);
       if (lane == 0) stamp(8 + warp - 2, it);  // every compute warp's finish
     }
+    float2 csr[32];
+    if (rope_cs) load_cs32(rope_cs + (long long)key * 64, half, csr);
     mbar_wait(done, 0);
     if (warp == 2 && lane == 0) stamp(7, 1);
     tc_fence_after();
     __nv_bfloat16* dk = dqkv + (long long)(b * s + key) * 3 * nd + nd + head * DH;
     __nv_bfloat16* dv = dk + nd;
-    store_row_rope(dk, tbase + lane_off + 384, scale, rope_cs ? rope_cs + (long long)key * 64 : nullptr, half, half + 1);
-    store_row_rope(dv, tbase + lane_off + 256, 1.f, nullptr, half, half + 1);
+    store_row_rope_pre(dk, tbase + lane_off + 384, scale, rope_cs != nullptr, csr, half);
+    store_row_rope_pre(dv, tbase + lane_off + 256, 1.f, false, csr, half);
     if (warp == 2 && lane == 0) stamp(7, 2);
   }
   tc_fence_before();
@@ -775,10 +765,12 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
       if (lane == 0) mbar_arrive(ds_full);
       if (warp == 2 && lane == 0) stamp(6, i);
     }
+    float2 csr[32];
+    if (rope_cs) load_cs32(rope_cs + (long long)q * 64, half, csr);
     mbar_wait(done, 0);
     tc_fence_after();
     __nv_bfloat16* dq = dqkv + (long long)(b * s + q) * 3 * nd + head * DH;
-    store_row_rope(dq, tbase + lane_off + 384, scale, rope_cs ? rope_cs + (long long)q * 64 : nullptr, half, half + 1);
+    store_row_rope_pre(dq, tbase + lane_off + 384, scale, rope_cs != nullptr, csr, half);
   }
   tc_fence_before();
   __syncthreads();

@@ -4,6 +4,8 @@
 // math, warp-shuffle reductions, deterministic column reductions (fixed order, no atomics) for
 // the norm-gain gradients.  bf16 rounding points follow reading R6.
 #include <cuda_bf16.h>
+#include <algorithm>
+#include <cstdlib>
 #include "kernels.h"
 
 namespace mls {
@@ -209,6 +211,79 @@ __global__ void __launch_bounds__(1024) colsum_accum_kernel(int nb, int h, const
 #pragma unroll
     for (int i = 0; i < 32; ++i) t += sh[i][lane];
     dg[c] += t;
+  }
+}
+
+// Warp-per-row variant for bf16 dy and h % 256 == 0 (every hot-path shape): lane l holds columns
+// 8 l + 256 i of its row in registers (NV = h / 256 vectors of x and dy), so the row statistic is a
+// warp shuffle (no block barrier per row) and many rows are in flight per SM.  The gain gradient
+// sum_rows dy * x * r accumulates per warp in its own shared-memory slice (no atomics), the CTA adds
+// its slices in warp order into part[blockIdx.x][h], and colsum_accum_kernel adds the CTA partials in
+// CTA order: deterministic, and the partial array is grid x h (one CTA per SM) instead of a row band
+// per 3 rows.
+constexpr int BWDW_SMEM = 128 * 1024;
+template <int NV>
+__global__ void __launch_bounds__(256, 1)
+rmsnorm_bwd_warp_kernel(int T, int h, const uint4* __restrict__ x, const uint4* __restrict__ g,
+                        const float* __restrict__ rstd, const uint4* __restrict__ dy, const uint4* __restrict__ dres,
+                        uint4* __restrict__ dx_out, float* __restrict__ dg_part) {
+  extern __shared__ float4 sdg4[];  // [warps][h] fp32
+  float* sdg = reinterpret_cast<float*>(sdg4);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nv = h / 8;
+  float* my = sdg + (size_t)w * h;
+  for (int c = lane; c < h / 4; c += 32) reinterpret_cast<float4*>(my)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();
+  for (int row = blockIdx.x * nw + w; row < T; row += gridDim.x * nw) {
+    const float r = rstd[row];
+    uint4 xq[NV], dq[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      xq[i] = x[(long long)row * nv + lane + 32 * i];
+      dq[i] = dy[(long long)row * nv + lane + 32 * i];
+    }
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float xv[8], dv[8];
+      unpack8(xq[i], xv);
+      unpack8(dq[i], dv);
+      float4* d4 = reinterpret_cast<float4*>(my + (lane + 32 * i) * 8);
+      float gv[8];
+      unpack8(__ldg(g + lane + 32 * i), gv);
+      float4 a = d4[0], b = d4[1];
+      a.x += dv[0] * xv[0] * r; a.y += dv[1] * xv[1] * r; a.z += dv[2] * xv[2] * r; a.w += dv[3] * xv[3] * r;
+      b.x += dv[4] * xv[4] * r; b.y += dv[5] * xv[5] * r; b.z += dv[6] * xv[6] * r; b.w += dv[7] * xv[7] * r;
+      d4[0] = a;
+      d4[1] = b;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dot += xv[j] * gv[j] * dv[j];
+    }
+    dot = warp_sum(dot);
+    const float coef = r * r * r * dot / (float)h;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float xv[8], dv[8], o[8], rs[8], gv[8];
+      unpack8(xq[i], xv);
+      unpack8(dq[i], dv);
+      unpack8(__ldg(g + lane + 32 * i), gv);
+      if (dres) unpack8(dres[(long long)row * nv + lane + 32 * i], rs);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o[j] = r * gv[j] * dv[j] - xv[j] * coef;
+        if (dres) o[j] += rs[j];
+      }
+      dx_out[(long long)row * nv + lane + 32 * i] = pack8(o);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < h / 4; c += blockDim.x) {  // CTA partial: warp slices in warp order
+    float4 acc = reinterpret_cast<const float4*>(sdg)[c];
+    for (int k = 1; k < nw; ++k) {
+      const float4 v = reinterpret_cast<const float4*>(sdg + (size_t)k * h)[c];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(dg_part + (long long)blockIdx.x * h)[c] = acc;
   }
 }
 
@@ -522,10 +597,43 @@ cudaError_t rmsnorm_fwd(int T, int h, const void* x, const float* partial, void*
 
 size_t rmsnorm_bwd_scratch_floats(int T, int h) { return (size_t)BWD_BLOCKS * h; }
 
+// warp-per-row kernel instance for h (NV = h / 256 vectors per lane), or nullptr
+using BwdWarpFn = void (*)(int, int, const uint4*, const uint4*, const float*, const uint4*, const uint4*, uint4*,
+                           float*);
+static BwdWarpFn bwd_warp_fn(int h) {
+  if (h % 256) return nullptr;
+  switch (h / 256) {
+    case 1: return rmsnorm_bwd_warp_kernel<1>;
+    case 2: return rmsnorm_bwd_warp_kernel<2>;
+    case 4: return rmsnorm_bwd_warp_kernel<4>;
+    case 8: return rmsnorm_bwd_warp_kernel<8>;
+    case 12: return rmsnorm_bwd_warp_kernel<12>;
+    case 16: return rmsnorm_bwd_warp_kernel<16>;  // larger h: the block kernel (registers)
+    default: return nullptr;
+  }
+}
+
 cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float* rstd, const void* dy,
                         const void* dres, void* dx_out, float* dg_accum, float* scratch, cudaStream_t st,
                         bool dy_bf16) {
   if (h % 8 || h > 8 * NORM_MAXV * NORM_THREADS || T <= 0) return cudaErrorInvalidValue;
+  if (dy_bf16 && !getenv("MALLEUS_NORM_BWD_BLOCK")) {
+    if (BwdWarpFn fn = bwd_warp_fn(h)) {
+      const int warps = std::min(8, BWDW_SMEM / (h * 4));
+      const int smem = warps * h * 4;
+      static int attr_h = 0;
+      if (attr_h != h) {  // opt in to > 48 KB of dynamic shared memory for this instance
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, BWDW_SMEM);
+        if (e != cudaSuccess) return e;
+        attr_h = h;
+      }
+      int nb = std::min(148, (T + warps - 1) / warps);
+      fn<<<nb, warps * 32, smem, st>>>(T, h, (const uint4*)x, (const uint4*)g, rstd, (const uint4*)dy,
+                                       (const uint4*)dres, (uint4*)dx_out, scratch); count_launch();
+      colsum_accum_kernel<<<(h + 31) / 32, 1024, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
+      return cudaGetLastError();
+    }
+  }
   int rpb = (T + BWD_BLOCKS - 1) / BWD_BLOCKS;
   int nb = (T + rpb - 1) / rpb;
   const int vpt = (h / 8 + NORM_THREADS - 1) / NORM_THREADS;

@@ -22,6 +22,7 @@
 #include <utility>
 #include <vector>
 #include <cstring>
+#include <cstdio>
 #include <cstdlib>
 #include "ptx.cuh"
 #include "kernels.h"
@@ -840,6 +841,19 @@ struct GemmProf {
 };
 static GemmProf g_prof;
 
+// MALLEUS_GEMM_LOG=<path>: append "M N K a_mn b_mn mode epi kernel" per launch (measurement aid: the
+// n-th line is the n-th gemm_tcgen05 launch of an ncu launch list of the same program)
+static void gemm_log(const GemmParams& p, bool a_mn, bool b_mn, const char* kern) {
+  static FILE* f = [] {
+    const char* e = getenv("MALLEUS_GEMM_LOG");
+    return e ? fopen(e, "a") : nullptr;
+  }();
+  if (f) {
+    fprintf(f, "%d %d %d %d %d %d %d %s\n", p.M, p.N, p.K, (int)a_mn, (int)b_mn, p.mode, p.glu, kern);
+    fflush(f);
+  }
+}
+
 void gemm_profile_enable(bool on) {
   g_prof.on = on;
   g_prof.used = 0;
@@ -875,6 +889,7 @@ static cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
     int dev; cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  gemm_log(p, A_MN, B_MN, "cta1");
   int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   const int sms = g_num_sms;
   int grid = tiles < sms ? tiles : sms;
@@ -919,6 +934,7 @@ static cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const C
     int dev; cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  gemm_log(p, A_MN, B_MN, "cta2");
   const int tiles_n = p.glu == 1 ? ((p.N >> 1) + BN2 / 2 - 1) / (BN2 / 2) : (p.N + BN2 - 1) / BN2;
   const int tiles = ((p.M + 2 * BM2 - 1) / (2 * BM2)) * tiles_n;
   const int sms = g_num_sms;

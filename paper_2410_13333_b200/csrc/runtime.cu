@@ -752,9 +752,13 @@ static bool tp_peer(const Layout& L) { return L.TP > 1 && L.p2p && L.tpflags != 
 // where the next row-parallel GEMM writes its fp32 partial
 static float* tp_part(Layout& L) { return tp_peer(L) ? L.tpp[(L.tp_epoch + 1) & 1] : L.part; }
 // the row-parallel GEMM's store mode for that buffer
-static int tp_part_mode(const Layout& L) { return tp_peer(L) && L.tp_bf16 ? GEMM_STORE_BF16 : GEMM_STORE_F32; }
+// (TP 1: the row-parallel dgrad output is the full sum, stored in bf16 like every activation gradient
+// between kernels, reading R6; the forward fuses its residual into the GEMM epilogue instead)
+static int tp_part_mode(const Layout& L) {
+  return (tp_peer(L) && L.tp_bf16) || (L.TP == 1 && !L.f32) ? GEMM_STORE_BF16 : GEMM_STORE_F32;
+}
 // the backward TP sums (input gradients of the norms) are bf16 when the partials are
-static bool tp_sum_bf16(const Layout& L) { return tp_peer(L) && L.tp_bf16; }
+static bool tp_sum_bf16(const Layout& L) { return (tp_peer(L) && L.tp_bf16) || (L.TP == 1 && !L.f32); }
 // reduce-scatter fused into the GEMM epilogue: each member's GEMM stores the rows owned by member d
 // straight into d's receive slot (its own index) over NVLink, overlapping the transfer with the
 // GEMM; the reduction kernel then reads only local slots.  Needs bf16 partials and T / k rows per
@@ -1395,14 +1399,14 @@ malleus_status malleus_wait(malleus_ctx* ctx, void* stream, int32_t timeout_ms) 
   comm_abort(1u);
   if (ctx->L && ctx->L->tp_comm) { ncclCommAbort(ctx->L->tp_comm); ctx->L->tp_comm = nullptr; }
   if (ctx->world_comm) { ncclCommAbort(ctx->world_comm); ctx->world_comm = nullptr; }
+  // drain: with the abort word set every later TP reduction of the enqueued work gives up at once
+  // too; the word stays set until malleus_destroy has drained the device
   const auto t1 = std::chrono::steady_clock::now();
   while (cudaEventQuery(ev) == cudaErrorNotReady &&
-         std::chrono::steady_clock::now() - t1 < std::chrono::seconds(30))
+         std::chrono::steady_clock::now() - t1 < std::chrono::seconds(60))
     std::this_thread::sleep_for(std::chrono::microseconds(100));
   cudaEventDestroy(ev);
   cudaGetLastError();
-  comm_abort(0u);
-  comm_status(true);
   ctx->sticky = true;
   ctx->failed = true;
   char msg[256];
@@ -1417,7 +1421,21 @@ malleus_status malleus_wait(malleus_ctx* ctx, void* stream, int32_t timeout_ms) 
 malleus_status malleus_destroy(malleus_ctx* ctx) {
   if (!ctx) return MALLEUS_E_ARG;
   cudaSetDevice(ctx->device);
-  cudaDeviceSynchronize();
+  if (ctx->failed) {  // bounded drain (the abort word is still set), then re-arm the guard
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(ev, cudaStreamLegacy);  // the legacy stream waits for every blocking stream
+      const auto t0 = std::chrono::steady_clock::now();
+      while (cudaEventQuery(ev) == cudaErrorNotReady &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::seconds(60))
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+      cudaEventDestroy(ev);
+    }
+    comm_abort(0u);
+    comm_status(true);
+  } else {
+    cudaDeviceSynchronize();
+  }
   cudaGetLastError();
   if (ctx->L) free_layout(ctx, ctx->L.get());
   if (ctx->world_comm) ncclCommDestroy(ctx->world_comm);

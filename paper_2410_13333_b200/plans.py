@@ -82,6 +82,21 @@ def plan_matrix_c1(cfg, B=8, b=2):
     return P
 
 
+def plan_matrix_gqa(cfg, B=8, b=2):
+    """Parity plans for a GQA model (n_kv < n: every member holds whole KV groups, so the head splits
+    are multiples of the group size): P0 1 GPU; P1 TP2 even; P3 DP2 m = (3, 1); P4 DP2 = {TP2, TP1}
+    m = (1, 3) (cross-layout, different TP degrees); P6 PP2 = {TP1 layer 0, TP2 layer 1}."""
+    L, m = cfg.n_layers, B // b
+    ev = lambda ranks, layers: even_stage(cfg, ranks, layers)
+    return {
+        "P0": plan([pipe([ev([0], [0, L])], m)], b, B),
+        "P1": plan([pipe([ev([0, 1], [0, L])], m)], b, B),
+        "P3": plan([pipe([ev([0], [0, L])], 3 * m // 4), pipe([ev([1], [0, L])], m - 3 * m // 4)], b, B),
+        "P4": plan([pipe([ev([0, 1], [0, L])], m // 4), pipe([ev([2], [0, L])], m - m // 4)], b, B),
+        "P6": plan([pipe([ev([0], [0, 1]), ev([1, 2], [1, L])], m)], b, B),
+    }
+
+
 def ladder_plan(cfg, n_gpus: int, B: int, b: int = 1, straggle: bool = True):
     """1/2/4/8-GPU ladder on the C2 shape (SURVEY §8(d) 'Ladder 1/2/4/8').
 

@@ -14,7 +14,8 @@ shared code").  Recipe:
 
 Logical tensor storage (reading R9): every matrix is stored
 split-axis-outermost with the hidden dim innermost, i.e. shape [rows, h]:
-  Wq, Wk, Wv : [n*d, h]     (out, in)
+  Wq         : [n*d, h]     (out, in)
+  Wk, Wv     : [n_kv*d, h]  (GQA: n_kv KV heads, each shared by n/n_kv query heads)
   WoT        : [n*d, h]     (= W_o transposed: x += o @ WoT)
   Wg, Wu     : [F, h]
   WdT        : [F, h]       (= W_d transposed: x += u @ WdT)
@@ -44,9 +45,15 @@ class ModelCfg:
     seq_len: int
     rms_eps: float = 1e-5
     rope_theta: float = 10000.0
+    n_kv_heads: int = 0  # GQA: 0 = MHA (n_kv = n_heads, reading R1)
 
     def __post_init__(self):
-        assert self.hidden == self.n_heads * self.head_dim, "MHA: h = n*d (reading R1)"
+        assert self.hidden == self.n_heads * self.head_dim, "h = n*d (reading R1)"
+        assert self.kv_heads >= 1 and self.n_heads % self.kv_heads == 0, "query heads in whole KV groups"
+
+    @property
+    def kv_heads(self) -> int:
+        return self.n_kv_heads or self.n_heads
 
 
 # Named configurations (BASELINE.json configs)
@@ -62,14 +69,21 @@ C5_110B_SLICE = ModelCfg(n_layers=4, hidden=8192, n_heads=64, head_dim=128, ffn=
 # C1 with d = 128 and 256-token sequences: exercises the tcgen05 attention and CTA-pair GEMM paths
 C1_MED = ModelCfg(n_layers=2, hidden=512, n_heads=4, head_dim=128, ffn=1536, vocab=2048, seq_len=256)
 MICRO = ModelCfg(n_layers=2, hidden=16, n_heads=2, head_dim=8, ffn=32, vocab=16, seq_len=8)
+# GQA variants (LLaMA-2-70B groups 8 query heads per KV head; here 2 per KV head): the tiny model on the
+# mma.sync attention and the d = 128 model on the tcgen05 kernels
+C1_GQA = ModelCfg(n_layers=2, hidden=128, n_heads=4, head_dim=32, ffn=512, vocab=256, seq_len=64, n_kv_heads=2)
+C1_MED_GQA = ModelCfg(n_layers=2, hidden=512, n_heads=4, head_dim=128, ffn=1536, vocab=2048, seq_len=256,
+                      n_kv_heads=2)
+MICRO_GQA = ModelCfg(n_layers=2, hidden=32, n_heads=4, head_dim=8, ffn=32, vocab=16, seq_len=8, n_kv_heads=2)
 
 
 def tensor_shapes(cfg: ModelCfg) -> dict:
     """name -> shape of every logical tensor (storage layout above)."""
     h, nd, F, V = cfg.hidden, cfg.n_heads * cfg.head_dim, cfg.ffn, cfg.vocab
+    kd = cfg.kv_heads * cfg.head_dim
     shapes = {"E": (V, h), "gf": (h,), "Wlm": (V, h)}
     for l in range(cfg.n_layers):
-        shapes.update({f"{l}.g1": (h,), f"{l}.wq": (nd, h), f"{l}.wk": (nd, h), f"{l}.wv": (nd, h),
+        shapes.update({f"{l}.g1": (h,), f"{l}.wq": (nd, h), f"{l}.wk": (kd, h), f"{l}.wv": (kd, h),
                        f"{l}.wo": (nd, h), f"{l}.g2": (h,), f"{l}.wg": (F, h), f"{l}.wu": (F, h),
                        f"{l}.wd": (F, h)})
     return shapes

@@ -141,8 +141,14 @@ def test_failure_detected_and_survivor_resumes(tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29541", os.path.join(ROOT, "tests", "mp_failure_worker.py"),
            str(tmp_path), str(out)]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    assert out.exists(), p.stdout[-3000:] + p.stderr[-3000:]
+    p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=ROOT,
+                         start_new_session=True)
+    try:
+        so, se = p.communicate(timeout=400)
+    except subprocess.TimeoutExpired:  # kill the whole process group (torchrun and both workers)
+        os.killpg(p.pid, 9)
+        so, se = p.communicate()
+    assert out.exists(), so[-3000:] + se[-3000:]
     r = json.loads(out.read_text())
     assert r["timeout_status"] == "CommTimeout", r
     assert r["detect_s"] < 30, r

@@ -85,6 +85,30 @@ def test_rmsnorm_bwd(L, T, h):
     assert torch.equal(dg, dg2)
 
 
+@pytest.mark.parametrize("T,h", [(64, 256), (300, 512), (2048, 4096), (1000, 3072), (97, 6656), (64, 128)])
+def test_rmsnorm_bwd_bf16_dy(L, T, h):
+    """bf16 input gradient (TP sums, TP-1 dgrad output): the warp-per-row kernel with per-warp
+    shared-memory gain-gradient slices (h % 256 == 0, h <= 4096), else the block kernel."""
+    x = bf(normal_matrix((T, h), 14))
+    g = bf(1 + 0.1 * normal_matrix((h,), 15))
+    dy = bf(normal_matrix((T, h), 16))
+    dres = bf(normal_matrix((T, h), 17))
+    _, rr = M.rmsnorm_fwd(f64(x), f64(g), 1e-5)
+    r = torch.tensor(rr[:, 0], dtype=torch.float32).cuda()
+    dx = torch.empty_like(x)
+    dg = torch.full((h,), 0.5, device="cuda")
+    args = (T, h, x.data_ptr(), g.data_ptr(), r.data_ptr(), dy.data_ptr(), dres.data_ptr(), dx.data_ptr())
+    assert L.lib.malleus_k_rmsnorm_bwd16(*args, dg.data_ptr(), stream()) == 0
+    torch.cuda.synchronize()
+    rdx, rdg = M.rmsnorm_bwd(f64(x), f64(g), r.double().cpu().numpy()[:, None], f64(dy))
+    assert rel(f64(dx), rdx + f64(dres)) < 1e-2
+    assert rel(dg.double().cpu().numpy() - 0.5, rdg) < 1e-4
+    dg2 = torch.full((h,), 0.5, device="cuda")
+    assert L.lib.malleus_k_rmsnorm_bwd16(*args, dg2.data_ptr(), stream()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(dg, dg2)  # deterministic
+
+
 def _attn_ref(q4, k4, v4, d, s, theta):
     cfg = ModelCfg(n_layers=1, hidden=d, n_heads=1, head_dim=d, ffn=16, vocab=16, seq_len=s,
                    rope_theta=theta)

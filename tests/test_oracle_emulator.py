@@ -4,7 +4,7 @@ The fp64 partition emulator must match oracle/model.py to <= 1e-12 relative."""
 import numpy as np
 import pytest
 
-from synth.gen import C1_TINY, MICRO, make_weights, make_tokens
+from synth.gen import C1_TINY, C1_GQA, MICRO, make_weights, make_tokens
 from oracle import model as M
 from oracle.emulator import emulate_step
 from paper_2410_13333_b200 import plans as Pl
@@ -15,7 +15,7 @@ def _rel(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
 
 
-def _compare(cfg, plan, B, seed=0, steps=1):
+def _compare(cfg, plan, B, seed=0, steps=1, adam_tol=1e-12):
     P = M.params_f64(make_weights(cfg))
     tok, tgt = make_tokens(cfg, B)
     Mo = {k: np.zeros_like(v) for k, v in P.items()}
@@ -25,9 +25,9 @@ def _compare(cfg, plan, B, seed=0, steps=1):
     assert abs(eloss - loss) <= 1e-12 * abs(loss)
     for k in P:
         assert _rel(eg[k], g[k]) <= 1e-12, (k, _rel(eg[k], g[k]))
-        assert _rel(enP[k], nP[k]) <= 1e-12
-        assert _rel(enM[k], nM[k]) <= 1e-12
-        assert _rel(enV[k], nV[k]) <= 1e-12
+        assert _rel(enP[k], nP[k]) <= adam_tol
+        assert _rel(enM[k], nM[k]) <= adam_tol
+        assert _rel(enV[k], nV[k]) <= adam_tol
 
 
 @pytest.mark.parametrize("name", ["P0", "P1", "P2", "P3", "P4", "P5", "P6", "P7", "P8", "P9", "P10", "P11"])
@@ -41,3 +41,13 @@ def test_random_plans_micro():
     for _ in range(200):
         p, world = random_plan(rng, MICRO, world_max=8, B=8, b=2)
         _compare(MICRO, p, B=8)
+
+
+@pytest.mark.parametrize("name", ["P0", "P1", "P3", "P4", "P6"])
+def test_plan_matrix_gqa(name):
+    """GQA (n_kv = n/2): members hold whole KV groups; the partitioned step is still lossless."""
+    cfg = C1_GQA
+    # gradients to 1e-12 as for MHA; the AdamW-updated state to 1e-10: at t = 1 the update is
+    # ~lr * sign(g), ill-conditioned where |g| is tiny (reading R16), and the GQA dK / dV group sums
+    # re-associate differently in the member-split emulator
+    _compare(cfg, Pl.plan_matrix_gqa(cfg)[name], B=8, adam_tol=1e-10)

@@ -189,3 +189,22 @@ def test_plan_matrix_validates():
     cfg = C1_TINY
     for name, p in Pl.plan_matrix_c1(cfg).items():
         Lo.validate(cfg, p, Pl.world_of(p))
+
+
+def test_gqa_rows_and_validation():
+    """GQA: W_k / W_v rows follow the member's KV groups (query heads / g); a split that cuts a KV
+    group is rejected."""
+    from synth.gen import C1_GQA
+    cfg = C1_GQA  # 4 query heads, 2 KV heads, d 32
+    p = Pl.plan_matrix_gqa(cfg)["P1"]
+    Lo.validate(cfg, p, 2)
+    st = p["pipes"][0]["stages"][0]
+    assert Lo.member_rows(cfg, st, "0.wq", 1) == (64, 128)
+    assert Lo.member_rows(cfg, st, "0.wk", 0) == (0, 32) and Lo.member_rows(cfg, st, "0.wv", 1) == (32, 64)
+    bad = Pl.plan([Pl.pipe([Pl.stage([0, 1], [3, 1], [256, 256], [128, 128], [0, cfg.n_layers])], 4)], 2, 8)
+    with pytest.raises(Lo.PlanError):
+        Lo.validate(cfg, bad, 2)
+    # ownership still partitions every element exactly once (brute force)
+    for name in ("0.wk", "1.wv", "0.wq"):
+        own = Lo.owner_map(cfg, Pl.plan_matrix_gqa(cfg)["P4"], name)
+        assert len(own) == Lo.n_elems(cfg, name) and all(o is not None for o in own)

@@ -13,7 +13,7 @@ import pytest
 import torch
 import torch.nn.functional as F
 
-from synth.gen import MICRO, C1_TINY, ModelCfg, make_weights, make_tokens
+from synth.gen import MICRO, MICRO_GQA, C1_TINY, C1_GQA, ModelCfg, make_weights, make_tokens
 from oracle import model as M
 
 
@@ -23,8 +23,8 @@ def _setup(cfg, B=2, seed=1234):
     return P, tok, tgt
 
 
-def test_finite_differences_micro():
-    cfg = MICRO
+@pytest.mark.parametrize("cfg", [MICRO, MICRO_GQA], ids=["mha", "gqa"])
+def test_finite_differences_micro(cfg):
     P, tok, tgt = _setup(cfg)
     # larger weights so that every term matters at fp64 FD resolution
     rng = np.random.default_rng(0)
@@ -50,6 +50,7 @@ def _torch_loss(cfg: ModelCfg, P: dict, tok, tgt):
     T = {k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in P.items()}
     Bn, s = tok.shape
     n, d, h = cfg.n_heads, cfg.head_dim, cfg.hidden
+    nkv = cfg.kv_heads
     tok_t = torch.tensor(tok, dtype=torch.long)
     x = T["E"][tok_t]
     pos = torch.arange(s, dtype=torch.float64)
@@ -68,9 +69,9 @@ def _torch_loss(cfg: ModelCfg, P: dict, tok, tgt):
         p = lambda t: T[f"{l}.{t}"]
         a = rms(x, p("g1"))
         q = (a @ p("wq").T).view(Bn, s, n, d).transpose(1, 2)
-        k = (a @ p("wk").T).view(Bn, s, n, d).transpose(1, 2)
-        v = (a @ p("wv").T).view(Bn, s, n, d).transpose(1, 2)
-        o = F.scaled_dot_product_attention(rope(q), rope(k), v, is_causal=True)
+        k = (a @ p("wk").T).view(Bn, s, nkv, d).transpose(1, 2)
+        v = (a @ p("wv").T).view(Bn, s, nkv, d).transpose(1, 2)
+        o = F.scaled_dot_product_attention(rope(q), rope(k), v, is_causal=True, enable_gqa=nkv != n)
         x = x + o.transpose(1, 2).reshape(Bn, s, n * d) @ p("wo")
         a2 = rms(x, p("g2"))
         x = x + (F.silu(a2 @ p("wg").T) * (a2 @ p("wu").T)) @ p("wd")
@@ -80,7 +81,7 @@ def _torch_loss(cfg: ModelCfg, P: dict, tok, tgt):
     return loss.item(), {k: t.grad.numpy() for k, t in T.items()}
 
 
-@pytest.mark.parametrize("cfg", [MICRO, C1_TINY])
+@pytest.mark.parametrize("cfg", [MICRO, C1_TINY, MICRO_GQA, C1_GQA])
 def test_torch_autograd_fp64(cfg):
     P, tok, tgt = _setup(cfg, B=2)
     loss, g = M.forward_backward(cfg, P, tok, tgt)
@@ -195,3 +196,28 @@ def test_clip_grad_norm_vs_torch(max_norm):
         assert abs(new_norm - max_norm) <= 1e-5 * max_norm
     else:
         assert abs(new_norm - tot_ref) <= 1e-12 * tot_ref
+
+
+def test_gqa_equals_mha_with_repeated_kv_weights():
+    """GQA with n_kv KV heads is exactly MHA whose W_k / W_v repeat each KV head's rows for the g
+    query heads of its group (query head j <- KV head j // g); the GQA weight gradient of a KV head
+    is the sum of the MHA gradients of its g copies."""
+    import dataclasses
+    cfg = C1_GQA
+    mha = dataclasses.replace(cfg, n_kv_heads=0)
+    P, tok, tgt = _setup(cfg, B=2)
+    g_sz, d = cfg.n_heads // cfg.kv_heads, cfg.head_dim
+    Q = dict(P)
+    for l in range(cfg.n_layers):
+        for t in ("wk", "wv"):
+            w = P[f"{l}.{t}"].reshape(cfg.kv_heads, d, -1)
+            Q[f"{l}.{t}"] = np.repeat(w, g_sz, axis=0).reshape(cfg.n_heads * d, -1)
+    la, ga = M.forward_backward(cfg, P, tok, tgt)
+    lb, gb = M.forward_backward(mha, Q, tok, tgt)
+    assert abs(la - lb) <= 1e-13 * abs(lb)
+    for k in P:
+        if k.endswith((".wk", ".wv")):
+            red = gb[k].reshape(cfg.kv_heads, g_sz, d, -1).sum(axis=1).reshape(ga[k].shape)
+            assert np.abs(ga[k] - red).max() <= 1e-12 * max(np.abs(red).max(), 1e-300), k
+        else:
+            assert np.abs(ga[k] - gb[k]).max() <= 1e-12 * max(np.abs(gb[k]).max(), 1e-300), k
