@@ -158,14 +158,14 @@ malleus_status malleus_create(const malleus_model_cfg* cfg, int32_t rank, int32_
  * for communication calls during training in order to detect failures"): a step whose TP
  * reductions, pipeline transfers or gradient exchange wait for an unresponsive GPU does not finish.
  * On timeout — or when a device-side communication wait of the peer-memory TP reduction gave up
- * after MALLEUS_COMM_TIMEOUT_MS (default 20000) — the context enters the failed state: the device
- * spin-waits are released (process-wide abort word, kept set until malleus_destroy has drained the
- * device), every NCCL communicator of the context is aborted (ncclCommAbort), the stream is drained,
- * and MALLEUS_E_TIMEOUT is returned; every later call
- * except malleus_last_error / malleus_destroy returns MALLEUS_E_STATE.  Recovery is
- * the caller's: destroy the context, create one on the surviving GPUs, apply a plan computed with
- * the unresponsive GPUs' straggling rates set to infinity, and load the latest checkpoint
- * (write_tensor of every kind).  Caller-owned arenas stay valid (they are not freed here). */
+ * after MALLEUS_COMM_TIMEOUT_MS (default 20000) — the context enters the failed state and
+ * MALLEUS_E_TIMEOUT is returned: the process-wide abort word is set, so every device-side
+ * communication wait of the enqueued work gives up at once; every later call except
+ * malleus_last_error / malleus_destroy returns MALLEUS_E_STATE, and malleus_destroy of a failed
+ * context only releases host resources (NCCL communicators and kernels that still wait on the lost
+ * peer are left to process teardown).  Recovery is PAPER.md:735's: the job restarts on the
+ * surviving GPUs (a new process) with the unresponsive GPUs' straggling rates set to infinity
+ * (a plan without them) and loads the latest checkpoint (write_tensor of every kind). */
 malleus_status malleus_wait(malleus_ctx* ctx, void* stream, int32_t timeout_ms);
 malleus_status malleus_destroy(malleus_ctx* ctx);
 const char* malleus_last_error(const malleus_ctx* ctx); /* never NULL; static if ctx == NULL */

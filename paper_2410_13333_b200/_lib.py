@@ -153,7 +153,7 @@ DTYPES = {"bf16": 0, "fp32": 1}
 
 
 def make_cfg(cfg, dtype: str = "bf16") -> ModelCfg:
-    return ModelCfg(cfg.n_layers, cfg.hidden, cfg.n_heads, cfg.n_heads, cfg.head_dim, cfg.ffn,
+    return ModelCfg(cfg.n_layers, cfg.hidden, cfg.n_heads, getattr(cfg, "kv_heads", cfg.n_heads), cfg.head_dim, cfg.ffn,
                     cfg.vocab, cfg.seq_len, cfg.rms_eps, cfg.rope_theta, DTYPES[dtype])
 
 

@@ -80,7 +80,7 @@ extern "C" malleus_status malleus_k_attention_fwd(int32_t nb, int32_t s, int32_t
                                                   void* o, float* lse, float rope_theta, void* stream) {
   if (!qkv || !o || !lse) return MALLEUS_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = rope_inplace(nb * s, s, n, d, qkv, 3LL * n * d, 0, rope_theta, false, st);
+  cudaError_t e = rope_inplace(nb * s, s, 2 * n, d, qkv, 3LL * n * d, 0, rope_theta, false, st);
   if (e == cudaSuccess) e = attention_fwd(nb, s, n, d, qkv, o, lse, st);
   return cu(e);
 }
@@ -94,7 +94,7 @@ extern "C" malleus_status malleus_k_attention_bwd(int32_t nb, int32_t s, int32_t
   cudaError_t e = cudaMallocAsync((void**)&dsum, (size_t)nb * s * n * sizeof(float), st);
   if (e != cudaSuccess) return MALLEUS_E_CUDA;
   e = attention_bwd(nb, s, n, d, qkv, o, lse, dout, dqkv, dsum, st);
-  if (e == cudaSuccess) e = rope_inplace(nb * s, s, n, d, dqkv, 3LL * n * d, 0, rope_theta, true, st);
+  if (e == cudaSuccess) e = rope_inplace(nb * s, s, 2 * n, d, dqkv, 3LL * n * d, 0, rope_theta, true, st);
   cudaFreeAsync(dsum, st);
   return cu(e);
 }

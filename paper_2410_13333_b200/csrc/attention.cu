@@ -533,9 +533,14 @@ cudaError_t bwd_impl(int nb, int s, int n, const void* qkv, const void* o, const
 static int g_attn_variant = 0;  // 0 auto (tcgen05 when supported), 1 mma.sync only
 void attention_set_variant(int v) { g_attn_variant = v; }
 
-cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o, float* lse, cudaStream_t st) {
+cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o, float* lse, cudaStream_t st,
+                          int n_kv) {
   if (s % 64) return cudaErrorInvalidValue;
-  if (g_attn_variant == 0 && attention_fwd_tc_supported(s, d)) return attention_fwd_tc(nb, s, n, qkv, o, lse, st);
+  if (n_kv <= 0) n_kv = n;
+  if (n % n_kv) return cudaErrorInvalidValue;
+  if (g_attn_variant == 0 && attention_fwd_tc_supported(s, d))
+    return attention_fwd_tc(nb, s, n, qkv, o, lse, st, n_kv);
+  if (n_kv != n) return cudaErrorInvalidValue;  // GQA: the tcgen05 kernels (head_dim 128) only
   switch (d) {
     case 32: return fwd_impl<32>(nb, s, n, qkv, o, lse, st);
     case 64: return fwd_impl<64>(nb, s, n, qkv, o, lse, st);
@@ -547,14 +552,18 @@ cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o,
 bool attention_bwd_fuses_rope(int s, int d) { return g_attn_variant == 0 && attention_fwd_tc_supported(s, d); }
 
 cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const void* o, const float* lse,
-                          const void* dout, void* dqkv, float* dsum, cudaStream_t st, const float2* rope_cs) {
+                          const void* dout, void* dqkv, float* dsum, cudaStream_t st, const float2* rope_cs,
+                          int n_kv) {
   if (s % 64) return cudaErrorInvalidValue;
+  if (n_kv <= 0) n_kv = n;
+  if (n % n_kv) return cudaErrorInvalidValue;
   if (g_attn_variant == 0 && attention_fwd_tc_supported(s, d)) {
     const long long T = (long long)nb * s;
     attn_dsum_kernel<128><<<(unsigned)((T * n * 8 + 255) / 256), 256, 0, st>>>(
         s, n, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dsum, T); count_launch();
-    return attention_bwd_tc(nb, s, n, qkv, lse, dout, dqkv, dsum, rope_cs, st);
+    return attention_bwd_tc(nb, s, n, qkv, lse, dout, dqkv, dsum, rope_cs, st, n_kv);
   }
+  if (n_kv != n) return cudaErrorInvalidValue;
   switch (d) {
     case 32: return bwd_impl<32>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);
     case 64: return bwd_impl<64>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);

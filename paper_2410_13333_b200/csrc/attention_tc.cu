@@ -1,7 +1,7 @@
 // Causal attention forward on the 5th-gen tensor cores (tcgen05 / TMEM / TMA) for head_dim 128
 // and sequence lengths that are multiples of 128 (PAPER.md:780 FlashAttention).
 //
-// One CTA = 128 queries of one (sequence, head).  Warp roles:
+// One CTA = 128 queries of one (sequence, query head); GQA: K / V of the head's KV group.  Warp roles:
 //   warp 0      TMA producer: Q once; K and V tiles of 128 keys through separate 3-stage rings
 //               (K_i is released when S_i is done, a full tile before V_i, so its reload is hidden);
 //   warp 1      MMA issuer (one thread) + TMEM owner: S_i = Q K_i^T into one of two TMEM S buffers,
@@ -71,7 +71,7 @@ constexpr int SMEM_FWD = Q_BYTES + 2 * FWD_STAGES * K_BYTES + 1024 + 1024;
 // NPOLY of every 8 consecutive P elements take ex2_poly, the rest the MUFU ex2
 template <int NPOLY>
 __global__ void __launch_bounds__(320, 1)
-attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bfloat16* __restrict__ o,
+attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, int n_kv, __nv_bfloat16* __restrict__ o,
                    float* __restrict__ lse, float scale, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -99,6 +99,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
   const int n_tiles = qb + 1;           // causal: key tiles 0..qb
   const int row0 = b * s + qb * TQ;     // first query row in qkv
   const int nd = n * DH;
+  // qkv = q (n heads) | k (n_kv heads) | v (n_kv heads); GQA: this query head reads KV head head / g
+  const int kcol = nd + (head / (n / n_kv)) * DH, vcol = nd + n_kv * DH + (head / (n / n_kv)) * DH;
   // debugging aid (MALLEUS_ATTN_TRACE): globaltimer stamps of CTAs (0, 0..1, 0), [event][tile]
   unsigned long long* tr = (trace && blockIdx.x == 0 && blockIdx.y < 2 && blockIdx.z == 0)
                                ? trace + blockIdx.y * 8 * 64 : nullptr;
@@ -141,8 +143,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         mbar_wait(&k_empty[st], ((i / FWD_STAGES) & 1) ^ 1);
         stamp(0, i);
         mbar_arrive_expect_tx(&k_full[st], K_BYTES);
-        tma_load_2d(k, &tm, &k_full[st], nd + head * DH, b * s + i * TK);
-        tma_load_2d(k + PANEL, &tm, &k_full[st], nd + head * DH + 64, b * s + i * TK);
+        tma_load_2d(k, &tm, &k_full[st], kcol, b * s + i * TK);
+        tma_load_2d(k + PANEL, &tm, &k_full[st], kcol + 64, b * s + i * TK);
       };
       auto load_v = [&](int i) {
         const int st = i % FWD_STAGES;
@@ -150,8 +152,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, __nv_bf
         mbar_wait(&v_empty[st], ((i / FWD_STAGES) & 1) ^ 1);
         stamp(1, i);
         mbar_arrive_expect_tx(&v_full[st], K_BYTES);
-        tma_load_2d(v, &tm, &v_full[st], 2 * nd + head * DH, b * s + i * TK);
-        tma_load_2d(v + PANEL, &tm, &v_full[st], 2 * nd + head * DH + 64, b * s + i * TK);
+        tma_load_2d(v, &tm, &v_full[st], vcol, b * s + i * TK);
+        tma_load_2d(v + PANEL, &tm, &v_full[st], vcol + 64, b * s + i * TK);
       };
       load_k(0);
       for (int i = 0; i < n_tiles; ++i) {
@@ -396,7 +398,9 @@ constexpr int NSUB1 = 4;                  // Q | dO ring depth (dK / dV kernel)
 // measured (tools/attn_trace.py): a 32 KB TMA sub-tile load takes ~1.4 us under full load, so the ring
 // must cover load latency + MMA + compute: with 3 stages the loop ran at (that chain) / 3 per sub-tile
 
-// dK / dV: CTA = 128 keys of one (sequence, head); loop over 64-query sub-tiles j >= 2 kb.
+// dK / dV: CTA = 128 keys of one (sequence, KV head); loop over the 64-query sub-tiles j >= 2 kb of
+// each query head that reads this KV head (MHA: one; GQA: the g heads of the group, one after another,
+// all accumulating into the same dK / dV in TMEM — the group sum of the GQA backward).
 //   TMEM: S^T[b] cols [64b, 64b+64), dP^T[b] [128+64b, ..), dV [256,384), dK [384,512); warp half h
 //   overwrites its own 32 S^T / dP^T columns with 16 columns of packed bf16 P^T / dS^T at 32h.
 //   S^T = K Q_j^T and dP^T = V dO_j^T (M = 128 keys, N = 64 queries, A = K / V from smem);
@@ -405,7 +409,7 @@ constexpr int BWD1_SMEM = 2 * 2 * PANEL + NSUB1 * SUB_STAGE + NSUB1 * 512 + 256 
 
 __global__ void __launch_bounds__(320, 1)
 attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm64,
-                       const __grid_constant__ CUtensorMap tmo64, int s, int n, const float* __restrict__ lse,
+                       const __grid_constant__ CUtensorMap tmo64, int s, int n, int n_kv, const float* __restrict__ lse,
                        const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv, float scale,
                        const float2* __restrict__ rope_cs, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -432,10 +436,12 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x;  // kb = 0 has the most query sub-tiles: scheduled first
-  const int head = blockIdx.y, b = blockIdx.z;
-  const int nd = n * DH;
-  const int j0 = 2 * kb, n_it = s / 64 - j0;
-  const long long lrow = ((long long)b * n + head) * s;
+  const int kvh = blockIdx.y, b = blockIdx.z;  // KV head (GQA: shared by the g query heads of its group)
+  const int nd = n * DH, g = n / n_kv, ldq = nd + 2 * n_kv * DH;
+  const int j0 = 2 * kb, n_sub = s / 64 - j0;  // query sub-tiles per query head
+  const int n_it = g * n_sub;                   // iterations: the group's query heads one after another
+  auto head_of = [&](int it) { return kvh * g + it / n_sub; };
+  auto sub_of = [&](int it) { return j0 + it % n_sub; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
@@ -457,12 +463,13 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
     if (lane == 0) {
       const int krow = b * s + kb * TK;
       mbar_arrive_expect_tx(kv_full, 4 * PANEL);
-      tma_load_2d(sK, &tm, kv_full, nd + head * DH, krow);
-      tma_load_2d(sK + PANEL, &tm, kv_full, nd + head * DH + 64, krow);
-      tma_load_2d(sV, &tm, kv_full, 2 * nd + head * DH, krow);
-      tma_load_2d(sV + PANEL, &tm, kv_full, 2 * nd + head * DH + 64, krow);
+      tma_load_2d(sK, &tm, kv_full, nd + kvh * DH, krow);
+      tma_load_2d(sK + PANEL, &tm, kv_full, nd + kvh * DH + 64, krow);
+      tma_load_2d(sV, &tm, kv_full, nd + (n_kv + kvh) * DH, krow);
+      tma_load_2d(sV + PANEL, &tm, kv_full, nd + (n_kv + kvh) * DH + 64, krow);
       for (int it = 0; it < n_it; ++it) {
-        const int st = it % NSUB1, j = j0 + it;
+        const int st = it % NSUB1, j = sub_of(it), head = head_of(it);
+        const long long lrow = ((long long)b * n + head) * s;
         mbar_wait(&qd_empty[st], ((it / NSUB1) & 1) ^ 1);
         stamp(0, it);
         uint8_t* q = ring + st * SUB_STAGE;
@@ -525,7 +532,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = scale * LOG2E;
     for (int it = 0; it < n_it; ++it) {
-      const int bb = it & 1, st = it % NSUB1, j = j0 + it;
+      const int bb = it & 1, st = it % NSUB1, j = sub_of(it);
       mbar_wait(&sd_full[bb], (it >> 1) & 1);
       if (warp == 2 && lane == 0) stamp(4, it);
       tc_fence_after();
@@ -575,8 +582,8 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
     mbar_wait(done, 0);
     if (warp == 2 && lane == 0) stamp(7, 1);
     tc_fence_after();
-    __nv_bfloat16* dk = dqkv + (long long)(b * s + key) * 3 * nd + nd + head * DH;
-    __nv_bfloat16* dv = dk + nd;
+    __nv_bfloat16* dk = dqkv + (long long)(b * s + key) * ldq + nd + kvh * DH;
+    __nv_bfloat16* dv = dk + n_kv * DH;
     store_row_rope_pre(dk, tbase + lane_off + 384, scale, rope_cs != nullptr, csr, half);
     store_row_rope_pre(dv, tbase + lane_off + 256, 1.f, false, csr, half);
     if (warp == 2 && lane == 0) stamp(7, 2);
@@ -600,6 +607,7 @@ constexpr int BWD2_SMEM = 2 * 2 * PANEL + 2 * KV2_STAGE + 256 + 1024;
 
 __global__ void __launch_bounds__(320, 1)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s, int n,
+                      int n_kv,
                       const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
                       float scale, const float2* __restrict__ rope_cs, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -664,10 +672,11 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
         uint8_t* k = ring + st * KV2_STAGE;
         const int krow = b * s + i * TK;
         mbar_arrive_expect_tx(&kv_full[st], KV2_STAGE);
-        tma_load_2d(k, &tm, &kv_full[st], nd + head * DH, krow);
-        tma_load_2d(k + PANEL, &tm, &kv_full[st], nd + head * DH + 64, krow);
-        tma_load_2d(k + 2 * PANEL, &tm, &kv_full[st], 2 * nd + head * DH, krow);
-        tma_load_2d(k + 3 * PANEL, &tm, &kv_full[st], 2 * nd + head * DH + 64, krow);
+        const int kvh = head / (n / n_kv);  // GQA: the group's KV head
+        tma_load_2d(k, &tm, &kv_full[st], nd + kvh * DH, krow);
+        tma_load_2d(k + PANEL, &tm, &kv_full[st], nd + kvh * DH + 64, krow);
+        tma_load_2d(k + 2 * PANEL, &tm, &kv_full[st], nd + (n_kv + kvh) * DH, krow);
+        tma_load_2d(k + 3 * PANEL, &tm, &kv_full[st], nd + (n_kv + kvh) * DH + 64, krow);
       }
     }
   } else if (warp == 1) {
@@ -769,7 +778,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
     if (rope_cs) load_cs32(rope_cs + (long long)q * 64, half, csr);
     mbar_wait(done, 0);
     tc_fence_after();
-    __nv_bfloat16* dq = dqkv + (long long)(b * s + q) * 3 * nd + head * DH;
+    __nv_bfloat16* dq = dqkv + (long long)(b * s + q) * (nd + 2 * n_kv * DH) + head * DH;
     store_row_rope_pre(dq, tbase + lane_off + 384, scale, rope_cs != nullptr, csr, half);
   }
   tc_fence_before();
@@ -813,11 +822,12 @@ static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long
 
 // dsum (= rowsum(dO * O)) must already be in `dsum`; writes dq, dk, dv column blocks of dqkv.
 cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float* lse, const void* dout,
-                             void* dqkv, const float* dsum, const float2* rope_cs, cudaStream_t st) {
+                             void* dqkv, const float* dsum, const float2* rope_cs, cudaStream_t st, int n_kv) {
   CUtensorMap tm, tmo, tm64, tmo64;
-  const long long T = (long long)nb * s;
-  if (!map_rows(&tm, qkv, 3LL * n * DH, T) || !map_rows(&tmo, dout, (long long)n * DH, T) ||
-      !map_rows(&tm64, qkv, 3LL * n * DH, T, 64) || !map_rows(&tmo64, dout, (long long)n * DH, T, 64))
+  const long long T = (long long)nb * s, cols = (long long)(n + 2 * n_kv) * DH;
+  if (n_kv < 1 || n % n_kv) return cudaErrorInvalidValue;
+  if (!map_rows(&tm, qkv, cols, T) || !map_rows(&tmo, dout, (long long)n * DH, T) ||
+      !map_rows(&tm64, qkv, cols, T, 64) || !map_rows(&tmo64, dout, (long long)n * DH, T, 64))
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -833,23 +843,25 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
     if (cudaMallocManaged(&trace, 2 * 16 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
     attn_bwd_trace_buffer = trace;
   }
-  attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, lse, dsum,
+  attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n_kv, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, n_kv, lse, dsum,
                                                                       (__nv_bfloat16*)dqkv, scale, rope_cs, trace); count_launch();
   static unsigned long long* trace2 = nullptr;
   if (getenv("MALLEUS_ATTN_TRACE") && !trace2) {
     if (cudaMallocManaged(&trace2, 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace2 = nullptr;
     attn_dq_trace_buffer = trace2;
   }
-  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, s, n, lse, dsum,
+  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, s, n, n_kv, lse, dsum,
                                                                      (__nv_bfloat16*)dqkv, scale, rope_cs, trace2); count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st) {
+cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st,
+                             int n_kv) {
   auto enc = encoder();
   if (!enc) return cudaErrorNotSupported;
+  if (n_kv < 1 || n % n_kv) return cudaErrorInvalidValue;
   CUtensorMap tm;
-  const long long T = (long long)nb * s, cols = 3LL * n * DH;
+  const long long T = (long long)nb * s, cols = (long long)(n + 2 * n_kv) * DH;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)T};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
   cuuint32_t box[2] = {64, 128};
@@ -877,7 +889,7 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
   }();
   auto fn = npoly <= 0 ? attn_fwd_tc_kernel<0> : npoly == 1 ? attn_fwd_tc_kernel<1>
           : npoly == 2 ? attn_fwd_tc_kernel<2> : attn_fwd_tc_kernel<3>;
-  fn<<<dim3(s / TQ, n, nb), 320, SMEM_FWD, st>>>(tm, s, n, (__nv_bfloat16*)o, lse, rsqrtf((float)DH), trace);
+  fn<<<dim3(s / TQ, n, nb), 320, SMEM_FWD, st>>>(tm, s, n, n_kv, (__nv_bfloat16*)o, lse, rsqrtf((float)DH), trace);
   count_launch();
   return cudaGetLastError();
 }

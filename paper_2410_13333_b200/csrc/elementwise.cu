@@ -325,7 +325,7 @@ __global__ void rope_kernel(int T, int s, int n, int d, __nv_bfloat16* __restric
       sn[u] *= sign;
     }
     __nv_bfloat16* row = buf + t * ld + col0;
-    for (int j = 0; j < 2 * n; ++j) {  // q heads then k heads
+    for (int j = 0; j < n; ++j) {  // the n rotated heads: q heads then k heads (GQA: fewer k heads)
       uint4* p1 = reinterpret_cast<uint4*>(row + j * d + gi * 8);
       uint4* p2 = reinterpret_cast<uint4*>(row + j * d + half + gi * 8);
       float a[8], b[8], o1[8], o2[8];

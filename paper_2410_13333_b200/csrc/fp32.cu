@@ -138,12 +138,12 @@ __global__ void residual_add_f32_kernel(long long n, const float* __restrict__ x
 __global__ void rope_f32_kernel(int T, int s, int n, int d, float* __restrict__ buf, long long ld, int col0,
                                 float theta, float sign) {
   const int half = d / 2;
-  const long long total = (long long)T * 2 * n * half;
+  const long long total = (long long)T * n * half;  // n rotated heads (q then k)
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = idx % half;
-    const int j = (idx / half) % (2 * n);
-    const long long t = idx / half / (2 * n);
+    const int j = (idx / half) % n;
+    const long long t = idx / half / n;
     const double ang = (double)(t % s) * pow((double)theta, -2.0 * i / d);
     const float cs = (float)cos(ang), sn = sign * (float)sin(ang);
     float* p = buf + t * ld + col0 + (long long)j * d;

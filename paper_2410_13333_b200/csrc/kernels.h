@@ -142,19 +142,22 @@ cudaError_t reduce_adam(int n_chunks, const ChunkDesc* d_chunks, const PieceDesc
 cudaError_t sq_total(int n, const float* sq, double* local, cudaStream_t st);
 cudaError_t clip_coef(const double* total, float max_norm, float* coef, float* norm, cudaStream_t st);
 
-// ---- attention (attention.cu): qkv [T, 3*n*d] bf16 (rope already applied to q,k)
+// ---- attention (attention.cu): qkv [T, (n + 2 n_kv) d] bf16 = q | k | v column blocks (rope already
+// applied to q, k); GQA (n_kv < n, query head j reads KV head j / (n / n_kv)) runs on the tcgen05
+// kernels only (head_dim 128); n_kv <= 0 means n (MHA)
 cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o, float* lse,
-                          cudaStream_t st);
+                          cudaStream_t st, int n_kv = 0);
 cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const void* o,
                           const float* lse, const void* dout, void* dqkv, float* dsum,
-                          cudaStream_t st, const float2* rope_cs = nullptr);
+                          cudaStream_t st, const float2* rope_cs = nullptr, int n_kv = 0);
 
 // tcgen05/TMEM/TMA forward for d = 128, s % 128 == 0 (attention_tc.cu)
 bool attention_fwd_tc_supported(int s, int d);
-cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st);
+cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st,
+                             int n_kv);
 void attention_set_variant(int v);
 cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float* lse, const void* dout,
-                             void* dqkv, const float* dsum, const float2* rope_cs, cudaStream_t st);
+                             void* dqkv, const float* dsum, const float2* rope_cs, cudaStream_t st, int n_kv);
 // true when attention_bwd with this (s, d) runs the tcgen05 kernels, which apply the RoPE backward
 // rotation to dq / dk in their epilogues when given a (cos, sin) table
 bool attention_bwd_fuses_rope(int s, int d);

@@ -35,7 +35,9 @@ PlanInfo plan_from_c(const malleus_plan* p) {
 
 std::string validate_plan(const malleus_model_cfg& cfg, const PlanInfo& p, int world) {
   std::ostringstream e;
-  if (cfg.n_kv_heads != cfg.n_heads) return "only MHA (n_kv_heads == n_heads) is supported (reading R1)";
+  if (cfg.n_kv_heads < 1 || cfg.n_heads % cfg.n_kv_heads)
+    return "n_kv_heads must divide n_heads (MHA: n_kv_heads == n_heads; GQA: whole query-head groups)";
+  const int grp = cfg.n_heads / cfg.n_kv_heads;  // query heads per KV head
   if (cfg.hidden != cfg.n_heads * cfg.head_dim) return "hidden must equal n_heads * head_dim";
   if (p.b < 1 || p.B < 1 || p.pipes.empty()) return "b >= 1, B >= 1, DP >= 1";
   if (p.pipes.size() > 8) return "DP <= 8";
@@ -63,6 +65,7 @@ std::string validate_plan(const malleus_model_cfg& cfg, const PlanInfo& p, int w
       long long sh = 0, sf = 0, sv = 0;
       for (size_t m = 0; m < k; ++m) {
         if (st.heads[m] < 1) return "every member needs >= 1 head (zero-work GPUs are standby, PAPER.md:556)";
+        if (st.heads[m] % grp) return "GQA: every member holds whole KV groups (heads split in multiples of n_heads / n_kv_heads)";
         if (st.ffn[m] < 16 || st.ffn[m] % 16) return "ffn split entries must be >= 16 and multiples of 16";
         if (st.vocab[m] < 16 || st.vocab[m] % 16) return "vocab split entries must be >= 16 and multiples of 16";
         sh += st.heads[m]; sf += st.ffn[m]; sv += st.vocab[m];
@@ -101,18 +104,21 @@ std::string check_kernel_limits(const malleus_model_cfg& cfg, const PlanInfo& p)
   if (cfg.hidden > 8192 || cfg.hidden % 128) return "hidden must be a multiple of 128 and <= 8192";
   if (cfg.head_dim != 32 && cfg.head_dim != 64 && cfg.head_dim != 128) return "head_dim must be 32, 64 or 128";
   if (cfg.seq_len % 64 || cfg.seq_len < 64) return "seq_len must be a multiple of 64";
+  if (cfg.n_kv_heads != cfg.n_heads && (cfg.head_dim != 128 || cfg.seq_len % 128 || cfg.dtype != MALLEUS_BF16))
+    return "GQA runs on the tcgen05 attention kernels: head_dim 128, seq_len a multiple of 128, bf16";
   return "";
 }
 
 std::vector<TensorInfo> all_tensors(const malleus_model_cfg& c) {
   std::vector<TensorInfo> v;
   const int64_t h = c.hidden, nd = (int64_t)c.n_heads * c.head_dim, F = c.ffn, V = c.vocab;
+  const int64_t kd = (int64_t)c.n_kv_heads * c.head_dim;  // W_k / W_v rows (GQA: n_kv heads)
   for (int l = 0; l < c.n_layers; ++l) {
     const int32_t b = l * 16;
     v.push_back({b + LT_G1, l, LT_G1, h, 1, SPLIT_REP, false});
     v.push_back({b + LT_WQ, l, LT_WQ, nd, h, SPLIT_HEADS, true});
-    v.push_back({b + LT_WK, l, LT_WK, nd, h, SPLIT_HEADS, true});
-    v.push_back({b + LT_WV, l, LT_WV, nd, h, SPLIT_HEADS, true});
+    v.push_back({b + LT_WK, l, LT_WK, kd, h, SPLIT_HEADS, true});
+    v.push_back({b + LT_WV, l, LT_WV, kd, h, SPLIT_HEADS, true});
     v.push_back({b + LT_WO, l, LT_WO, nd, h, SPLIT_HEADS, true});
     v.push_back({b + LT_G2, l, LT_G2, h, 1, SPLIT_REP, false});
     v.push_back({b + LT_WG, l, LT_WG, F, h, SPLIT_FFN, true});
@@ -147,10 +153,12 @@ int stage_of(const malleus_model_cfg& cfg, const PipeInfo& pipe, const TensorInf
 Range member_rows(const malleus_model_cfg& cfg, const StageInfo& st, const TensorInfo& t, int k) {
   if (t.kind == SPLIT_REP) return {0, t.rows};
   const std::vector<int>& v = t.kind == SPLIT_HEADS ? st.heads : (t.kind == SPLIT_FFN ? st.ffn : st.vocab);
-  const int64_t unit = t.kind == SPLIT_HEADS ? cfg.head_dim : 1;
+  int64_t unit = t.kind == SPLIT_HEADS ? cfg.head_dim : 1;
+  int64_t div = 1;
+  if (t.kind == SPLIT_HEADS && (t.idx == LT_WK || t.idx == LT_WV)) div = cfg.n_heads / cfg.n_kv_heads;  // KV groups
   int64_t r0 = 0;
   for (int i = 0; i < k; ++i) r0 += v[i];
-  return {r0 * unit, (r0 + v[k]) * unit};
+  return {r0 / div * unit, (r0 + v[k]) / div * unit};
 }
 
 void locate(const PlanInfo& p, int rank, int* pipe, int* stage, int* member) {

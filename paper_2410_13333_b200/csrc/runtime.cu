@@ -78,7 +78,7 @@ struct Layout {
   PlanInfo plan;
   int pipe = -1, stage = -1, member = -1;
   bool standby = true;
-  int T = 0, n_loc = 0, F_loc = 0, V_loc = 0, v0 = 0;
+  int T = 0, n_loc = 0, kv_loc = 0, F_loc = 0, V_loc = 0, v0 = 0;  // kv_loc: KV heads (GQA groups)
   int lb = 0, le = 0, n_local = 0, PP = 0, TP = 0, slots = 0;
   bool first = false, last = false;
   std::vector<TState> ts;
@@ -221,6 +221,7 @@ static void build_shape(const malleus_model_cfg& cfg, const PlanInfo& p, int ran
   L.first = L.stage == 0;
   L.last = L.stage == L.PP - 1;
   L.n_loc = st.heads[L.member];
+  L.kv_loc = L.n_loc * cfg.n_kv_heads / cfg.n_heads;
   L.F_loc = st.ffn[L.member];
   L.V_loc = st.vocab[L.member];
   L.v0 = 0;
@@ -306,6 +307,7 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
     }
     // activations
     const int64_t T = L.T, nd = (int64_t)L.n_loc * d, F = L.F_loc;
+    const int64_t qkvw = (int64_t)(L.n_loc + 2 * L.kv_loc) * d;  // q | k | v columns (GQA: kv_loc KV heads)
     // activation buffers: bf16, or fp32 in the parity mode
     auto act = [&](int64_t n) { return L.f32 ? reinterpret_cast<uint16_t*>(W.take<float>(n)) : W.take<uint16_t>(n); };
     L.slot.assign(L.slots, Slot{});
@@ -315,7 +317,7 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
       sl.L.resize(L.n_local);
       for (SlotLayer& y : sl.L) {
         y.a1 = act(T * h);
-        y.qkv = act(T * 3 * nd);
+        y.qkv = act(T * qkvw);
         y.o = act(T * nd);
         y.x1 = act(T * h);
         y.a2 = act(T * h);
@@ -344,7 +346,7 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
     L.dxb = act(T * h);
     L.dxc = act(T * h);
     L.dyrecv = act(T * h);
-    L.dqkv = act(T * 3 * nd);
+    L.dqkv = act(T * qkvw);
     L.dout = act(T * nd);
     L.dgu = act(T * 2 * F);
     L.du = act(T * F);
@@ -930,14 +932,15 @@ static cudaError_t k_rope(const Layout& L, int T, int s, int n, int d, void* buf
 }
 static cudaError_t k_attn_fwd(const Layout& L, int nb, int s, int n, int d, const void* qkv, void* o, float* lse,
                               cudaStream_t st) {
-  if (L.f32) return attention_fwd_f32(nb, s, n, d, F(qkv), F(o), lse, st);
-  return attention_fwd(nb, s, n, d, qkv, o, lse, st);
+  if (L.f32) return L.kv_loc == n ? attention_fwd_f32(nb, s, n, d, F(qkv), F(o), lse, st) : cudaErrorInvalidValue;
+  return attention_fwd(nb, s, n, d, qkv, o, lse, st, L.kv_loc);
 }
 static cudaError_t k_attn_bwd(const Layout& L, int nb, int s, int n, int d, const void* qkv, const void* o,
                               const float* lse, const void* dout, void* dqkv, float* dsum, cudaStream_t st,
                               const float2* rope_cs) {
-  if (L.f32) return attention_bwd_f32(nb, s, n, d, F(qkv), F(o), lse, F(dout), F(dqkv), dsum, st);
-  return attention_bwd(nb, s, n, d, qkv, o, lse, dout, dqkv, dsum, st, rope_cs);
+  if (L.f32) return L.kv_loc == n ? attention_bwd_f32(nb, s, n, d, F(qkv), F(o), lse, F(dout), F(dqkv), dsum, st)
+                                  : cudaErrorInvalidValue;
+  return attention_bwd(nb, s, n, d, qkv, o, lse, dout, dqkv, dsum, st, rope_cs, L.kv_loc);
 }
 static cudaError_t k_swiglu_fwd(const Layout& L, int T, int Fc, const void* gu, void* u, cudaStream_t st) {
   if (L.f32) return swiglu_fwd_f32(T, Fc, F(gu), F(u), st);
@@ -976,14 +979,15 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   CK(k_norm_fwd(L, T, h, S.x[li], nullptr, nullptr, P.g1, c.rms_eps, Y.a1, Y.r1, st));
   {  // QKV projection; RoPE fused into the epilogue when the kernel supports it
     bool rope_done = false;
-    GemmDesc g{T, 3 * nd, h, Y.a1, h, false, P.wqkv, h, false, Y.qkv, 3 * nd, GEMM_STORE_BF16};
+    const int qkvw = (L.n_loc + 2 * L.kv_loc) * d, nrot = L.n_loc + L.kv_loc;  // q | k | v; RoPE on q and k
+    GemmDesc g{T, qkvw, h, Y.a1, h, false, P.wqkv, h, false, Y.qkv, qkvw, GEMM_STORE_BF16};
     g.f32 = L.f32;
     g.rope_cs = L.rope_cs;
-    g.rope_cols = 2 * nd;
+    g.rope_cols = nrot * d;
     g.rope_s = c.seq_len;
     g.rope_done = &rope_done;
     CK(gemm_bf16(g, st));
-    if (!rope_done) CK(k_rope(L, T, c.seq_len, L.n_loc, d, Y.qkv, 3LL * nd, c.rope_theta, false, st));
+    if (!rope_done) CK(k_rope(L, T, c.seq_len, nrot, d, Y.qkv, qkvw, c.rope_theta, false, st));
   }
   CK(k_attn_fwd(L, L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, st));
   if (debug_sync()) { fprintf(stderr, "[malleus] attn fwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
@@ -1090,15 +1094,16 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   RET(gemm(ctx, nd, h, T, Y.o, nd, true, dx1, h, true, P.dwo, h, wm, st));
   CK(k_attn_bwd(L, L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, L.dqkv, L.dsum, st, L.rope_cs));
   if (debug_sync()) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
+  const int qkvw = (L.n_loc + 2 * L.kv_loc) * d;
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
-    CK(k_rope(L, T, c.seq_len, L.n_loc, d, L.dqkv, 3LL * nd, c.rope_theta, true, st));
-  RET(part_gemm(ctx, T, h, 3 * nd, L.dqkv, 3 * nd, false, P.wqkv, h, true, st));
+    CK(k_rope(L, T, c.seq_len, L.n_loc + L.kv_loc, d, L.dqkv, qkvw, c.rope_theta, true, st));
+  RET(part_gemm(ctx, T, h, qkvw, L.dqkv, qkvw, false, P.wqkv, h, true, st));
   if (tp_overlap(L)) {
     RET(tp_sum_begin(ctx, st));
-    RET(gemm_co(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
+    RET(gemm_co(ctx, qkvw, h, T, L.dqkv, qkvw, true, Y.a1, h, true, P.dwqkv, h, wm, st));
     RET(tp_sum_end(ctx, st));
   } else {
-    RET(gemm(ctx, 3 * nd, h, T, L.dqkv, 3 * nd, true, Y.a1, h, true, P.dwqkv, h, wm, st));
+    RET(gemm(ctx, qkvw, h, T, L.dqkv, qkvw, true, Y.a1, h, true, P.dwqkv, h, wm, st));
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 5, st);
@@ -1394,17 +1399,13 @@ malleus_status malleus_wait(malleus_ctx* ctx, void* stream, int32_t timeout_ms) 
     cudaEventDestroy(ev);
     return MALLEUS_OK;
   }
-  // failure path: release our spin-waits, abort every NCCL communicator (their kernels exit), drain
+  // failure path: release our spin-waits (the abort word stays set: every later TP reduction of the
+  // enqueued work gives up at once too).  NCCL communicators are not aborted here — ncclCommAbort
+  // can block behind collectives that wait for the lost peer — and the failed context is not
+  // reused: the process is expected to exit and the job to restart from the latest checkpoint
+  // (PAPER.md:735), which process teardown makes safe for any kernel still waiting on the peer.
   const double waited = elapsed_ms();
   comm_abort(1u);
-  if (ctx->L && ctx->L->tp_comm) { ncclCommAbort(ctx->L->tp_comm); ctx->L->tp_comm = nullptr; }
-  if (ctx->world_comm) { ncclCommAbort(ctx->world_comm); ctx->world_comm = nullptr; }
-  // drain: with the abort word set every later TP reduction of the enqueued work gives up at once
-  // too; the word stays set until malleus_destroy has drained the device
-  const auto t1 = std::chrono::steady_clock::now();
-  while (cudaEventQuery(ev) == cudaErrorNotReady &&
-         std::chrono::steady_clock::now() - t1 < std::chrono::seconds(60))
-    std::this_thread::sleep_for(std::chrono::microseconds(100));
   cudaEventDestroy(ev);
   cudaGetLastError();
   ctx->sticky = true;
@@ -1421,21 +1422,12 @@ malleus_status malleus_wait(malleus_ctx* ctx, void* stream, int32_t timeout_ms) 
 malleus_status malleus_destroy(malleus_ctx* ctx) {
   if (!ctx) return MALLEUS_E_ARG;
   cudaSetDevice(ctx->device);
-  if (ctx->failed) {  // bounded drain (the abort word is still set), then re-arm the guard
-    cudaEvent_t ev;
-    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
-      cudaEventRecord(ev, cudaStreamLegacy);  // the legacy stream waits for every blocking stream
-      const auto t0 = std::chrono::steady_clock::now();
-      while (cudaEventQuery(ev) == cudaErrorNotReady &&
-             std::chrono::steady_clock::now() - t0 < std::chrono::seconds(60))
-        std::this_thread::sleep_for(std::chrono::microseconds(200));
-      cudaEventDestroy(ev);
-    }
-    comm_abort(0u);
-    comm_status(true);
-  } else {
-    cudaDeviceSynchronize();
+  if (ctx->failed) {  // host-side cleanup only: kernels may still wait on the lost peer (see malleus_wait)
+    for (auto& e : ctx->ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    delete ctx;
+    return MALLEUS_OK;
   }
+  cudaDeviceSynchronize();
   cudaGetLastError();
   if (ctx->L) free_layout(ctx, ctx->L.get());
   if (ctx->world_comm) ncclCommDestroy(ctx->world_comm);

@@ -32,12 +32,13 @@ def name_to_id(name: str) -> int:
 
 def _numel(cfg, name: str) -> int:
     h, nd, F, V = cfg.hidden, cfg.n_heads * cfg.head_dim, cfg.ffn, cfg.vocab
+    kd = getattr(cfg, "kv_heads", cfg.n_heads) * cfg.head_dim
     if name in ("E", "Wlm"):
         return V * h
     if name == "gf":
         return h
     t = name.split(".")[1]
-    return {"g1": h, "g2": h, "wq": nd * h, "wk": nd * h, "wv": nd * h, "wo": nd * h,
+    return {"g1": h, "g2": h, "wq": nd * h, "wk": kd * h, "wv": kd * h, "wo": nd * h,
             "wg": F * h, "wu": F * h, "wd": F * h}[t]
 
 

@@ -133,24 +133,31 @@ def test_checkpoint_roundtrip_bitwise(L, tmp_path):
     g.close()
 
 
-def test_failure_detected_and_survivor_resumes(tmp_path):
-    """2 GPUs: TP2 plan; rank 1 hangs mid-training; rank 0 detects it (E_TIMEOUT), resumes alone."""
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
-    out = tmp_path / "r.json"
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29541", os.path.join(ROOT, "tests", "mp_failure_worker.py"),
-           str(tmp_path), str(out)]
+def _run_group(cmd, timeout):
     p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=ROOT,
                          start_new_session=True)
     try:
-        so, se = p.communicate(timeout=400)
-    except subprocess.TimeoutExpired:  # kill the whole process group (torchrun and both workers)
+        so, se = p.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:  # kill the whole process group (torchrun and its workers)
         os.killpg(p.pid, 9)
         so, se = p.communicate()
+    return p.returncode, so, se
+
+
+def test_failure_detected_and_survivor_resumes(tmp_path):
+    """2 GPUs: TP2 plan; rank 1 hangs; rank 0 detects it (E_TIMEOUT, then E_STATE); the job restarts
+    on GPU 0 alone from the checkpoint with rank 1 at x = infinity."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    worker = os.path.join(ROOT, "tests", "mp_failure_worker.py")
+    rc, so, se = _run_group([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                             "--master-addr=127.0.0.1", "--master-port=29541", worker, "detect", str(tmp_path)], 240)
+    assert (tmp_path / "detected.json").exists(), so[-3000:] + se[-3000:]
+    out = tmp_path / "r.json"
+    rc, so, se = _run_group([sys.executable, worker, "recover", str(tmp_path), str(out)], 240)
     assert out.exists(), so[-3000:] + se[-3000:]
     r = json.loads(out.read_text())
     assert r["timeout_status"] == "CommTimeout", r
-    assert r["detect_s"] < 30, r
+    assert r["detect_s"] < 30 and r["state_after"] == 6, r  # MALLEUS_E_STATE: the context is failed
     assert r["survivor_world"] == 1 and r["loaded_step"] == 2
     assert r["resumed_loss"] == r["reference_loss"], r

@@ -129,3 +129,21 @@ def test_migration_matches_oracle(L):
         assert got == ref
         done += 1
     assert _migration(L, cfg, a, a, wa) == set()
+
+
+@pytest.mark.parametrize("pname", ["P0", "P1", "P3", "P4", "P6"])
+def test_layout_gqa_plans(L, pname):
+    """GQA: the library's W_k / W_v rows follow whole KV groups, as the oracle's member_rows."""
+    from synth.gen import C1_GQA
+    cfg = C1_GQA
+    p = Pl.plan_matrix_gqa(cfg)[pname]
+    _check_plan(L, cfg, p, Pl.world_of(p), names=["0.wq", "0.wk", "1.wv", "0.wo", "E", "Wlm"])
+
+
+def test_layout_gqa_rejects_split_group(L):
+    from synth.gen import C1_GQA
+    cfg = C1_GQA
+    p = Pl.plan([Pl.pipe([Pl.stage([0, 1], [3, 1], [256, 256], [128, 128], [0, cfg.n_layers])], 4)], 2, 8)
+    ccfg = L.make_cfg(cfg)
+    n = C.c_int32(0)
+    assert L.lib.malleus_layout_query(C.byref(ccfg), L.PlanStruct(p).ref, 2, 0, 1, 0, None, C.byref(n)) == 2
