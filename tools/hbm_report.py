@@ -2,7 +2,7 @@
 roofline bounds what"): achieved GB/s = algorithmic bytes per launch / mean ncu launch time
 (cold-cache, serialised: a lower bound on the in-step rate), against the measured 6550 GB/s.
 
-  python tools/hbm_report.py profiles/r01_launches_c2_n1_v4.csv > profiles/r01_hbm_roofline.md
+  python tools/hbm_report.py profiles/r02/launches_c2_n1_final.csv > profiles/r02/hbm_roofline.md
 """
 import csv
 import json
@@ -15,10 +15,13 @@ T, h, F, V, nd = 2048, 4096, 11008, 32000, 4096
 P_TOTAL = 4 * (4 * h * h + 3 * h * F) + 2 * V * h + 9 * h  # C2 slice parameters (1.07 B)
 # algorithmic bytes per launch (reads + writes), C2 shapes at N = 1
 ALG = {
-    "rmsnorm_fwd_kernel": ("x bf16 + partial fp32 in, x' + a bf16 out (fused residual; half the launches have no partial)",
-                           (2 + 2 + 2) * T * h + 4 * T * h / 2),
+    # round 2 (TP 1): the residual adds are fused into the O / down GEMM epilogues, so the forward
+    # norm reads x1 (bf16) and writes a (bf16); the backward norm reads a bf16 dy
+    "rmsnorm_fwd_kernel": ("x bf16 in, a bf16 out (+ rstd)", (2 + 2) * T * h + 4 * T),
+    "rmsnorm_bwd_warp_kernel": ("x, dy, dres bf16 in, dx bf16 out (+ 148 x h fp32 dg partials)",
+                                (2 + 2 + 2 + 2) * T * h + 4 * 148 * h),
     "rmsnorm_bwd_kernel": ("x, dres, dx bf16 + dy fp32 (+ 888 x h fp32 dg partials)", (2 + 2 + 2 + 4) * T * h + 4 * 888 * h),
-    "colsum_accum_kernel": ("888 x h fp32 partials", 4 * 888 * h),
+    "colsum_accum_kernel": ("148 x h fp32 CTA partials (warp kernel)", 4 * 148 * h),
     "swiglu_fwd_kernel": ("gu bf16 in, u bf16 out", 2 * T * 2 * F + 2 * T * F),
     "swiglu_bwd_kernel": ("gu, du in, dgu out (bf16)", 2 * T * 2 * F + 2 * T * F + 2 * T * 2 * F),
     "ce_stats_kernel": ("logits fp32", 4 * T * V),
