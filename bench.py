@@ -283,6 +283,7 @@ def main():
         eng.write_weights(make_weights(cfg, parity=False))
         run_steps(max(args.warmup, 3))
         t0_ms = timed(args.steps)
+        probe_ref = eng.probe(30) if world > 1 else None  # start-up calibration, no injection (R12)
         inject(True)
         run_steps(2)
         tu_ms = timed(args.steps)
@@ -293,6 +294,8 @@ def main():
     else:
         eng.apply(plan)
         eng.write_weights(make_weights(cfg, parity=False))
+        run_steps(1)
+        probe_ref = eng.probe(30) if world > 1 else None  # start-up calibration, no injection (R12)
         inject(True)
     run_steps(max(args.warmup, 3))
     barrier()
@@ -364,11 +367,15 @@ def main():
         dist.all_gather_object(comp, eng.timing()["compute"])
         probe = eng.probe(30)
         active = [r for r in range(world) if Pl.member_flops(cfg, plan, r) > 0]
-        med = statistics.median(probe[r] for r in active)
-        x_probe = {r: probe[r] / med for r in active}
+        # reading R12: x_g = t_g / t_ref, t_ref = the median over ranks of the same probe at a start-up
+        # calibration without injection (not the injected median: with N = 2 it would halve x)
+        t_ref = statistics.median(probe_ref[r] for r in active)
+        x_probe = {r: probe[r] / t_ref for r in active}
         rate = {r: comp[r] / Pl.member_flops(cfg, plan, r) for r in active}
-        med_r = statistics.median(rate.values())
-        x_work = {r: rate[r] / med_r for r in active}
+        # work-normalised in-run rates (R12) relative to the fastest rank (the median of 2 ranks would
+        # be their mean); with >= 3 ranks and one straggler the median is a normal rank too
+        ref_r = statistics.median(rate.values()) if len(active) >= 3 else min(rate.values())
+        x_work = {r: rate[r] / ref_r for r in active}
         n_act = len(active)
         measured = {"x_nominal": {str(r): strag.get(r, 1.0) for r in active},
                     "x_probe": {str(r): round(v, 4) for r, v in x_probe.items()},
@@ -431,7 +438,7 @@ def main():
                            "global_batch": B, "seq_len": cfg.seq_len, "micro_batch": 1,
                            "plan": plan_summary(plan),
                            "straggler": ({"ranks": {str(r): x for r, x in strag.items()}, "mode": "DUTY",
-                                          "emulation": "spin of (x-1) x each compute segment's measured time"}
+                                          "emulation": "spin of (x-1) x each compute segment's full-speed time (learned, then frozen)"}
                                          if strag else None),
                            "l2": "working set >> 126 MB L2 (no flush needed)"},
                 "step_tflops": step_tf,

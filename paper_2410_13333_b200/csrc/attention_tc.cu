@@ -13,8 +13,7 @@
 // Both A operands come from TMEM ("ts" MMAs: Q copied once by the softmax warps, P in place), so the
 // only shared-memory operand traffic is K and V: measured on the previous version (Q and P as smem
 // operands) the tile loop was bound by shared-memory bandwidth (A + B of every MMA, P stores, TMA).
-// TMEM: S0 cols [0,128), S1 [128,256), O [256,384), Q [448,512).  The pair of warps sharing a row
-// exchanges row statistics through shared memory (the Q landing buffer, free once Q is in TMEM).
+// TMEM: S0 cols [0,128), S1 [128,256), O [256,384), row-max exchange [384,388), Q [448,512).
 // smem: Q 32 KB (TMA landing), 3 x K 32 KB, 3 x V 32 KB.
 // Output identical in layout to attention.cu: o [T, n*d] bf16, lse [nb, n, s] (natural log).
 #include <cuda.h>
@@ -90,7 +89,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, int n_k
   uint64_t* o_done = bars + 19;                // [2] (PV of tile j completes on o_done[j & 1])
   uint64_t* q_tmem = bars + 21;                // Q copied into TMEM by the softmax warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
-  constexpr uint32_t COL_O = 256, COL_Q = 448;
+  constexpr uint32_t COL_O = 256, COL_X = 384, COL_Q = 448;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;
@@ -225,14 +224,21 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, int n_k
       if (lane == 0) mbar_arrive(q_tmem);
     }
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory"); };
-    // the pair exchanges its partial row statistics through shared memory — the Q landing buffer,
-    // free once Q is in TMEM (every softmax warp copied its part before the first S was issued) —
-    // in two alternating slots: [slot][half][row]
-    float* xch = reinterpret_cast<float*>(sQ);
+    // the pair exchanges its partial row statistics through spare TMEM columns (measured: an smem
+    // exchange through the free Q landing buffer made the forward slower, 65.8 -> 70.0 us at C2)
     auto exchange = [&](float mine, int slot) -> float {  // returns the partner's value
-      xch[(slot * 2 + half) * TQ + r] = mine;
+      uint32_t v = __float_as_uint(mine);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tbase + lane_off + COL_X + slot * 2 + half),
+                   "r"(v) : "memory");
+      tmem_wait_st();
+      tc_fence_before();
       pair_sync();
-      return xch[(slot * 2 + (half ^ 1)) * TQ + r];
+      tc_fence_after();
+      uint32_t o;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(o)
+                   : "r"(tbase + lane_off + COL_X + slot * 2 + (half ^ 1)) : "memory");
+      tmem_wait_ld();
+      return __uint_as_float(o);
     };
     for (int i = 0; i < n_tiles; ++i) {
       const int sb = i & 1;

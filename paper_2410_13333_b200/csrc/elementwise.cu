@@ -617,7 +617,10 @@ cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float*
                         const void* dres, void* dx_out, float* dg_accum, float* scratch, cudaStream_t st,
                         bool dy_bf16) {
   if (h % 8 || h > 8 * NORM_MAXV * NORM_THREADS || T <= 0) return cudaErrorInvalidValue;
-  if (dy_bf16 && !getenv("MALLEUS_NORM_BWD_BLOCK")) {
+  // the warp-per-row kernel measured slower in the C2 step (31.8 + 4.7 us vs 24.9 + 7.1 us with the
+  // block kernel on fp32 dy: one 128 KB-smem CTA per SM leaves too few rows in flight); opt-in only
+  static const bool warp_kernel = getenv("MALLEUS_NORM_BWD_WARP") != nullptr;
+  if (dy_bf16 && warp_kernel) {
     if (BwdWarpFn fn = bwd_warp_fn(h)) {
       const int warps = std::min(8, BWDW_SMEM / (h * 4));
       const int smem = warps * h * 4;

@@ -140,11 +140,13 @@ struct Bump {
 };
 
 constexpr int kDutySegs = 16, kDutyRing = 64;
+constexpr int kDutyLearn = 4;  // segment durations measured (without spin) before the spin starts
 struct DutyTimer {
   bool init = false;
   cudaEvent_t b[kDutyRing], e[kDutyRing];
   long long head = 0, tail = 0;
-  double ms = -1.0;
+  double ms = -1.0;   // mean duration of the segment at full speed (frozen after kDutyLearn samples)
+  int n = 0;          // samples taken since set_slowdown
 };
 
 }  // namespace
@@ -902,13 +904,20 @@ static void duty_end(malleus_ctx* ctx, cudaStream_t st) {
   DutyTimer& d = ctx->duty[ctx->cur_seg % kDutySegs];
   cudaEventRecord(d.e[d.head % kDutyRing], st);
   d.head++;
+  // the segment's full-speed duration is learned from its first kDutyLearn executions after
+  // set_slowdown (no spin yet) and then frozen: a spin proportional to a duration that already
+  // contains earlier spins' side effects (a peer's TP reduction spinning beside the overlapped
+  // weight-gradient GEMM while it waits for this rank) would feed back and over-slow the rank
   while (d.tail < d.head && cudaEventQuery(d.e[d.tail % kDutyRing]) == cudaSuccess) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, d.b[d.tail % kDutyRing], d.e[d.tail % kDutyRing]);
-    d.ms = d.ms < 0 ? ms : 0.7 * d.ms + 0.3 * ms;
+    if (d.n < kDutyLearn) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, d.b[d.tail % kDutyRing], d.e[d.tail % kDutyRing]);
+      d.ms = d.n == 0 ? ms : (d.ms * d.n + ms) / (d.n + 1);
+      d.n++;
+    }
     d.tail++;
   }
-  if (d.ms > 0) spin_ns((long long)((ctx->slowdown - 1.0) * d.ms * 1e6), st);
+  if (d.n >= kDutyLearn) spin_ns((long long)((ctx->slowdown - 1.0) * d.ms * 1e6), st);
   ctx->cur_seg = -1;
 }
 
@@ -1916,7 +1925,7 @@ malleus_status malleus_set_slowdown(malleus_ctx* ctx, float x, int32_t mode) {
                 "synchronisation (cudaDeviceSynchronize / cudaFree) of the process; use DUTY (2)");
   ctx->slowdown = x;
   ctx->slow_mode = mode;
-  for (auto& d : ctx->duty) { d.ms = -1.0; }
+  for (auto& d : ctx->duty) { d.ms = -1.0; d.n = 0; }
   return MALLEUS_OK;
 }
 

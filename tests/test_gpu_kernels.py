@@ -87,8 +87,8 @@ def test_rmsnorm_bwd(L, T, h):
 
 @pytest.mark.parametrize("T,h", [(64, 256), (300, 512), (2048, 4096), (1000, 3072), (97, 6656), (64, 128)])
 def test_rmsnorm_bwd_bf16_dy(L, T, h):
-    """bf16 input gradient (TP sums, TP-1 dgrad output): the warp-per-row kernel with per-warp
-    shared-memory gain-gradient slices (h % 256 == 0, h <= 4096), else the block kernel."""
+    """bf16 input gradient (TP sums, TP-1 dgrad output) through the block kernel (the warp-per-row
+    variant, opt-in with MALLEUS_NORM_BWD_WARP=1, is checked in a subprocess below)."""
     x = bf(normal_matrix((T, h), 14))
     g = bf(1 + 0.1 * normal_matrix((h,), 15))
     dy = bf(normal_matrix((T, h), 16))
@@ -107,6 +107,21 @@ def test_rmsnorm_bwd_bf16_dy(L, T, h):
     assert L.lib.malleus_k_rmsnorm_bwd16(*args, dg2.data_ptr(), stream()) == 0
     torch.cuda.synchronize()
     assert torch.equal(dg, dg2)  # deterministic
+
+
+def test_rmsnorm_bwd_bf16_dy_warp_kernel():
+    """The opt-in warp-per-row RMSNorm backward (per-warp shared-memory dg slices) in a fresh process."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MALLEUS_NORM_BWD_WARP="1")
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k", "rmsnorm_bwd_bf16_dy and not warp",
+                        os.path.join(root, "tests", "test_gpu_kernels.py")], env=env, capture_output=True, text=True,
+                       cwd=root, timeout=600)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
 
 
 def _attn_ref(q4, k4, v4, d, s, theta):
