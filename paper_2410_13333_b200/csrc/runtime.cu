@@ -740,6 +740,7 @@ static malleus_status gemm_co(malleus_ctx* ctx, int M, int N, int K, const void*
 
 static void duty_begin(malleus_ctx* ctx, int seg, cudaStream_t st);
 static void duty_end(malleus_ctx* ctx, cudaStream_t st);
+static void duty_relearn(malleus_ctx* ctx);
 
 static malleus_status tp_allreduce(malleus_ctx* ctx, float* buf, size_t n, ncclRedOp_t op, cudaStream_t st) {
   Layout& L = *ctx->L;
@@ -886,6 +887,10 @@ static malleus_status part_gemm(malleus_ctx* ctx, int M, int N, int K, const voi
 // stream, where t_segment is a moving average of that segment's own measured duration (events are
 // polled without blocking).  Only compute is stretched, not communication, as with a GPU that is
 // x times slower (PAPER.md:400-401 defines x as the slowdown vs a normal GPU).
+// a new plan changes every segment's work: the full-speed durations are learned again
+static void duty_relearn(malleus_ctx* ctx) {
+  for (auto& d : ctx->duty) { d.ms = -1.0; d.n = 0; }
+}
 static void duty_begin(malleus_ctx* ctx, int seg, cudaStream_t st) {
   if (ctx->slow_mode != 2 || ctx->slowdown <= 1.f) return;
   DutyTimer& d = ctx->duty[seg % kDutySegs];
@@ -1476,6 +1481,7 @@ malleus_status malleus_plan_apply(malleus_ctx* ctx, const malleus_plan* plan, co
   CK(cudaDeviceSynchronize());
   if (ctx->L) free_layout(ctx, ctx->L.get());
   ctx->L = std::move(L);
+  duty_relearn(ctx);
   CK(cudaMemset(arenas->grads, 0, ctx->L->grads_bytes));
   return MALLEUS_OK;
 }
@@ -1743,6 +1749,7 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     free_layout(ctx, ctx->L.get());
     ctx->L = std::move(NL);
+    duty_relearn(ctx);
     if (stats) {
       stats->bytes_sent = sent;
       stats->bytes_recv = recvd;
@@ -1846,6 +1853,7 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
   const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   free_layout(ctx, ctx->L.get());
   ctx->L = std::move(NL);
+  duty_relearn(ctx);
   if (stats) {
     stats->bytes_sent = sent;
     stats->bytes_recv = recvd;
