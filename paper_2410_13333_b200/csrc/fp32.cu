@@ -198,12 +198,13 @@ __global__ void embed_bwd_f32_kernel(int T, int h, const int32_t* __restrict__ t
 // Forward: one warp per (query i, head, sequence); online softmax over keys j <= i; each lane
 // holds d/32 dimensions (d <= 128).
 constexpr int AD = 4;  // dims per lane (d <= 128)
-__global__ void attn_fwd_f32_kernel(int s, int n, int d, int nb, const float* __restrict__ qkv, float* __restrict__ o,
-                                    float* __restrict__ lse, float scale) {
+// GQA: qkv = q (n heads) | k (n_kv) | v (n_kv); query head hd reads KV head hd / (n / n_kv).
+__global__ void attn_fwd_f32_kernel(int s, int n, int n_kv, int d, int nb, const float* __restrict__ qkv,
+                                    float* __restrict__ o, float* __restrict__ lse, float scale) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= nb * n * s) return;
-  const int i = warp % s, hd = (warp / s) % n, b = warp / s / n;
-  const long long ld = 3LL * n * d, t0 = (long long)b * s;
+  const int i = warp % s, hd = (warp / s) % n, b = warp / s / n, kvh = hd / (n / n_kv);
+  const long long ld = (long long)(n + 2 * n_kv) * d, t0 = (long long)b * s;
   const float* q = qkv + (t0 + i) * ld + (long long)hd * d;
   float qv[AD], acc[AD];
 #pragma unroll
@@ -214,8 +215,8 @@ __global__ void attn_fwd_f32_kernel(int s, int n, int d, int nb, const float* __
   }
   float m = -INFINITY, l = 0.f;
   for (int j = 0; j <= i; ++j) {
-    const float* k = qkv + (t0 + j) * ld + (long long)(n + hd) * d;
-    const float* v = qkv + (t0 + j) * ld + (long long)(2 * n + hd) * d;
+    const float* k = qkv + (t0 + j) * ld + (long long)(n + kvh) * d;
+    const float* v = qkv + (t0 + j) * ld + (long long)(n + n_kv + kvh) * d;
     float sc = 0.f;
 #pragma unroll
     for (int u = 0; u < AD; ++u) {
@@ -259,13 +260,13 @@ __global__ void attn_dsum_f32_kernel(long long T, int n, int d, const float* __r
 }
 
 // dQ_i = scale * sum_{j<=i} dS_ij K_j,  dS_ij = P_ij (dO_i . V_j - D_i),  P_ij = exp(scale q_i.k_j - lse_i)
-__global__ void attn_dq_f32_kernel(int s, int n, int d, int nb, const float* __restrict__ qkv,
+__global__ void attn_dq_f32_kernel(int s, int n, int n_kv, int d, int nb, const float* __restrict__ qkv,
                                    const float* __restrict__ dout, const float* __restrict__ lse,
                                    const float* __restrict__ dsum, float* __restrict__ dqkv, float scale) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= nb * n * s) return;
-  const int i = warp % s, hd = (warp / s) % n, b = warp / s / n;
-  const long long ld = 3LL * n * d, t0 = (long long)b * s, ti = t0 + i;
+  const int i = warp % s, hd = (warp / s) % n, b = warp / s / n, kvh = hd / (n / n_kv);
+  const long long ld = (long long)(n + 2 * n_kv) * d, t0 = (long long)b * s, ti = t0 + i;
   const float* q = qkv + ti * ld + (long long)hd * d;
   const float* dO = dout + ti * (long long)n * d + (long long)hd * d;
   float qv[AD], dov[AD], acc[AD];
@@ -278,8 +279,8 @@ __global__ void attn_dq_f32_kernel(int s, int n, int d, int nb, const float* __r
   }
   const float L = lse[((long long)b * n + hd) * s + i], D = dsum[ti * n + hd];
   for (int j = 0; j <= i; ++j) {
-    const float* k = qkv + (t0 + j) * ld + (long long)(n + hd) * d;
-    const float* v = qkv + (t0 + j) * ld + (long long)(2 * n + hd) * d;
+    const float* k = qkv + (t0 + j) * ld + (long long)(n + kvh) * d;
+    const float* v = qkv + (t0 + j) * ld + (long long)(n + n_kv + kvh) * d;
     float sc = 0.f, dp = 0.f;
 #pragma unroll
     for (int u = 0; u < AD; ++u) {
@@ -306,16 +307,17 @@ __global__ void attn_dq_f32_kernel(int s, int n, int d, int nb, const float* __r
   }
 }
 
-// dV_j = sum_{i>=j} P_ij dO_i;  dK_j = scale * sum_{i>=j} dS_ij Q_i   (one warp per key j)
-__global__ void attn_dkv_f32_kernel(int s, int n, int d, int nb, const float* __restrict__ qkv,
+// dV_j = sum_{i>=j} P_ij dO_i;  dK_j = scale * sum_{i>=j} dS_ij Q_i   (one warp per key j and KV
+// head; GQA: summed over the group's query heads in head order)
+__global__ void attn_dkv_f32_kernel(int s, int n, int n_kv, int d, int nb, const float* __restrict__ qkv,
                                     const float* __restrict__ dout, const float* __restrict__ lse,
                                     const float* __restrict__ dsum, float* __restrict__ dqkv, float scale) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= nb * n * s) return;
-  const int j = warp % s, hd = (warp / s) % n, b = warp / s / n;
-  const long long ld = 3LL * n * d, t0 = (long long)b * s, tj = t0 + j;
-  const float* k = qkv + tj * ld + (long long)(n + hd) * d;
-  const float* v = qkv + tj * ld + (long long)(2 * n + hd) * d;
+  if (warp >= nb * n_kv * s) return;
+  const int j = warp % s, kvh = (warp / s) % n_kv, b = warp / s / n_kv, g = n / n_kv;
+  const long long ld = (long long)(n + 2 * n_kv) * d, t0 = (long long)b * s, tj = t0 + j;
+  const float* k = qkv + tj * ld + (long long)(n + kvh) * d;
+  const float* v = qkv + tj * ld + (long long)(n + n_kv + kvh) * d;
   float kv[AD], vv[AD], dk[AD], dv[AD];
 #pragma unroll
   for (int u = 0; u < AD; ++u) {
@@ -324,7 +326,8 @@ __global__ void attn_dkv_f32_kernel(int s, int n, int d, int nb, const float* __
     vv[u] = c < d ? v[c] : 0.f;
     dk[u] = dv[u] = 0.f;
   }
-  for (int i = j; i < s; ++i) {
+  for (int hi = 0; hi < g * (s - j); ++hi) {
+    const int hd = kvh * g + hi / (s - j), i = j + hi % (s - j);
     const long long ti = t0 + i;
     const float* q = qkv + ti * ld + (long long)hd * d;
     const float* dO = dout + ti * (long long)n * d + (long long)hd * d;
@@ -347,8 +350,8 @@ __global__ void attn_dkv_f32_kernel(int s, int n, int d, int nb, const float* __
       if (c < d) { dv[u] += p * dO[c]; dk[u] += ds * q[c]; }
     }
   }
-  float* dkp = dqkv + tj * ld + (long long)(n + hd) * d;
-  float* dvp = dqkv + tj * ld + (long long)(2 * n + hd) * d;
+  float* dkp = dqkv + tj * ld + (long long)(n + kvh) * d;
+  float* dvp = dqkv + tj * ld + (long long)(n + n_kv + kvh) * d;
 #pragma unroll
   for (int u = 0; u < AD; ++u) {
     const int c = lane + 32 * u;
@@ -427,24 +430,28 @@ cudaError_t embed_bwd_f32(int T, int h, const int32_t* tok, const float* dx, flo
   return cudaGetLastError();
 }
 
-cudaError_t attention_fwd_f32(int nb, int s, int n, int d, const float* qkv, float* o, float* lse, cudaStream_t st) {
-  if (d > 32 * AD || d < 1) return cudaErrorInvalidValue;
+cudaError_t attention_fwd_f32(int nb, int s, int n, int d, const float* qkv, float* o, float* lse, cudaStream_t st,
+                              int n_kv) {
+  if (n_kv <= 0) n_kv = n;
+  if (d > 32 * AD || d < 1 || n % n_kv) return cudaErrorInvalidValue;
   const long long warps = (long long)nb * n * s;
-  attn_fwd_f32_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(s, n, d, nb, qkv, o, lse,
+  attn_fwd_f32_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(s, n, n_kv, d, nb, qkv, o, lse,
                                                                             1.f / sqrtf((float)d));
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t attention_bwd_f32(int nb, int s, int n, int d, const float* qkv, const float* o, const float* lse,
-                              const float* dout, float* dqkv, float* dsum, cudaStream_t st) {
-  if (d > 32 * AD || d < 1) return cudaErrorInvalidValue;
+                              const float* dout, float* dqkv, float* dsum, cudaStream_t st, int n_kv) {
+  if (n_kv <= 0) n_kv = n;
+  if (d > 32 * AD || d < 1 || n % n_kv) return cudaErrorInvalidValue;
   const long long T = (long long)nb * s, warps = T * n;
   const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+  const unsigned blocks_kv = (unsigned)((T * n_kv * 32 + 255) / 256);
   const float scale = 1.f / sqrtf((float)d);
   attn_dsum_f32_kernel<<<blocks, 256, 0, st>>>(T, n, d, o, dout, dsum); count_launch();
-  attn_dq_f32_kernel<<<blocks, 256, 0, st>>>(s, n, d, nb, qkv, dout, lse, dsum, dqkv, scale); count_launch();
-  attn_dkv_f32_kernel<<<blocks, 256, 0, st>>>(s, n, d, nb, qkv, dout, lse, dsum, dqkv, scale); count_launch();
+  attn_dq_f32_kernel<<<blocks, 256, 0, st>>>(s, n, n_kv, d, nb, qkv, dout, lse, dsum, dqkv, scale); count_launch();
+  attn_dkv_f32_kernel<<<blocks_kv, 256, 0, st>>>(s, n, n_kv, d, nb, qkv, dout, lse, dsum, dqkv, scale); count_launch();
   return cudaGetLastError();
 }
 

@@ -66,9 +66,10 @@ cudaError_t swiglu_fwd_f32(int T, int F, const float* gu, float* u, cudaStream_t
 cudaError_t swiglu_bwd_f32(int T, int F, const float* gu, const float* du, float* dgu, cudaStream_t st);
 cudaError_t embed_fwd_f32(int T, int h, const int32_t* tok, const float* E, float* x, cudaStream_t st);
 cudaError_t embed_bwd_f32(int T, int h, const int32_t* tok, const float* dx, float* dE, cudaStream_t st);
-cudaError_t attention_fwd_f32(int nb, int s, int n, int d, const float* qkv, float* o, float* lse, cudaStream_t st);
+cudaError_t attention_fwd_f32(int nb, int s, int n, int d, const float* qkv, float* o, float* lse, cudaStream_t st,
+                              int n_kv = 0);  // n_kv <= 0: MHA
 cudaError_t attention_bwd_f32(int nb, int s, int n, int d, const float* qkv, const float* o, const float* lse,
-                              const float* dout, float* dqkv, float* dsum, cudaStream_t st);
+                              const float* dout, float* dqkv, float* dsum, cudaStream_t st, int n_kv = 0);
 
 // ---- elementwise / normalisation (elementwise.cu)
 cudaError_t rmsnorm_fwd(int T, int h, const void* x, const float* partial, void* x_out,

@@ -837,9 +837,13 @@ static malleus_status tp_sum(malleus_ctx* ctx, cudaStream_t st) {
 // buffers; the wgrad GEMM touches neither) while the GEMM, given a 5-stage ring so the reduction's
 // CTAs fit beside it on every SM, runs on the main stream; the main stream joins before the norm's
 // backward reads the sum.  MALLEUS_TP_NO_OVERLAP=1 serialises them.
-static bool tp_overlap(const Layout& L) {
+static bool duty_learning(const malleus_ctx* ctx);
+static bool tp_overlap(const malleus_ctx* ctx) {
   static const bool off = getenv("MALLEUS_TP_NO_OVERLAP") != nullptr;
-  return !off && tp_peer(L);
+  // while the DUTY emulation learns the current segment's full-speed duration the reduction is
+  // not overlapped: the learned time is the segment's compute alone, without the interference of
+  // a reduction spinning beside the weight-gradient GEMM while it waits for a slower peer
+  return !off && tp_peer(*ctx->L) && !duty_learning(ctx);
 }
 static malleus_status tp_sum_begin(malleus_ctx* ctx, cudaStream_t st) {
   if (!ctx->tp_side) {
@@ -887,6 +891,10 @@ static malleus_status part_gemm(malleus_ctx* ctx, int M, int N, int K, const voi
 // stream, where t_segment is a moving average of that segment's own measured duration (events are
 // polled without blocking).  Only compute is stretched, not communication, as with a GPU that is
 // x times slower (PAPER.md:400-401 defines x as the slowdown vs a normal GPU).
+static bool duty_learning(const malleus_ctx* ctx) {
+  return ctx->slow_mode == 2 && ctx->slowdown > 1.f && ctx->cur_seg >= 0 &&
+         ctx->duty[ctx->cur_seg % kDutySegs].n < kDutyLearn;
+}
 // a new plan changes every segment's work: the full-speed durations are learned again
 static void duty_relearn(malleus_ctx* ctx) {
   for (auto& d : ctx->duty) { d.ms = -1.0; d.n = 0; }
@@ -946,14 +954,13 @@ static cudaError_t k_rope(const Layout& L, int T, int s, int n, int d, void* buf
 }
 static cudaError_t k_attn_fwd(const Layout& L, int nb, int s, int n, int d, const void* qkv, void* o, float* lse,
                               cudaStream_t st) {
-  if (L.f32) return L.kv_loc == n ? attention_fwd_f32(nb, s, n, d, F(qkv), F(o), lse, st) : cudaErrorInvalidValue;
+  if (L.f32) return attention_fwd_f32(nb, s, n, d, F(qkv), F(o), lse, st, L.kv_loc);
   return attention_fwd(nb, s, n, d, qkv, o, lse, st, L.kv_loc);
 }
 static cudaError_t k_attn_bwd(const Layout& L, int nb, int s, int n, int d, const void* qkv, const void* o,
                               const float* lse, const void* dout, void* dqkv, float* dsum, cudaStream_t st,
                               const float2* rope_cs) {
-  if (L.f32) return L.kv_loc == n ? attention_bwd_f32(nb, s, n, d, F(qkv), F(o), lse, F(dout), F(dqkv), dsum, st)
-                                  : cudaErrorInvalidValue;
+  if (L.f32) return attention_bwd_f32(nb, s, n, d, F(qkv), F(o), lse, F(dout), F(dqkv), dsum, st, L.kv_loc);
   return attention_bwd(nb, s, n, d, qkv, o, lse, dout, dqkv, dsum, st, rope_cs, L.kv_loc);
 }
 static cudaError_t k_swiglu_fwd(const Layout& L, int T, int Fc, const void* gu, void* u, cudaStream_t st) {
@@ -1093,7 +1100,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
     if (!glu_done) CK(k_swiglu_bwd(L, T, F, Y.gu, L.du, L.dgu, st));
   }
   RET(part_gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, st));
-  if (tp_overlap(L)) {
+  if (tp_overlap(ctx)) {
     RET(tp_sum_begin(ctx, st));
     RET(gemm_co(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
     RET(tp_sum_end(ctx, st));
@@ -1112,7 +1119,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
     CK(k_rope(L, T, c.seq_len, L.n_loc + L.kv_loc, d, L.dqkv, qkvw, c.rope_theta, true, st));
   RET(part_gemm(ctx, T, h, qkvw, L.dqkv, qkvw, false, P.wqkv, h, true, st));
-  if (tp_overlap(L)) {
+  if (tp_overlap(ctx)) {
     RET(tp_sum_begin(ctx, st));
     RET(gemm_co(ctx, qkvw, h, T, L.dqkv, qkvw, true, Y.a1, h, true, P.dwqkv, h, wm, st));
     RET(tp_sum_end(ctx, st));
@@ -1149,7 +1156,7 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
     CK(reduce_loss(T, L.loss_rows, (float)(1.0 / ((double)L.plan.B * c.seq_len)), L.loss_acc, 1, st));
   RET(part_gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, st));
   const int wm_lm = first ? GEMM_STORE_F32 : GEMM_ACCUM_F32;
-  if (tp_overlap(L)) {
+  if (tp_overlap(ctx)) {
     RET(tp_sum_begin(ctx, st));
     RET(gemm_co(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, wm_lm, st));
     RET(tp_sum_end(ctx, st));
@@ -1720,6 +1727,15 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
     // no rank frees an old arena that a peer is still reading.
     const auto trp = migration_transfers(ctx->cfg, O.plan, np);
     std::vector<CopyDesc> descs = keep;
+    // large remote ranges go to the copy engines (one cudaMemcpyAsync each, on a side stream, in
+    // parallel with the SM kernel doing the keep-copies and the small pulls); MALLEUS_MIGRATE_CE=0
+    // keeps every pull in the SM kernel
+    static const long long ce_min = [] {
+      const char* e = getenv("MALLEUS_MIGRATE_CE");
+      return e && atoi(e) == 0 ? -1LL : (1LL << 20);
+    }();
+    struct CeCopy { const char* src; char* dst; long long bytes; };
+    std::vector<CeCopy> ce;
     for (auto& t : trp) {
       if (t.dst != me) {
         if (t.src == me) sent += (t.e1 - t.e0) * (t.kind == MALLEUS_KIND_PARAM ? O.aes : 4);
@@ -1728,7 +1744,9 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
       size_t es;
       const char* src = locate_ptr(*O.peer[t.src], t.tensor, t.kind, t.e0, &es);
       char* dst = locate_ptr(*NL, t.tensor, t.kind, t.e0, &es);
-      add_copy(descs, src, dst, (t.e1 - t.e0) * (long long)es);
+      const long long bytes = (t.e1 - t.e0) * (long long)es;
+      if (ce_min > 0 && bytes >= ce_min) ce.push_back({src, dst, bytes});
+      else add_copy(descs, src, dst, bytes);
       recvd += (t.e1 - t.e0) * es;
     }
     CopyDesc* d_desc = nullptr;
@@ -1741,7 +1759,19 @@ malleus_status malleus_migrate(malleus_ctx* ctx, const malleus_plan* new_plan, c
     NK(ncclAllReduce(bar, bar, 1, ncclFloat, ncclSum, ctx->world_comm, st));  // everyone ready
     CK(cudaStreamSynchronize(st));
     const auto t1 = std::chrono::steady_clock::now();
+    if (!ce.empty()) {
+      if (!ctx->tp_side) {
+        CK(cudaStreamCreateWithFlags(&ctx->tp_side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->tp_ev_a, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->tp_ev_b, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(ctx->tp_ev_a, st));
+      CK(cudaStreamWaitEvent(ctx->tp_side, ctx->tp_ev_a, 0));
+      for (const CeCopy& c : ce) CK(cudaMemcpyAsync(c.dst, c.src, (size_t)c.bytes, cudaMemcpyDeviceToDevice, ctx->tp_side));
+      CK(cudaEventRecord(ctx->tp_ev_b, ctx->tp_side));
+    }
     CK(copy_ranges((int)descs.size(), d_desc, st));
+    if (!ce.empty()) CK(cudaStreamWaitEvent(st, ctx->tp_ev_b, 0));
     NK(ncclAllReduce(bar, bar, 1, ncclFloat, ncclSum, ctx->world_comm, st));  // everyone done reading
     CK(cudaStreamSynchronize(st));
     const double xfer = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();

@@ -23,12 +23,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-from synth.gen import C1_TINY, C1_MED, C1_MED_GQA, make_weights, make_tokens, bf16_rne, tensor_shapes  # noqa: E402
+from synth.gen import C1_TINY, C1_MED, C1_MED_GQA, C1_GQA, make_weights, make_tokens, bf16_rne, tensor_shapes  # noqa: E402
 from paper_2410_13333_b200 import plans as Pl  # noqa: E402
 from paper_2410_13333_b200 import _lib as L  # noqa: E402
 from paper_2410_13333_b200.engine import Engine, gather_logical  # noqa: E402
 
-CONFIGS = {"c1": C1_TINY, "c1m": C1_MED, "c1mg": C1_MED_GQA}
+CONFIGS = {"c1": C1_TINY, "c1m": C1_MED, "c1mg": C1_MED_GQA, "c1g": C1_GQA}
 
 
 def run(plan_name: str, rank: int = 0, world: int = 1, local_rank: int = 0, group=None, steps: int = 1,

@@ -50,6 +50,33 @@ def test_gqa_multi_gpu_plans(plan, tmp_path):
     _ok(json.loads(out.read_text()))
 
 
+@pytest.mark.parametrize("cfg_name", ["c1g", "c1mg"])
+def test_gqa_p0_fp32(cfg_name):
+    """FP32 parity mode with GQA (SIMT attention, any head_dim): <= 1e-4 against the oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from tests.mp_worker import run
+    from tests.test_gpu_fp32 import _assert_fp32
+    _assert_fp32(run("P0", steps=2, cfg_name=cfg_name, dtype="fp32"))
+
+
+@pytest.mark.parametrize("plan", ["P1", "P4"])
+def test_gqa_multi_gpu_fp32(plan, tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    n = WORLD[plan]
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"{plan} needs {n} GPUs")
+    from tests.test_gpu_fp32 import _assert_fp32
+    out = tmp_path / "r.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29538", os.path.join(ROOT, "tests", "mp_worker.py"), plan,
+           str(out), "2", "c1g", "fp32"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    _assert_fp32(json.loads(out.read_text()))
+
+
 def test_gqa_plan_rejections():
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
@@ -63,7 +90,7 @@ def test_gqa_plan_rejections():
     e = Engine(cfg, 0, 1, 0)
     e.apply(bad)  # a valid single-GPU plan applies
     e.close()
-    # d = 32 GQA has no tensor-core attention kernel: refused at plan time, not mid-step
+    # bf16 GQA with d = 32 has no tensor-core attention kernel: refused at plan time, not mid-step
     e = Engine(C1_GQA, 0, 1, 0)
     with pytest.raises(L.MalleusError):
         e.apply(Pl.plan_matrix_gqa(C1_GQA)["P0"])
