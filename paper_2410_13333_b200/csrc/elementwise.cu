@@ -117,6 +117,42 @@ rmsnorm_fwd_kernel(int h, const uint4* __restrict__ x, const float4* __restrict_
   }
 }
 
+// Warp-per-row variant (no fused partial, h % 256 == 0): lane l holds columns 8 l + 256 i of its
+// row (NV = h / 256 vectors), the sum of squares is a warp shuffle — no block barrier per row, 8 rows
+// per CTA in flight.  Same arithmetic and rounding as rmsnorm_fwd_kernel.
+template <int NV>
+__global__ void __launch_bounds__(256) rmsnorm_fwd_warp_kernel(int T, int h, const uint4* __restrict__ x,
+                                                               const uint4* __restrict__ g, float eps,
+                                                               uint4* __restrict__ y, float* __restrict__ rstd) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= T) return;
+  const int nv = h / 8;
+  uint4 xq[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) xq[i] = x[(long long)row * nv + lane + 32 * i];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float v[8];
+    unpack8(xq[i], v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += v[j] * v[j];
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / (float)h + eps);
+  if (lane == 0) rstd[row] = r;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float v[8], gg[8], o[8];
+    unpack8(xq[i], v);
+    unpack8(__ldg(g + lane + 32 * i), gg);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = v[j] * r * gg[j];
+    y[(long long)row * nv + lane + 32 * i] = pack8(o);
+  }
+}
+
 // ---------------------------------------------------------------- RMSNorm backward
 // dx = r*u - x*r^3*mean(x*u), u = g*dy; dx_out = bf16(dres + dx); dg partial per block.
 // Two passes over each row (the second re-reads x / dy / g from L1) so that only the dg
@@ -590,6 +626,23 @@ cudaError_t rmsnorm_fwd(int T, int h, const void* x, const float* partial, void*
                         float eps, void* y, float* rstd, cudaStream_t st) {
   if (h % 8 || h > 8 * NORM_MAXV * NORM_THREADS || T <= 0) return cudaErrorInvalidValue;
   if (partial && !x_out) return cudaErrorInvalidValue;
+  if (!partial && h % 256 == 0) {  // warp per row
+    using Fn = void (*)(int, int, const uint4*, const uint4*, float, uint4*, float*);
+    Fn fn = nullptr;
+    switch (h / 256) {
+      case 1: fn = rmsnorm_fwd_warp_kernel<1>; break;
+      case 2: fn = rmsnorm_fwd_warp_kernel<2>; break;
+      case 4: fn = rmsnorm_fwd_warp_kernel<4>; break;
+      case 8: fn = rmsnorm_fwd_warp_kernel<8>; break;
+      case 12: fn = rmsnorm_fwd_warp_kernel<12>; break;
+      case 16: fn = rmsnorm_fwd_warp_kernel<16>; break;
+      default: break;
+    }
+    if (fn) {
+      fn<<<(T + 7) / 8, 256, 0, st>>>(T, h, (const uint4*)x, (const uint4*)g, eps, (uint4*)y, rstd); count_launch();
+      return cudaGetLastError();
+    }
+  }
   rmsnorm_fwd_kernel<<<T, NORM_THREADS, 0, st>>>(h, (const uint4*)x, (const float4*)partial, (uint4*)x_out,
                                                  (const uint4*)g, eps, (uint4*)y, rstd); count_launch();
   return cudaGetLastError();

@@ -36,7 +36,7 @@ def stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-@pytest.mark.parametrize("T,h", [(64, 128), (300, 4096), (129, 6656), (33, 8192)])
+@pytest.mark.parametrize("T,h", [(64, 128), (300, 4096), (129, 6656), (33, 8192), (257, 512), (2048, 3072)])
 @pytest.mark.parametrize("with_partial", [False, True])
 def test_rmsnorm_fwd(L, T, h, with_partial):
     x = bf(normal_matrix((T, h), 1))
