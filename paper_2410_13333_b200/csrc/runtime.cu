@@ -927,6 +927,9 @@ static void duty_end(malleus_ctx* ctx, cudaStream_t st) {
       cudaEventElapsedTime(&ms, d.b[d.tail % kDutyRing], d.e[d.tail % kDutyRing]);
       d.ms = d.n == 0 ? ms : (d.ms * d.n + ms) / (d.n + 1);
       d.n++;
+      static const bool dbg = getenv("MALLEUS_DUTY_DEBUG") != nullptr;  // measurement aid
+      if (dbg && d.n == kDutyLearn)
+        fprintf(stderr, "[duty] rank %d seg %d learned %.3f ms (last %.3f)\n", ctx->rank, ctx->cur_seg, d.ms, ms);
     }
     d.tail++;
   }
