@@ -202,6 +202,7 @@ struct TpArgs {
   int row0[MAX_TP + 1];
   unsigned long long* trace;             // optional: per-call globaltimer stamps (MALLEUS_TP_TRACE)
   CommGuard guard;                       // filled by tp_reduce()
+  int co_resident;                       // TP_SUM beside the overlapped wgrad GEMM: <= 1 CTA / SM, 64 regs
 };
 constexpr int TP_TRACE_CALLS = 4096;
 unsigned long long* tp_trace_buffer(int member);  // managed [TP_TRACE_CALLS][4] per member, lazily allocated

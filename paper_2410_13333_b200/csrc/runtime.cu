@@ -784,7 +784,7 @@ static Layout& member_layout(Layout& L, int j) {
 // sel(M, a, j) fills member j's destinations a.d0/d1/d2[j] from its layout M
 template <class Sel>
 static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, const void* g, Sel sel,
-                                     cudaStream_t st, bool async = false) {
+                                     cudaStream_t st, bool async = false) {  // async: beside the wgrad GEMM
   Layout& L = *ctx->L;
   if (!async) {  // async: the caller handles DUTY and times only the exposed wait
     duty_end(ctx, st);
@@ -803,6 +803,7 @@ static malleus_status tp_reduce_peer(malleus_ctx* ctx, int mode, const void* x, 
   a.part_bf16 = L.tp_bf16 ? 1 : 0;
   a.sum_bf16 = L.tp_bf16 ? 1 : 0;  // bf16 partials => the backward sums go out in bf16 too
   a.uneven = L.tp_uneven ? 1 : 0;
+  a.co_resident = async ? 1 : 0;
   for (int j = 0; j <= L.TP; ++j) a.row0[j] = L.tp_row0[j];
   static const bool trace = getenv("MALLEUS_TP_TRACE") != nullptr;  // debugging aid (tools/tp_step_trace.py)
   if (trace) a.trace = tp_trace_buffer(0);

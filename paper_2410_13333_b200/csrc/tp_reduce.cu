@@ -107,8 +107,10 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 
 // K > 0: member count known at compile time, V = vectors of 8 per thread (h <= 8 * V * TPR_THREADS):
 // the loads of up to KC members are issued before their adds.  K == 0: generic runtime k.
-template <int MODE, int K, int V, bool PB>
-__global__ void __launch_bounds__(TPR_THREADS, 2) tp_reduce_kernel(const __grid_constant__ TpArgs a) {
+// MINB 4 (registers capped at 64 per thread): the co-resident variant that runs beside the weight-
+// gradient GEMM (one CTA per SM fits next to the GEMM's 192 x 256 registers); MINB 2 otherwise
+template <int MODE, int K, int V, bool PB, int MINB = 2>
+__global__ void __launch_bounds__(TPR_THREADS, MINB) tp_reduce_kernel(const __grid_constant__ TpArgs a) {
   constexpr int KC = V >= 4 ? 2 : 3;
   __shared__ float sh[TPR_THREADS / 32];
   __shared__ bool last, gave_up;
@@ -335,7 +337,36 @@ cudaError_t tp_reduce(const TpArgs& a0, cudaStream_t st) {
   const int vpt = (a.h / 8 + TPR_THREADS - 1) / TPR_THREADS;
   int r0, r1;
   tp_rows(a, a.me, &r0, &r1);
-  const int grid = tp_grid(r1 - r0);
+  static int n_sms = 0;
+  if (!n_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // co-resident (beside the overlapped weight-gradient GEMM): at most one CTA per SM, 64 registers, so
+  // the reduction never keeps the GEMM's CTAs off an SM while it waits for a slower peer (a waiting
+  // 592-CTA reduction used to hold every SM's registers and serialise the GEMM behind the wait)
+  const bool co = a.co_resident != 0 && a.mode == TP_SUM;
+  const int grid = co ? std::min(tp_grid(r1 - r0), n_sms) : tp_grid(r1 - r0);
+  if (co) {
+    auto launch_co = [&](auto k_c) {
+      constexpr int K = decltype(k_c)::value;
+      if (a.part_bf16) {
+        if (vpt <= 2) tp_reduce_kernel<TP_SUM, K, 2, true, 4><<<grid, TPR_THREADS, 0, st>>>(a);
+        else tp_reduce_kernel<TP_SUM, K, TPR_MAXV, true, 4><<<grid, TPR_THREADS, 0, st>>>(a);
+      } else {
+        if (vpt <= 2) tp_reduce_kernel<TP_SUM, K, 2, false, 4><<<grid, TPR_THREADS, 0, st>>>(a);
+        else tp_reduce_kernel<TP_SUM, K, TPR_MAXV, false, 4><<<grid, TPR_THREADS, 0, st>>>(a);
+      }
+    };
+    switch (a.k) {
+      case 2: launch_co(std::integral_constant<int, 2>{}); break;
+      case 4: launch_co(std::integral_constant<int, 4>{}); break;
+      default: launch_co(std::integral_constant<int, 0>{}); break;
+    }
+    count_launch();
+    return cudaGetLastError();
+  }
   auto launch_kv = [&](auto mode_c, auto k_c) {
     constexpr int M = decltype(mode_c)::value, K = decltype(k_c)::value;
     if (a.part_bf16) {
