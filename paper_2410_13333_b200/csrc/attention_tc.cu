@@ -603,14 +603,11 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
 }
 
 // dQ: CTA = 128 queries; loop over 128-key tiles i <= qb (2-stage K | V ring, 64 KB per stage).
-//   TMEM: S cols [0,128) (single), dP[b] [128+128b, ..) (double-buffered), dQ [384,512).  Warp half h
+//   TMEM: S[b] cols [128b, 128b+128) (double-buffered), dP [256,384), dQ [384,512).  Warp half h
 //   overwrites its own 64 dP columns with 32 columns of packed bf16 dS, the A operand of
-//   dQ += dS K_i (K = 128 keys, K_i MN-major B).  MMA order per tile: S_i (once the math warps have
-//   read S_{i-1}), dP_i (into the other dP buffer), then dQ_{i-1} (once dS_{i-1} is written): S_{i+1}
-//   and dP_{i+1} are computed while the softmax-gradient math of tile i runs, so the math of
-//   consecutive tiles runs back to back and dQ_{i-1} overlaps it (round 2; with dP single-buffered,
-//   dP_i had to wait for dQ_{i-1} and the chain dQ -> dP -> math serialised every tile).  All MMAs are
-//   N = 128 (full rate; N = 64 runs at 2/3, profiles/r01_mma_probe.log).
+//   dQ += dS K_i (K = 128 keys, K_i MN-major B).  MMA order per tile: S_i (overlaps the softmax-
+//   gradient math of tile i-1), then dQ_{i-1} (reads dS_{i-1}), then dP_i (overwrites it; the tensor
+//   pipe runs in order).  All MMAs are N = 128 (full rate; N = 64 runs at 2/3, profiles/r01_mma_probe.log).
 constexpr int KV2_STAGE = 4 * PANEL;  // K (2 panels of 128 rows) | V (2 panels)
 constexpr int BWD2_SMEM = 2 * 2 * PANEL + 2 * KV2_STAGE + 256 + 1024;
 
@@ -633,10 +630,10 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* s_free = bars + 6;    // 8 warp arrivals: S_i read into registers
-  uint64_t* dp_full = bars + 7;   // [2]
-  uint64_t* ds_full = bars + 9;   // [2] 8 warp arrivals: dS_i written over dP_i
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_free = bars + 7;    // [2] (8 warp arrivals: S_i read into registers)
+  uint64_t* dp_full = bars + 9;
+  uint64_t* ds_full = bars + 10;  // 8 warp arrivals
   uint64_t* done = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
@@ -654,10 +651,10 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1);
-      mbar_init(&dp_full[i], 1); mbar_init(&ds_full[i], 8);
+      mbar_init(&s_full[i], 1); mbar_init(&s_free[i], 8);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_free, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 8);
     mbar_init(done, 1);
     fence_barrier_init();
   }
@@ -693,14 +690,14 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
       constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_q = umma_idesc_bf16(128, 128, false, true);
       const uint32_t aq = smem_u32(sQ), ao = smem_u32(sO);
-      auto issue_dq = [&](int i) {  // dQ += dS_i K_i, dS_i over dP buffer i & 1
-        mbar_wait(&ds_full[i & 1], (i >> 1) & 1);
+      auto issue_dq = [&](int i) {  // dQ += dS_i K_i
+        mbar_wait(ds_full, i & 1);
         stamp(3, i);
         tc_fence_after();
         const uint32_t k = smem_u32(ring + (i & 1) * KV2_STAGE);
 #pragma unroll
         for (int kk = 0; kk < TK / 16; ++kk)
-          umma_f16_ts(tbase + 384, tbase + 128 + 128 * (i & 1) + (kk >> 2) * 64 + (kk & 3) * 8,
+          umma_f16_ts(tbase + 384, tbase + 256 + (kk >> 2) * 64 + (kk & 3) * 8,
                       umma_desc_sw128(k + kk * 2048, PANEL, 1024), id_q, (i > 0 || kk > 0) ? 1u : 0u);
         umma_commit(&kv_empty[i & 1]);
       };
@@ -708,26 +705,25 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
       for (int i = 0; i < n_it; ++i) {
         const int sb = i & 1;
         mbar_wait(&kv_full[sb], (i >> 1) & 1);
-        if (i > 0) mbar_wait(s_free, (i - 1) & 1);  // S_{i-1} read by the math warps
+        mbar_wait(&s_free[sb], ((i >> 1) & 1) ^ 1);  // S_{i-2} read by the math warps
         stamp(2, i);
         tc_fence_after();
         const uint32_t k = smem_u32(ring + sb * KV2_STAGE), v = k + 2 * PANEL;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          umma_f16(tbase, umma_desc_sw128(aq + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024), id_s,
+          umma_f16(tbase + sb * 128, umma_desc_sw128(aq + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024), id_s,
                    kk > 0 ? 1u : 0u);
         }
-        umma_commit(s_full);
-        // dP_i into buffer sb: its previous contents (dS_{i-2}) were read by dQ_{i-2}, issued earlier
+        umma_commit(&s_full[sb]);
+        if (i > 0) issue_dq(i - 1);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t off = (kk >> 2) * PANEL + (kk & 3) * 32;
-          umma_f16(tbase + 128 + 128 * sb, umma_desc_sw128(ao + off, 16, 1024), umma_desc_sw128(v + off, 16, 1024),
-                   id_s, kk > 0 ? 1u : 0u);
+          umma_f16(tbase + 256, umma_desc_sw128(ao + off, 16, 1024), umma_desc_sw128(v + off, 16, 1024), id_s,
+                   kk > 0 ? 1u : 0u);
         }
-        umma_commit(&dp_full[sb]);
-        if (i > 0) issue_dq(i - 1);
+        umma_commit(dp_full);
       }
       issue_dq(n_it - 1);
       umma_commit(done);
@@ -743,12 +739,12 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
     const float L2 = lse[lrow + q] * LOG2E, Dq = dsum[lrow + q];
     for (int i = 0; i < n_it; ++i) {
       const int sb = i & 1;
-      mbar_wait(s_full, i & 1);
+      mbar_wait(&s_full[sb], (i >> 1) & 1);
       if (warp == 2 && lane == 0) stamp(1, i);
-      mbar_wait(&dp_full[sb], (i >> 1) & 1);
+      mbar_wait(dp_full, i & 1);
       if (warp == 2 && lane == 0) stamp(4, i);
       tc_fence_after();
-      const uint32_t cs = tbase + lane_off + half * 64, cd = tbase + lane_off + 128 + 128 * sb + half * 64;
+      const uint32_t cs = tbase + lane_off + sb * 128 + half * 64, cd = tbase + lane_off + 256 + half * 64;
       const bool diag = i == n_it - 1;
       uint32_t dd[2][16];
 #pragma unroll
@@ -757,10 +753,10 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
         tmem_ld32(cs + c * 32, us);
         tmem_ld32(cd + c * 32, ud);
         tmem_wait_ld();
-        if (c == 1) {  // S_i fully in registers: its TMEM columns may take S_{i+1}
+        if (c == 1) {  // S_i fully in registers: its TMEM buffer may take S_{i+2}
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(s_free);
+          if (lane == 0) mbar_arrive(&s_free[sb]);
         }
         const int k0 = i * TK + half * 64 + c * 32;
 #pragma unroll
@@ -781,7 +777,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_full[sb]);
+      if (lane == 0) mbar_arrive(ds_full);
       if (warp == 2 && lane == 0) stamp(6, i);
     }
     float2 csr[32];
