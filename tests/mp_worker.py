@@ -28,15 +28,33 @@ from paper_2410_13333_b200 import plans as Pl  # noqa: E402
 from paper_2410_13333_b200 import _lib as L  # noqa: E402
 from paper_2410_13333_b200.engine import Engine, gather_logical  # noqa: E402
 
-CONFIGS = {"c1": C1_TINY, "c1m": C1_MED, "c1mg": C1_MED_GQA, "c1g": C1_GQA}
+import dataclasses  # noqa: E402
+from synth.gen import C2_7B_SLICE  # noqa: E402
+
+# c2l1: the bench's C2 shapes (h 4096, 32 heads of 128, ffn 11008, V 32000, s 2048) with one layer:
+# full-size parity in the launch configuration bench.py times (CTA-pair GEMMs with the fused
+# epilogues, tcgen05 attention at s = 2048, the TP-2 peer reduction with the scatter epilogue)
+C2_1L = dataclasses.replace(C2_7B_SLICE, n_layers=1)
+CONFIGS = {"c1": C1_TINY, "c1m": C1_MED, "c1mg": C1_MED_GQA, "c1g": C1_GQA, "c2l1": C2_1L}
+
+
+def _plans(cfg_name, cfg, B, b):
+    if cfg_name == "c2l1":  # B = 2 sequences, b = 1: two micro-batches (STORE then ACCUM weight gradients)
+        L = cfg.n_layers
+        tp2 = Pl.stage([0, 1], [22, 10], Pl._ffn_split(cfg.ffn, [1.0, 2.0]), Pl._vocab_split(cfg.vocab, [1.0, 2.0]),
+                       [0, L])
+        return {"P0": Pl.plan([Pl.pipe([Pl.even_stage(cfg, [0], [0, L])], B // b)], b, B),
+                "P2": Pl.plan([Pl.pipe([tp2], B // b)], b, B)}
+    if cfg.kv_heads != cfg.n_heads:
+        return Pl.plan_matrix_gqa(cfg, B=B, b=b)
+    return Pl.plan_matrix_c1(cfg, B=B, b=b)
 
 
 def run(plan_name: str, rank: int = 0, world: int = 1, local_rank: int = 0, group=None, steps: int = 1,
         cfg_name: str = "c1", dtype: str = "bf16"):
     cfg = CONFIGS[cfg_name]
-    B, b = 8, 2
-    plans = Pl.plan_matrix_gqa(cfg, B=B, b=b) if cfg.kv_heads != cfg.n_heads else Pl.plan_matrix_c1(cfg, B=B, b=b)
-    plan = plans[plan_name]
+    B, b = (2, 1) if cfg_name == "c2l1" else (8, 2)
+    plan = _plans(cfg_name, cfg, B, b)[plan_name]
     assert Pl.world_of(plan) == world, (plan_name, world)
     torch.cuda.set_device(local_rank)
     eng = Engine(cfg, rank, world, local_rank, group=group, dtype=dtype)
