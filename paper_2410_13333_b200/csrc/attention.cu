@@ -5,7 +5,9 @@
 // into a dK/dV kernel (one CTA per key block) and a dQ kernel (one CTA per query block) so that
 // no atomics are needed and results are bitwise reproducible run to run.
 //
-// Layout: qkv [T, 3*n*d] bf16, T = nb * s; q | k | v column blocks, head j at columns j*d.
+// Layout: qkv [T, (n + 2 n_kv) d] bf16, T = nb * s; q | k | v column blocks, head j at columns j*d;
+// GQA (n_kv < n): query head j reads KV head j / (n / n_kv), the dK/dV CTA of a KV head loops over its
+// group's query heads.
 // RoPE has already been applied to q and k (elementwise.cu).  o [T, n*d]; lse [nb, n, s] fp32.
 // This mma.sync path serves the shapes the tcgen05 kernels (attention_tc.cu: d = 128, s % 128 == 0)
 // do not cover, e.g. the tiny parity model C1 (d = 32).
@@ -92,7 +94,7 @@ __device__ __forceinline__ void frag_b_kn(const __nv_bfloat16* sm, int k0, int n
 // CTA = NW warps x 16 queries; K/V tiles of 64 keys streamed with a 2-deep cp.async ring.
 template <int D, int NW>
 __global__ void __launch_bounds__(NW * 32)
-attn_fwd_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ o,
+attn_fwd_kernel(int s, int n, int n_kv, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ o,
                 float* __restrict__ lse, float scale) {
   constexpr int BQ = NW * 16;
   extern __shared__ __align__(16) uint8_t sraw[];
@@ -102,10 +104,11 @@ attn_fwd_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat
   const int qb = nqb - 1 - blockIdx.x;  // heaviest (most keys) first
   const int head = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const long long ld = 3LL * n * D;
+  const long long ld = (long long)(n + 2 * n_kv) * D;  // q | k | v (GQA: n_kv KV heads)
+  const int kvh = head / (n / n_kv);
   const __nv_bfloat16* Qg = qkv + ((long long)b * s + qb * BQ) * ld + head * D;
-  const __nv_bfloat16* Kg = qkv + (long long)b * s * ld + n * D + head * D;
-  const __nv_bfloat16* Vg = Kg + n * D;
+  const __nv_bfloat16* Kg = qkv + (long long)b * s * ld + n * D + kvh * D;
+  const __nv_bfloat16* Vg = Kg + n_kv * D;
   const int last_kb = ((qb + 1) * BQ - 1) / BKV;
   auto kv = [&](int stage, int which) { return sKV + (stage * 2 + which) * BKV * Tile<D>::LD; };
 
@@ -262,7 +265,7 @@ __global__ void attn_dsum_kernel(int s, int n, const __nv_bfloat16* __restrict__
 // 2-deep cp.async ring.
 template <int D>
 __global__ void __launch_bounds__(128)
-attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ dout,
+attn_bwd_dkv_kernel(int s, int n, int n_kv, const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ dout,
                     const float* __restrict__ lse, const float* __restrict__ dsum,
                     __nv_bfloat16* __restrict__ dqkv, float scale) {
   extern __shared__ __align__(16) uint8_t sraw[];
@@ -273,15 +276,19 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
   float* sLD = reinterpret_cast<float*>(sQO + 4 * BQB * LDT);  // [2 stages][lse | D][64]
   const int nkb = s / BKV;
   const int kb = blockIdx.x;  // light blocks last: kb = 0 has the most query blocks
-  const int head = blockIdx.y, b = blockIdx.z;
+  const int kvh = blockIdx.y, b = blockIdx.z;  // KV head; GQA: its group's query heads one after another
+  const int grp = n / n_kv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const long long ld = 3LL * n * D, ldo = (long long)n * D;
+  const long long ld = (long long)(n + 2 * n_kv) * D, ldo = (long long)n * D;
   const __nv_bfloat16* base = qkv + (long long)b * s * ld;
-  const float* Lrow = lse + ((long long)b * n + head) * s;
-  const float* Drow = dsum + ((long long)b * n + head) * s;
   auto qo = [&](int stage, int which) { return sQO + (stage * 2 + which) * BQB * LDT; };
   auto ldv = [&](int stage, int which) { return sLD + (stage * 2 + which) * BQB; };
-  auto issue = [&](int qb, int stage) {
+  const int qb0 = (kb * BKV) / BQB;
+  const int nqb_all = s / BQB, per_head = nqb_all - qb0;  // query blocks per query head
+  auto issue = [&](int it, int stage) {  // iteration it = (query head of the group, query block)
+    const int head = kvh * grp + it / per_head, qb = qb0 + it % per_head;
+    const float* Lrow = lse + ((long long)b * n + head) * s;
+    const float* Drow = dsum + ((long long)b * n + head) * s;
     load_tile_async<D>(qo(stage, 0), base + (long long)qb * BQB * ld + head * D, ld, BQB);
     load_tile_async<D>(qo(stage, 1), dout + ((long long)b * s + qb * BQB) * ldo + head * D, ldo, BQB);
     for (int i = threadIdx.x; i < BQB / 4; i += blockDim.x) {
@@ -289,10 +296,9 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
       cp_async16(ldv(stage, 1) + 4 * i, Drow + qb * BQB + 4 * i);
     }
   };
-  load_tile_async<D>(sK, base + (long long)kb * BKV * ld + n * D + head * D, ld, BKV);
-  load_tile_async<D>(sV, base + (long long)kb * BKV * ld + 2 * n * D + head * D, ld, BKV);
-  const int qb0 = (kb * BKV) / BQB;
-  issue(qb0, 0);
+  load_tile_async<D>(sK, base + (long long)kb * BKV * ld + n * D + kvh * D, ld, BKV);
+  load_tile_async<D>(sV, base + (long long)kb * BKV * ld + (n + n_kv) * D + kvh * D, ld, BKV);
+  issue(0, 0);
   cp_commit();
 
   float dK[D / 8][4], dV[D / 8][4];
@@ -302,12 +308,13 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
     for (int e = 0; e < 4; ++e) dK[j][e] = dV[j][e] = 0.f;
   const float sl2 = scale * LOG2E;
   const int key0 = kb * BKV + warp * 16 + g;
-  const int nqb = s / BQB;
   (void)nkb;
+  const int n_it = grp * per_head;
 
-  for (int qb = qb0; qb < nqb; ++qb) {
-    const int stg = (qb - qb0) & 1;
-    if (qb + 1 < nqb) issue(qb + 1, stg ^ 1);
+  for (int it = 0; it < n_it; ++it) {
+    const int qb = qb0 + it % per_head;
+    const int stg = it & 1;
+    if (it + 1 < n_it) issue(it + 1, stg ^ 1);
     cp_commit();
     cp_wait<1>();
     __syncthreads();
@@ -368,8 +375,8 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
     }
     __syncthreads();
   }
-  __nv_bfloat16* dK0 = dqkv + ((long long)b * s + key0) * ld + n * D + head * D;
-  __nv_bfloat16* dV0 = dK0 + n * D;
+  __nv_bfloat16* dK0 = dqkv + ((long long)b * s + key0) * ld + n * D + kvh * D;
+  __nv_bfloat16* dV0 = dK0 + n_kv * D;
 #pragma unroll
   for (int j = 0; j < D / 8; ++j) {
     *reinterpret_cast<uint32_t*>(dK0 + j * 8 + 2 * tq) = pk(dK[j][0] * scale, dK[j][1] * scale);
@@ -383,7 +390,7 @@ attn_bwd_dkv_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const _
 // CTA = 4 warps x 16 queries; K/V tiles streamed with a 2-deep cp.async ring.
 template <int D>
 __global__ void __launch_bounds__(128)
-attn_bwd_dq_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ dout,
+attn_bwd_dq_kernel(int s, int n, int n_kv, const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ dout,
                    const float* __restrict__ lse, const float* __restrict__ dsum,
                    __nv_bfloat16* __restrict__ dqkv, float scale) {
   constexpr int BQ = 64;
@@ -396,10 +403,10 @@ attn_bwd_dq_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __
   const int qb = nqb - 1 - blockIdx.x;  // heaviest first
   const int head = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const long long ld = 3LL * n * D, ldo = (long long)n * D;
+  const long long ld = (long long)(n + 2 * n_kv) * D, ldo = (long long)n * D;
   const __nv_bfloat16* base = qkv + (long long)b * s * ld;
-  const __nv_bfloat16* Kg = base + n * D + head * D;
-  const __nv_bfloat16* Vg = Kg + n * D;
+  const __nv_bfloat16* Kg = base + n * D + (head / (n / n_kv)) * D;  // GQA: the group's KV head
+  const __nv_bfloat16* Vg = Kg + n_kv * D;
   auto kv = [&](int stage, int which) { return sKV + (stage * 2 + which) * BKV * LDT; };
   load_tile_async<D>(sQ, base + (long long)qb * BQ * ld + head * D, ld, BQ);
   load_tile_async<D>(sO, dout + ((long long)b * s + qb * BQ) * ldo + head * D, ldo, BQ);
@@ -486,27 +493,27 @@ attn_bwd_dq_kernel(int s, int n, const __nv_bfloat16* __restrict__ qkv, const __
 constexpr int FWD_NW = 8;  // 128 queries per forward CTA
 
 template <int D>
-cudaError_t fwd_impl(int nb, int s, int n, const void* qkv, void* o, float* lse, cudaStream_t st) {
+cudaError_t fwd_impl(int nb, int s, int n, int n_kv, const void* qkv, void* o, float* lse, cudaStream_t st) {
   constexpr int BQ = FWD_NW * 16;
   if (s % BQ) {
     // short sequences: 64-query CTAs
     constexpr int smem = (64 + 4 * BKV) * Tile<D>::BYTES;
     auto k = attn_fwd_kernel<D, 4>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<<<dim3(s / 64, n, nb), 128, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse,
+    k<<<dim3(s / 64, n, nb), 128, smem, st>>>(s, n, n_kv, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse,
                                               rsqrtf((float)D)); count_launch();
     return cudaGetLastError();
   }
   constexpr int smem = (BQ + 4 * BKV) * Tile<D>::BYTES;
   auto k = attn_fwd_kernel<D, FWD_NW>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k<<<dim3(s / BQ, n, nb), FWD_NW * 32, smem, st>>>(s, n, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse,
+  k<<<dim3(s / BQ, n, nb), FWD_NW * 32, smem, st>>>(s, n, n_kv, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)o, lse,
                                                     rsqrtf((float)D)); count_launch();
   return cudaGetLastError();
 }
 
 template <int D>
-cudaError_t bwd_impl(int nb, int s, int n, const void* qkv, const void* o, const float* lse, const void* dout,
+cudaError_t bwd_impl(int nb, int s, int n, int n_kv, const void* qkv, const void* o, const float* lse, const void* dout,
                      void* dqkv, float* dsum, cudaStream_t st) {
   const long long T = (long long)nb * s;
   {
@@ -521,9 +528,9 @@ cudaError_t bwd_impl(int nb, int s, int n, const void* qkv, const void* o, const
   cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
   cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
   const float scale = rsqrtf((float)D);
-  k1<<<dim3(s / BKV, n, nb), 128, smem1, st>>>(s, n, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse,
-                                               dsum, (__nv_bfloat16*)dqkv, scale); count_launch();
-  k2<<<dim3(s / 64, n, nb), 128, smem2, st>>>(s, n, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse,
+  k1<<<dim3(s / BKV, n_kv, nb), 128, smem1, st>>>(s, n, n_kv, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout,
+                                                  lse, dsum, (__nv_bfloat16*)dqkv, scale); count_launch();
+  k2<<<dim3(s / 64, n, nb), 128, smem2, st>>>(s, n, n_kv, (const __nv_bfloat16*)qkv, (const __nv_bfloat16*)dout, lse,
                                               dsum, (__nv_bfloat16*)dqkv, scale); count_launch();
   return cudaGetLastError();
 }
@@ -540,11 +547,10 @@ cudaError_t attention_fwd(int nb, int s, int n, int d, const void* qkv, void* o,
   if (n % n_kv) return cudaErrorInvalidValue;
   if (g_attn_variant == 0 && attention_fwd_tc_supported(s, d))
     return attention_fwd_tc(nb, s, n, qkv, o, lse, st, n_kv);
-  if (n_kv != n) return cudaErrorInvalidValue;  // GQA: the tcgen05 kernels (head_dim 128) only
   switch (d) {
-    case 32: return fwd_impl<32>(nb, s, n, qkv, o, lse, st);
-    case 64: return fwd_impl<64>(nb, s, n, qkv, o, lse, st);
-    case 128: return fwd_impl<128>(nb, s, n, qkv, o, lse, st);
+    case 32: return fwd_impl<32>(nb, s, n, n_kv, qkv, o, lse, st);
+    case 64: return fwd_impl<64>(nb, s, n, n_kv, qkv, o, lse, st);
+    case 128: return fwd_impl<128>(nb, s, n, n_kv, qkv, o, lse, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -563,11 +569,10 @@ cudaError_t attention_bwd(int nb, int s, int n, int d, const void* qkv, const vo
         s, n, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dsum, T); count_launch();
     return attention_bwd_tc(nb, s, n, qkv, lse, dout, dqkv, dsum, rope_cs, st, n_kv);
   }
-  if (n_kv != n) return cudaErrorInvalidValue;
   switch (d) {
-    case 32: return bwd_impl<32>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);
-    case 64: return bwd_impl<64>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);
-    case 128: return bwd_impl<128>(nb, s, n, qkv, o, lse, dout, dqkv, dsum, st);
+    case 32: return bwd_impl<32>(nb, s, n, n_kv, qkv, o, lse, dout, dqkv, dsum, st);
+    case 64: return bwd_impl<64>(nb, s, n, n_kv, qkv, o, lse, dout, dqkv, dsum, st);
+    case 128: return bwd_impl<128>(nb, s, n, n_kv, qkv, o, lse, dout, dqkv, dsum, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -104,8 +104,6 @@ std::string check_kernel_limits(const malleus_model_cfg& cfg, const PlanInfo& p)
   if (cfg.hidden > 8192 || cfg.hidden % 128) return "hidden must be a multiple of 128 and <= 8192";
   if (cfg.head_dim != 32 && cfg.head_dim != 64 && cfg.head_dim != 128) return "head_dim must be 32, 64 or 128";
   if (cfg.seq_len % 64 || cfg.seq_len < 64) return "seq_len must be a multiple of 64";
-  if (cfg.n_kv_heads != cfg.n_heads && cfg.dtype == MALLEUS_BF16 && (cfg.head_dim != 128 || cfg.seq_len % 128))
-    return "bf16 GQA runs on the tcgen05 attention kernels: head_dim 128, seq_len a multiple of 128 (FP32 mode: any)";
   return "";
 }
 

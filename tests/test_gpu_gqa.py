@@ -1,7 +1,8 @@
 """GQA on the GPU path: n_kv = n/2 KV heads, query head j reads KV head
 j // g (oracle/model.py).  Whole-step parity against the oracle (readings R15 / R16) on one GPU and on
 the GQA plan matrix (TP 2 with whole KV groups per member, cross-layout DP, PP), plus the rejection of
-a head split that cuts a KV group and of GQA outside the tcgen05 attention shapes."""
+a head split that cuts a KV group.  head_dim 128 runs the tcgen05 attention, head_dim 32 the
+mma.sync kernels; FP32 mode the SIMT kernels."""
 import json
 import os
 import subprocess
@@ -27,15 +28,17 @@ def _ok(r):
         assert abs(a - b) / abs(b) <= 1e-3
 
 
-def test_gqa_p0_single_gpu():
+@pytest.mark.parametrize("cfg_name", ["c1g", "c1mg"], ids=["d32_mma_sync", "d128_tcgen05"])
+def test_gqa_p0_single_gpu(cfg_name):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     from tests.mp_worker import run
-    _ok(run("P0", steps=3, cfg_name="c1mg"))
+    _ok(run("P0", steps=3, cfg_name=cfg_name))
 
 
-@pytest.mark.parametrize("plan", ["P1", "P3", "P4", "P6"])
-def test_gqa_multi_gpu_plans(plan, tmp_path):
+@pytest.mark.parametrize("plan,cfg_name", [("P1", "c1mg"), ("P3", "c1mg"), ("P4", "c1mg"), ("P6", "c1mg"),
+                                           ("P1", "c1g"), ("P6", "c1g")])
+def test_gqa_multi_gpu_plans(plan, cfg_name, tmp_path):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     n = WORLD[plan]
@@ -44,7 +47,7 @@ def test_gqa_multi_gpu_plans(plan, tmp_path):
     out = tmp_path / "r.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", "--master-port=29537", os.path.join(ROOT, "tests", "mp_worker.py"), plan,
-           str(out), "2", "c1mg"]
+           str(out), "2", cfg_name]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     _ok(json.loads(out.read_text()))
@@ -78,20 +81,20 @@ def test_gqa_multi_gpu_fp32(plan, tmp_path):
 
 
 def test_gqa_plan_rejections():
+    """A head split that cuts a KV group is refused at plan time (E_PLAN), not mid-step."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
-    import dataclasses
-    from synth.gen import C1_MED_GQA, C1_GQA
+    from synth.gen import C1_MED_GQA
     from paper_2410_13333_b200 import plans as Pl
     from paper_2410_13333_b200 import _lib as L
     from paper_2410_13333_b200.engine import Engine
     cfg = C1_MED_GQA
-    bad = Pl.plan([Pl.pipe([Pl.stage([0], [4], [cfg.ffn], [cfg.vocab], [0, cfg.n_layers])], 4)], 2, 8)
+    ok = Pl.plan([Pl.pipe([Pl.stage([0], [4], [cfg.ffn], [cfg.vocab], [0, cfg.n_layers])], 4)], 2, 8)
     e = Engine(cfg, 0, 1, 0)
-    e.apply(bad)  # a valid single-GPU plan applies
+    e.apply(ok)
     e.close()
-    # bf16 GQA with d = 32 has no tensor-core attention kernel: refused at plan time, not mid-step
-    e = Engine(C1_GQA, 0, 1, 0)
-    with pytest.raises(L.MalleusError):
-        e.apply(Pl.plan_matrix_gqa(C1_GQA)["P0"])
+    bad = Pl.plan([Pl.pipe([Pl.stage([0, 1], [3, 1], [768, 768], [1024, 1024], [0, cfg.n_layers])], 4)], 2, 8)
+    e = Engine(cfg, 0, 1, 0)
+    with pytest.raises(L.MalleusError, match="KV groups"):
+        e.requirements(bad)
     e.close()
