@@ -44,10 +44,13 @@ typedef enum {
 } malleus_status;
 
 /* ---------------------------------------------------------------- model and plan
- * Model: LLaMA-2 architecture (§7.1), MHA (n_kv_heads == n_heads, reading R1),
- * RMSNorm eps, RoPE half-split with theta (readings R2/R3), SwiGLU FFN, untied embedding and
- * LM head.  Logical tensors are stored split-axis-outermost with hidden innermost (reading R9):
- * Wq, Wk, Wv, WoT [n*d, h]; Wg, Wu, WdT [ffn, h]; E, Wlm [vocab, h]; norm gains [h]. */
+ * Model: LLaMA-2 architecture (§7.1), MHA (n_kv_heads == n_heads, reading R1) or GQA
+ * (n_kv_heads dividing n_heads: query head j reads KV head j / (n_heads / n_kv_heads), the
+ * LLaMA-2-70B grouping), RMSNorm eps, RoPE half-split with theta (readings
+ * R2/R3), SwiGLU FFN, untied embedding and LM head.  Logical tensors are stored split-axis-outermost
+ * with hidden innermost (reading R9): Wq, WoT [n*d, h]; Wk, Wv [n_kv*d, h]; Wg, Wu, WdT [ffn, h];
+ * E, Wlm [vocab, h]; norm gains [h].  With GQA every TP member holds whole KV groups (its heads split
+ * entry is a multiple of n_heads / n_kv_heads). */
 /* Arithmetic of the step (reading R6).  BF16: bf16 params and activations, fp32 accumulation,
  * statistics, gradients and optimizer state; tcgen05 tensor-core GEMMs and attention.  FP32: the
  * parity mode of the north star ("<= 1e-4 in fp32 mode"): fp32 params and activations everywhere,
