@@ -11,7 +11,9 @@ training continues, and the Malleus loop reacts:
     the pipelines) on a background thread while all ranks keep training on the stale plan; after
     every step the ranks agree (one broadcast) whether the new plan is ready, and migrate at that
     step boundary (malleus_migrate, PAPER.md:731-733);
-  * the step time with the stale plan and with the new plan is measured.
+  * the profiler's in-run view refines the new plan once (plans.rebalance from the measured compute
+    times, reading R12; kept if faster);
+  * the step time with the stale plan and with the (refined) new plan is measured.
 
   python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 tools/trace_run.py [--sync]
 
@@ -131,6 +133,26 @@ def main():
         dist.all_gather_object(allm, mig)
         steps(2)
         t_new = steps(4)
+        # the profiler keeps measuring: one refinement from the measured compute
+        # times of the new plan (reading R12, plans.rebalance re-splits within the groups), kept only
+        # if it is faster — the planner's FLOP-proportional costs miss the narrow shards' lower
+        # GEMM efficiency (wave quantisation on 148 SMs)
+        refined = False
+        if not args.sync and changed:
+            comp = [None] * world
+            dist.all_gather_object(comp, eng.timing()["compute"])
+            obj = [Pl.rebalance(cfg, plan, {r: comp[r] for r in range(world)}) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            cand = obj[0]
+            if json.dumps(cand["pipes"]) != json.dumps(plan["pipes"]):
+                eng.migrate(cand)
+                steps(2)
+                t_cand = steps(4)
+                if t_cand < t_new:
+                    plan, t_new, refined = cand, t_cand, True
+                else:
+                    eng.migrate(plan)
+                    steps(2)
         xs_all = [xs.get(r, 1.0) for r in range(world)]
         r_opt = world / sum(1.0 / v for v in xs_all)
         rows.append({
@@ -138,6 +160,7 @@ def main():
             "plan": [{"m": p["n_micro"], "ranks": [s["ranks"] for s in p["stages"]],
                       "heads": [s["heads"] for s in p["stages"]]} for p in plan["pipes"]],
             "standby": plan["standby"], "planner_s": round(plan_s, 4), "steps_during_planning": stale_steps,
+            "refined_from_measured_compute": refined,
             "ms_stale_plan": round(t_stale, 2), "ms_replanned": round(t_new, 2),
             "migration_s": round(max(m["total_seconds"] for m in allm), 4),
             "migration_GB": round(sum(m["bytes_recv"] for m in allm) / 1e9, 3),
