@@ -123,6 +123,13 @@ struct Layout {
   bool f32 = false;
   int aes = 2;
   int tp_row0[MAX_TP + 1] = {};
+  // weight gradients of micro-batch pairs as one GEMM with K = 2T (single-stage pipelines, bf16, m >= 2):
+  // the pair's activations sit in two adjacent slots and its output gradients in per-layer [2][T]
+  // stashes, so every weight-gradient operand is one [2T, cols] matrix; the fp32 accumulator is read
+  // and written once per pair instead of once per micro-batch
+  bool pair = false;
+  std::vector<uint16_t*> pdy, pdgu, pdx1, pdqkv;  // per local layer, [2][T][cols]
+  uint16_t* pdlogits = nullptr;                   // [2][T][V_loc]
 };
 
 // bump allocator over an arena whose base may be 0 (sizing pass)
@@ -229,6 +236,9 @@ static void build_shape(const malleus_model_cfg& cfg, const PlanInfo& p, int ran
   L.v0 = 0;
   for (int k = 0; k < L.member; ++k) L.v0 += st.vocab[k];
   L.slots = std::max(1, std::min(L.PP - L.stage, std::max(pp.n_micro, 1)));
+  static const bool pair_off = getenv("MALLEUS_WGRAD_PAIR_OFF") != nullptr;
+  L.pair = !pair_off && L.PP == 1 && !L.f32 && pp.n_micro >= 2;
+  if (L.pair) L.slots = 2;
   L.prev_ranks.clear();
   L.next_ranks.clear();
   if (!L.first) L.prev_ranks = pp.stages[L.stage - 1].ranks;
@@ -309,7 +319,6 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
     }
     // activations
     const int64_t T = L.T, nd = (int64_t)L.n_loc * d, F = L.F_loc;
-    const int64_t qkvw = (int64_t)(L.n_loc + 2 * L.kv_loc) * d;  // q | k | v columns (GQA: kv_loc KV heads)
     // activation buffers: bf16, or fp32 in the parity mode
     auto act = [&](int64_t n) { return L.f32 ? reinterpret_cast<uint16_t*>(W.take<float>(n)) : W.take<uint16_t>(n); };
     L.slot.assign(L.slots, Slot{});
@@ -317,23 +326,53 @@ static void assign(const malleus_model_cfg& cfg, int rank, Layout& L, uintptr_t 
       sl.x.resize(L.n_local + 1);
       for (auto& x : sl.x) x = act(T * h);
       sl.L.resize(L.n_local);
-      for (SlotLayer& y : sl.L) {
-        y.a1 = act(T * h);
-        y.qkv = act(T * qkvw);
-        y.o = act(T * nd);
-        y.x1 = act(T * h);
-        y.a2 = act(T * h);
-        y.gu = act(T * 2 * F);
-        y.u = act(T * F);
+    }
+    // per-layer activations with the slots adjacent ([slots][T][cols]): in pair mode the two
+    // micro-batches of a pair are one [2T, cols] operand of the weight-gradient GEMMs
+    auto at = [&](uint16_t* p, int64_t elems) {
+      return reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(p) + elems * L.aes);
+    };
+    const int64_t qkvw = (int64_t)(L.n_loc + 2 * L.kv_loc) * d;
+    for (int li = 0; li < L.n_local; ++li) {
+      auto adj = [&](int64_t cols, uint16_t* SlotLayer::*f) {
+        uint16_t* base = act(T * cols * L.slots);
+        for (int sidx = 0; sidx < L.slots; ++sidx) L.slot[sidx].L[li].*f = at(base, sidx * T * cols);
+      };
+      adj(h, &SlotLayer::a1);
+      adj(qkvw, &SlotLayer::qkv);
+      adj(nd, &SlotLayer::o);
+      adj(h, &SlotLayer::x1);
+      adj(h, &SlotLayer::a2);
+      adj(2 * F, &SlotLayer::gu);
+      adj(F, &SlotLayer::u);
+      for (Slot& sl : L.slot) {
+        SlotLayer& y = sl.L[li];
         y.r1 = W.take<float>(T);
         y.r2 = W.take<float>(T);
         y.lse = W.take<float>(T * L.n_loc);
       }
-      if (L.last) {
-        sl.xf = act(T * h);
-        sl.dlast = act(T * h);
+    }
+    L.pdy.assign(L.n_local, nullptr);
+    L.pdgu.assign(L.n_local, nullptr);
+    L.pdx1.assign(L.n_local, nullptr);
+    L.pdqkv.assign(L.n_local, nullptr);
+    if (L.pair)
+      for (int li = 0; li < L.n_local; ++li) {
+        L.pdy[li] = act(2 * T * h);
+        L.pdgu[li] = act(2 * T * 2 * F);
+        L.pdx1[li] = act(2 * T * h);
+        L.pdqkv[li] = act(2 * T * qkvw);
+      }
+    if (L.last) {
+      uint16_t* xf = act(T * h * L.slots);
+      for (int sidx = 0; sidx < L.slots; ++sidx) {
+        Slot& sl = L.slot[sidx];
+        sl.xf = at(xf, sidx * T * h);
+        // pair mode: the head's output gradient lands in the top layer's dy stash
+        sl.dlast = (L.pair && L.n_local > 0) ? at(L.pdy[L.n_local - 1], sidx * T * h) : act(T * h);
         sl.rf = W.take<float>(T);
       }
+      if (L.pair) L.pdlogits = act(2 * T * L.V_loc);
     }
     L.part = W.take<float>(T * h);
     if (L.TP > 1) {
@@ -1076,17 +1115,34 @@ static malleus_status layer_fwd_impl(malleus_ctx* ctx, int li, int si, cudaStrea
   return MALLEUS_OK;
 }
 
-// dy: grad of x[li+1]; writes grad of x[li] to dx.  first: STORE into wgrad (first micro-batch).
+// dy: grad of x[li+1]; writes grad of x[li] to dx.  first: STORE into wgrad (first micro-batch, or the
+// first pair).  pair: -1 = this micro-batch's weight gradients now (K = T); 0 = the first micro-batch of
+// a pair (slot 0): output gradients into the stash, weight gradients deferred; 1 = the second (slot 1):
+// the pair's weight gradients as one GEMM each with K = 2T over the adjacent slots / stash halves.
 static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uint16_t* dy, uint16_t* dx,
-                                     bool first, cudaStream_t st) {
+                                     bool first, cudaStream_t st, int pair = -1) {
   Layout& L = *ctx->L;
   const malleus_model_cfg& c = ctx->cfg;
   const int T = L.T, h = c.hidden, d = c.head_dim, nd = L.n_loc * d, F = L.F_loc;
+  const int qkvw = (L.n_loc + 2 * L.kv_loc) * d;
   Slot& S = L.slot[si];
   SlotLayer& Y = S.L[li];
   LayerPtrs& P = L.lp[li];
   const int wm = first ? GEMM_STORE_F32 : GEMM_ACCUM_F32;
-  uint16_t* dx1 = L.dxc;
+  const bool stash = pair >= 0;
+  const int half = stash ? si : 0;
+  uint16_t* dgu = stash ? L.pdgu[li] + (size_t)half * T * 2 * F : L.dgu;
+  uint16_t* dx1 = stash ? L.pdx1[li] + (size_t)half * T * h : L.dxc;
+  uint16_t* dqkv = stash ? L.pdqkv[li] + (size_t)half * T * qkvw : L.dqkv;
+  // weight-gradient operands: this micro-batch (K = T) or the pair (K = 2T, slot 0 / stash half 0 base)
+  const bool wg = pair != 0;
+  const int Kw = pair == 1 ? 2 * T : T;
+  const SlotLayer& Y0 = pair == 1 ? L.slot[0].L[li] : Y;
+  const uint16_t* w_dy = pair == 1 ? L.pdy[li] : dy;
+  const uint16_t* w_dgu = pair == 1 ? L.pdgu[li] : dgu;
+  const uint16_t* w_dx1 = pair == 1 ? L.pdx1[li] : dx1;
+  const uint16_t* w_dqkv = pair == 1 ? L.pdqkv[li] : dqkv;
+  const bool ovl = wg && tp_overlap(ctx);
   // MLP
   duty_begin(ctx, 3, st);
   {  // du = dy W_d with the SwiGLU backward fused into the epilogue (dgu straight from the GEMM)
@@ -1095,40 +1151,39 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
     g.f32 = L.f32;
     if (!L.f32) {
       g.glu = 2;
-      g.aux = L.dgu;
+      g.aux = dgu;
       g.aux_in = Y.gu;
       g.glu_done = &glu_done;
     }
     CK(gemm_bf16(g, st));
-    RET(gemm(ctx, F, h, T, Y.u, F, true, dy, h, true, P.dwd, h, wm, st));
-    if (!glu_done) CK(k_swiglu_bwd(L, T, F, Y.gu, L.du, L.dgu, st));
+    if (wg) RET(gemm(ctx, F, h, Kw, Y0.u, F, true, w_dy, h, true, P.dwd, h, wm, st));
+    if (!glu_done) CK(k_swiglu_bwd(L, T, F, Y.gu, L.du, dgu, st));
   }
-  RET(part_gemm(ctx, T, h, 2 * F, L.dgu, 2 * F, false, P.wgu, h, true, st));
-  if (tp_overlap(ctx)) {
+  RET(part_gemm(ctx, T, h, 2 * F, dgu, 2 * F, false, P.wgu, h, true, st));
+  if (ovl) {
     RET(tp_sum_begin(ctx, st));
-    RET(gemm_co(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
+    RET(gemm_co(ctx, 2 * F, h, Kw, w_dgu, 2 * F, true, Y0.a2, h, true, P.dwgu, h, wm, st));
     RET(tp_sum_end(ctx, st));
   } else {
-    RET(gemm(ctx, 2 * F, h, T, L.dgu, 2 * F, true, Y.a2, h, true, P.dwgu, h, wm, st));
+    if (wg) RET(gemm(ctx, 2 * F, h, Kw, w_dgu, 2 * F, true, Y0.a2, h, true, P.dwgu, h, wm, st));
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 4, st);
   CK(k_norm_bwd(L, T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st, tp_sum_bf16(L)));
   // attention
   RET(gemm(ctx, T, nd, h, dx1, h, false, P.wo, h, false, L.dout, nd, GEMM_STORE_BF16, st));
-  RET(gemm(ctx, nd, h, T, Y.o, nd, true, dx1, h, true, P.dwo, h, wm, st));
-  CK(k_attn_bwd(L, L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, L.dqkv, L.dsum, st, L.rope_cs));
+  if (wg) RET(gemm(ctx, nd, h, Kw, Y0.o, nd, true, w_dx1, h, true, P.dwo, h, wm, st));
+  CK(k_attn_bwd(L, L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, dqkv, L.dsum, st, L.rope_cs));
   if (debug_sync()) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
-  const int qkvw = (L.n_loc + 2 * L.kv_loc) * d;
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
-    CK(k_rope(L, T, c.seq_len, L.n_loc + L.kv_loc, d, L.dqkv, qkvw, c.rope_theta, true, st));
-  RET(part_gemm(ctx, T, h, qkvw, L.dqkv, qkvw, false, P.wqkv, h, true, st));
-  if (tp_overlap(ctx)) {
+    CK(k_rope(L, T, c.seq_len, L.n_loc + L.kv_loc, d, dqkv, qkvw, c.rope_theta, true, st));
+  RET(part_gemm(ctx, T, h, qkvw, dqkv, qkvw, false, P.wqkv, h, true, st));
+  if (ovl) {
     RET(tp_sum_begin(ctx, st));
-    RET(gemm_co(ctx, qkvw, h, T, L.dqkv, qkvw, true, Y.a1, h, true, P.dwqkv, h, wm, st));
+    RET(gemm_co(ctx, qkvw, h, Kw, w_dqkv, qkvw, true, Y0.a1, h, true, P.dwqkv, h, wm, st));
     RET(tp_sum_end(ctx, st));
   } else {
-    RET(gemm(ctx, qkvw, h, T, L.dqkv, qkvw, true, Y.a1, h, true, P.dwqkv, h, wm, st));
+    if (wg) RET(gemm(ctx, qkvw, h, Kw, w_dqkv, qkvw, true, Y0.a1, h, true, P.dwqkv, h, wm, st));
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 5, st);
@@ -1138,11 +1193,17 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
 }
 
 // last stage: final norm, LM head, vocab-parallel CE, and the head's backward (dlast).
-static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt, bool first, cudaStream_t st) {
+static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt, bool first, cudaStream_t st,
+                                   int pair = -1) {  // pair: as layer_bwd_impl (LM-head weight gradient)
   Layout& L = *ctx->L;
   const malleus_model_cfg& c = ctx->cfg;
   const int T = L.T, h = c.hidden, V = L.V_loc;
   Slot& S = L.slot[si];
+  uint16_t* dlogits = pair >= 0 ? L.pdlogits + (size_t)si * T * V : L.dlogits;
+  const bool wg = pair != 0;
+  const int Kw = pair == 1 ? 2 * T : T;
+  const uint16_t* w_dl = pair == 1 ? L.pdlogits : dlogits;
+  const uint16_t* w_xf = pair == 1 ? L.slot[0].xf : S.xf;
   const PipeInfo& pp = L.plan.pipes[L.pipe];
   duty_begin(ctx, 6, st);
   CK(k_norm_fwd(L, T, h, S.x[L.n_local], nullptr, nullptr, L.gf, c.rms_eps, S.xf, S.rf, st));
@@ -1154,18 +1215,18 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
   RET(tp_allreduce(ctx, L.sumtgt, (size_t)2 * T, ncclSum, st));
   duty_begin(ctx, 7, st);
   const double n_tok = (double)pp.n_micro * L.plan.b * c.seq_len;
-  CK(ce_grad(T, V, L.logits, tgt, L.v0, L.gmax, L.sumtgt, L.sumtgt + T, (float)(1.0 / n_tok), L.dlogits,
+  CK(ce_grad(T, V, L.logits, tgt, L.v0, L.gmax, L.sumtgt, L.sumtgt + T, (float)(1.0 / n_tok), dlogits,
              L.loss_rows, st, L.f32));
   if (L.member == 0)
     CK(reduce_loss(T, L.loss_rows, (float)(1.0 / ((double)L.plan.B * c.seq_len)), L.loss_acc, 1, st));
-  RET(part_gemm(ctx, T, h, V, L.dlogits, V, false, L.Wlm, h, true, st));
+  RET(part_gemm(ctx, T, h, V, dlogits, V, false, L.Wlm, h, true, st));
   const int wm_lm = first ? GEMM_STORE_F32 : GEMM_ACCUM_F32;
-  if (tp_overlap(ctx)) {
+  if (wg && tp_overlap(ctx)) {
     RET(tp_sum_begin(ctx, st));
-    RET(gemm_co(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, wm_lm, st));
+    RET(gemm_co(ctx, V, h, Kw, w_dl, V, true, w_xf, h, true, L.dWlm, h, wm_lm, st));
     RET(tp_sum_end(ctx, st));
   } else {
-    RET(gemm(ctx, V, h, T, L.dlogits, V, true, S.xf, h, true, L.dWlm, h, wm_lm, st));
+    if (wg) RET(gemm(ctx, V, h, Kw, w_dl, V, true, w_xf, h, true, L.dWlm, h, wm_lm, st));
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 8, st);
@@ -1288,12 +1349,17 @@ static malleus_status train_step_impl(malleus_ctx* ctx, const int32_t* tokens, c
     auto tgt_mb = [&](int j) { return targets + (seq0 + (long long)j * L.plan.b) * s; };
     const int warm = std::min(L.PP - L.stage - 1, m);
     const int rem = m - warm;
+    // pair mode (L.pair): micro-batches (2p, 2p + 1) share their weight-gradient GEMMs; an odd last one
+    // runs alone.  pair_of(j) = -1 (alone), 0 (defer), 1 (flush the pair); first = the first GEMM that
+    // writes the fp32 gradient (STORE), every later one accumulates.
+    auto pair_of = [&](int j) { return !L.pair ? -1 : (j & 1) ? 1 : (j + 1 < m ? 0 : -1); };
+    auto first_of = [&](int j) { return L.pair ? j <= 1 : j == 0; };
     auto fwd = [&](int j) -> malleus_status {
       const int si = j % L.slots;
       Slot& S = L.slot[si];
       if (L.first) CK(k_embed_fwd(L, L.T, c.hidden, tok_mb(j), L.E, S.x[0], st));
       for (int li = 0; li < L.n_local; ++li) RET(layer_fwd_impl(ctx, li, si, st));
-      if (L.last) RET(head_fwd_bwd(ctx, si, tgt_mb(j), j == 0, st));
+      if (L.last) RET(head_fwd_bwd(ctx, si, tgt_mb(j), first_of(j), st, pair_of(j)));
       return MALLEUS_OK;
     };
     // backward of micro-batch j; dy = grad of the stage output; returns grad of the stage input in *dx_out
@@ -1303,9 +1369,10 @@ static malleus_status train_step_impl(malleus_ctx* ctx, const int32_t* tokens, c
       uint16_t* bufs[2] = {L.dxa, L.dxb};
       int k = 0;
       for (int li = L.n_local - 1; li >= 0; --li) {
-        uint16_t* out = bufs[k];
+        // pair mode: layer li's input gradient is layer li-1's dy, kept in that layer's stash half
+        uint16_t* out = (L.pair && li > 0) ? L.pdy[li - 1] + (size_t)si * L.T * c.hidden : bufs[k];
         k ^= 1;
-        RET(layer_bwd_impl(ctx, li, si, cur, out, j == 0, st));
+        RET(layer_bwd_impl(ctx, li, si, cur, out, first_of(j), st, pair_of(j)));
         cur = out;
       }
       if (L.first) CK(k_embed_bwd(L, L.T, c.hidden, tok_mb(j), cur, L.dE, st));
