@@ -22,8 +22,8 @@ def main(csv_path, log_path, skip):
     h = rows[hi]
     kid, kn, mn, mv = h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
     mu = h.index("Metric Unit")
-    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1.0, "usecond": 1e3,
-             "msecond": 1e6, "%": 1.0}
+    scale = {"byte": 1.0, "B": 1.0, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6, "Gbyte": 1e9, "GB": 1e9,
+             "nsecond": 1.0, "ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "%": 1.0}
     per = OrderedDict()
     for r in rows[hi + 1:]:
         if len(r) <= mv or "gemm_tcgen05" not in r[kn]:
