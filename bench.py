@@ -307,29 +307,43 @@ def main():
         ms_before = timed(3)
         comp = [None] * world
         dist.all_gather_object(comp, eng.timing()["compute"])
-        obj = [Pl.rebalance(cfg, plan, {r: comp[r] for r in range(world)}) if rank == 0 else None]
+        # candidates: the speed-proportional re-split and two damped ones (plans.rebalance: compute is
+        # not proportional to a member's share, so the full step can overshoot); each is migrated to
+        # and measured, and the fastest plan (the initial one included) is kept
+        obj = [[Pl.rebalance(cfg, plan, {r: comp[r] for r in range(world)}, damp=a) for a in (1.0, 2 / 3, 1 / 3)]
+               if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        new_plan = obj[0]
-        mig = eng.migrate(new_plan)
-        allm = [None] * world
-        dist.all_gather_object(allm, mig)
-        run_steps(2)
-        ms_after = timed(3)
-        kept = ms_after <= ms_before
-        if kept:
-            plan = new_plan
-        else:  # the measured re-plan did not pay off: migrate back (a planner keeps the faster plan)
-            eng.migrate(plan)
+        cands, seen = [], {json.dumps(plan["pipes"])}
+        for c in obj[0]:
+            if json.dumps(c["pipes"]) not in seen:
+                seen.add(json.dumps(c["pipes"]))
+                cands.append(c)
+        best, best_ms, tried, allm = plan, ms_before, [], []
+        for c in cands:
+            mig = eng.migrate(c)
+            got = [None] * world
+            dist.all_gather_object(got, mig)
+            allm.append(got)
             run_steps(2)
+            t = timed(3)
+            tried.append({"plan": plan_summary(c), "tokens_s": tokens_per_step / (t / 1e3)})
+            if t < best_ms:
+                best, best_ms = c, t
+        kept = best is not plan
+        if cands and best is not cands[-1]:  # migrate to the fastest (back to the initial plan if none won)
+            eng.migrate(best)
+            run_steps(2)
+        plan = best
         barrier()
+        mig0 = allm[0] if allm else [{"bytes_recv": 0, "seconds": 0.0, "total_seconds": 0.0}]
         replan = {"tokens_s_before": tokens_per_step / (ms_before / 1e3), "ms_per_step_before": ms_before,
-                  "tokens_s_replanned": tokens_per_step / (ms_after / 1e3), "replanned_plan_kept": kept,
-                  "replanned_plan": plan_summary(new_plan),
+                  "tokens_s_replanned": tokens_per_step / (best_ms / 1e3), "replanned_plan_kept": kept,
+                  "replanned_plan": plan_summary(best), "candidates": tried,
                   "compute_ms_per_rank_before": comp,
-                  "migration": {"bytes": sum(m["bytes_recv"] for m in allm),
-                                "seconds_max": max(m["seconds"] for m in allm),
-                                "GBps": sum(m["bytes_recv"] for m in allm) / max(max(m["seconds"] for m in allm), 1e-9) / 1e9,
-                                "total_seconds_max": max(m["total_seconds"] for m in allm)}}
+                  "migration": {"bytes": sum(m["bytes_recv"] for m in mig0),
+                                "seconds_max": max(m["seconds"] for m in mig0),
+                                "GBps": sum(m["bytes_recv"] for m in mig0) / max(max(m["seconds"] for m in mig0), 1e-9) / 1e9,
+                                "total_seconds_max": max(m["total_seconds"] for m in mig0)}}
     clocks = ClockSampler(local)
     clocks.start()
     if not os.environ.get("MALLEUS_BENCH_NO_GEMM_EVENTS"):  # experiment switch: timed region without per-GEMM events

@@ -1142,7 +1142,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   const uint16_t* w_dgu = pair == 1 ? L.pdgu[li] : dgu;
   const uint16_t* w_dx1 = pair == 1 ? L.pdx1[li] : dx1;
   const uint16_t* w_dqkv = pair == 1 ? L.pdqkv[li] : dqkv;
-  const bool ovl = wg && tp_overlap(ctx);
+  // overlap decided inside each segment (tp_overlap: not while DUTY learns that segment's duration)
   // MLP
   duty_begin(ctx, 3, st);
   {  // du = dy W_d with the SwiGLU backward fused into the epilogue (dgu straight from the GEMM)
@@ -1160,7 +1160,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
     if (!glu_done) CK(k_swiglu_bwd(L, T, F, Y.gu, L.du, dgu, st));
   }
   RET(part_gemm(ctx, T, h, 2 * F, dgu, 2 * F, false, P.wgu, h, true, st));
-  if (ovl) {
+  if (wg && tp_overlap(ctx)) {
     RET(tp_sum_begin(ctx, st));
     RET(gemm_co(ctx, 2 * F, h, Kw, w_dgu, 2 * F, true, Y0.a2, h, true, P.dwgu, h, wm, st));
     RET(tp_sum_end(ctx, st));
@@ -1178,7 +1178,7 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
     CK(k_rope(L, T, c.seq_len, L.n_loc + L.kv_loc, d, dqkv, qkvw, c.rope_theta, true, st));
   RET(part_gemm(ctx, T, h, qkvw, dqkv, qkvw, false, P.wqkv, h, true, st));
-  if (ovl) {
+  if (wg && tp_overlap(ctx)) {
     RET(tp_sum_begin(ctx, st));
     RET(gemm_co(ctx, qkvw, h, Kw, w_dqkv, qkvw, true, Y0.a1, h, true, P.dwqkv, h, wm, st));
     RET(tp_sum_end(ctx, st));

@@ -171,7 +171,15 @@ def _apportion(n_units, weights, min_units=1):
     return out
 
 
-def rebalance(cfg, plan, compute_ms: dict, min_micro: int = 0):
+def _damped(cur, target, damp):
+    """(1 - damp) x the current shares + damp x the target weights, both normalised."""
+    if damp >= 1.0:
+        return target
+    sc, st = float(sum(cur)), float(sum(target))
+    return [(1.0 - damp) * c / sc + damp * w / st for c, w in zip(cur, target)]
+
+
+def rebalance(cfg, plan, compute_ms: dict, min_micro: int = 0, damp: float = 1.0):
     """Re-plan from measured speeds (the profiler -> planner -> migration loop of PAPER.md:378-384).
 
     Reading R12 (work-normalised rates): member k of a TP group that processed share f_k of the
@@ -179,7 +187,12 @@ def rebalance(cfg, plan, compute_ms: dict, min_micro: int = 0):
     speeds (heads whole, FFN / vocab in 128-wide tiles).  Pipelines: a pipeline's time per
     micro-batch is the max over its members' compute; m_i is re-apportioned proportional to
     m_i / T_i (Eq.(3)'s min-max objective, with measured o_i).  Layers, groups
-    and stage order are kept."""
+    and stage order are kept.
+
+    damp in (0, 1]: the new shares are (1 - damp) x the current ones + damp x the speed-proportional
+    ones.  A member's compute is not proportional to its share (per-kernel fixed costs, narrow
+    GEMMs' wave quantisation on 148 SMs), so the full step (damp = 1) can overshoot; callers measure
+    a damped candidate beside it and keep the faster (bench.py, tools/trace_run.py)."""
     import copy
     p = copy.deepcopy(plan)
     p["plan_id"] = plan.get("plan_id", 0) + 1
@@ -192,19 +205,20 @@ def rebalance(cfg, plan, compute_ms: dict, min_micro: int = 0):
             t_pipe = max(t_pipe, max(t))
             if len(ranks) == 1:
                 continue
-            speed = [st["heads"][k] / t[k] for k in range(len(ranks))]
+            speed = _damped(st["heads"], [st["heads"][k] / t[k] for k in range(len(ranks))], damp)
             st["heads"] = _apportion(cfg.n_heads, speed)
             for key, total in (("ffn", cfg.ffn), ("vocab", cfg.vocab)):
                 tile = 128 if total // 128 >= 4 * len(ranks) else 16  # GEMM-friendly tiles when possible
                 n_t, rem = divmod(total, tile)
-                spd = [st[key][k] / t[k] for k in range(len(ranks))]
+                spd = _damped(st[key], [st[key][k] / t[k] for k in range(len(ranks))], damp)
                 tiles = _apportion(n_t, spd)
                 st[key] = [x * tile for x in tiles]
                 st[key][-1] += rem
         pipe_speed.append(pp["n_micro"] / t_pipe if pp["n_micro"] > 0 else 1.0 / t_pipe)
     total_m = sum(pp["n_micro"] for pp in p["pipes"])
     if len(p["pipes"]) > 1:
-        ms = _apportion(total_m, pipe_speed, min_units=min_micro)
+        ms = _apportion(total_m, _damped([pp["n_micro"] for pp in p["pipes"]], pipe_speed, damp),
+                        min_units=min_micro)
         for pp, m in zip(p["pipes"], ms):
             pp["n_micro"] = m
     return p

@@ -27,6 +27,23 @@ def test_rebalance_moves_work_to_fast_ranks():
     assert abs(r["pipes"][0]["stages"][0]["heads"][0] - 22) <= 1
 
 
+def test_rebalance_damped_between_current_and_full():
+    """damp = 1: speed-proportional shares; damp -> 0: the current shares; in between, monotone
+    (the measured 22/10 -> 25/7 overshoot of the C2 N = 2 straggler, bench_n2_r02z.json)."""
+    cfg = C2_7B_SLICE
+    p = Pl.ladder_plan(cfg, 2, 16)
+    t = {0: 111.9, 1: 172.8}
+    full = Pl.rebalance(cfg, p, t)["pipes"][0]["stages"][0]["heads"]
+    assert full == [25, 7]  # 32 * (22/111.9) / (22/111.9 + 10/172.8) = 24.7
+    h = [Pl.rebalance(cfg, p, t, damp=a)["pipes"][0]["stages"][0]["heads"][0] for a in (1e-6, 1 / 3, 2 / 3, 1.0)]
+    assert h[0] == 22 and h == sorted(h) and h[2] == 24
+    for a in (1 / 3, 2 / 3):
+        validate(cfg, Pl.rebalance(cfg, p, t, damp=a), 2)
+    q = Pl.ladder_plan(cfg, 4, 16)
+    mm = [Pl.rebalance(cfg, q, {0: 60.0, 1: 60.0, 2: 40.0, 3: 40.0}, damp=a)["pipes"][1]["n_micro"] for a in (1e-6, 0.5, 1.0)]
+    assert mm[0] == q["pipes"][1]["n_micro"] and mm == sorted(mm)
+
+
 def test_rebalance_micro_batches():
     cfg = C2_7B_SLICE
     p = Pl.ladder_plan(cfg, 4, 16)

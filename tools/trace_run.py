@@ -12,7 +12,7 @@ training continues, and the Malleus loop reacts:
     every step the ranks agree (one broadcast) whether the new plan is ready, and migrate at that
     step boundary (malleus_migrate, PAPER.md:731-733);
   * the profiler's in-run view refines the new plan once (plans.rebalance from the measured compute
-    times, reading R12; kept if faster);
+    times, reading R12, full and damped re-split; the fastest is kept);
   * the step time with the stale plan and with the (refined) new plan is measured.
 
   python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 tools/trace_run.py [--sync]
@@ -141,18 +141,25 @@ def main():
         if not args.sync and changed:
             comp = [None] * world
             dist.all_gather_object(comp, eng.timing()["compute"])
-            obj = [Pl.rebalance(cfg, plan, {r: comp[r] for r in range(world)}) if rank == 0 else None]
+            obj = [[Pl.rebalance(cfg, plan, {r: comp[r] for r in range(world)}, damp=a) for a in (1.0, 2 / 3)]
+                   if rank == 0 else None]  # full and damped re-split (plans.rebalance docstring)
             dist.broadcast_object_list(obj, src=0)
-            cand = obj[0]
-            if json.dumps(cand["pipes"]) != json.dumps(plan["pipes"]):
+            seen, at = {json.dumps(plan["pipes"])}, plan
+            best = plan
+            for cand in obj[0]:
+                if json.dumps(cand["pipes"]) in seen:
+                    continue
+                seen.add(json.dumps(cand["pipes"]))
                 eng.migrate(cand)
+                at = cand
                 steps(2)
                 t_cand = steps(4)
                 if t_cand < t_new:
-                    plan, t_new, refined = cand, t_cand, True
-                else:
-                    eng.migrate(plan)
-                    steps(2)
+                    best, t_new, refined = cand, t_cand, True
+            if at is not best:
+                eng.migrate(best)
+                steps(2)
+            plan = best
         xs_all = [xs.get(r, 1.0) for r in range(world)]
         r_opt = world / sum(1.0 / v for v in xs_all)
         rows.append({
