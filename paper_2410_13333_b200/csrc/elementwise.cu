@@ -323,6 +323,126 @@ rmsnorm_bwd_warp_kernel(int T, int h, const uint4* __restrict__ x, const uint4* 
   }
 }
 
+// Row-group variant (h / 8 a multiple of 32, h / 8 <= 1024): TPR = h / 8 threads own one row, one
+// 8-column vector each, RB = 1024 / TPR rows per 1024-thread CTA, two CTAs per SM.  Every load of a
+// row (x, dy, dres) is issued one row ahead, before the row statistic's barrier of the current row,
+// so the latency chain per row is one barrier, not two dependent global round trips.  The gain
+// gradient stays in 8 registers per thread over all rows of the CTA; at the end the RB row groups'
+// partials are added in group order into part[blockIdx.x][h] (grid = 148 x resident CTAs per SM, so
+// the partial array and colsum_accum_kernel's pass are >= 3x smaller than the block kernel's).
+// Deterministic (the row -> CTA assignment depends only on T and the grid).
+constexpr int BWDR_THREADS = 1024;
+template <bool DY16>
+__global__ void __launch_bounds__(BWDR_THREADS, 1)
+rmsnorm_bwd_rows_kernel(int T, int h, const uint4* __restrict__ x, const uint4* __restrict__ g,
+                        const float* __restrict__ rstd, const void* __restrict__ dyv, const uint4* __restrict__ dres,
+                        uint4* __restrict__ dx_out, float* __restrict__ dg_part) {
+  __shared__ float sdot[2][32];
+  __shared__ __align__(16) float sdg[BWDR_THREADS * 8];
+  const int nv = h / 8, rb = blockDim.x / nv;  // threads per row, rows per CTA (blockDim = rb * nv)
+  const int c = threadIdx.x % nv, grp = threadIdx.x / nv;
+  const int w = threadIdx.x >> 5, wpr = nv >> 5;  // warps per row
+  const int stride = gridDim.x * rb;
+  const uint4* dyq = static_cast<const uint4*>(dyv);  // bf16: 1 vector of 8; fp32: 2 vectors of 4
+  constexpr int DQ = DY16 ? 1 : 2;
+  float dg[8];  // g is re-read per row (L1-resident): registers go to the rows in flight
+#pragma unroll
+  for (int j = 0; j < 8; ++j) dg[j] = 0.f;
+  int row = blockIdx.x * rb + grp;
+  const uint4* xc = x + c;
+  const uint4* dyc = dyq + (size_t)c * DQ;
+  const uint4* rc = dres ? dres + c : nullptr;
+  // the current row's operands, packed as loaded, and the next row's (loaded one row ahead, so their
+  // latency overlaps this row's barrier)
+  uint4 cx = make_uint4(0, 0, 0, 0), cres = cx, cdy[DQ];
+  float cr = 0.f;
+#pragma unroll
+  for (int k = 0; k < DQ; ++k) cdy[k] = cx;
+  if (row < T) {
+    const size_t o = (size_t)row * nv;
+    cx = xc[o];
+#pragma unroll
+    for (int k = 0; k < DQ; ++k) cdy[k] = dyc[o * DQ + k];
+    if (rc) cres = rc[o];
+    cr = rstd[row];
+  }
+#pragma unroll 1
+  for (int it = 0, base = blockIdx.x * rb; base < T; base += stride, row += stride, ++it) {
+    const int nrow = row + stride;
+    uint4 nx = cx, nres = cres, ndy[DQ];
+    float nr = cr;
+#pragma unroll
+    for (int k = 0; k < DQ; ++k) ndy[k] = cdy[k];
+    if (nrow < T) {
+      const size_t o = (size_t)nrow * nv;
+      nx = xc[o];
+#pragma unroll
+      for (int k = 0; k < DQ; ++k) ndy[k] = dyc[o * DQ + k];
+      if (rc) nres = rc[o];
+      nr = rstd[nrow];
+    }
+    // unpacked twice (before and after the barrier) so only the packed operands live across it
+    auto unpack_row = [&](float (&xv)[8], float (&dv)[8], float (&gv)[8]) {
+      unpack8(cx, xv);
+      unpack8(__ldg(g + c), gv);
+      if (DY16) {
+        unpack8(cdy[0], dv);
+      } else {
+#pragma unroll
+        for (int k = 0; k < DQ; ++k) {
+          dv[4 * k] = __uint_as_float(cdy[k].x); dv[4 * k + 1] = __uint_as_float(cdy[k].y);
+          dv[4 * k + 2] = __uint_as_float(cdy[k].z); dv[4 * k + 3] = __uint_as_float(cdy[k].w);
+        }
+      }
+    };
+    float dot = 0.f;
+    if (row < T) {
+      float xv[8], dv[8], gv[8];
+      unpack_row(xv, dv, gv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        dot += xv[j] * gv[j] * dv[j];
+        dg[j] += dv[j] * xv[j] * cr;
+      }
+    }
+    dot = warp_sum(dot);
+    if ((threadIdx.x & 31) == 0) sdot[it & 1][w] = dot;
+    __syncthreads();
+    float tot = 0.f;
+    for (int k = 0; k < wpr; ++k) tot += sdot[it & 1][grp * wpr + k];  // the row's warps in order
+    if (row < T) {
+      float xv[8], dv[8], gv[8];
+      unpack_row(xv, dv, gv);
+      const float coef = cr * cr * cr * tot / (float)h;
+      float o[8], rs[8];
+      if (dres) unpack8(cres, rs);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o[j] = cr * gv[j] * dv[j] - xv[j] * coef;
+        if (dres) o[j] += rs[j];
+      }
+      dx_out[(size_t)row * nv + c] = pack8(o);
+    }
+    cx = nx;
+    cres = nres;
+    cr = nr;
+#pragma unroll
+    for (int k = 0; k < DQ; ++k) cdy[k] = ndy[k];
+  }
+  float4* s4 = reinterpret_cast<float4*>(sdg + (size_t)threadIdx.x * 8);
+  s4[0] = make_float4(dg[0], dg[1], dg[2], dg[3]);
+  s4[1] = make_float4(dg[4], dg[5], dg[6], dg[7]);
+  __syncthreads();
+  for (int q = threadIdx.x; q < h / 4; q += blockDim.x) {  // column quad q: groups in order
+    float4 acc = reinterpret_cast<const float4*>(sdg)[q];
+    for (int k = 1; k < rb; ++k) {
+      const float4 v = reinterpret_cast<const float4*>(sdg + (size_t)k * h)[q];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(dg_part + (long long)blockIdx.x * h)[q] = acc;
+  }
+}
+
 constexpr int BWD_BLOCKS = 148 * 6;  // 6 per SM (80 registers at h = 4096): rows in flight to cover the per-row latency chain
 
 // ---------------------------------------------------------------- residual add
@@ -689,6 +809,25 @@ cudaError_t rmsnorm_bwd(int T, int h, const void* x, const void* g, const float*
       colsum_accum_kernel<<<(h + 31) / 32, 1024, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
       return cudaGetLastError();
     }
+  }
+  // row-group kernel (default where h / 8 is a multiple of 32 and at most 1024); MALLEUS_NORM_BWD_BLOCK=1
+  // selects the block kernel below (A/B switch)
+  static const bool block_kernel = getenv("MALLEUS_NORM_BWD_BLOCK") != nullptr;
+  if (!block_kernel && (h / 8) % 32 == 0 && h / 8 <= BWDR_THREADS) {
+    const int rb = BWDR_THREADS / (h / 8);
+    auto kern = dy_bf16 ? rmsnorm_bwd_rows_kernel<true> : rmsnorm_bwd_rows_kernel<false>;
+    static int per_sm[2][BWDR_THREADS / 32 + 1] = {};  // resident CTAs per SM per (instance, block size)
+    int& occ = per_sm[dy_bf16 ? 1 : 0][rb * (h / 8) / 32];
+    if (!occ) {
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, rb * (h / 8), 0);
+      if (e != cudaSuccess) return e;
+      occ = std::max(1, occ);
+    }
+    const int nb = std::min(148 * occ, (T + rb - 1) / rb);
+    kern<<<nb, rb * (h / 8), 0, st>>>(T, h, (const uint4*)x, (const uint4*)g, rstd, dy, (const uint4*)dres,
+                                      (uint4*)dx_out, scratch); count_launch();
+    colsum_accum_kernel<<<(h + 31) / 32, 1024, 0, st>>>(nb, h, scratch, dg_accum); count_launch();
+    return cudaGetLastError();
   }
   int rpb = (T + BWD_BLOCKS - 1) / BWD_BLOCKS;
   int nb = (T + rpb - 1) / rpb;

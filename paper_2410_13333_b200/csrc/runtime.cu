@@ -236,8 +236,13 @@ static void build_shape(const malleus_model_cfg& cfg, const PlanInfo& p, int ran
   L.v0 = 0;
   for (int k = 0; k < L.member; ++k) L.v0 += st.vocab[k];
   L.slots = std::max(1, std::min(L.PP - L.stage, std::max(pp.n_micro, 1)));
+  // pair mode on TP-1 single-stage pipelines: on a TP > 1 stage the deferring micro-batch has no
+  // weight-gradient GEMM for the backward TP sums to overlap, so its waits for a slower member are
+  // exposed (C2 N = 2, rank 1 at 2x: 176.5 K tokens/s paired vs 208.4 K unpaired, profiles/r02);
+  // MALLEUS_WGRAD_PAIR_TP=1 allows it there too (tests), MALLEUS_WGRAD_PAIR_OFF=1 disables it
   static const bool pair_off = getenv("MALLEUS_WGRAD_PAIR_OFF") != nullptr;
-  L.pair = !pair_off && L.PP == 1 && !L.f32 && pp.n_micro >= 2;
+  static const bool pair_tp = getenv("MALLEUS_WGRAD_PAIR_TP") != nullptr;
+  L.pair = !pair_off && L.PP == 1 && !L.f32 && pp.n_micro >= 2 && (L.TP == 1 || pair_tp);
   if (L.pair) L.slots = 2;
   L.prev_ranks.clear();
   L.next_ranks.clear();

@@ -87,8 +87,10 @@ def test_rmsnorm_bwd(L, T, h):
 
 @pytest.mark.parametrize("T,h", [(64, 256), (300, 512), (2048, 4096), (1000, 3072), (97, 6656), (64, 128)])
 def test_rmsnorm_bwd_bf16_dy(L, T, h):
-    """bf16 input gradient (TP sums, TP-1 dgrad output) through the block kernel (the warp-per-row
-    variant, opt-in with MALLEUS_NORM_BWD_WARP=1, is checked in a subprocess below)."""
+    """bf16 input gradient (TP sums, TP-1 dgrad output) through the row-group kernel (h / 8 a multiple
+    of 32; ragged T, one or several rows per CTA, h = 3072 / 6656 with partial blocks) or the block
+    kernel (h = 128); the block kernel for every shape (MALLEUS_NORM_BWD_BLOCK=1) and the warp-per-row
+    variant (MALLEUS_NORM_BWD_WARP=1) are checked in subprocesses below."""
     x = bf(normal_matrix((T, h), 14))
     g = bf(1 + 0.1 * normal_matrix((h,), 15))
     dy = bf(normal_matrix((T, h), 16))
@@ -109,16 +111,19 @@ def test_rmsnorm_bwd_bf16_dy(L, T, h):
     assert torch.equal(dg, dg2)  # deterministic
 
 
-def test_rmsnorm_bwd_bf16_dy_warp_kernel():
-    """The opt-in warp-per-row RMSNorm backward (per-warp shared-memory dg slices) in a fresh process."""
+@pytest.mark.parametrize("switch", ["MALLEUS_NORM_BWD_WARP", "MALLEUS_NORM_BWD_BLOCK"])
+def test_rmsnorm_bwd_kernel_variants(switch):
+    """The opt-in RMSNorm backward variants in a fresh process: the warp-per-row kernel (per-warp
+    shared-memory dg slices) and the block kernel (row band per CTA) on every shape above."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, MALLEUS_NORM_BWD_WARP="1")
-    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k", "rmsnorm_bwd_bf16_dy and not warp",
+    env = dict(os.environ, **{switch: "1"})
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k",
+                        "(test_rmsnorm_bwd or rmsnorm_bwd_bf16_dy) and not variants",
                         os.path.join(root, "tests", "test_gpu_kernels.py")], env=env, capture_output=True, text=True,
                        cwd=root, timeout=600)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]

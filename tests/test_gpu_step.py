@@ -127,6 +127,26 @@ def test_tp_scatter_epilogue_bitwise(plan, tmp_path):
     assert res["scatter"]["losses"] == res["pull"]["losses"], (res["scatter"]["losses"], res["pull"]["losses"])
 
 
+@pytest.mark.parametrize("plan", ["P2", "P9"])
+def test_wgrad_pair_on_tp_stage(plan, tmp_path):
+    """Paired weight-gradient GEMMs (K = 2T over micro-batches 2p, 2p + 1) are on by default only on
+    TP-1 single-stage pipelines; MALLEUS_WGRAD_PAIR_TP=1 turns them on for TP > 1 stages too (the
+    backward TP sums then overlap the flush micro-batch's GEMMs only): oracle parity of the step."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    n = PLAN_WORLD[plan]
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"{plan} needs {n} GPUs")
+    out = tmp_path / "r.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29537", os.path.join(ROOT, "tests", "mp_worker.py"), plan,
+           str(out), "2", "c1m"]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "MALLEUS_WGRAD_PAIR_TP": "1"})
+    assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+    _assert_ok(json.load(open(out)))
+
+
 def test_p0_run_to_run_bitwise():
     """Determinism: every reduction runs in a fixed order (no float atomics; the
     embedding backward sums repeated tokens in position order), so two runs of the same plan give
