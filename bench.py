@@ -432,19 +432,16 @@ def main():
     gemm_share = (gms.value / args.steps) / ms if ms > 0 else None
     # peak: the measured sustained bf16 figure (the GEMMs run inside a long, power-capped step); when a
     # run's GEMMs beat it (a cooler step, e.g. a rank that waits for a straggler runs at ~1.9 GHz) the
-    # burst figure is the bound instead.  frac_at_run_clock scales the burst peak to the median SM clock
-    # sampled in the timed region (the clock-normalised efficiency).
+    # burst figure is the bound instead; frac_of_burst is reported beside it.
     sus, burst = pk["bf16_tflops_sustained"], pk["bf16_tflops"]
     use_burst = bool(gemm_tf and gemm_tf > sus)
     peak = burst if use_burst else sus
-    run_mhz, max_mhz = (clk or {}).get("sm_mhz"), (clk or {}).get("sm_max_mhz") or pk.get("sm_max_mhz")
     roof = {"bound": "tensor", "kernel": "gemm_tcgen05_kernel (all layer/head GEMMs)",
             "achieved": gemm_tf, "peak": peak, "unit": "TFLOP/s",
             "frac": (gemm_tf / peak) if gemm_tf else None,
             "peak_kind": (f"{pk_kind} bf16 burst (the GEMMs ran above the sustained {sus} TF/s)" if use_burst
                           else f"{pk_kind} bf16 sustained (kernel timed inside a long step)"),
             "frac_of_burst": (gemm_tf / burst) if gemm_tf else None,
-            "frac_at_run_clock": (gemm_tf / (burst * run_mhz / max_mhz)) if (gemm_tf and run_mhz and max_mhz) else None,
             "traffic": None, "gemm_launches_per_step": gl.value // max(1, args.steps),
             "gemm_share_of_step": gemm_share}
     prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
