@@ -849,6 +849,31 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
     if (cudaMallocManaged(&trace, 2 * 16 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace = nullptr;
     attn_bwd_trace_buffer = trace;
   }
+  // dK/dV and dQ are independent (same inputs, disjoint column blocks of dqkv): dQ runs on a side
+  // stream forked from `st` and joined back, so its CTAs fill the SMs the dK/dV grid's last wave
+  // leaves idle (one CTA of either kernel per SM: ~190 KB of shared memory each).
+  // MALLEUS_ATTN_BWD_SERIAL=1 launches both on `st`.
+  static const bool serial = getenv("MALLEUS_ATTN_BWD_SERIAL") != nullptr;
+  cudaStream_t side = st;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (!serial) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static cudaStream_t sides[64] = {};
+    static cudaEvent_t forks[64] = {}, joins[64] = {};
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!sides[dev]) {
+      if ((e = cudaStreamCreateWithFlags(&sides[dev], cudaStreamNonBlocking)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    side = sides[dev];
+    fork = forks[dev];
+    join = joins[dev];
+    if ((e = cudaEventRecord(fork, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
+  }
   attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n_kv, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, n_kv, lse, dsum,
                                                                       (__nv_bfloat16*)dqkv, scale, rope_cs, trace); count_launch();
   static unsigned long long* trace2 = nullptr;
@@ -856,8 +881,13 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
     if (cudaMallocManaged(&trace2, 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace2 = nullptr;
     attn_dq_trace_buffer = trace2;
   }
-  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, st>>>(tm, tmo, s, n, n_kv, lse, dsum,
-                                                                     (__nv_bfloat16*)dqkv, scale, rope_cs, trace2); count_launch();
+  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, side>>>(tm, tmo, s, n, n_kv, lse, dsum,
+                                                                       (__nv_bfloat16*)dqkv, scale, rope_cs, trace2); count_launch();
+  if (!serial) {
+    cudaError_t e = cudaEventRecord(join, side);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, join, 0)) != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
