@@ -21,6 +21,7 @@
 #include <atomic>
 #include <utility>
 #include <vector>
+#include <algorithm>
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
@@ -859,16 +860,34 @@ void gemm_profile_enable(bool on) {
   g_prof.used = 0;
   g_prof.flops.clear();
 }
+// ms = the length of the union of the launches' [start, end] intervals (GEMM-busy wall time): the sum of
+// their durations when they run one after another on one stream; when weight-gradient GEMMs run on a
+// side stream beside the dgrad chain (pair mode) overlapping intervals are counted once
 cudaError_t gemm_profile_query(long long* launches, double* flops, double* ms) {
-  double f = 0, t = 0;
+  double f = 0;
+  std::vector<std::pair<double, double>> iv;
+  iv.reserve(g_prof.used);
   for (size_t i = 0; i < g_prof.used; ++i) {
     cudaError_t e = cudaEventSynchronize(g_prof.ev[i].second);
     if (e != cudaSuccess) return e;
-    float x = 0.f;
-    cudaEventElapsedTime(&x, g_prof.ev[i].first, g_prof.ev[i].second);
-    t += x;
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, g_prof.ev[0].first, g_prof.ev[i].first);
+    cudaEventElapsedTime(&b, g_prof.ev[0].first, g_prof.ev[i].second);
+    iv.push_back({a, b});
     f += g_prof.flops[i];
   }
+  std::sort(iv.begin(), iv.end());
+  double t = 0, cur_a = 0, cur_b = -1;
+  for (const auto& x : iv) {
+    if (x.first > cur_b) {
+      if (cur_b > cur_a) t += cur_b - cur_a;
+      cur_a = x.first;
+      cur_b = x.second;
+    } else {
+      cur_b = std::max(cur_b, x.second);
+    }
+  }
+  if (cur_b > cur_a) t += cur_b - cur_a;
   *launches = (long long)g_prof.used;
   *flops = f;
   *ms = t;

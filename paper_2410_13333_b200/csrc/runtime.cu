@@ -168,6 +168,9 @@ struct malleus_ctx {
   bool failed = false;                        // malleus_wait timed out: communicators aborted
   cudaStream_t tp_side = nullptr;             // backward TP reductions overlapping the wgrad GEMM
   cudaEvent_t tp_ev_a = nullptr, tp_ev_b = nullptr;
+  cudaStream_t wg_side = nullptr;             // pair-flush weight-gradient GEMMs beside the dgrad chain
+  cudaEvent_t wg_fork_ev = nullptr, wg_join_ev = nullptr;
+  bool wg_pending = false;
   float slowdown = 1.f;
   int slow_mode = 0;
   DutyTimer duty[kDutySegs];
@@ -786,6 +789,40 @@ static void duty_begin(malleus_ctx* ctx, int seg, cudaStream_t st);
 static void duty_end(malleus_ctx* ctx, cudaStream_t st);
 static void duty_relearn(malleus_ctx* ctx);
 
+// Weight-gradient GEMMs of a pair's flush micro-batch on a side stream (TP-1 stages, pair mode): they
+// read only saved activations of the pair's two slots and the per-layer gradient stashes, which
+// nothing overwrites before the next micro-batch's forward, so they run beside the dgrad chain and
+// fill the SMs its GEMM tails, norms and attention leave idle (the persistent GEMM grids take every
+// SM, so this is tail filling, not sharing).  Each is forked from the main stream once its inputs
+// are enqueued; the side stream is joined before the next forward and before the gradient sync.
+// Not under DUTY emulation (its segment timers live on the main stream); MALLEUS_WGRAD_SIDE_OFF=1.
+static bool wg_side_on(const malleus_ctx* ctx, int pair) {
+  static const bool off = getenv("MALLEUS_WGRAD_SIDE_OFF") != nullptr;
+  const Layout& L = *ctx->L;
+  return !off && pair == 1 && L.pair && L.TP == 1 && !(ctx->slow_mode == 2 && ctx->slowdown > 1.f);
+}
+static malleus_status wg_stream(malleus_ctx* ctx, int pair, cudaStream_t st, cudaStream_t* out) {
+  *out = st;
+  if (!wg_side_on(ctx, pair)) return MALLEUS_OK;
+  if (!ctx->wg_side) {
+    CK(cudaStreamCreateWithFlags(&ctx->wg_side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->wg_fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->wg_join_ev, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(ctx->wg_fork_ev, st));
+  CK(cudaStreamWaitEvent(ctx->wg_side, ctx->wg_fork_ev, 0));
+  ctx->wg_pending = true;
+  *out = ctx->wg_side;
+  return MALLEUS_OK;
+}
+static malleus_status wg_join(malleus_ctx* ctx, cudaStream_t st) {
+  if (!ctx->wg_pending) return MALLEUS_OK;
+  CK(cudaEventRecord(ctx->wg_join_ev, ctx->wg_side));
+  CK(cudaStreamWaitEvent(st, ctx->wg_join_ev, 0));
+  ctx->wg_pending = false;
+  return MALLEUS_OK;
+}
+
 static malleus_status tp_allreduce(malleus_ctx* ctx, float* buf, size_t n, ncclRedOp_t op, cudaStream_t st) {
   Layout& L = *ctx->L;
   duty_end(ctx, st);
@@ -1161,7 +1198,11 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
       g.glu_done = &glu_done;
     }
     CK(gemm_bf16(g, st));
-    if (wg) RET(gemm(ctx, F, h, Kw, Y0.u, F, true, w_dy, h, true, P.dwd, h, wm, st));
+    if (wg) {
+      cudaStream_t ws;
+      RET(wg_stream(ctx, pair, st, &ws));
+      RET(gemm(ctx, F, h, Kw, Y0.u, F, true, w_dy, h, true, P.dwd, h, wm, ws));
+    }
     if (!glu_done) CK(k_swiglu_bwd(L, T, F, Y.gu, L.du, dgu, st));
   }
   RET(part_gemm(ctx, T, h, 2 * F, dgu, 2 * F, false, P.wgu, h, true, st));
@@ -1170,14 +1211,22 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
     RET(gemm_co(ctx, 2 * F, h, Kw, w_dgu, 2 * F, true, Y0.a2, h, true, P.dwgu, h, wm, st));
     RET(tp_sum_end(ctx, st));
   } else {
-    if (wg) RET(gemm(ctx, 2 * F, h, Kw, w_dgu, 2 * F, true, Y0.a2, h, true, P.dwgu, h, wm, st));
+    if (wg) {
+      cudaStream_t ws;
+      RET(wg_stream(ctx, pair, st, &ws));
+      RET(gemm(ctx, 2 * F, h, Kw, w_dgu, 2 * F, true, Y0.a2, h, true, P.dwgu, h, wm, ws));
+    }
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 4, st);
   CK(k_norm_bwd(L, T, h, Y.x1, P.g2, Y.r2, L.part, dy, dx1, P.dg2, L.scratch, st, tp_sum_bf16(L)));
   // attention
   RET(gemm(ctx, T, nd, h, dx1, h, false, P.wo, h, false, L.dout, nd, GEMM_STORE_BF16, st));
-  if (wg) RET(gemm(ctx, nd, h, Kw, Y0.o, nd, true, w_dx1, h, true, P.dwo, h, wm, st));
+  if (wg) {
+    cudaStream_t ws;
+    RET(wg_stream(ctx, pair, st, &ws));
+    RET(gemm(ctx, nd, h, Kw, Y0.o, nd, true, w_dx1, h, true, P.dwo, h, wm, ws));
+  }
   CK(k_attn_bwd(L, L.plan.b, c.seq_len, L.n_loc, d, Y.qkv, Y.o, Y.lse, L.dout, dqkv, L.dsum, st, L.rope_cs));
   if (debug_sync()) { fprintf(stderr, "[malleus] attn bwd ..."); CK(cudaStreamSynchronize(st)); fprintf(stderr, " ok\n"); }
   if (!(L.rope_cs && attention_bwd_fuses_rope(c.seq_len, d)))
@@ -1188,7 +1237,11 @@ static malleus_status layer_bwd_impl(malleus_ctx* ctx, int li, int si, const uin
     RET(gemm_co(ctx, qkvw, h, Kw, w_dqkv, qkvw, true, Y0.a1, h, true, P.dwqkv, h, wm, st));
     RET(tp_sum_end(ctx, st));
   } else {
-    if (wg) RET(gemm(ctx, qkvw, h, Kw, w_dqkv, qkvw, true, Y0.a1, h, true, P.dwqkv, h, wm, st));
+    if (wg) {
+      cudaStream_t ws;
+      RET(wg_stream(ctx, pair, st, &ws));
+      RET(gemm(ctx, qkvw, h, Kw, w_dqkv, qkvw, true, Y0.a1, h, true, P.dwqkv, h, wm, ws));
+    }
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 5, st);
@@ -1231,7 +1284,11 @@ static malleus_status head_fwd_bwd(malleus_ctx* ctx, int si, const int32_t* tgt,
     RET(gemm_co(ctx, V, h, Kw, w_dl, V, true, w_xf, h, true, L.dWlm, h, wm_lm, st));
     RET(tp_sum_end(ctx, st));
   } else {
-    if (wg) RET(gemm(ctx, V, h, Kw, w_dl, V, true, w_xf, h, true, L.dWlm, h, wm_lm, st));
+    if (wg) {
+      cudaStream_t ws;
+      RET(wg_stream(ctx, pair, st, &ws));
+      RET(gemm(ctx, V, h, Kw, w_dl, V, true, w_xf, h, true, L.dWlm, h, wm_lm, ws));
+    }
     RET(tp_sum(ctx, st));
   }
   duty_begin(ctx, 8, st);
@@ -1362,6 +1419,7 @@ static malleus_status train_step_impl(malleus_ctx* ctx, const int32_t* tokens, c
     auto fwd = [&](int j) -> malleus_status {
       const int si = j % L.slots;
       Slot& S = L.slot[si];
+      RET(wg_join(ctx, st));  // the previous pair's side-stream wgrads read the slots this forward overwrites
       if (L.first) CK(k_embed_fwd(L, L.T, c.hidden, tok_mb(j), L.E, S.x[0], st));
       for (int li = 0; li < L.n_local; ++li) RET(layer_fwd_impl(ctx, li, si, st));
       if (L.last) RET(head_fwd_bwd(ctx, si, tgt_mb(j), first_of(j), st, pair_of(j)));
@@ -1412,6 +1470,7 @@ static malleus_status train_step_impl(malleus_ctx* ctx, const int32_t* tokens, c
       RET(pp_exchange(ctx, nullptr, nullptr, L.first ? nullptr : dx, nullptr, st));
     }
   }
+  RET(wg_join(ctx, st));
   RET(grad_sync_impl(ctx, adam, st));
   // world loss: sum over pipelines of w_i * loss_i (only last-stage member 0 contributes)
   NK(ncclAllReduce(L.loss_acc, L.loss_acc, 1, ncclFloat, ncclSum, ctx->world_comm, st));
@@ -1535,6 +1594,12 @@ malleus_status malleus_destroy(malleus_ctx* ctx) {
     cudaStreamDestroy(ctx->tp_side);
     cudaEventDestroy(ctx->tp_ev_a);
     cudaEventDestroy(ctx->tp_ev_b);
+  }
+  if (ctx->wg_side) {
+    cudaStreamSynchronize(ctx->wg_side);
+    cudaStreamDestroy(ctx->wg_side);
+    cudaEventDestroy(ctx->wg_fork_ev);
+    cudaEventDestroy(ctx->wg_join_ev);
   }
   delete ctx;
   return MALLEUS_OK;
