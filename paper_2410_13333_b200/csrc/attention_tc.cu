@@ -71,7 +71,7 @@ constexpr int SMEM_FWD = Q_BYTES + 2 * FWD_STAGES * K_BYTES + 1024 + 1024;
 template <int NPOLY>
 __global__ void __launch_bounds__(320, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, int n_kv, __nv_bfloat16* __restrict__ o,
-                   float* __restrict__ lse, float scale, unsigned long long* __restrict__ trace) {
+                   float* __restrict__ lse, float scale, unsigned long long* __restrict__ trace, int order) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -93,16 +93,19 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int n, int n_k
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;
-  const int qb = nqb - 1 - blockIdx.x;  // heaviest first
-  const int head = blockIdx.y, b = blockIdx.z;
+  // grid (heads, query blocks, sequences): CTAs are dispatched x-fastest, so every head's heaviest
+  // query block goes first and the last wave holds the lightest (longest-processing-time-first order)
+  // (order = 1: the previous head-major grid (query blocks, heads, sequences), MALLEUS_ATTN_GRID_HEADMAJOR=1)
+  const int qb = nqb - 1 - (order ? blockIdx.x : blockIdx.y);
+  const int head = order ? blockIdx.y : blockIdx.x, b = blockIdx.z;
   const int n_tiles = qb + 1;           // causal: key tiles 0..qb
   const int row0 = b * s + qb * TQ;     // first query row in qkv
   const int nd = n * DH;
   // qkv = q (n heads) | k (n_kv heads) | v (n_kv heads); GQA: this query head reads KV head head / g
   const int kcol = nd + (head / (n / n_kv)) * DH, vcol = nd + n_kv * DH + (head / (n / n_kv)) * DH;
   // debugging aid (MALLEUS_ATTN_TRACE): globaltimer stamps of CTAs (0, 0..1, 0), [event][tile]
-  unsigned long long* tr = (trace && blockIdx.x == 0 && blockIdx.y < 2 && blockIdx.z == 0)
-                               ? trace + blockIdx.y * 8 * 64 : nullptr;
+  unsigned long long* tr = (trace && blockIdx.y == 0 && blockIdx.x < 2 && blockIdx.z == 0)
+                               ? trace + blockIdx.x * 8 * 64 : nullptr;
   auto stamp = [&](int ev, int i) {
     if (tr && i < 64) { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); tr[ev * 64 + i] = t; }
   };
@@ -417,12 +420,12 @@ __global__ void __launch_bounds__(320, 1)
 attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm64,
                        const __grid_constant__ CUtensorMap tmo64, int s, int n, int n_kv, const float* __restrict__ lse,
                        const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv, float scale,
-                       const float2* __restrict__ rope_cs, unsigned long long* __restrict__ trace) {
+                       const float2* __restrict__ rope_cs, unsigned long long* __restrict__ trace, int order) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // debugging aid (MALLEUS_ATTN_TRACE): stamps of CTAs (0, 0..1, 0), [event][iteration]
-  unsigned long long* tr = (trace && blockIdx.x == 0 && blockIdx.y < 2 && blockIdx.z == 0)
-                               ? trace + blockIdx.y * 16 * 64 : nullptr;
+  unsigned long long* tr = (trace && blockIdx.y == 0 && blockIdx.x < 2 && blockIdx.z == 0)
+                               ? trace + blockIdx.x * 16 * 64 : nullptr;
   auto stamp = [&](int ev, int i) {
     if (tr && i < 64) { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); tr[ev * 64 + i] = t; }
   };
@@ -441,8 +444,10 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_cons
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x;  // kb = 0 has the most query sub-tiles: scheduled first
-  const int kvh = blockIdx.y, b = blockIdx.z;  // KV head (GQA: shared by the g query heads of its group)
+  // grid (KV heads, key blocks, sequences), dispatched x-fastest: kb = 0 (the most query sub-tiles) of
+  // every KV head first, the lightest key blocks in the last wave
+  const int kb = order ? blockIdx.x : blockIdx.y;
+  const int kvh = order ? blockIdx.y : blockIdx.x, b = blockIdx.z;  // KV head (GQA: shared by the g query heads of its group)
   const int nd = n * DH, g = n / n_kv, ldq = nd + 2 * n_kv * DH;
   const int j0 = 2 * kb, n_sub = s / 64 - j0;  // query sub-tiles per query head
   const int n_it = g * n_sub;                   // iterations: the group's query heads one after another
@@ -615,7 +620,8 @@ __global__ void __launch_bounds__(320, 1)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, int s, int n,
                       int n_kv,
                       const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                      float scale, const float2* __restrict__ rope_cs, unsigned long long* __restrict__ trace) {
+                      float scale, const float2* __restrict__ rope_cs, unsigned long long* __restrict__ trace,
+                      int order) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   unsigned long long* tr = (trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? trace : nullptr;
   auto stamp = [&](int ev, int i) {
@@ -639,8 +645,9 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_const
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / TQ;
-  const int qb = nqb - 1 - blockIdx.x;  // heaviest first
-  const int head = blockIdx.y, b = blockIdx.z;
+  // grid (heads, query blocks, sequences): heaviest first overall (order = 1: head-major, as before)
+  const int qb = nqb - 1 - (order ? blockIdx.x : blockIdx.y);
+  const int head = order ? blockIdx.y : blockIdx.x, b = blockIdx.z;
   const int n_it = qb + 1;              // key tiles up to the diagonal
   const int nd = n * DH;
   const int row0 = b * s + qb * TQ;
@@ -814,6 +821,15 @@ unsigned long long* attn_trace_buffer = nullptr;
 unsigned long long* attn_bwd_trace_buffer = nullptr;
 unsigned long long* attn_dq_trace_buffer = nullptr;
 
+// CTA order of the attention grids: 0 = (heads, blocks, sequences) — dispatched x-fastest, so the heaviest
+// block of every head goes first and the last wave holds the lightest (longest-processing-time first);
+// 1 = the earlier head-major (blocks, heads, sequences) order (MALLEUS_ATTN_GRID_HEADMAJOR=1, A/B switch)
+static int grid_order() {
+  static const int o = getenv("MALLEUS_ATTN_GRID_HEADMAJOR") ? 1 : 0;
+  return o;
+}
+static dim3 grid_of(int heads, int blocks, int nb) { return grid_order() ? dim3(blocks, heads, nb) : dim3(heads, blocks, nb); }
+
 static bool map_rows(CUtensorMap* m, const void* base, long long cols, long long rows, int box_rows = 128) {
   auto enc = encoder();
   if (!enc) return false;
@@ -874,15 +890,17 @@ cudaError_t attention_bwd_tc(int nb, int s, int n, const void* qkv, const float*
     if ((e = cudaEventRecord(fork, st)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
   }
-  attn_bwd_dkv_tc_kernel<<<dim3(s / TK, n_kv, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, n_kv, lse, dsum,
-                                                                      (__nv_bfloat16*)dqkv, scale, rope_cs, trace); count_launch();
+  attn_bwd_dkv_tc_kernel<<<grid_of(n_kv, s / TK, nb), 320, BWD1_SMEM, st>>>(tm, tm64, tmo64, s, n, n_kv, lse, dsum,
+                                                                         (__nv_bfloat16*)dqkv, scale, rope_cs, trace,
+                                                                         grid_order()); count_launch();
   static unsigned long long* trace2 = nullptr;
   if (getenv("MALLEUS_ATTN_TRACE") && !trace2) {
     if (cudaMallocManaged(&trace2, 8 * 64 * sizeof(unsigned long long)) != cudaSuccess) trace2 = nullptr;
     attn_dq_trace_buffer = trace2;
   }
-  attn_bwd_dq_tc_kernel<<<dim3(s / TQ, n, nb), 320, BWD2_SMEM, side>>>(tm, tmo, s, n, n_kv, lse, dsum,
-                                                                       (__nv_bfloat16*)dqkv, scale, rope_cs, trace2); count_launch();
+  attn_bwd_dq_tc_kernel<<<grid_of(n, s / TQ, nb), 320, BWD2_SMEM, side>>>(tm, tmo, s, n, n_kv, lse, dsum,
+                                                                          (__nv_bfloat16*)dqkv, scale, rope_cs, trace2,
+                                                                          grid_order()); count_launch();
   if (!serial) {
     cudaError_t e = cudaEventRecord(join, side);
     if (e != cudaSuccess) return e;
@@ -925,7 +943,8 @@ cudaError_t attention_fwd_tc(int nb, int s, int n, const void* qkv, void* o, flo
   }();
   auto fn = npoly <= 0 ? attn_fwd_tc_kernel<0> : npoly == 1 ? attn_fwd_tc_kernel<1>
           : npoly == 2 ? attn_fwd_tc_kernel<2> : attn_fwd_tc_kernel<3>;
-  fn<<<dim3(s / TQ, n, nb), 320, SMEM_FWD, st>>>(tm, s, n, n_kv, (__nv_bfloat16*)o, lse, rsqrtf((float)DH), trace);
+  fn<<<grid_of(n, s / TQ, nb), 320, SMEM_FWD, st>>>(tm, s, n, n_kv, (__nv_bfloat16*)o, lse, rsqrtf((float)DH), trace,
+                                                    grid_order());
   count_launch();
   return cudaGetLastError();
 }
