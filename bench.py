@@ -310,14 +310,9 @@ def main():
         # candidates: the speed-proportional re-split and two damped ones (plans.rebalance: compute is
         # not proportional to a member's share, so the full step can overshoot); each is migrated to
         # and measured, and the fastest plan (the initial one included) is kept
-        obj = [[Pl.rebalance(cfg, plan, {r: comp[r] for r in range(world)}, damp=a) for a in (1.0, 2 / 3, 1 / 3)]
-               if rank == 0 else None]
+        obj = [Pl.resplit_candidates(cfg, plan, {r: comp[r] for r in range(world)}) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        cands, seen = [], {json.dumps(plan["pipes"])}
-        for c in obj[0]:
-            if json.dumps(c["pipes"]) not in seen:
-                seen.add(json.dumps(c["pipes"]))
-                cands.append(c)
+        cands = obj[0]
         best, best_ms, tried, allm = plan, ms_before, [], []
         for c in cands:
             mig = eng.migrate(c)

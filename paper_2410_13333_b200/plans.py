@@ -224,6 +224,21 @@ def rebalance(cfg, plan, compute_ms: dict, min_micro: int = 0, damp: float = 1.0
     return p
 
 
+def resplit_candidates(cfg, plan, compute_ms: dict, damps=(1.0, 2 / 3, 1 / 3)):
+    """The measured re-split candidates of the straggler loop (DESIGN §3 "Measured re-split"):
+    rebalance() with each damping, duplicates and the current plan's own split dropped, in damp order.
+    The caller migrates to each, times it and keeps the fastest (the current plan included)."""
+    import json
+    seen, out = {json.dumps(plan["pipes"])}, []
+    for a in damps:
+        c = rebalance(cfg, plan, compute_ms, damp=a)
+        key = json.dumps(c["pipes"])
+        if key not in seen:
+            seen.add(key)
+            out.append(c)
+    return out
+
+
 def _heads_split(H, rates):
     return _minmax(H, rates)
 

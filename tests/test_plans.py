@@ -44,6 +44,25 @@ def test_rebalance_damped_between_current_and_full():
     assert mm[0] == q["pipes"][1]["n_micro"] and mm == sorted(mm)
 
 
+def test_resplit_candidates():
+    """The straggler loop's measured candidates: distinct, valid, never the current split, full first."""
+    cfg = C2_7B_SLICE
+    p = Pl.ladder_plan(cfg, 2, 16)
+    c = Pl.resplit_candidates(cfg, p, {0: 111.9, 1: 172.8})
+    assert [x["pipes"][0]["stages"][0]["heads"] for x in c] == [[25, 7], [24, 8], [23, 9]]
+    for x in c:
+        validate(cfg, x, 2)
+    # both members take equally long on their shares (the split is balanced): the heads stay (FFN /
+    # vocab tiles may move by one tile of rounding)
+    for x in Pl.resplit_candidates(cfg, p, {0: 100.0, 1: 100.0}):
+        assert x["pipes"][0]["stages"][0]["heads"] == [22, 10]
+    q = Pl.ladder_plan(cfg, 4, 16)
+    cq = Pl.resplit_candidates(cfg, q, {0: 60.0, 1: 80.0, 2: 40.0, 3: 40.0})
+    assert cq and len({str(x["pipes"]) for x in cq}) == len(cq)
+    for x in cq:
+        validate(cfg, x, 4)
+
+
 def test_rebalance_micro_batches():
     cfg = C2_7B_SLICE
     p = Pl.ladder_plan(cfg, 4, 16)

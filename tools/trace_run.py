@@ -141,15 +141,11 @@ def main():
         if not args.sync and changed:
             comp = [None] * world
             dist.all_gather_object(comp, eng.timing()["compute"])
-            obj = [[Pl.rebalance(cfg, plan, {r: comp[r] for r in range(world)}, damp=a) for a in (1.0, 2 / 3)]
+            obj = [Pl.resplit_candidates(cfg, plan, {r: comp[r] for r in range(world)}, damps=(1.0, 2 / 3))
                    if rank == 0 else None]  # full and damped re-split (plans.rebalance docstring)
             dist.broadcast_object_list(obj, src=0)
-            seen, at = {json.dumps(plan["pipes"])}, plan
-            best = plan
+            at = best = plan
             for cand in obj[0]:
-                if json.dumps(cand["pipes"]) in seen:
-                    continue
-                seen.add(json.dumps(cand["pipes"]))
                 eng.migrate(cand)
                 at = cand
                 steps(2)
